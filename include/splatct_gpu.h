@@ -1,0 +1,197 @@
+/*
+ * splatct_gpu.h — C ABI of the B200-native R²-Gaussian hot-path engine.
+ *
+ * Drop-in boundary for the reference's C++ host API (splatct, CPU/fp64):
+ *   render            rasterizer.hpp:53-54   (rasterizer.cpp:112-157)
+ *   render_backward   rasterizer.hpp:61-64   (rasterizer.cpp:195-342)
+ *   project_kernel    rasterizer.hpp:36-38   (rasterizer.cpp:103-110)
+ *   voxelize          voxelizer.hpp:60-61    (voxelizer.cpp:108-138)
+ *   voxelize_backward voxelizer.hpp:65-67    (voxelizer.cpp:140-224)
+ *   tv3d_loss         objectives.hpp:31      (objectives.cpp:169-202)
+ *   l1_loss/dssim_loss objectives.hpp        (objectives.cpp:113-167)
+ *   Adam::step + normalize_rotations         (trainer.cpp:144-163,310-319;
+ *                                             gaussian_cloud.cpp:112-117)
+ *   lr_at             trainer.hpp            (trainer.cpp:34-36)
+ * Types:
+ *   sct_scanner  = ScannerConfig minus angles (geometry.hpp:12-31); thetas are per call
+ *   sct_raster_opts = RasterOptions (rasterizer.hpp:15-21)
+ *   sct_grid     = GridSpec (voxelizer.hpp:13-24)
+ *   sct_cloud    = GaussianCloud raw arrays (gaussian_cloud.hpp:62-66), fp32,
+ *                  same field order/layout: rho_raw[M], pos[3M] (xyz per kernel),
+ *                  scale_raw[3M], rot[4M] (w,x,y,z)
+ *   sct_grads    = CloudGrads (gaussian_cloud.hpp:84-96): ACCUMULATE (+=) semantics
+ *   sct_stats    = adaptive-control statistics (gaussian_cloud.hpp:74-77)
+ *
+ * Conventions
+ *   - Every function returns an int status: 0 ok, 2 config error (ConfigError),
+ *     3 data/dims error (DataError / DimMismatch), 4 divergence (non-finite
+ *     loss), 5 CUDA error, 1 other. sct_last_error() returns a thread-local
+ *     message for the last failure (common.hpp:27-64 exception taxonomy,
+ *     splatct_main.cpp:327-339 exit codes).
+ *   - Pointers in sct_cloud / sct_grads / sct_stats and image/volume buffers are
+ *     DEVICE pointers unless the function name ends in _host.
+ *   - Images are [n_views][H][W] row-major (pixel (u,v) at v*W+u, common.hpp:66-79);
+ *     volumes are x-fastest [(z*Y+y)*X+x] (voxelizer.hpp:29-31).
+ *   - One context serialises its calls on its stream (the reference's
+ *     exclusive-mutation contract); distinct contexts may run
+ *     concurrently. All work is enqueued on the context's stream.
+ *   - The cloud must not change between sct_render_fwd and sct_render_bwd
+ *     (the backward re-derives the projection chain from it, rasterizer.cpp:266-268).
+ */
+#ifndef SPLATCT_GPU_H
+#define SPLATCT_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCT_OK 0
+#define SCT_ERR_OTHER 1
+#define SCT_ERR_CONFIG 2
+#define SCT_ERR_DATA 3
+#define SCT_ERR_DIVERGENCE 4
+#define SCT_ERR_CUDA 5
+
+#define SCT_MODE_RECTIFIED 0
+#define SCT_MODE_BIASED 1
+
+typedef struct sct_ctx sct_ctx;
+typedef struct sct_fwd sct_fwd;
+
+typedef struct {
+  double l_so_mm;          /* source to rotation axis */
+  double l_sd_mm;          /* source to detector plane */
+  double det_size_mm[2];   /* detector_size_mm */
+  int32_t det_res_px[2];   /* detector_res_px (W, H) */
+  double extent_min_mm[3];
+  double extent_max_mm[3];
+  double near_clip_mm;     /* <= 0 selects 1% of l_so_mm (geometry.hpp:24-28) */
+} sct_scanner;
+
+typedef struct {
+  int32_t mode;                  /* SCT_MODE_RECTIFIED | SCT_MODE_BIASED */
+  double lowpass_eps_px;         /* 0.3 */
+  int32_t dilation_compensation; /* 1 */
+  int32_t freeze_jacobian;       /* 0 */
+  double cull_mahalanobis;       /* 3.0348542587702925 */
+} sct_raster_opts;
+
+typedef struct {
+  int32_t dims[3];
+  double origin_mm[3];
+  double spacing_mm[3];
+} sct_grid;
+
+typedef struct {
+  int64_t m;
+  double s_min_mm;
+  float* rho_raw;   /* [m] */
+  float* pos;       /* [3m] */
+  float* scale_raw; /* [3m] */
+  float* rot;       /* [4m] (w,x,y,z) */
+} sct_cloud;
+
+typedef struct {
+  float* rho_raw;
+  float* pos;
+  float* scale_raw;
+  float* rot;
+} sct_grads;
+
+typedef struct {
+  float* grad2d_norm_accum; /* [m] */
+  int32_t* grad_count;      /* [m] */
+  float* grad3d_accum;      /* [3m] */
+} sct_stats;
+
+typedef struct {
+  float *m_rho, *v_rho;     /* [m]  */
+  float *m_pos, *v_pos;     /* [3m] */
+  float *m_scale, *v_scale; /* [3m] */
+  float *m_rot, *v_rot;     /* [4m] */
+} sct_adam_state;
+
+/* ---- context ------------------------------------------------------------ */
+/* stream: a cudaStream_t (NULL = legacy default stream). */
+int sct_ctx_create(int device, void* stream, sct_ctx** out);
+int sct_ctx_destroy(sct_ctx* ctx);
+int sct_ctx_set_stream(sct_ctx* ctx, void* stream);
+int sct_ctx_sync(sct_ctx* ctx);
+/* deterministic != 0: fixed-order reductions everywhere (default 1). */
+int sct_ctx_set_deterministic(sct_ctx* ctx, int deterministic);
+const char* sct_last_error(void);
+const char* sct_version(void);
+/* number of engine kernels launched by this context so far (instrumentation). */
+int64_t sct_ctx_kernel_launches(const sct_ctx* ctx);
+
+/* ---- rasterizer --------------------------------------------------------- */
+/* Projects + bins + composites n_views views (one batched launch sequence).
+ * images: device [n_views][H][W] float. *state receives the forward state
+ * (tile lists, projected records) that sct_render_bwd consumes. */
+int sct_render_fwd(sct_ctx* ctx, const sct_cloud* cloud, const sct_scanner* scanner,
+                   const double* thetas, int32_t n_views, const sct_raster_opts* opts,
+                   float* images, sct_fwd** state);
+/* Accumulates dL/d(raw params) of all views of `state` into grads (+=);
+ * stats (nullable) receives the adaptive statistics as render_backward with
+ * accumulate_stats=true. dL_dimages: device [n_views][H][W]. */
+int sct_render_bwd(sct_ctx* ctx, sct_fwd* state, const sct_cloud* cloud, const float* dL_dimages,
+                   sct_grads* grads, sct_stats* stats);
+int sct_fwd_free(sct_fwd* state);
+/* forward-state introspection (host outputs; synchronises the context) */
+int sct_fwd_info(sct_fwd* state, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y,
+                 int64_t* n_visible);
+/* per-view tile lists in kernel indices: offsets[T+1], kernel_idx[pairs of this view]
+ * (host arrays; kernel_idx may be NULL to query offsets only). */
+int sct_fwd_tile_lists(sct_fwd* state, int32_t view, int64_t* offsets, int32_t* kernel_idx);
+/* per-view projected kernels (project_kernel for every kernel): host outputs
+ * visible[m] (0/1) and rec[m][11] = cx cy cov00 cov01 cov11 conic00 conic01
+ * conic11 amplitude mu depth, computed in FP64. */
+int sct_project_kernels(sct_ctx* ctx, const sct_cloud* cloud, const sct_scanner* scanner, double theta,
+                        const sct_raster_opts* opts, int32_t* visible, double* rec);
+
+/* Host-buffer entry points (reference-facing: host arrays in, host arrays out;
+ * the H2D/D2H copies run on the context stream). cloud arrays are host fp32.
+ * images_host [n_views][H][W]. */
+int sct_render_fwd_host(sct_ctx* ctx, const sct_cloud* cloud_host, const sct_scanner* scanner,
+                        const double* thetas, int32_t n_views, const sct_raster_opts* opts,
+                        float* images_host, sct_fwd** state);
+int sct_render_bwd_host(sct_ctx* ctx, sct_fwd* state, const sct_cloud* cloud_host,
+                        const float* dL_dimages_host, sct_grads* grads_host, sct_stats* stats_host);
+
+/* ---- voxelizer ---------------------------------------------------------- */
+/* Evaluates the brick-binned kernel sum on the grid. Only bricks with z index
+ * in [z_brick_begin, z_brick_end) are evaluated/written (z-slab sharding;
+ * pass 0, INT32_MAX for the whole grid). vol: device x-fastest [Z][Y][X];
+ * the slab's voxels are overwritten, others untouched. */
+int sct_voxelize_fwd(sct_ctx* ctx, const sct_cloud* cloud, const sct_grid* grid, double cull_mahalanobis,
+                     int32_t z_brick_begin, int32_t z_brick_end, float* vol);
+int sct_voxelize_bwd(sct_ctx* ctx, const sct_cloud* cloud, const sct_grid* grid, double cull_mahalanobis,
+                     int32_t z_brick_begin, int32_t z_brick_end, const float* dL_dvol, sct_grads* grads);
+/* brick lists for parity checks (host outputs, synchronises) */
+int sct_voxel_bins(sct_ctx* ctx, const sct_cloud* cloud, const sct_grid* grid, double cull_mahalanobis,
+                   int64_t* n_pairs, int64_t* offsets, int32_t* kernel_idx);
+int sct_voxelize_fwd_host(sct_ctx* ctx, const sct_cloud* cloud_host, const sct_grid* grid,
+                          double cull_mahalanobis, float* vol_host);
+
+/* ---- objectives / optimizer -------------------------------------------- */
+/* TV value (device double [1], written) and lambda-scaled gradient (device, overwritten). */
+int sct_tv3d(sct_ctx* ctx, const float* vol, const int32_t dims[3], float lambda, double* value_dev,
+             float* grad);
+/* L1 + lambda_ssim * D-SSIM of n images (device [n][H][W]) against measured;
+ * writes per-image values (device double [n][2]: l1, dssim) and
+ * dL/dI = (g_l1 + lambda_ssim*g_dssim) * grad_scale (device [n][H][W]). */
+int sct_photometric_loss(sct_ctx* ctx, const float* rendered, const float* measured, int32_t n, int32_t w,
+                         int32_t h, float render_scale, float lambda_ssim, float grad_scale,
+                         double* values_dev, float* dL_dI);
+/* Fused Adam over all four parameter groups + quaternion renormalisation.
+ * lr[4] = {pos, rho, scale, rot} (trainer.cpp:310-318 order), step t >= 1. */
+int sct_adam_step(sct_ctx* ctx, sct_cloud* params, sct_adam_state* state, const sct_grads* grads, int32_t t,
+                  const double lr[4], double beta1, double beta2, double eps);
+double sct_lr_at(double lr_init, double final_ratio, int32_t t, int32_t iters);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLATCT_GPU_H */

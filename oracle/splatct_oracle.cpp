@@ -439,15 +439,23 @@ static bool project_impl(const Cloud& c, int i, const View& view, const Det& det
 struct TileRange {
   int tx0, tx1, ty0, ty1;
 };
+// static_cast<int>(std::floor(v)) for every in-range value; clamped first so
+// that degenerate (huge) footprints convert deterministically (the reference's
+// cast is undefined there). The device kernels use the identical clamp.
+static inline int floor_int(double v) {
+  double f = std::floor(v);
+  f = std::fmin(std::fmax(f, -1073741824.0), 1073741824.0);
+  return static_cast<int>(f);
+}
 // rasterizer.cpp:89-99
 static TileRange tile_range(const Projected& g, const RasterOptions& o, int tiles_x, int tiles_y) {
   const double rx = o.cull_mahalanobis * std::sqrt(g.cov.m[0][0]);
   const double ry = o.cull_mahalanobis * std::sqrt(g.cov.m[1][1]);
   TileRange r;
-  r.tx0 = std::max(0, static_cast<int>(std::floor((g.center.x - rx) / kTilePx)));
-  r.tx1 = std::min(tiles_x - 1, static_cast<int>(std::floor((g.center.x + rx) / kTilePx)));
-  r.ty0 = std::max(0, static_cast<int>(std::floor((g.center.y - ry) / kTilePx)));
-  r.ty1 = std::min(tiles_y - 1, static_cast<int>(std::floor((g.center.y + ry) / kTilePx)));
+  r.tx0 = std::max(0, floor_int((g.center.x - rx) / kTilePx));
+  r.tx1 = std::min(tiles_x - 1, floor_int((g.center.x + rx) / kTilePx));
+  r.ty0 = std::max(0, floor_int((g.center.y - ry) / kTilePx));
+  r.ty1 = std::min(tiles_y - 1, floor_int((g.center.y + ry) / kTilePx));
   return r;
 }
 
@@ -725,8 +733,8 @@ static Bins bin_kernels(const Cloud& c, const Grid& g, double radius) {
       const double r = radius * std::sqrt(std::max(sigma.m[k][k], 0.0));
       const double a = (p[k] - r - g.origin[k]) / g.spacing[k];
       const double bb = (p[k] + r - g.origin[k]) / g.spacing[k];
-      int v0 = static_cast<int>(std::floor(a));
-      int v1 = static_cast<int>(std::floor(bb));
+      int v0 = floor_int(a);
+      int v1 = floor_int(bb);
       v0 = std::max(v0, 0);
       v1 = std::min(v1, g.dims[k] - 1);
       if (v0 > v1) {

@@ -1,0 +1,110 @@
+"""ctypes binding of include/splatct_gpu.h (libsplatct_b200.so).
+
+This is the only way the Python layer reaches the engine: there is no
+PyTorch/NumPy compute fallback. If the shared library is missing the import
+fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsplatct_b200.so")
+
+F = C.POINTER(C.c_float)
+D = C.POINTER(C.c_double)
+I32 = C.POINTER(C.c_int32)
+I64 = C.POINTER(C.c_int64)
+VP = C.c_void_p
+
+
+class sct_scanner(C.Structure):
+    _fields_ = [("l_so_mm", C.c_double), ("l_sd_mm", C.c_double), ("det_size_mm", C.c_double * 2),
+                ("det_res_px", C.c_int32 * 2), ("extent_min_mm", C.c_double * 3),
+                ("extent_max_mm", C.c_double * 3), ("near_clip_mm", C.c_double)]
+
+
+class sct_raster_opts(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("lowpass_eps_px", C.c_double), ("dilation_compensation", C.c_int32),
+                ("freeze_jacobian", C.c_int32), ("cull_mahalanobis", C.c_double)]
+
+
+class sct_grid(C.Structure):
+    _fields_ = [("dims", C.c_int32 * 3), ("origin_mm", C.c_double * 3), ("spacing_mm", C.c_double * 3)]
+
+
+class sct_cloud(C.Structure):
+    _fields_ = [("m", C.c_int64), ("s_min_mm", C.c_double), ("rho_raw", VP), ("pos", VP), ("scale_raw", VP),
+                ("rot", VP)]
+
+
+class sct_grads(C.Structure):
+    _fields_ = [("rho_raw", VP), ("pos", VP), ("scale_raw", VP), ("rot", VP)]
+
+
+class sct_stats(C.Structure):
+    _fields_ = [("grad2d_norm_accum", VP), ("grad_count", VP), ("grad3d_accum", VP)]
+
+
+class sct_adam_state(C.Structure):
+    _fields_ = [("m_rho", VP), ("v_rho", VP), ("m_pos", VP), ("v_pos", VP), ("m_scale", VP), ("v_scale", VP),
+                ("m_rot", VP), ("v_rot", VP)]
+
+
+P = C.POINTER
+
+SIGNATURES = {
+    "sct_ctx_create": (C.c_int, [C.c_int, VP, P(VP)]),
+    "sct_ctx_destroy": (C.c_int, [VP]),
+    "sct_ctx_set_stream": (C.c_int, [VP, VP]),
+    "sct_ctx_sync": (C.c_int, [VP]),
+    "sct_ctx_set_deterministic": (C.c_int, [VP, C.c_int]),
+    "sct_last_error": (C.c_char_p, []),
+    "sct_version": (C.c_char_p, []),
+    "sct_ctx_kernel_launches": (C.c_int64, [VP]),
+    "sct_render_fwd": (C.c_int, [VP, P(sct_cloud), P(sct_scanner), D, C.c_int32, P(sct_raster_opts), VP, P(VP)]),
+    "sct_render_bwd": (C.c_int, [VP, VP, P(sct_cloud), VP, P(sct_grads), P(sct_stats)]),
+    "sct_fwd_free": (C.c_int, [VP]),
+    "sct_fwd_info": (C.c_int, [VP, I64, I32, I32, I64]),
+    "sct_fwd_tile_lists": (C.c_int, [VP, C.c_int32, I64, I32]),
+    "sct_project_kernels": (C.c_int, [VP, P(sct_cloud), P(sct_scanner), C.c_double, P(sct_raster_opts), I32, D]),
+    "sct_render_fwd_host": (C.c_int, [VP, P(sct_cloud), P(sct_scanner), D, C.c_int32, P(sct_raster_opts), VP,
+                                      P(VP)]),
+    "sct_render_bwd_host": (C.c_int, [VP, VP, P(sct_cloud), VP, P(sct_grads), P(sct_stats)]),
+    "sct_voxelize_fwd": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, C.c_int32, C.c_int32, VP]),
+    "sct_voxelize_bwd": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, C.c_int32, C.c_int32, VP,
+                                   P(sct_grads)]),
+    "sct_voxel_bins": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, I64, I64, I32]),
+    "sct_voxelize_fwd_host": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, VP]),
+    "sct_tv3d": (C.c_int, [VP, VP, I32, C.c_float, VP, VP]),
+    "sct_photometric_loss": (C.c_int, [VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float,
+                                       C.c_float, VP, VP]),
+    "sct_adam_step": (C.c_int, [VP, P(sct_cloud), P(sct_adam_state), P(sct_grads), C.c_int32, D, C.c_double,
+                                C.c_double, C.c_double]),
+    "sct_lr_at": (C.c_double, [C.c_double, C.c_double, C.c_int32, C.c_int32]),
+}
+
+_lib = None
+
+
+def load():
+    """Load the engine library (raises ImportError if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} not found: the CUDA engine is not built. Run "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (nvcc, sm_100a). "
+                "There is no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(SIGNATURES.keys())

@@ -1,0 +1,172 @@
+// Binning preprocess kernels, FP64. This translation unit is compiled with
+// -fmad=false: together with the fixed operation order in fp64_math.cuh /
+// project.cuh it makes the cull decisions, tile rectangles and brick ranges
+// bit-identical to the reference restatement (oracle/splatct_oracle.cpp).
+//
+//   K1 raster_preprocess  — rasterizer.cpp:24-99 over every (view, kernel)
+//   K6 voxel_preprocess   — voxelizer.cpp:52-104 over every kernel
+//   project_export        — project_kernel (rasterizer.cpp:103-110)
+#include "project.cuh"
+#include "sct_internal.cuh"
+
+namespace sct {
+
+namespace {
+
+// One thread per (view, kernel) item; item = view * m + kernel (view-major, so
+// a stable sort on the (view, tile) key leaves each tile list ascending in
+// kernel index exactly like the reference's serial push_back, rasterizer.cpp:124-133).
+__global__ void __launch_bounds__(256) raster_preprocess_kernel(
+    long long m, long long n_items, double s_min, const float* __restrict__ rho_raw,
+    const float* __restrict__ pos, const float* __restrict__ scale_raw, const float* __restrict__ rot,
+    const ViewParams* __restrict__ views, DetParams det, RasterParams rp, float4* __restrict__ rec,
+    short4* __restrict__ rect, int32_t* __restrict__ count, uint8_t* __restrict__ vis) {
+  const double kA = -0.5 * kLog2e;
+  for (long long item = blockIdx.x * (long long)blockDim.x + threadIdx.x; item < n_items;
+       item += (long long)gridDim.x * blockDim.x) {
+    const long long v = item / m;
+    const long long i = item - v * m;
+    const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
+    const ViewParams view = views[v];
+    dProj g;
+    if (!d_project(k, view, det, rp, g)) {
+      count[item] = 0;
+      vis[item] = 0;
+      rect[item] = make_short4(1, 0, 1, 0);
+      continue;
+    }
+    int tx0, tx1, ty0, ty1;
+    d_tile_range(g, rp, det.tiles_x, det.tiles_y, tx0, tx1, ty0, ty1);
+    const int nx = tx1 - tx0 + 1, ny = ty1 - ty0 + 1;
+    const int c = (nx > 0 && ny > 0) ? nx * ny : 0;
+    count[item] = c;
+    vis[item] = 1;
+    rect[item] = make_short4((short)tx0, (short)tx1, (short)ty0, (short)ty1);
+    // exp(-1/2 d^T Q d) = exp2(A dx^2 + B dx dy + C dy^2)
+    rec[2 * item + 0] = make_float4((float)g.cx, (float)g.cy, (float)g.amp, 0.f);
+    rec[2 * item + 1] = make_float4((float)(kA * g.conic.m[0][0]), (float)(2.0 * kA * g.conic.m[0][1]),
+                                    (float)(kA * g.conic.m[1][1]), 0.f);
+  }
+}
+
+// voxelizer.cpp:52-88 bin_kernels (+ :96-104 precompute). Brick ranges are
+// restricted to the z-slab [zb0, zb1) for z-sharding; inside the slab the
+// lists equal the full-grid lists.
+__global__ void __launch_bounds__(256) voxel_preprocess_kernel(
+    long long m, double s_min, const float* __restrict__ rho_raw, const float* __restrict__ pos,
+    const float* __restrict__ scale_raw, const float* __restrict__ rot, int3 dims, double3 origin,
+    double3 spacing, double cull, int32_t zb0, int32_t zb1, float4* __restrict__ rec,
+    short4* __restrict__ lo_out, short4* __restrict__ hi_out, int32_t* __restrict__ count) {
+  const double kA = -0.5 * kLog2e;
+  const int dimv[3] = {dims.x, dims.y, dims.z};
+  const double org[3] = {origin.x, origin.y, origin.z};
+  const double sp[3] = {spacing.x, spacing.y, spacing.z};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
+    const dM3 sigma = d_covariance(k);
+    int lo[3], hi[3];
+    bool empty = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double r = cull * sqrt(fmax(sigma.m[a][a], 0.0));
+      const double fa = (k.p[a] - r - org[a]) / sp[a];
+      const double fb = (k.p[a] + r - org[a]) / sp[a];
+      int v0 = d_floor_int(fa);
+      int v1 = d_floor_int(fb);
+      v0 = max(v0, 0);
+      v1 = min(v1, dimv[a] - 1);
+      if (v0 > v1) empty = true;
+      lo[a] = v0 / kTileVox;
+      hi[a] = v1 / kTileVox;
+    }
+    if (!empty) {
+      lo[2] = max(lo[2], zb0);
+      hi[2] = min(hi[2], zb1 - 1);
+      if (lo[2] > hi[2]) empty = true;
+    }
+    count[i] = empty ? 0 : (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
+    lo_out[i] = make_short4((short)lo[0], (short)lo[1], (short)lo[2], 0);
+    hi_out[i] = make_short4((short)hi[0], (short)hi[1], (short)hi[2], 0);
+    // precompute(): Q = Sigma^-1, rho (log2-scaled for exp2; cross terms doubled)
+    const dM3 q = d_inv3(sigma);
+    const double rho = d_act_density(k.rho_raw);
+    rec[3 * i + 0] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], (float)rho);
+    rec[3 * i + 1] = make_float4((float)(kA * q.m[0][0]), (float)(kA * q.m[1][1]), (float)(kA * q.m[2][2]), 0.f);
+    rec[3 * i + 2] = make_float4((float)(2.0 * kA * q.m[0][1]), (float)(2.0 * kA * q.m[0][2]),
+                                 (float)(2.0 * kA * q.m[1][2]), 0.f);
+  }
+}
+
+__global__ void project_export_kernel(long long m, double s_min, const float* __restrict__ rho_raw,
+                                      const float* __restrict__ pos, const float* __restrict__ scale_raw,
+                                      const float* __restrict__ rot, const ViewParams* __restrict__ view,
+                                      DetParams det, RasterParams rp, int32_t* __restrict__ vis,
+                                      double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
+    dProj g;
+    const bool ok = d_project(k, view[0], det, rp, g);
+    vis[i] = ok ? 1 : 0;
+    double* o = out + 11 * i;
+    if (!ok) {
+      for (int a = 0; a < 11; ++a) o[a] = 0.0;
+      continue;
+    }
+    o[0] = g.cx;
+    o[1] = g.cy;
+    o[2] = g.cov.m[0][0];
+    o[3] = g.cov.m[0][1];
+    o[4] = g.cov.m[1][1];
+    o[5] = g.conic.m[0][0];
+    o[6] = g.conic.m[0][1];
+    o[7] = g.conic.m[1][1];
+    o[8] = g.amp;
+    o[9] = g.mu;
+    o[10] = g.depth;
+  }
+}
+
+int grid_for(Ctx* c, long long n, int block) {
+  long long b = (n + block - 1) / block;
+  const long long cap = (long long)c->sm_count * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+void launch_raster_preprocess(Ctx* c, const sct_cloud& cl, const ViewParams* d_views, int n_views,
+                              const DetParams& det, const RasterParams& rp, float4* rec, short4* rect,
+                              int32_t* count, uint8_t* vis) {
+  const long long n_items = (long long)cl.m * n_views;
+  if (n_items == 0) return;
+  raster_preprocess_kernel<<<grid_for(c, n_items, 256), 256, 0, c->stream>>>(
+      cl.m, n_items, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, d_views, det, rp, rec, rect, count,
+      vis);
+  c->launches++;
+}
+
+void launch_voxel_preprocess(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull, int32_t zb0,
+                             int32_t zb1, int32_t, int32_t, float4* rec, short4* rect_lo, short4* rect_hi,
+                             int32_t* count) {
+  if (cl.m == 0) return;
+  voxel_preprocess_kernel<<<grid_for(c, cl.m, 256), 256, 0, c->stream>>>(
+      cl.m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, make_int3(g.dims[0], g.dims[1], g.dims[2]),
+      make_double3(g.origin_mm[0], g.origin_mm[1], g.origin_mm[2]),
+      make_double3(g.spacing_mm[0], g.spacing_mm[1], g.spacing_mm[2]), cull, zb0, zb1, rec, rect_lo, rect_hi,
+      count);
+  c->launches++;
+}
+
+void launch_project_export(Ctx* c, const sct_cloud& cl, const ViewParams* d_view, const DetParams& det,
+                           const RasterParams& rp, int32_t* vis, double* rec) {
+  if (cl.m == 0) return;
+  project_export_kernel<<<grid_for(c, cl.m, 128), 128, 0, c->stream>>>(
+      cl.m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, d_view, det, rp, vis, rec);
+  c->launches++;
+}
+
+}  // namespace sct

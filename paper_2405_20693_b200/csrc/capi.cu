@@ -1,0 +1,722 @@
+// C ABI (include/splatct_gpu.h): contexts, forward state, binning pipeline
+// (scan -> emit -> stable radix sort -> ranges) and the host-buffer entry points.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sct_internal.cuh"
+
+namespace sct {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+DetParams make_det(const sct_scanner& s) {  // geometry.cpp:88-98
+  DetParams d;
+  d.w = s.det_res_px[0];
+  d.h = s.det_res_px[1];
+  d.fx = s.l_sd_mm * d.w / s.det_size_mm[0];
+  d.fy = s.l_sd_mm * d.h / s.det_size_mm[1];
+  d.cx = 0.5 * d.w;
+  d.cy = 0.5 * d.h;
+  d.near_clip = s.near_clip_mm > 0.0 ? s.near_clip_mm : 0.01 * s.l_so_mm;
+  d.tiles_x = (d.w + kTilePx - 1) / kTilePx;
+  d.tiles_y = (d.h + kTilePx - 1) / kTilePx;
+  return d;
+}
+
+ViewParams make_view(const sct_scanner& s, double theta) {  // geometry.cpp:76-86
+  const double sn = std::sin(theta), cs = std::cos(theta);
+  ViewParams v;
+  const double r[9] = {-sn, cs, 0.0, 0.0, 0.0, -1.0, -cs, -sn, 0.0};
+  for (int i = 0; i < 9; ++i) v.rot[i] = r[i];
+  v.t[0] = 0.0;
+  v.t[1] = 0.0;
+  v.t[2] = s.l_so_mm;
+  return v;
+}
+
+RasterParams make_raster(const sct_raster_opts& o) {
+  RasterParams r;
+  r.mode = o.mode;
+  r.dilation_compensation = o.dilation_compensation;
+  r.freeze_jacobian = o.freeze_jacobian;
+  r.eps2 = o.lowpass_eps_px * o.lowpass_eps_px;
+  r.cull = o.cull_mahalanobis;
+  return r;
+}
+
+int dev_alloc(Ctx* c, void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 16;
+  SCT_CUDA_TRY(cudaMallocAsync(p, bytes, c->stream));
+  return SCT_OK;
+}
+void dev_free(Ctx* c, void* p) {
+  if (p) cudaFreeAsync(p, c->stream);
+}
+int ensure_cub_tmp(Ctx* c, size_t bytes) {
+  if (bytes <= c->cub_tmp_bytes) return SCT_OK;
+  if (c->cub_tmp) cudaFreeAsync(c->cub_tmp, c->stream);
+  c->cub_tmp = nullptr;
+  const size_t b = bytes + bytes / 4 + 4096;
+  SCT_CUDA_TRY(cudaMallocAsync(&c->cub_tmp, b, c->stream));
+  c->cub_tmp_bytes = b;
+  return SCT_OK;
+}
+
+static int bits_for(uint64_t n) {  // smallest b with 2^b >= n (n >= 1)
+  int b = 0;
+  while ((1ull << b) < n) ++b;
+  return b;
+}
+
+// exclusive scan of count[0..n] (count[n] == 0) into offset[0..n]; returns offset[n]
+static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t* total) {
+  SCT_CUDA_TRY(cudaMemsetAsync(count + n, 0, sizeof(int32_t), c->stream));
+  size_t tmp = 0;
+  SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, offset, n + 1, c->stream));
+  SCT_TRY(ensure_cub_tmp(c, tmp));
+  tmp = c->cub_tmp_bytes;
+  SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, offset, n + 1, c->stream));
+  int32_t t = 0;
+  SCT_CUDA_TRY(cudaMemcpyAsync(c->pinned_count, offset + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  std::memcpy(&t, c->pinned_count, sizeof(int32_t));
+  if (t < 0) {
+    set_error("DataError: more than 2^31-1 (tile, kernel) pairs in one call; split the views into batches");
+    return SCT_ERR_DATA;
+  }
+  *total = t;
+  return SCT_OK;
+}
+
+// stable LSD radix sort of (key, value) pairs on key bits [0, end_bit)
+static int sort_pairs(Ctx* c, uint32_t*& keys, int32_t*& vals, int64_t n, int end_bit) {
+  if (n == 0) return SCT_OK;
+  uint32_t* k2 = nullptr;
+  int32_t* v2 = nullptr;
+  SCT_TRY(dev_alloc(c, (void**)&k2, n * sizeof(uint32_t)));
+  SCT_TRY(dev_alloc(c, (void**)&v2, n * sizeof(int32_t)));
+  size_t tmp = 0;
+  SCT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, k2, vals, v2, (int)n, 0, end_bit, c->stream));
+  SCT_TRY(ensure_cub_tmp(c, tmp));
+  tmp = c->cub_tmp_bytes;
+  SCT_CUDA_TRY(
+      cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, k2, vals, v2, (int)n, 0, end_bit, c->stream));
+  dev_free(c, keys);
+  dev_free(c, vals);
+  keys = k2;
+  vals = v2;
+  return SCT_OK;
+}
+
+static int check_cloud(const sct_cloud* cl) {
+  if (!cl || cl->m < 0) {
+    set_error("ConfigError: null or negative-size cloud");
+    return SCT_ERR_CONFIG;
+  }
+  if (cl->m > 0 && (!cl->rho_raw || !cl->pos || !cl->scale_raw || !cl->rot)) {
+    set_error("ConfigError: cloud has null parameter arrays");
+    return SCT_ERR_CONFIG;
+  }
+  if (cl->m > (int64_t)INT32_MAX) {
+    set_error("ConfigError: more than 2^31-1 kernels");
+    return SCT_ERR_CONFIG;
+  }
+  return SCT_OK;
+}
+
+static int check_scanner(const sct_scanner* s) {
+  if (!s || s->det_res_px[0] <= 0 || s->det_res_px[1] <= 0 || !(s->det_size_mm[0] > 0.0) ||
+      !(s->det_size_mm[1] > 0.0) || !(s->l_so_mm > 0.0) || !(s->l_sd_mm > s->l_so_mm)) {
+    set_error("ConfigError: scanner: invalid detector resolution/size or distances (geometry.cpp:26-34)");
+    return SCT_ERR_CONFIG;
+  }
+  if (s->det_res_px[0] > 32767 * kTilePx || s->det_res_px[1] > 32767 * kTilePx) {
+    set_error("ConfigError: detector too large");
+    return SCT_ERR_CONFIG;
+  }
+  return SCT_OK;
+}
+
+static int check_grid(const sct_grid* g) {
+  if (!g || g->dims[0] <= 0 || g->dims[1] <= 0 || g->dims[2] <= 0 || !(g->spacing_mm[0] > 0.0) ||
+      !(g->spacing_mm[1] > 0.0) || !(g->spacing_mm[2] > 0.0)) {
+    set_error("ConfigError: grid dims and spacing must be positive");
+    return SCT_ERR_CONFIG;
+  }
+  const uint64_t nb = (uint64_t)((g->dims[0] + 7) / 8) * ((g->dims[1] + 7) / 8) * ((g->dims[2] + 7) / 8);
+  if (nb >= (1ull << 31)) {
+    set_error("ConfigError: grid too large");
+    return SCT_ERR_CONFIG;
+  }
+  return SCT_OK;
+}
+
+// ------------------------------------------------------------------ voxel binning
+struct VoxelBins {
+  int32_t bx = 0, by = 0, bz = 0, zb0 = 0, zb1 = 0;
+  int64_t n_pairs = 0;
+  float4* rec = nullptr;
+  short4* lo = nullptr;
+  short4* hi = nullptr;
+  int32_t* count = nullptr;
+  int32_t* offset = nullptr;
+  uint32_t* keys = nullptr;
+  int32_t* vals = nullptr;
+  int2* ranges = nullptr;
+  void release(Ctx* c) {
+    dev_free(c, rec);
+    dev_free(c, lo);
+    dev_free(c, hi);
+    dev_free(c, count);
+    dev_free(c, offset);
+    dev_free(c, keys);
+    dev_free(c, vals);
+    dev_free(c, ranges);
+    rec = nullptr;
+    lo = hi = nullptr;
+    count = offset = nullptr;
+    keys = nullptr;
+    vals = nullptr;
+    ranges = nullptr;
+  }
+};
+
+static int voxel_bin(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull, int32_t zb0, int32_t zb1,
+                     VoxelBins& b) {
+  b.bx = (g.dims[0] + kTileVox - 1) / kTileVox;
+  b.by = (g.dims[1] + kTileVox - 1) / kTileVox;
+  b.bz = (g.dims[2] + kTileVox - 1) / kTileVox;
+  b.zb0 = zb0 < 0 ? 0 : (zb0 > b.bz ? b.bz : zb0);
+  b.zb1 = zb1 > b.bz ? b.bz : (zb1 < b.zb0 ? b.zb0 : zb1);
+  const int64_t m = cl.m;
+  const int64_t nbr = (int64_t)b.bx * b.by * b.bz;
+  SCT_TRY(dev_alloc(c, (void**)&b.rec, 3 * m * sizeof(float4)));
+  SCT_TRY(dev_alloc(c, (void**)&b.lo, m * sizeof(short4)));
+  SCT_TRY(dev_alloc(c, (void**)&b.hi, m * sizeof(short4)));
+  SCT_TRY(dev_alloc(c, (void**)&b.count, (m + 1) * sizeof(int32_t)));
+  SCT_TRY(dev_alloc(c, (void**)&b.offset, (m + 1) * sizeof(int32_t)));
+  SCT_TRY(dev_alloc(c, (void**)&b.ranges, nbr * sizeof(int2)));
+  SCT_CUDA_TRY(cudaMemsetAsync(b.ranges, 0, nbr * sizeof(int2), c->stream));
+  launch_voxel_preprocess(c, cl, g, cull, b.zb0, b.zb1, b.bx, b.by, b.rec, b.lo, b.hi, b.count);
+  SCT_TRY(scan_counts(c, b.count, b.offset, m, &b.n_pairs));
+  SCT_TRY(dev_alloc(c, (void**)&b.keys, b.n_pairs * sizeof(uint32_t)));
+  SCT_TRY(dev_alloc(c, (void**)&b.vals, b.n_pairs * sizeof(int32_t)));
+  launch_voxel_emit(c, m, b.lo, b.hi, b.offset, b.bx, b.by, b.keys, b.vals);
+  SCT_TRY(sort_pairs(c, b.keys, b.vals, b.n_pairs, bits_for((uint64_t)nbr)));
+  launch_ranges(c, b.n_pairs, b.keys, 31, nbr, b.ranges);
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
+
+}  // namespace sct
+
+using namespace sct;
+
+static void free_state_buffers(sct_fwd* s) {
+  Ctx* c = s->ctx;
+  dev_free(c, s->d_views);
+  dev_free(c, s->d_rec);
+  dev_free(c, s->d_rect);
+  dev_free(c, s->d_count);
+  dev_free(c, s->d_offset);
+  dev_free(c, s->d_vis);
+  dev_free(c, s->d_keys);
+  dev_free(c, s->d_vals);
+  dev_free(c, s->d_ranges);
+}
+
+extern "C" {
+
+const char* sct_last_error(void) { return g_last_error.c_str(); }
+const char* sct_version(void) { return "splatct-b200 0.1 (sm_100a)"; }
+
+int sct_ctx_create(int device, void* stream, sct_ctx** out) {
+  if (!out) return SCT_ERR_CONFIG;
+  *out = nullptr;
+  SCT_CUDA_TRY(cudaSetDevice(device));
+  auto* c = new sct_ctx();
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
+    c->sm_count = sms;
+  // keep freed blocks in the stream-ordered pool: steady-state calls do not
+  // return memory to the driver
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (cudaMallocHost((void**)&c->pinned_count, 64) != cudaSuccess) {
+    delete c;
+    set_error("CUDA error: cudaMallocHost failed");
+    return SCT_ERR_CUDA;
+  }
+  *out = c;
+  return SCT_OK;
+}
+
+int sct_ctx_destroy(sct_ctx* c) {
+  if (!c) return SCT_OK;
+  cudaStreamSynchronize(c->stream);
+  if (c->cub_tmp) cudaFree(c->cub_tmp);
+  if (c->pinned_count) cudaFreeHost(c->pinned_count);
+  delete c;
+  return SCT_OK;
+}
+
+int sct_ctx_set_stream(sct_ctx* c, void* stream) {
+  if (!c) return SCT_ERR_CONFIG;
+  c->stream = (cudaStream_t)stream;
+  return SCT_OK;
+}
+
+int sct_ctx_sync(sct_ctx* c) {
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
+
+int sct_ctx_set_deterministic(sct_ctx* c, int d) {
+  c->deterministic = d != 0;
+  return SCT_OK;
+}
+
+int64_t sct_ctx_kernel_launches(const sct_ctx* c) { return c ? c->launches : 0; }
+
+double sct_lr_at(double lr_init, double final_ratio, int32_t t, int32_t iters) {  // trainer.cpp:34-36
+  return lr_init * std::pow(final_ratio, static_cast<double>(t) / iters);
+}
+
+// ------------------------------------------------------------------ rasterizer
+int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanner, const double* thetas,
+                   int32_t n_views, const sct_raster_opts* opts, float* images, sct_fwd** state) {
+  if (!c || !state || !opts) {
+    set_error("ConfigError: null argument");
+    return SCT_ERR_CONFIG;
+  }
+  *state = nullptr;
+  SCT_TRY(check_cloud(cloud));
+  SCT_TRY(check_scanner(scanner));
+  if (n_views < 1 || n_views > 65535 || !thetas) {
+    set_error("ConfigError: need 1..65535 views");
+    return SCT_ERR_CONFIG;
+  }
+  for (int v = 0; v < n_views; ++v)
+    if (!std::isfinite(thetas[v])) {
+      set_error("ConfigError: scanner: non-finite view angle");
+      return SCT_ERR_CONFIG;
+    }
+  auto* s = new sct_fwd();
+  s->ctx = c;
+  s->n_views = n_views;
+  s->m = cloud->m;
+  s->det = make_det(*scanner);
+  s->rp = make_raster(*opts);
+  s->opts = *opts;
+  s->scanner = *scanner;
+  s->s_min = cloud->s_min_mm;
+  s->thetas.assign(thetas, thetas + n_views);
+  const int64_t T = (int64_t)s->det.tiles_x * s->det.tiles_y;
+  s->tile_bits = bits_for((uint64_t)T);
+  if (s->tile_bits + bits_for((uint64_t)n_views) > 32) {
+    delete s;
+    set_error("ConfigError: (view, tile) key exceeds 32 bits; split the views into batches");
+    return SCT_ERR_CONFIG;
+  }
+  s->n_items = s->m * n_views;
+  int rc = SCT_OK;
+  auto fail = [&](int r) {
+    free_state_buffers(s);
+    delete s;
+    return r;
+  };
+  std::vector<ViewParams> hv(n_views);
+  for (int v = 0; v < n_views; ++v) hv[v] = make_view(*scanner, thetas[v]);
+  if ((rc = dev_alloc(c, (void**)&s->d_views, n_views * sizeof(ViewParams)))) return fail(rc);
+  if (cudaMemcpyAsync(s->d_views, hv.data(), n_views * sizeof(ViewParams), cudaMemcpyHostToDevice, c->stream) !=
+      cudaSuccess) {
+    set_error("CUDA error: view upload");
+    return fail(SCT_ERR_CUDA);
+  }
+  const int64_t ni = s->n_items;
+  if ((rc = dev_alloc(c, (void**)&s->d_rec, 2 * ni * sizeof(float4)))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&s->d_rect, ni * sizeof(short4)))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&s->d_count, (ni + 1) * sizeof(int32_t)))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&s->d_offset, (ni + 1) * sizeof(int32_t)))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&s->d_vis, ni + 1))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&s->d_ranges, n_views * T * sizeof(int2)))) return fail(rc);
+  if (cudaMemsetAsync(s->d_ranges, 0, n_views * T * sizeof(int2), c->stream) != cudaSuccess) {
+    set_error("CUDA error: memset");
+    return fail(SCT_ERR_CUDA);
+  }
+  launch_raster_preprocess(c, *cloud, s->d_views, n_views, s->det, s->rp, s->d_rec, s->d_rect, s->d_count,
+                           s->d_vis);
+  if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&s->d_keys, s->n_pairs * sizeof(uint32_t)))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&s->d_vals, s->n_pairs * sizeof(int32_t)))) return fail(rc);
+  launch_raster_emit(c, ni, s->m, s->d_rect, s->d_offset, s->det.tiles_x, s->tile_bits, s->d_keys, s->d_vals);
+  if ((rc = sort_pairs(c, s->d_keys, s->d_vals, s->n_pairs, s->tile_bits + bits_for((uint64_t)n_views))))
+    return fail(rc);
+  launch_ranges(c, s->n_pairs, s->d_keys, s->tile_bits, T, s->d_ranges);
+  if (images) launch_raster_composite(c, s, images);
+  if (cudaGetLastError() != cudaSuccess) {
+    set_error("CUDA error: kernel launch in sct_render_fwd");
+    return fail(SCT_ERR_CUDA);
+  }
+  *state = s;
+  return SCT_OK;
+}
+
+int sct_render_bwd(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
+                   sct_stats* stats) {
+  if (!c || !s || !grads || !dL) {
+    set_error("ConfigError: null argument");
+    return SCT_ERR_CONFIG;
+  }
+  SCT_TRY(check_cloud(cloud));
+  if (cloud->m != s->m) {
+    set_error("DimMismatch: render_backward: cloud size differs from the forward state");
+    return SCT_ERR_DATA;
+  }
+  if (s->n_items == 0) return SCT_OK;
+  float4* pair_stats = nullptr;
+  float* item_grads = nullptr;
+  SCT_TRY(dev_alloc(c, (void**)&pair_stats, 2 * s->n_pairs * sizeof(float4)));
+  SCT_TRY(dev_alloc(c, (void**)&item_grads, 11 * s->n_items * sizeof(float)));
+  launch_raster_backward_stats(c, s, dL, pair_stats);
+  launch_raster_chain(c, s, *cloud, pair_stats, item_grads);
+  launch_raster_finalize(c, s, *cloud, item_grads, grads, stats);
+  dev_free(c, pair_stats);
+  dev_free(c, item_grads);
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
+
+int sct_fwd_free(sct_fwd* s) {
+  if (!s) return SCT_OK;
+  free_state_buffers(s);
+  delete s;
+  return SCT_OK;
+}
+
+int sct_fwd_info(sct_fwd* s, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y, int64_t* n_visible) {
+  if (!s) return SCT_ERR_CONFIG;
+  if (n_pairs) *n_pairs = s->n_pairs;
+  if (tiles_x) *tiles_x = s->det.tiles_x;
+  if (tiles_y) *tiles_y = s->det.tiles_y;
+  if (n_visible) {
+    std::vector<uint8_t> v(s->n_items);
+    SCT_CUDA_TRY(cudaMemcpyAsync(v.data(), s->d_vis, s->n_items, cudaMemcpyDeviceToHost, s->ctx->stream));
+    SCT_CUDA_TRY(cudaStreamSynchronize(s->ctx->stream));
+    int64_t n = 0;
+    for (uint8_t x : v) n += x;
+    *n_visible = n;
+  }
+  return SCT_OK;
+}
+
+int sct_fwd_tile_lists(sct_fwd* s, int32_t view, int64_t* offsets, int32_t* kernel_idx) {
+  if (!s || view < 0 || view >= s->n_views || !offsets) {
+    set_error("ConfigError: bad view");
+    return SCT_ERR_CONFIG;
+  }
+  Ctx* c = s->ctx;
+  const int64_t T = (int64_t)s->det.tiles_x * s->det.tiles_y;
+  std::vector<int2> r(T);
+  SCT_CUDA_TRY(cudaMemcpyAsync(r.data(), s->d_ranges + view * T, T * sizeof(int2), cudaMemcpyDeviceToHost,
+                               c->stream));
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  int64_t lo = -1, hi = -1;
+  for (int64_t t = 0; t < T; ++t)
+    if (r[t].y > r[t].x) {
+      if (lo < 0) lo = r[t].x;
+      hi = r[t].y;
+    }
+  int64_t o = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    offsets[t] = o;
+    o += r[t].y > r[t].x ? r[t].y - r[t].x : 0;
+  }
+  offsets[T] = o;
+  if (kernel_idx && lo >= 0) {
+    std::vector<int32_t> v(hi - lo);
+    SCT_CUDA_TRY(cudaMemcpyAsync(v.data(), s->d_vals + lo, (hi - lo) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                 c->stream));
+    SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const int64_t base = (int64_t)view * s->m;
+    for (int64_t k = 0; k < hi - lo; ++k) kernel_idx[k] = (int32_t)(v[k] - base);
+  }
+  return SCT_OK;
+}
+
+int sct_project_kernels(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanner, double theta,
+                        const sct_raster_opts* opts, int32_t* visible, double* rec) {
+  SCT_TRY(check_cloud(cloud));
+  SCT_TRY(check_scanner(scanner));
+  const int64_t m = cloud->m;
+  if (m == 0) return SCT_OK;
+  ViewParams hv = make_view(*scanner, theta);
+  ViewParams* dv = nullptr;
+  int32_t* dvis = nullptr;
+  double* drec = nullptr;
+  SCT_TRY(dev_alloc(c, (void**)&dv, sizeof(ViewParams)));
+  SCT_TRY(dev_alloc(c, (void**)&dvis, m * sizeof(int32_t)));
+  SCT_TRY(dev_alloc(c, (void**)&drec, 11 * m * sizeof(double)));
+  SCT_CUDA_TRY(cudaMemcpyAsync(dv, &hv, sizeof(hv), cudaMemcpyHostToDevice, c->stream));
+  launch_project_export(c, *cloud, dv, make_det(*scanner), make_raster(*opts), dvis, drec);
+  SCT_CUDA_TRY(cudaMemcpyAsync(visible, dvis, m * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  SCT_CUDA_TRY(cudaMemcpyAsync(rec, drec, 11 * m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  dev_free(c, dv);
+  dev_free(c, dvis);
+  dev_free(c, drec);
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return SCT_OK;
+}
+
+// ---- host-buffer variants ----------------------------------------------------
+static int upload_cloud(Ctx* c, const sct_cloud* h, sct_cloud* d) {
+  *d = *h;
+  const int64_t m = h->m;
+  float** dst[4] = {&d->rho_raw, &d->pos, &d->scale_raw, &d->rot};
+  float* src[4] = {h->rho_raw, h->pos, h->scale_raw, h->rot};
+  const int64_t n[4] = {m, 3 * m, 3 * m, 4 * m};
+  for (int a = 0; a < 4; ++a) {
+    SCT_TRY(dev_alloc(c, (void**)dst[a], n[a] * sizeof(float)));
+    SCT_CUDA_TRY(cudaMemcpyAsync(*dst[a], src[a], n[a] * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  }
+  return SCT_OK;
+}
+static void free_cloud(Ctx* c, sct_cloud* d) {
+  dev_free(c, d->rho_raw);
+  dev_free(c, d->pos);
+  dev_free(c, d->scale_raw);
+  dev_free(c, d->rot);
+}
+
+int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scanner* scanner, const double* thetas,
+                        int32_t n_views, const sct_raster_opts* opts, float* images_host, sct_fwd** state) {
+  SCT_TRY(check_cloud(cloud_host));
+  SCT_TRY(check_scanner(scanner));
+  sct_cloud d;
+  SCT_TRY(upload_cloud(c, cloud_host, &d));
+  const size_t img = (size_t)n_views * scanner->det_res_px[0] * scanner->det_res_px[1];
+  float* dimg = nullptr;
+  SCT_TRY(dev_alloc(c, (void**)&dimg, img * sizeof(float)));
+  int rc = sct_render_fwd(c, &d, scanner, thetas, n_views, opts, dimg, state);
+  if (rc == SCT_OK && images_host)
+    if (cudaMemcpyAsync(images_host, dimg, img * sizeof(float), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) {
+      set_error("CUDA error: image download");
+      rc = SCT_ERR_CUDA;
+    }
+  dev_free(c, dimg);
+  free_cloud(c, &d);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess && rc == SCT_OK) {
+    set_error("CUDA error in sct_render_fwd_host");
+    rc = SCT_ERR_CUDA;
+  }
+  return rc;
+}
+
+int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, const float* dL_host,
+                        sct_grads* grads_host, sct_stats* stats_host) {
+  if (!s || !grads_host) return SCT_ERR_CONFIG;
+  SCT_TRY(check_cloud(cloud_host));
+  sct_cloud d;
+  SCT_TRY(upload_cloud(c, cloud_host, &d));
+  const int64_t m = cloud_host->m;
+  const size_t img = (size_t)s->n_views * s->det.w * s->det.h;
+  float* ddl = nullptr;
+  SCT_TRY(dev_alloc(c, (void**)&ddl, img * sizeof(float)));
+  SCT_CUDA_TRY(cudaMemcpyAsync(ddl, dL_host, img * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  // accumulate semantics: bring the caller's running sums to the device
+  sct_grads dg;
+  float** gd[4] = {&dg.rho_raw, &dg.pos, &dg.scale_raw, &dg.rot};
+  float* gh[4] = {grads_host->rho_raw, grads_host->pos, grads_host->scale_raw, grads_host->rot};
+  const int64_t n[4] = {m, 3 * m, 3 * m, 4 * m};
+  for (int a = 0; a < 4; ++a) {
+    SCT_TRY(dev_alloc(c, (void**)gd[a], n[a] * sizeof(float)));
+    SCT_CUDA_TRY(cudaMemcpyAsync(*gd[a], gh[a], n[a] * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  }
+  sct_stats dst{};
+  if (stats_host) {
+    SCT_TRY(dev_alloc(c, (void**)&dst.grad2d_norm_accum, m * sizeof(float)));
+    SCT_TRY(dev_alloc(c, (void**)&dst.grad_count, m * sizeof(int32_t)));
+    SCT_TRY(dev_alloc(c, (void**)&dst.grad3d_accum, 3 * m * sizeof(float)));
+    SCT_CUDA_TRY(cudaMemcpyAsync(dst.grad2d_norm_accum, stats_host->grad2d_norm_accum, m * sizeof(float),
+                                 cudaMemcpyHostToDevice, c->stream));
+    SCT_CUDA_TRY(cudaMemcpyAsync(dst.grad_count, stats_host->grad_count, m * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, c->stream));
+    SCT_CUDA_TRY(cudaMemcpyAsync(dst.grad3d_accum, stats_host->grad3d_accum, 3 * m * sizeof(float),
+                                 cudaMemcpyHostToDevice, c->stream));
+  }
+  int rc = sct_render_bwd(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr);
+  if (rc == SCT_OK) {
+    for (int a = 0; a < 4; ++a)
+      SCT_CUDA_TRY(cudaMemcpyAsync(gh[a], *gd[a], n[a] * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    if (stats_host) {
+      SCT_CUDA_TRY(cudaMemcpyAsync(stats_host->grad2d_norm_accum, dst.grad2d_norm_accum, m * sizeof(float),
+                                   cudaMemcpyDeviceToHost, c->stream));
+      SCT_CUDA_TRY(cudaMemcpyAsync(stats_host->grad_count, dst.grad_count, m * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost, c->stream));
+      SCT_CUDA_TRY(cudaMemcpyAsync(stats_host->grad3d_accum, dst.grad3d_accum, 3 * m * sizeof(float),
+                                   cudaMemcpyDeviceToHost, c->stream));
+    }
+  }
+  for (int a = 0; a < 4; ++a) dev_free(c, *gd[a]);
+  if (stats_host) {
+    dev_free(c, dst.grad2d_norm_accum);
+    dev_free(c, dst.grad_count);
+    dev_free(c, dst.grad3d_accum);
+  }
+  dev_free(c, ddl);
+  free_cloud(c, &d);
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return rc;
+}
+
+// ------------------------------------------------------------------ voxelizer
+int sct_voxelize_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_grid* grid, double cull, int32_t zb0, int32_t zb1,
+                     float* vol) {
+  SCT_TRY(check_cloud(cloud));
+  SCT_TRY(check_grid(grid));
+  VoxelBins b;
+  int rc = voxel_bin(c, *cloud, *grid, cull, zb0, zb1, b);
+  if (rc == SCT_OK) launch_voxel_eval(c, *grid, b.zb0, b.zb1, b.bx, b.by, b.ranges, b.vals, b.rec, *cloud, vol);
+  b.release(c);
+  if (rc == SCT_OK && cudaGetLastError() != cudaSuccess) {
+    set_error("CUDA error: kernel launch in sct_voxelize_fwd");
+    rc = SCT_ERR_CUDA;
+  }
+  return rc;
+}
+
+int sct_voxelize_bwd(sct_ctx* c, const sct_cloud* cloud, const sct_grid* grid, double cull, int32_t zb0, int32_t zb1,
+                     const float* dL, sct_grads* grads) {
+  SCT_TRY(check_cloud(cloud));
+  SCT_TRY(check_grid(grid));
+  if (!grads || !dL) {
+    set_error("ConfigError: null argument");
+    return SCT_ERR_CONFIG;
+  }
+  VoxelBins b;
+  int rc = voxel_bin(c, *cloud, *grid, cull, zb0, zb1, b);
+  float4* ps = nullptr;
+  if (rc == SCT_OK) rc = dev_alloc(c, (void**)&ps, 3 * b.n_pairs * sizeof(float4));
+  if (rc == SCT_OK) {
+    launch_voxel_backward_stats(c, *grid, b.zb0, b.zb1, b.bx, b.by, b.ranges, b.vals, b.rec, b.lo, b.hi, b.offset,
+                                *cloud, dL, ps);
+    launch_voxel_chain(c, *cloud, b.offset, b.count, ps, grads);
+  }
+  dev_free(c, ps);
+  b.release(c);
+  if (rc == SCT_OK && cudaGetLastError() != cudaSuccess) {
+    set_error("CUDA error: kernel launch in sct_voxelize_bwd");
+    rc = SCT_ERR_CUDA;
+  }
+  return rc;
+}
+
+int sct_voxel_bins(sct_ctx* c, const sct_cloud* cloud, const sct_grid* grid, double cull, int64_t* n_pairs,
+                   int64_t* offsets, int32_t* kernel_idx) {
+  SCT_TRY(check_cloud(cloud));
+  SCT_TRY(check_grid(grid));
+  VoxelBins b;
+  int rc = voxel_bin(c, *cloud, *grid, cull, 0, INT32_MAX, b);
+  if (rc == SCT_OK) {
+    const int64_t nbr = (int64_t)b.bx * b.by * b.bz;
+    if (n_pairs) *n_pairs = b.n_pairs;
+    if (offsets) {
+      std::vector<int2> r(nbr);
+      cudaMemcpyAsync(r.data(), b.ranges, nbr * sizeof(int2), cudaMemcpyDeviceToHost, c->stream);
+      cudaStreamSynchronize(c->stream);
+      int64_t o = 0;
+      for (int64_t t = 0; t < nbr; ++t) {
+        offsets[t] = o;
+        o += r[t].y > r[t].x ? r[t].y - r[t].x : 0;
+      }
+      offsets[nbr] = o;
+    }
+    if (kernel_idx && b.n_pairs > 0) {
+      cudaMemcpyAsync(kernel_idx, b.vals, b.n_pairs * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream);
+      cudaStreamSynchronize(c->stream);
+    }
+  }
+  b.release(c);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess && rc == SCT_OK) {
+    set_error("CUDA error in sct_voxel_bins");
+    rc = SCT_ERR_CUDA;
+  }
+  return rc;
+}
+
+int sct_voxelize_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_grid* grid, double cull,
+                          float* vol_host) {
+  SCT_TRY(check_cloud(cloud_host));
+  SCT_TRY(check_grid(grid));
+  sct_cloud d;
+  SCT_TRY(upload_cloud(c, cloud_host, &d));
+  const size_t nv = (size_t)grid->dims[0] * grid->dims[1] * grid->dims[2];
+  float* dv = nullptr;
+  SCT_TRY(dev_alloc(c, (void**)&dv, nv * sizeof(float)));
+  int rc = sct_voxelize_fwd(c, &d, grid, cull, 0, INT32_MAX, dv);
+  if (rc == SCT_OK)
+    if (cudaMemcpyAsync(vol_host, dv, nv * sizeof(float), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) {
+      set_error("CUDA error: volume download");
+      rc = SCT_ERR_CUDA;
+    }
+  dev_free(c, dv);
+  free_cloud(c, &d);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess && rc == SCT_OK) rc = SCT_ERR_CUDA;
+  return rc;
+}
+
+// ------------------------------------------------------------------ objectives / optimizer
+int sct_tv3d(sct_ctx* c, const float* vol, const int32_t dims[3], float lambda, double* value, float* grad) {
+  if (!dims || dims[0] < 2 || dims[1] < 2 || dims[2] < 2) {
+    set_error("DimMismatch: tv3d_loss: need at least 2 voxels per axis");
+    return SCT_ERR_DATA;
+  }
+  const long long n = (long long)dims[0] * dims[1] * dims[2];
+  int nb = (int)((n + 255) / 256);
+  if (nb > c->sm_count * 8) nb = c->sm_count * 8;
+  double* partials = nullptr;
+  SCT_TRY(dev_alloc(c, (void**)&partials, 3 * nb * sizeof(double)));
+  launch_tv3d(c, vol, dims, lambda, value, grad, partials, nb);
+  dev_free(c, partials);
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
+
+int sct_photometric_loss(sct_ctx* c, const float* rendered, const float* measured, int32_t n, int32_t w, int32_t h,
+                         float render_scale, float lambda_ssim, float grad_scale, double* values, float* dL) {
+  SCT_TRY(photometric_loss(c, rendered, measured, n, w, h, render_scale, lambda_ssim, grad_scale, values, dL));
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
+
+int sct_adam_step(sct_ctx* c, sct_cloud* p, sct_adam_state* st, const sct_grads* g, int32_t t, const double lr[4],
+                  double beta1, double beta2, double eps) {
+  if (!p || !st || !g || t < 1) {
+    set_error("ConfigError: adam: null argument or step < 1");
+    return SCT_ERR_CONFIG;
+  }
+  const double bc1 = 1.0 - std::pow(beta1, t);  // trainer.cpp:152-153
+  const double bc2 = 1.0 - std::pow(beta2, t);
+  const float lrf[4] = {(float)lr[0], (float)lr[1], (float)lr[2], (float)lr[3]};
+  launch_adam(c, p, st, g, lrf, (float)bc1, (float)bc2, (float)beta1, (float)beta2, (float)eps);
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
+
+}  // extern "C"

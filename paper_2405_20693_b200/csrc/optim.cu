@@ -1,0 +1,338 @@
+// Regulariser, photometric losses and optimizer (HBM-bound kernels).
+//
+//   K9  tv3d           — objectives.cpp:169-202 (value: deterministic two-pass
+//                        block reduction; gradient in gather form, no atomics)
+//   K10 adam           — trainer.cpp:144-163 for all four groups in one pass,
+//                        then gaussian_cloud.cpp:112-117 quaternion renorm
+//   K11 photometric    — objectives.cpp:11-167 L1 + D-SSIM (valid 11x11
+//                        separable window) and the dL/dI assembly of
+//                        trainer.cpp:277-287
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "sct_internal.cuh"
+
+namespace sct {
+
+namespace {
+
+// ---------------------------------------------------------------- TV
+__device__ __forceinline__ float sgnf(float d) { return d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f); }
+
+__global__ void __launch_bounds__(256) tv3d_kernel(const float* __restrict__ vol, int nx, int ny, int nz,
+                                                   float inv_x, float inv_y, float inv_z, float lambda,
+                                                   float* __restrict__ grad, double* __restrict__ partials) {
+  const long long n = (long long)nx * ny * nz;
+  double sx = 0.0, sy = 0.0, sz = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % nx);
+    const int y = (int)((i / nx) % ny);
+    const int z = (int)(i / ((long long)nx * ny));
+    const float c = vol[i];
+    float g = 0.f;
+    // reference accumulation order per voxel: x-, x+, y-, y+, z-, z+
+    if (x > 0) g += sgnf(c - vol[i - 1]) * inv_x;
+    if (x < nx - 1) {
+      const float d = vol[i + 1] - c;
+      g -= sgnf(d) * inv_x;
+      sx += fabs((double)d);
+    }
+    if (y > 0) g += sgnf(c - vol[i - nx]) * inv_y;
+    if (y < ny - 1) {
+      const float d = vol[i + nx] - c;
+      g -= sgnf(d) * inv_y;
+      sy += fabs((double)d);
+    }
+    if (z > 0) g += sgnf(c - vol[i - (long long)nx * ny]) * inv_z;
+    if (z < nz - 1) {
+      const float d = vol[i + (long long)nx * ny] - c;
+      g -= sgnf(d) * inv_z;
+      sz += fabs((double)d);
+    }
+    grad[i] = g * lambda;
+  }
+  // block reduction (fixed order) of the three axis sums
+  __shared__ double red[3][256];
+  red[0][threadIdx.x] = sx;
+  red[1][threadIdx.x] = sy;
+  red[2][threadIdx.x] = sz;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s)
+      for (int a = 0; a < 3; ++a) red[a][threadIdx.x] += red[a][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int a = 0; a < 3; ++a) partials[3 * blockIdx.x + a] = red[a][0];
+}
+
+__global__ void tv3d_finish_kernel(const double* __restrict__ partials, int n_blocks, double inv_x, double inv_y,
+                                   double inv_z, double* __restrict__ value) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s[3] = {0, 0, 0};
+  for (int b = 0; b < n_blocks; ++b)
+    for (int a = 0; a < 3; ++a) s[a] += partials[3 * b + a];
+  *value = s[0] * inv_x + s[1] * inv_y + s[2] * inv_z;
+}
+
+// ---------------------------------------------------------------- Adam
+__device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, float lr, float bc1, float bc2,
+                                      float b1, float b2, float eps) {
+  m = b1 * m + (1.f - b1) * g;
+  v = b2 * v + (1.f - b2) * g * g;
+  const float mhat = m / bc1;
+  const float vhat = v / bc2;
+  p -= lr * mhat / (sqrtf(vhat) + eps);
+}
+
+// One thread per kernel: rho (1), pos (3), scale (3), rot (4) + renormalisation.
+__global__ void __launch_bounds__(256) adam_kernel(long long m, float* __restrict__ rho, float* __restrict__ pos,
+                                                   float* __restrict__ sc, float* __restrict__ rot,
+                                                   sct_adam_state st, const float* __restrict__ g_rho,
+                                                   const float* __restrict__ g_pos, const float* __restrict__ g_sc,
+                                                   const float* __restrict__ g_rot, float lr_pos, float lr_rho,
+                                                   float lr_sc, float lr_rot, float bc1, float bc2, float b1,
+                                                   float b2, float eps) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const long long j = 3 * i + a;
+      float p = pos[j], mm = st.m_pos[j], vv = st.v_pos[j];
+      adam1(p, mm, vv, g_pos[j], lr_pos, bc1, bc2, b1, b2, eps);
+      pos[j] = p; st.m_pos[j] = mm; st.v_pos[j] = vv;
+    }
+    {
+      float p = rho[i], mm = st.m_rho[i], vv = st.v_rho[i];
+      adam1(p, mm, vv, g_rho[i], lr_rho, bc1, bc2, b1, b2, eps);
+      rho[i] = p; st.m_rho[i] = mm; st.v_rho[i] = vv;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const long long j = 3 * i + a;
+      float p = sc[j], mm = st.m_scale[j], vv = st.v_scale[j];
+      adam1(p, mm, vv, g_sc[j], lr_sc, bc1, bc2, b1, b2, eps);
+      sc[j] = p; st.m_scale[j] = mm; st.v_scale[j] = vv;
+    }
+    float q[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const long long j = 4 * i + a;
+      float p = rot[j], mm = st.m_rot[j], vv = st.v_rot[j];
+      adam1(p, mm, vv, g_rot[j], lr_rot, bc1, bc2, b1, b2, eps);
+      q[a] = p; st.m_rot[j] = mm; st.v_rot[j] = vv;
+    }
+    const float n = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) rot[4 * i + a] = q[a] / n;
+  }
+}
+
+// ---------------------------------------------------------------- photometric
+constexpr int kWin = 11;
+struct Taps {
+  float w[kWin];
+};
+
+// horizontal valid pass of the five SSIM moments: tmp[img][5][H][Wv]
+__global__ void ssim_h_kernel(const float* __restrict__ r, const float* __restrict__ mm, int n, int W, int H,
+                              float rscale, Taps taps, float* __restrict__ tmp) {
+  const int Wv = W - kWin + 1;
+  const long long total = (long long)n * H * Wv;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(t % Wv);
+    const int y = (int)((t / Wv) % H);
+    const long long img = t / ((long long)Wv * H);
+    const float* ra = r + (img * H + y) * W + x;
+    const float* rb = mm + (img * H + y) * W + x;
+    float s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+#pragma unroll
+    for (int i = 0; i < kWin; ++i) {
+      const float a = ra[i] * rscale, b = rb[i];
+      const float w = taps.w[i];
+      s0 = fmaf(w, a, s0);
+      s1 = fmaf(w, b, s1);
+      s2 = fmaf(w, a * a, s2);
+      s3 = fmaf(w, b * b, s3);
+      s4 = fmaf(w, a * b, s4);
+    }
+    const long long plane = (long long)H * Wv;
+    float* o = tmp + img * 5 * plane + (long long)y * Wv + x;
+    o[0] = s0; o[plane] = s1; o[2 * plane] = s2; o[3 * plane] = s3; o[4 * plane] = s4;
+  }
+}
+
+// vertical valid pass + per-window SSIM partials (objectives.cpp:93-149):
+// fields[img][5][Hv][Wv] = g1, g2, g2*mu1, g3, g3*mu2; ssim sum per image.
+__global__ void ssim_v_kernel(const float* __restrict__ tmp, int n, int W, int H, Taps taps,
+                              float* __restrict__ fields, double* __restrict__ values) {
+  const float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
+  const int Wv = W - kWin + 1, Hv = H - kWin + 1;
+  const long long total = (long long)n * Hv * Wv;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(t % Wv);
+    const int y = (int)((t / Wv) % Hv);
+    const long long img = t / ((long long)Wv * Hv);
+    const long long plane = (long long)H * Wv;
+    const float* src = tmp + img * 5 * plane + (long long)y * Wv + x;
+    float f[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < kWin; ++j)
+#pragma unroll
+      for (int k = 0; k < 5; ++k) f[k] = fmaf(taps.w[j], src[k * plane + (long long)j * Wv], f[k]);
+    const float mu1 = f[0], mu2 = f[1];
+    const float s1 = f[2] - mu1 * mu1, s2 = f[3] - mu2 * mu2, s12 = f[4] - mu1 * mu2;
+    const float a1 = 2.f * mu1 * mu2 + kC1, b1 = mu1 * mu1 + mu2 * mu2 + kC1;
+    const float a2 = 2.f * s12 + kC2, b2 = s1 + s2 + kC2;
+    const float l = a1 / b1, cs = a2 / b2;
+    const float g1 = cs * 2.f * (mu2 * b1 - mu1 * a1) / (b1 * b1);
+    const float g2 = -l * a2 / (b2 * b2);
+    const float g3 = l * 2.f / b2;
+    const long long vplane = (long long)Hv * Wv;
+    float* o = fields + img * 5 * vplane + (long long)y * Wv + x;
+    o[0] = g1; o[vplane] = g2; o[2 * vplane] = g2 * mu1; o[3 * vplane] = g3; o[4 * vplane] = g3 * mu2;
+    atomicAdd(values + 2 * img + 1, (double)(l * cs));
+  }
+}
+
+// adjoint vertical pass: atmp[img][5][H][Wv]
+__global__ void ssim_adj_v_kernel(const float* __restrict__ fields, int n, int W, int H, Taps taps,
+                                  float* __restrict__ atmp) {
+  const int Wv = W - kWin + 1, Hv = H - kWin + 1;
+  const long long total = (long long)n * H * Wv;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(t % Wv);
+    const int y = (int)((t / Wv) % H);
+    const long long img = t / ((long long)Wv * H);
+    const long long vplane = (long long)Hv * Wv, plane = (long long)H * Wv;
+    float f[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < kWin; ++j) {
+      const int yy = y - j;
+      if (yy < 0 || yy >= Hv) continue;
+      const float* src = fields + img * 5 * vplane + (long long)yy * Wv + x;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) f[k] = fmaf(taps.w[j], src[k * vplane], f[k]);
+    }
+    float* o = atmp + img * 5 * plane + (long long)y * Wv + x;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) o[k * plane] = f[k];
+  }
+}
+
+// adjoint horizontal pass + dL/dI assembly (objectives.cpp:151-166, trainer.cpp:284-287)
+__global__ void ssim_adj_h_kernel(const float* __restrict__ atmp, const float* __restrict__ r,
+                                  const float* __restrict__ mm, int n, int W, int H, float rscale, Taps taps,
+                                  float lambda_ssim, float grad_scale, float* __restrict__ dL,
+                                  double* __restrict__ values) {
+  const int Wv = W - kWin + 1, Hv = H - kWin + 1;
+  const float inv_p = 1.f / ((float)Wv * (float)Hv);
+  const float inv_n = 1.f / ((float)W * (float)H);
+  const long long total = (long long)n * H * W;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(t % W);
+    const int y = (int)((t / W) % H);
+    const long long img = t / ((long long)W * H);
+    const long long plane = (long long)H * Wv;
+    float f[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < kWin; ++i) {
+      const int xx = x - i;
+      if (xx < 0 || xx >= Wv) continue;
+      const float* src = atmp + img * 5 * plane + (long long)y * Wv + xx;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) f[k] = fmaf(taps.w[i], src[k * plane], f[k]);
+    }
+    const float a = r[t] * rscale, b = mm[t];
+    const float ds = f[0] + 2.f * a * f[1] - 2.f * f[2] + b * f[3] - f[4];
+    const float g_dssim = -0.5f * inv_p * ds;
+    const float d = a - b;
+    const float g_l1 = d > 0.f ? inv_n : (d < 0.f ? -inv_n : 0.f);
+    dL[t] = (g_l1 + lambda_ssim * g_dssim) * grad_scale;
+    atomicAdd(values + 2 * img, (double)fabsf(d));
+  }
+}
+
+__global__ void photometric_finish_kernel(double* values, int n, int W, int H) {
+  const int Wv = W - kWin + 1, Hv = H - kWin + 1;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    values[2 * i] = values[2 * i] / ((double)W * H);
+    values[2 * i + 1] = 0.5 * (1.0 - values[2 * i + 1] / ((double)Wv * Hv));
+  }
+}
+
+int grid_cap(Ctx* c, long long n, int block) {
+  long long b = (n + block - 1) / block;
+  const long long cap = (long long)c->sm_count * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+void launch_tv3d(Ctx* c, const float* vol, const int32_t dims[3], float lambda, double* value, float* grad,
+                 double* partials, int n_partials) {
+  const int nx = dims[0], ny = dims[1], nz = dims[2];
+  const double cx = (double)(nx - 1) * ny * nz, cy = (double)nx * (ny - 1) * nz, cz = (double)nx * ny * (nz - 1);
+  const double ix = cx > 0 ? 1.0 / cx : 0.0, iy = cy > 0 ? 1.0 / cy : 0.0, iz = cz > 0 ? 1.0 / cz : 0.0;
+  tv3d_kernel<<<n_partials, 256, 0, c->stream>>>(vol, nx, ny, nz, (float)ix, (float)iy, (float)iz, lambda, grad,
+                                                 partials);
+  tv3d_finish_kernel<<<1, 32, 0, c->stream>>>(partials, n_partials, ix, iy, iz, value);
+  c->launches += 2;
+}
+
+void launch_adam(Ctx* c, sct_cloud* p, sct_adam_state* st, const sct_grads* g, const float lr[4], float bc1,
+                 float bc2, float beta1, float beta2, float eps) {
+  if (p->m == 0) return;
+  adam_kernel<<<grid_cap(c, p->m, 256), 256, 0, c->stream>>>(p->m, p->rho_raw, p->pos, p->scale_raw, p->rot, *st,
+                                                             g->rho_raw, g->pos, g->scale_raw, g->rot, lr[0], lr[1],
+                                                             lr[2], lr[3], bc1, bc2, beta1, beta2, eps);
+  c->launches++;
+}
+
+int photometric_loss(Ctx* c, const float* rendered, const float* measured, int n, int w, int h,
+                     float render_scale, float lambda_ssim, float grad_scale, double* values, float* dL) {
+  if (w < kWin || h < kWin) {
+    set_error("DimMismatch: ssim: image smaller than the 11x11 window");
+    return SCT_ERR_DATA;
+  }
+  Taps taps;
+  {
+    double t[kWin], sum = 0.0;
+    for (int i = 0; i < kWin; ++i) {
+      const double x = i - (kWin - 1) / 2.0;
+      t[i] = std::exp(-x * x / (2.0 * 1.5 * 1.5));
+      sum += t[i];
+    }
+    for (int i = 0; i < kWin; ++i) taps.w[i] = (float)(t[i] / sum);
+  }
+  const int Wv = w - kWin + 1, Hv = h - kWin + 1;
+  const size_t tmp_elems = (size_t)n * 5 * h * Wv;
+  const size_t field_elems = (size_t)n * 5 * Hv * Wv;
+  float* tmp = nullptr;
+  float* fields = nullptr;
+  SCT_TRY(dev_alloc(c, (void**)&tmp, tmp_elems * sizeof(float)));
+  SCT_TRY(dev_alloc(c, (void**)&fields, field_elems * sizeof(float)));
+  SCT_CUDA_TRY(cudaMemsetAsync(values, 0, sizeof(double) * 2 * n, c->stream));
+  ssim_h_kernel<<<grid_cap(c, (long long)n * h * Wv, 256), 256, 0, c->stream>>>(rendered, measured, n, w, h,
+                                                                                 render_scale, taps, tmp);
+  ssim_v_kernel<<<grid_cap(c, (long long)n * Hv * Wv, 256), 256, 0, c->stream>>>(tmp, n, w, h, taps, fields,
+                                                                                  values);
+  ssim_adj_v_kernel<<<grid_cap(c, (long long)n * h * Wv, 256), 256, 0, c->stream>>>(fields, n, w, h, taps, tmp);
+  ssim_adj_h_kernel<<<grid_cap(c, (long long)n * h * w, 256), 256, 0, c->stream>>>(
+      tmp, rendered, measured, n, w, h, render_scale, taps, lambda_ssim, grad_scale, dL, values);
+  photometric_finish_kernel<<<1, 128, 0, c->stream>>>(values, n, w, h);
+  c->launches += 5;
+  dev_free(c, tmp);
+  dev_free(c, fields);
+  return SCT_OK;
+}
+
+}  // namespace sct

@@ -1,0 +1,162 @@
+// Internal declarations shared by the engine's translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "splatct_gpu.h"
+
+namespace sct {
+
+constexpr int kTilePx = 16;   // common.hpp:24 kImageTilePx
+constexpr int kTileVox = 8;   // common.hpp:25 kVolumeTileVox
+constexpr double kLog2e = 1.4426950408889634;
+constexpr double kPi = 3.14159265358979323846;  // M_PI
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+struct Status {
+  int code = SCT_OK;
+};
+#define SCT_CUDA_TRY(expr)                                                                 \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      ::sct::set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " +     \
+                       __FILE__ + ":" + std::to_string(__LINE__) + " (" #expr ")");       \
+      return SCT_ERR_CUDA;                                                                 \
+    }                                                                                      \
+  } while (0)
+#define SCT_TRY(expr)          \
+  do {                         \
+    int _rc = (expr);          \
+    if (_rc != SCT_OK) return _rc; \
+  } while (0)
+
+// ------------------------------------------------------------------ geometry
+// Per-view constants computed on the host in double (geometry.cpp:76-98).
+struct ViewParams {
+  double rot[9];  // W row-major
+  double t[3];
+};
+struct DetParams {
+  double fx, fy, cx, cy;
+  int32_t w, h;
+  double near_clip;
+  int32_t tiles_x, tiles_y;
+};
+DetParams make_det(const sct_scanner& s);
+ViewParams make_view(const sct_scanner& s, double theta);
+
+// Raster options as device-friendly POD.
+struct RasterParams {
+  int32_t mode;
+  int32_t dilation_compensation;
+  int32_t freeze_jacobian;
+  double eps2;      // lowpass_eps_px^2
+  double cull;      // cull_mahalanobis
+};
+RasterParams make_raster(const sct_raster_opts& o);
+
+// ------------------------------------------------------------------ device buffers
+// Stream-ordered device allocation (cudaMallocAsync on the context stream; the
+// pool keeps freed blocks, so steady-state calls allocate nothing from the driver).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+// ------------------------------------------------------------------ context
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool deterministic = true;
+  int64_t launches = 0;
+  // grow-only scratch reused across calls
+  void* cub_tmp = nullptr;
+  size_t cub_tmp_bytes = 0;
+  int64_t* pinned_count = nullptr;  // small pinned host word for D2H of counts
+  int sm_count = 148;
+};
+
+int ensure_cub_tmp(Ctx* c, size_t bytes);
+int dev_alloc(Ctx* c, void** p, size_t bytes);
+void dev_free(Ctx* c, void* p);
+
+}  // namespace sct
+
+// Forward state (opaque to callers).
+struct sct_fwd {
+  sct::Ctx* ctx = nullptr;
+  int32_t n_views = 0;
+  int64_t m = 0;
+  sct::DetParams det{};
+  sct::RasterParams rp{};
+  sct_raster_opts opts{};
+  sct_scanner scanner{};
+  double s_min = 0.0;
+  std::vector<double> thetas;
+  int32_t tile_bits = 0;
+  int64_t n_pairs = 0;
+  int64_t n_items = 0;
+  // device buffers
+  sct::ViewParams* d_views = nullptr;  // [V]
+  float4* d_rec = nullptr;             // [items][2]: {cx,cy,amp,-}, {A,B,C,-} (log2-scaled conic)
+  short4* d_rect = nullptr;            // [items] tx0,tx1,ty0,ty1 (tx0>tx1 => empty)
+  int32_t* d_count = nullptr;          // [items] tiles covered
+  int32_t* d_offset = nullptr;         // [items+1] exclusive scan of count
+  uint8_t* d_vis = nullptr;            // [items] visible flag
+  uint32_t* d_keys = nullptr;          // [pairs] sorted (view,tile) keys
+  int32_t* d_vals = nullptr;           // [pairs] sorted item index
+  int2* d_ranges = nullptr;            // [V*T] [start,end) into sorted pairs
+};
+
+struct sct_ctx : public sct::Ctx {};
+
+// ------------------------------------------------------------------ kernel entry points
+namespace sct {
+// binning preprocess (FP64, compiled with -fmad=false: bit-exact vs oracle)
+void launch_raster_preprocess(Ctx* c, const sct_cloud& cl, const ViewParams* d_views, int n_views,
+                              const DetParams& det, const RasterParams& rp, float4* rec, short4* rect,
+                              int32_t* count, uint8_t* vis);
+void launch_voxel_preprocess(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull, int32_t zb0,
+                             int32_t zb1, int32_t bricks_x, int32_t bricks_y, float4* rec, short4* rect_lo,
+                             short4* rect_hi, int32_t* count);
+// FP32 hot kernels
+void launch_raster_emit(Ctx* c, int64_t n_items, int64_t m, const short4* rect, const int32_t* offset,
+                        int tiles_x, int tile_bits, uint32_t* keys, int32_t* vals);
+void launch_ranges(Ctx* c, int64_t n_pairs, const uint32_t* keys, int tile_bits, int64_t tiles_per_view,
+                   int2* ranges);
+void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images);
+void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats);
+void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, const int32_t* offset,
+                       int32_t bricks_x, int32_t bricks_y, uint32_t* keys, int32_t* vals);
+void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
+                       int32_t bricks_y, const int2* ranges, const int32_t* vals, const float4* rec,
+                       const sct_cloud& cl, float* vol);
+void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
+                                 int32_t bricks_y, const int2* ranges, const int32_t* vals,
+                                 const float4* rec, const short4* lo, const short4* hi,
+                                 const int32_t* offset, const sct_cloud& cl, const float* dL,
+                                 float4* pair_stats);
+// FP64 chain rules
+void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float4* pair_stats,
+                         float* item_grads);
+void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float* item_grads,
+                            sct_grads* g, sct_stats* st);
+void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,
+                        const float4* pair_stats, sct_grads* g);
+// project_kernel export (FP64)
+void launch_project_export(Ctx* c, const sct_cloud& cl, const ViewParams* d_view, const DetParams& det,
+                           const RasterParams& rp, int32_t* vis, double* rec);
+// optimizer / objectives
+void launch_tv3d(Ctx* c, const float* vol, const int32_t dims[3], float lambda, double* value, float* grad,
+                 double* partials, int n_partials);
+void launch_adam(Ctx* c, sct_cloud* p, sct_adam_state* st, const sct_grads* g, const float lr[4], float bc1,
+                 float bc2, float beta1, float beta2, float eps);
+int photometric_loss(Ctx* c, const float* rendered, const float* measured, int n, int w, int h,
+                     float render_scale, float lambda_ssim, float grad_scale, double* values, float* dL);
+}  // namespace sct
