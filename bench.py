@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""Benchmark of the R²-Gaussian hot path on B200 (BASELINE.json).
+
+Headline workload (configs[2], "cfg3"): Shepp-Logan 256^3 phantom, 100k
+Gaussians (sample_init_cloud + trained-like anisotropy), 75 cone-beam views at
+512x512. One step = render (all of this rank's views, batched) + render_backward
+with a U(-1,1) upstream gradient into a zeroed CloudGrads, + the NCCL all-reduce
+of the per-Gaussian gradients when N > 1 (views sharded over ranks: strong
+scaling). Metric: projections/s (fwd+bwd) for the whole job.
+Secondary (configs[3], "cfg4"): voxelize + voxelize_backward of 200k Gaussians
+on a 256^3 grid (z-slab sharded), reported as voxels/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "projections/sec (fwd+bwd)"
+UNIT = "projections/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    p.add_argument("--cpu-views", type=int, default=4, help="views in the bounded CPU-oracle sample")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-voxel", action="store_true")
+    return p.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ workload
+def make_workload():
+    from paper_2405_20693_b200 import scenes
+    w = scenes.CONFIGS[3]
+    vol = scenes.phantom(w.n_vox)
+    ca = scenes.make_cloud(3, vol=vol)
+    thetas = [2.0 * np.pi * i / w.n_views for i in range(w.n_views)]
+    return w, ca, thetas, vol
+
+
+def upstream(n_views, res, views):
+    """U(-1,1) upstream gradient per view (seed 2 + view: independent of N)."""
+    out = np.empty((len(views), res, res), dtype=np.float32)
+    for k, v in enumerate(views):
+        out[k] = np.random.default_rng(1000 + v).uniform(-1.0, 1.0, (res, res)).astype(np.float32)
+    return out
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def cpu_oracle_rate(ca, thetas, res, n_views, steps=1):
+    """FP64 CPU restatement (oracle/, OpenMP on all host threads) timed on a
+    bounded sample of the same workload: n_views views of render +
+    render_backward. Returns (projections/s, threads, seconds)."""
+    from oracle import oracle as O
+    O.build()
+    O.set_threads(0)
+    threads = O.max_threads()
+    oc = O.Cloud.from_arrays(ca.s_min, *ca.as_float64())
+    cfg = O.test_scanner(res)
+    views = list(range(0, len(thetas), max(1, len(thetas) // n_views)))[:n_views]
+    ups = upstream(len(thetas), res, views).astype(np.float64)
+    done, t0 = 0, time.perf_counter()
+    for _ in range(steps):
+        for k, v in enumerate(views):
+            r = O.render(oc, cfg, thetas[v])
+            g = O.Grads.zeros(oc.m)
+            O.render_backward(oc, cfg, thetas[v], r, ups[k], g)
+            done += 1
+    dt = time.perf_counter() - t0
+    return done / dt, threads, dt, views
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    w, ca, thetas, _ = make_workload()
+    per_step = 1  # one view of render + render_backward per step (bounded sample)
+    for _ in range(args.warmup):
+        cpu_oracle_rate(ca, thetas, w.res, per_step)
+    rate, threads, dt, views = cpu_oracle_rate(ca, thetas, w.res, per_step, steps=args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * dt / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg3 (BASELINE configs[2]) " + w.description, "sample": "1 view/step"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} steps x 1 view (render+render_backward, fp64, OpenMP)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "CPU restatement of the reference (oracle/); the reference itself cannot be built here "
+                "(Eigen3/libpng/vendor absent) — see DESIGN.md",
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ engine arm
+def run_engine(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_20693_b200 as P
+    from paper_2405_20693_b200 import _capi, dist as pdist
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w, ca, thetas, vol = make_workload()
+    my_views = pdist.shard_views(len(thetas), rank, world)
+    my_thetas = [thetas[v] for v in my_views]
+    eng = P.Engine(local)
+    stream = eng.stream
+    cloud = P.GaussianCloud(ca.s_min, ca.rho_raw, ca.pos, ca.scale_raw, ca.rot, device=dev)
+    scanner = P.ScannerConfig(detector_res_px=(w.res, w.res))
+    up_host = upstream(len(thetas), w.res, my_views)
+    dL = torch.from_numpy(up_host).to(dev)
+    grads = P.CloudGrads(cloud.size(), device=dev)
+    images = torch.empty((len(my_views), w.res, w.res), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        grads.zero_()
+        fwd = eng.render(cloud, scanner, my_thetas, out=images)
+        eng.render_backward(cloud, fwd, dL, grads)
+        if world > 1:
+            pdist.allreduce_grads(grads)
+        return fwd
+
+    for _ in range(max(3, args.warmup)):
+        step().free()
+    torch.cuda.synchronize()
+    fwd = step()
+    gpe, n_pairs = fwd.work()  # this rank's algorithmic work per step
+    fwd.free()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = eng.kernel_launches()
+    eng.set_timing(True)
+    sampler.start()
+    barrier()
+    for k in range(args.steps):
+        flush.fill_(float(k))  # evict L2 between timed steps (256 MiB > 126 MB L2), outside the events
+        ev[k][0].record(stream)
+        f = step()
+        ev[k][1].record(stream)
+        f.free()
+    barrier()
+    clocks = sampler.stop()
+    kt = eng.timing_report()
+    eng.set_timing(False)
+    launches = eng.kernel_launches() - launches0
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = len(thetas) * args.steps / (total_ms / 1000.0)
+
+    # --- roofline of the dominant engine kernel (live CUDA-event timing above)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s at the measured max SM clock
+    flops_per_gpe = {"K3_composite": 15, "K4_backward_stats": 28}
+    engine_k = {k: v for k, v in kt.items() if "(cub)" not in k}
+    dom = max(engine_k, key=lambda k: engine_k[k][0])
+    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps} for k, v in kt.items()}
+    rf = None
+    for name in ("K3_composite", "K4_backward_stats"):
+        ms, n = kt[name]
+        ach = flops_per_gpe[name] * gpe / (ms / n / 1000.0) / 1e12
+        kernels[name]["achieved_tflops"] = ach
+        kernels[name]["frac_fp32_peak"] = ach / fp32_peak
+    dname = dom if dom in flops_per_gpe else max(flops_per_gpe, key=lambda k: kt[k][0])
+    ms, n = kt[dname]
+    ach = flops_per_gpe[dname] * gpe / (ms / n / 1000.0) / 1e12
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = prof.get(dname)
+    except Exception:
+        pass
+    rf = {"bound": "fp32", "kernel": dname, "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+          "frac": ach / fp32_peak, "traffic": traffic,
+          "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json); "
+                         "non-tensor path, so neither the copy nor the bf16 GEMM peak applies",
+          "algorithmic": f"{flops_per_gpe[dname]} FLOP/GPE x {gpe} GPE per launch (SURVEY.md §8d)",
+          "dominant_by_time": dom}
+
+    # --- e2e through the host-buffer C ABI
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, eng, ca, scanner, my_thetas, up_host, len(thetas), world, dev)
+
+    # --- voxelizer (configs[3])
+    vox = None if args.no_voxel else run_voxel(args, eng, vol, world, rank, dev)
+
+    # --- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, threads, dt, views = cpu_oracle_rate(ca, thetas, w.res, args.cpu_views)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{len(views)} of the 75 cfg3 views (render+render_backward, fp64 CPU restatement, "
+                         f"OpenMP {threads} threads), {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "fp32 (FP64 binning preprocess + chain rules)",
+            "data": "synthetic: Shepp-Logan phantom, sample_init_cloud + anisotropic jitter (seeded), U(-1,1) dL/dI",
+            "config": {"workload": "cfg3 (BASELINE configs[2]): " + w.description, "gaussians": ca.m,
+                       "views": len(thetas), "detector_px": [w.res, w.res], "pairs_per_step_rank0": n_pairs,
+                       "gpe_per_step_rank0": gpe, "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"views sharded over {world} rank(s); NCCL all-reduce of 11*M grads"},
+            "clocks": clocks, "gpu_launches": launches, "roofline": rf, "kernels": kernels, "e2e": e2e,
+            "cpu_baseline": cpu, "voxelizer": vox,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, eng, ca, scanner, thetas, up_host, n_total_views, world, dev):
+    """Same metric through sct_render_fwd_host / sct_render_bwd_host: pinned host
+    cloud, upstream and outputs; H2D/D2H copies inside the timed region."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_20693_b200 import _capi
+    L = _capi.load()
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    host = {k: pin(getattr(ca, k)) for k in ("rho_raw", "pos", "scale_raw", "rot")}
+    m = ca.m
+    cl = _capi.sct_cloud()
+    cl.m, cl.s_min_mm = m, ca.s_min
+    for k, t in host.items():
+        setattr(cl, k, t.data_ptr())
+    dL = pin(up_host)
+    imgs = torch.empty(up_host.shape, dtype=torch.float32).pin_memory()
+    gbuf = torch.zeros(11 * m, dtype=torch.float32).pin_memory()
+    gparts = torch.split(gbuf, [m, 3 * m, 3 * m, 4 * m])
+    g = _capi.sct_grads()
+    for k, t in zip(("rho_raw", "pos", "scale_raw", "rot"), gparts):
+        setattr(g, k, t.data_ptr())
+    sc = scanner._c()
+    import paper_2405_20693_b200 as P
+    op = P.RasterOptions()._c()
+    th = (C.c_double * len(thetas))(*thetas)
+    gdev = torch.empty(11 * m, dtype=torch.float32, device=dev)
+
+    def step():
+        gbuf.zero_()
+        st = C.c_void_p()
+        rc = L.sct_render_fwd_host(eng._h, C.byref(cl), C.byref(sc), th, len(thetas), C.byref(op),
+                                   C.c_void_p(imgs.data_ptr()), C.byref(st))
+        assert rc == 0, L.sct_last_error()
+        rc = L.sct_render_bwd_host(eng._h, st, C.byref(cl), C.c_void_p(dL.data_ptr()), C.byref(g), None)
+        assert rc == 0, L.sct_last_error()
+        L.sct_fwd_free(st)
+        if world > 1:
+            gdev.copy_(gbuf, non_blocking=True)
+            dist.all_reduce(gdev)
+            gbuf.copy_(gdev)
+        return float(gbuf[0])  # the step's result read on the host
+
+    for _ in range(2):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    cloud_b = 11 * m * 4
+    h2d = 2 * cloud_b + up_host.nbytes + 11 * m * 4  # cloud (fwd + bwd), dL/dI, running grads
+    d2h = imgs.numel() * 4 + 11 * m * 4
+    if world > 1:
+        h2d += 11 * m * 4
+        d2h += 11 * m * 4
+    return {"value": n_total_views * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "path": "C-ABI sct_render_fwd_host + sct_render_bwd_host (pinned host)",
+            "ms_per_step": 1000.0 * dt / args.steps}
+
+
+def run_voxel(args, eng, vol, world, rank, dev):
+    """configs[3]: 200k Gaussians, 256^3 grid, voxelize + voxelize_backward per step,
+    z-slab sharded (pair-balanced) with an all-reduce of the partial gradients."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_20693_b200 as P
+    from paper_2405_20693_b200 import dist as pdist, scenes
+    w = scenes.CONFIGS[4]
+    ca = scenes.make_cloud(4, vol=vol)
+    cloud = P.GaussianCloud(ca.s_min, ca.rho_raw, ca.pos, ca.scale_raw, ca.rot, device=dev)
+    grid = P.grid_for_extent((-1, -1, -1), (1, 1, 1), (w.n_vox,) * 3)
+    nl = (w.n_vox + 7) // 8
+    zb = pdist.shard_z_bricks(nl, rank, world)
+    vge, pairs = eng.voxel_work(cloud, grid)
+    out = torch.zeros(grid.shape_zyx, dtype=torch.float32, device=dev)
+    up = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, grid.shape_zyx).astype(np.float32)).to(dev)
+    grads = P.CloudGrads(cloud.size(), device=dev)
+
+    def step():
+        grads.zero_()
+        eng.voxelize(cloud, grid, z_bricks=zb, out=out)
+        eng.voxelize_backward(cloud, grid, up, grads, z_bricks=zb)
+        if world > 1:
+            pdist.allreduce_grads(grads)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    eng.set_timing(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        ev[k][0].record(eng.stream)
+        step()
+        ev[k][1].record(eng.stream)
+    torch.cuda.synchronize()
+    kt = eng.timing_report()
+    eng.set_timing(False)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    kern = {k: {"ms_per_step": v[0] / args.steps} for k, v in kt.items()}
+    for name, fl in (("K7_voxel_eval", 27), ("K8_voxel_backward_stats", 51)):
+        if name in kt and world == 1:
+            ms, n = kt[name]
+            ach = fl * vge / (ms / n / 1000.0) / 1e12
+            kern[name]["achieved_tflops"] = ach
+            kern[name]["frac_fp32_peak"] = ach / fp32_peak
+    return {"metric": "voxelized voxels/sec (fwd+bwd)", "value": grid.voxel_count() * args.steps / (total_ms / 1e3),
+            "unit": "voxels/s", "ms_per_step": total_ms / args.steps,
+            "workload": "cfg4 (BASELINE configs[3]): " + w.description, "vge_per_pass": vge, "pairs": pairs,
+            "kernels": kern}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_engine(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -126,6 +126,11 @@ const char* sct_version(void);
 /* number of engine kernels launched by this context so far (instrumentation). */
 int64_t sct_ctx_kernel_launches(const sct_ctx* ctx);
 
+/* per-kernel CUDA-event timing of engine launches on the context stream.
+ * report: JSON object {"kernel": [total_ms, launches], ...}; synchronises and resets. */
+int sct_ctx_set_timing(sct_ctx* ctx, int enable);
+int sct_ctx_timing_report(sct_ctx* ctx, char* buf, int32_t buflen);
+
 /* ---- rasterizer --------------------------------------------------------- */
 /* Projects + bins + composites n_views views (one batched launch sequence).
  * images: device [n_views][H][W] float. *state receives the forward state
@@ -139,6 +144,8 @@ int sct_render_fwd(sct_ctx* ctx, const sct_cloud* cloud, const sct_scanner* scan
 int sct_render_bwd(sct_ctx* ctx, sct_fwd* state, const sct_cloud* cloud, const float* dL_dimages,
                    sct_grads* grads, sct_stats* stats);
 int sct_fwd_free(sct_fwd* state);
+/* algorithmic work of a forward state: Gaussian-pixel evaluations (GPE) and pairs */
+int sct_fwd_work(sct_fwd* state, int64_t* gpe, int64_t* n_pairs);
 /* forward-state introspection (host outputs; synchronises the context) */
 int sct_fwd_info(sct_fwd* state, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y,
                  int64_t* n_visible);
@@ -172,6 +179,9 @@ int sct_voxelize_bwd(sct_ctx* ctx, const sct_cloud* cloud, const sct_grid* grid,
 /* brick lists for parity checks (host outputs, synchronises) */
 int sct_voxel_bins(sct_ctx* ctx, const sct_cloud* cloud, const sct_grid* grid, double cull_mahalanobis,
                    int64_t* n_pairs, int64_t* offsets, int32_t* kernel_idx);
+/* voxel-Gaussian evaluations (VGE) and (brick, kernel) pairs of a full-grid voxelize */
+int sct_voxel_work(sct_ctx* ctx, const sct_cloud* cloud, const sct_grid* grid, double cull_mahalanobis,
+                   int64_t* vge, int64_t* n_pairs);
 int sct_voxelize_fwd_host(sct_ctx* ctx, const sct_cloud* cloud_host, const sct_grid* grid,
                           double cull_mahalanobis, float* vol_host);
 

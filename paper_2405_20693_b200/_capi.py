@@ -63,6 +63,10 @@ SIGNATURES = {
     "sct_last_error": (C.c_char_p, []),
     "sct_version": (C.c_char_p, []),
     "sct_ctx_kernel_launches": (C.c_int64, [VP]),
+    "sct_ctx_set_timing": (C.c_int, [VP, C.c_int]),
+    "sct_ctx_timing_report": (C.c_int, [VP, C.c_char_p, C.c_int32]),
+    "sct_fwd_work": (C.c_int, [VP, I64, I64]),
+    "sct_voxel_work": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, I64, I64]),
     "sct_render_fwd": (C.c_int, [VP, P(sct_cloud), P(sct_scanner), D, C.c_int32, P(sct_raster_opts), VP, P(VP)]),
     "sct_render_bwd": (C.c_int, [VP, VP, P(sct_cloud), VP, P(sct_grads), P(sct_stats)]),
     "sct_fwd_free": (C.c_int, [VP]),

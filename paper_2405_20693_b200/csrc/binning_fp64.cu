@@ -143,30 +143,36 @@ void launch_raster_preprocess(Ctx* c, const sct_cloud& cl, const ViewParams* d_v
                               int32_t* count, uint8_t* vis) {
   const long long n_items = (long long)cl.m * n_views;
   if (n_items == 0) return;
-  raster_preprocess_kernel<<<grid_for(c, n_items, 256), 256, 0, c->stream>>>(
-      cl.m, n_items, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, d_views, det, rp, rec, rect, count,
-      vis);
-  c->launches++;
+  {
+    KScope _ks(c, "K1_raster_preprocess");
+    raster_preprocess_kernel<<<grid_for(c, n_items, 256), 256, 0, c->stream>>>(
+        cl.m, n_items, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, d_views, det, rp, rec, rect, count,
+        vis);
+  }
 }
 
 void launch_voxel_preprocess(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull, int32_t zb0,
                              int32_t zb1, int32_t, int32_t, float4* rec, short4* rect_lo, short4* rect_hi,
                              int32_t* count) {
   if (cl.m == 0) return;
-  voxel_preprocess_kernel<<<grid_for(c, cl.m, 256), 256, 0, c->stream>>>(
-      cl.m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, make_int3(g.dims[0], g.dims[1], g.dims[2]),
-      make_double3(g.origin_mm[0], g.origin_mm[1], g.origin_mm[2]),
-      make_double3(g.spacing_mm[0], g.spacing_mm[1], g.spacing_mm[2]), cull, zb0, zb1, rec, rect_lo, rect_hi,
-      count);
-  c->launches++;
+  {
+    KScope _ks(c, "K6_voxel_preprocess");
+    voxel_preprocess_kernel<<<grid_for(c, cl.m, 256), 256, 0, c->stream>>>(
+        cl.m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, make_int3(g.dims[0], g.dims[1], g.dims[2]),
+        make_double3(g.origin_mm[0], g.origin_mm[1], g.origin_mm[2]),
+        make_double3(g.spacing_mm[0], g.spacing_mm[1], g.spacing_mm[2]), cull, zb0, zb1, rec, rect_lo, rect_hi,
+        count);
+  }
 }
 
 void launch_project_export(Ctx* c, const sct_cloud& cl, const ViewParams* d_view, const DetParams& det,
                            const RasterParams& rp, int32_t* vis, double* rec) {
   if (cl.m == 0) return;
-  project_export_kernel<<<grid_for(c, cl.m, 128), 128, 0, c->stream>>>(
-      cl.m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, d_view, det, rp, vis, rec);
-  c->launches++;
+  {
+    KScope _ks(c, "project_export");
+    project_export_kernel<<<grid_for(c, cl.m, 128), 128, 0, c->stream>>>(
+        cl.m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, d_view, det, rp, vis, rec);
+  }
 }
 
 }  // namespace sct

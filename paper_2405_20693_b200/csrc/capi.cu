@@ -5,7 +5,9 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -53,6 +55,27 @@ RasterParams make_raster(const sct_raster_opts& o) {
   return r;
 }
 
+KScope::KScope(Ctx* ctx, const char* name, bool engine_kernel) : c(ctx) {
+  if (engine_kernel) c->launches++;
+  if (!c->timing) return;
+  TimingRec r;
+  r.name = name;
+  for (cudaEvent_t* e : {&r.a, &r.b}) {
+    if (!c->pool.empty()) {
+      *e = c->pool.back();
+      c->pool.pop_back();
+    } else {
+      cudaEventCreate(e);
+    }
+  }
+  cudaEventRecord(r.a, c->stream);
+  idx = (int)c->recs.size();
+  c->recs.push_back(r);
+}
+KScope::~KScope() {
+  if (idx >= 0) cudaEventRecord(c->recs[idx].b, c->stream);
+}
+
 int dev_alloc(Ctx* c, void** p, size_t bytes) {
   *p = nullptr;
   if (bytes == 0) bytes = 16;
@@ -85,7 +108,10 @@ static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64
   SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, offset, n + 1, c->stream));
   SCT_TRY(ensure_cub_tmp(c, tmp));
   tmp = c->cub_tmp_bytes;
-  SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, offset, n + 1, c->stream));
+  {
+    KScope _ks(c, "K2_scan(cub)", false);
+    SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, offset, n + 1, c->stream));
+  }
   int32_t t = 0;
   SCT_CUDA_TRY(cudaMemcpyAsync(c->pinned_count, offset + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -109,8 +135,11 @@ static int sort_pairs(Ctx* c, uint32_t*& keys, int32_t*& vals, int64_t n, int en
   SCT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, k2, vals, v2, (int)n, 0, end_bit, c->stream));
   SCT_TRY(ensure_cub_tmp(c, tmp));
   tmp = c->cub_tmp_bytes;
-  SCT_CUDA_TRY(
-      cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, k2, vals, v2, (int)n, 0, end_bit, c->stream));
+  {
+    KScope _ks(c, "K2_sort(cub)", false);
+    SCT_CUDA_TRY(
+        cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, k2, vals, v2, (int)n, 0, end_bit, c->stream));
+  }
   dev_free(c, keys);
   dev_free(c, vals);
   keys = k2;
@@ -294,6 +323,48 @@ int sct_ctx_set_deterministic(sct_ctx* c, int d) {
 
 int64_t sct_ctx_kernel_launches(const sct_ctx* c) { return c ? c->launches : 0; }
 
+int sct_ctx_set_timing(sct_ctx* c, int enable) {
+  if (!c) return SCT_ERR_CONFIG;
+  c->timing = enable != 0;
+  return SCT_OK;
+}
+
+// JSON {"kernel": [total_ms, launches], ...}; synchronises, then resets.
+int sct_ctx_timing_report(sct_ctx* c, char* buf, int32_t buflen) {
+  if (!c || !buf || buflen < 3) return SCT_ERR_CONFIG;
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  std::vector<std::pair<std::string, std::pair<double, int64_t>>> agg;
+  for (auto& r : c->recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    bool found = false;
+    for (auto& a : agg)
+      if (a.first == r.name) {
+        a.second.first += ms;
+        a.second.second += 1;
+        found = true;
+      }
+    if (!found) agg.push_back({r.name, {ms, 1}});
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->recs.clear();
+  std::string out = "{";
+  for (size_t i = 0; i < agg.size(); ++i) {
+    char tmp[256];
+    snprintf(tmp, sizeof(tmp), "%s\"%s\": [%.6f, %lld]", i ? ", " : "", agg[i].first.c_str(), agg[i].second.first,
+             (long long)agg[i].second.second);
+    out += tmp;
+  }
+  out += "}";
+  if ((int32_t)out.size() + 1 > buflen) {
+    set_error("ConfigError: timing report buffer too small");
+    return SCT_ERR_CONFIG;
+  }
+  std::memcpy(buf, out.c_str(), out.size() + 1);
+  return SCT_OK;
+}
+
 double sct_lr_at(double lr_init, double final_ratio, int32_t t, int32_t iters) {  // trainer.cpp:34-36
   return lr_init * std::pow(final_ratio, static_cast<double>(t) / iters);
 }
@@ -407,6 +478,28 @@ int sct_fwd_free(sct_fwd* s) {
   if (!s) return SCT_OK;
   free_state_buffers(s);
   delete s;
+  return SCT_OK;
+}
+
+// Algorithmic work of a forward state: GPE = sum over (view, tile) of
+// |tile list| x pixels inside the detector for that tile (the trip count of
+// rasterizer.cpp:144-153, identical for rasterizer.cpp:225-241).
+int sct_fwd_work(sct_fwd* s, int64_t* gpe, int64_t* n_pairs) {
+  if (!s) return SCT_ERR_CONFIG;
+  const int64_t T = (int64_t)s->det.tiles_x * s->det.tiles_y;
+  std::vector<int2> r(T * s->n_views);
+  SCT_CUDA_TRY(cudaMemcpyAsync(r.data(), s->d_ranges, r.size() * sizeof(int2), cudaMemcpyDeviceToHost,
+                               s->ctx->stream));
+  SCT_CUDA_TRY(cudaStreamSynchronize(s->ctx->stream));
+  int64_t g = 0;
+  for (int64_t k = 0; k < (int64_t)r.size(); ++k) {
+    const int64_t t = k % T;
+    const int tx = (int)(t % s->det.tiles_x), ty = (int)(t / s->det.tiles_x);
+    const int pw = std::min(kTilePx, s->det.w - tx * kTilePx), ph = std::min(kTilePx, s->det.h - ty * kTilePx);
+    g += (int64_t)(r[k].y - r[k].x) * pw * ph;
+  }
+  if (gpe) *gpe = g;
+  if (n_pairs) *n_pairs = s->n_pairs;
   return SCT_OK;
 }
 
@@ -657,6 +750,35 @@ int sct_voxel_bins(sct_ctx* c, const sct_cloud* cloud, const sct_grid* grid, dou
     set_error("CUDA error in sct_voxel_bins");
     rc = SCT_ERR_CUDA;
   }
+  return rc;
+}
+
+// VGE = sum over bricks of |brick list| x voxels of the brick inside the grid
+// (trip count of voxelizer.cpp:125-133 and :169-188).
+int sct_voxel_work(sct_ctx* c, const sct_cloud* cloud, const sct_grid* grid, double cull, int64_t* vge,
+                   int64_t* n_pairs) {
+  SCT_TRY(check_cloud(cloud));
+  SCT_TRY(check_grid(grid));
+  VoxelBins b;
+  int rc = voxel_bin(c, *cloud, *grid, cull, 0, INT32_MAX, b);
+  if (rc == SCT_OK) {
+    const int64_t nbr = (int64_t)b.bx * b.by * b.bz;
+    std::vector<int2> r(nbr);
+    cudaMemcpyAsync(r.data(), b.ranges, nbr * sizeof(int2), cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    int64_t g = 0;
+    for (int64_t t = 0; t < nbr; ++t) {
+      const int tx = (int)(t % b.bx), ty = (int)((t / b.bx) % b.by), tz = (int)(t / ((int64_t)b.bx * b.by));
+      const int64_t nv = (int64_t)std::min(kTileVox, grid->dims[0] - tx * kTileVox) *
+                         std::min(kTileVox, grid->dims[1] - ty * kTileVox) *
+                         std::min(kTileVox, grid->dims[2] - tz * kTileVox);
+      g += (int64_t)(r[t].y - r[t].x) * nv;
+    }
+    if (vge) *vge = g;
+    if (n_pairs) *n_pairs = b.n_pairs;
+  }
+  b.release(c);
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return rc;
 }
 

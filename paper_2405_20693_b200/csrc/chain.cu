@@ -314,29 +314,35 @@ int grid_cap(Ctx* c, long long n, int block) {
 void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float4* pair_stats,
                          float* item_grads) {
   if (s->n_items == 0) return;
-  raster_chain_kernel<<<grid_cap(c, s->n_items, 128), 128, 0, c->stream>>>(
-      s->m, s->n_items, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, s->d_views, s->det, s->rp, s->d_vis,
-      s->d_offset, pair_stats, item_grads);
-  c->launches++;
+  {
+    KScope _ks(c, "K5_raster_chain");
+    raster_chain_kernel<<<grid_cap(c, s->n_items, 128), 128, 0, c->stream>>>(
+        s->m, s->n_items, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, s->d_views, s->det, s->rp, s->d_vis,
+        s->d_offset, pair_stats, item_grads);
+  }
 }
 
 void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float* item_grads, sct_grads* g,
                             sct_stats* st) {
   if (s->m == 0) return;
-  raster_finalize_kernel<<<grid_cap(c, s->m, 128), 128, 0, c->stream>>>(
-      s->m, s->n_views, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, s->d_vis, item_grads, g->rho_raw,
-      g->pos, g->scale_raw, g->rot, st ? st->grad2d_norm_accum : nullptr, st ? st->grad_count : nullptr,
-      st ? st->grad3d_accum : nullptr);
-  c->launches++;
+  {
+    KScope _ks(c, "K5_raster_finalize");
+    raster_finalize_kernel<<<grid_cap(c, s->m, 128), 128, 0, c->stream>>>(
+        s->m, s->n_views, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, s->d_vis, item_grads, g->rho_raw,
+        g->pos, g->scale_raw, g->rot, st ? st->grad2d_norm_accum : nullptr, st ? st->grad_count : nullptr,
+        st ? st->grad3d_accum : nullptr);
+  }
 }
 
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,
                         const float4* pair_stats, sct_grads* g) {
   if (cl.m == 0) return;
-  voxel_chain_kernel<<<grid_cap(c, cl.m, 128), 128, 0, c->stream>>>(cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
-                                                                   cl.scale_raw, cl.rot, offset, count, pair_stats,
-                                                                   g->rho_raw, g->pos, g->scale_raw, g->rot);
-  c->launches++;
+  {
+    KScope _ks(c, "K8_voxel_chain");
+    voxel_chain_kernel<<<grid_cap(c, cl.m, 128), 128, 0, c->stream>>>(cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
+                                                                     cl.scale_raw, cl.rot, offset, count, pair_stats,
+                                                                     g->rho_raw, g->pos, g->scale_raw, g->rot);
+  }
 }
 
 }  // namespace sct

@@ -282,19 +282,26 @@ void launch_tv3d(Ctx* c, const float* vol, const int32_t dims[3], float lambda, 
   const int nx = dims[0], ny = dims[1], nz = dims[2];
   const double cx = (double)(nx - 1) * ny * nz, cy = (double)nx * (ny - 1) * nz, cz = (double)nx * ny * (nz - 1);
   const double ix = cx > 0 ? 1.0 / cx : 0.0, iy = cy > 0 ? 1.0 / cy : 0.0, iz = cz > 0 ? 1.0 / cz : 0.0;
-  tv3d_kernel<<<n_partials, 256, 0, c->stream>>>(vol, nx, ny, nz, (float)ix, (float)iy, (float)iz, lambda, grad,
-                                                 partials);
-  tv3d_finish_kernel<<<1, 32, 0, c->stream>>>(partials, n_partials, ix, iy, iz, value);
-  c->launches += 2;
+  {
+    KScope _ks(c, "K9_tv3d");
+    tv3d_kernel<<<n_partials, 256, 0, c->stream>>>(vol, nx, ny, nz, (float)ix, (float)iy, (float)iz, lambda, grad,
+                                                   partials);
+  }
+  {
+    KScope _ks(c, "K9_tv3d_finish");
+    tv3d_finish_kernel<<<1, 32, 0, c->stream>>>(partials, n_partials, ix, iy, iz, value);
+  }
 }
 
 void launch_adam(Ctx* c, sct_cloud* p, sct_adam_state* st, const sct_grads* g, const float lr[4], float bc1,
                  float bc2, float beta1, float beta2, float eps) {
   if (p->m == 0) return;
-  adam_kernel<<<grid_cap(c, p->m, 256), 256, 0, c->stream>>>(p->m, p->rho_raw, p->pos, p->scale_raw, p->rot, *st,
-                                                             g->rho_raw, g->pos, g->scale_raw, g->rot, lr[0], lr[1],
-                                                             lr[2], lr[3], bc1, bc2, beta1, beta2, eps);
-  c->launches++;
+  {
+    KScope _ks(c, "K10_adam");
+    adam_kernel<<<grid_cap(c, p->m, 256), 256, 0, c->stream>>>(p->m, p->rho_raw, p->pos, p->scale_raw, p->rot, *st,
+                                                               g->rho_raw, g->pos, g->scale_raw, g->rot, lr[0], lr[1],
+                                                               lr[2], lr[3], bc1, bc2, beta1, beta2, eps);
+  }
 }
 
 int photometric_loss(Ctx* c, const float* rendered, const float* measured, int n, int w, int h,
@@ -321,15 +328,29 @@ int photometric_loss(Ctx* c, const float* rendered, const float* measured, int n
   SCT_TRY(dev_alloc(c, (void**)&tmp, tmp_elems * sizeof(float)));
   SCT_TRY(dev_alloc(c, (void**)&fields, field_elems * sizeof(float)));
   SCT_CUDA_TRY(cudaMemsetAsync(values, 0, sizeof(double) * 2 * n, c->stream));
-  ssim_h_kernel<<<grid_cap(c, (long long)n * h * Wv, 256), 256, 0, c->stream>>>(rendered, measured, n, w, h,
-                                                                                 render_scale, taps, tmp);
-  ssim_v_kernel<<<grid_cap(c, (long long)n * Hv * Wv, 256), 256, 0, c->stream>>>(tmp, n, w, h, taps, fields,
-                                                                                  values);
-  ssim_adj_v_kernel<<<grid_cap(c, (long long)n * h * Wv, 256), 256, 0, c->stream>>>(fields, n, w, h, taps, tmp);
-  ssim_adj_h_kernel<<<grid_cap(c, (long long)n * h * w, 256), 256, 0, c->stream>>>(
-      tmp, rendered, measured, n, w, h, render_scale, taps, lambda_ssim, grad_scale, dL, values);
-  photometric_finish_kernel<<<1, 128, 0, c->stream>>>(values, n, w, h);
-  c->launches += 5;
+  {
+    KScope _ks(c, "K11_ssim_h");
+    ssim_h_kernel<<<grid_cap(c, (long long)n * h * Wv, 256), 256, 0, c->stream>>>(rendered, measured, n, w, h,
+                                                                                   render_scale, taps, tmp);
+  }
+  {
+    KScope _ks(c, "K11_ssim_v");
+    ssim_v_kernel<<<grid_cap(c, (long long)n * Hv * Wv, 256), 256, 0, c->stream>>>(tmp, n, w, h, taps, fields,
+                                                                                    values);
+  }
+  {
+    KScope _ks(c, "K11_ssim_adj_v");
+    ssim_adj_v_kernel<<<grid_cap(c, (long long)n * h * Wv, 256), 256, 0, c->stream>>>(fields, n, w, h, taps, tmp);
+  }
+  {
+    KScope _ks(c, "K11_ssim_adj_h");
+    ssim_adj_h_kernel<<<grid_cap(c, (long long)n * h * w, 256), 256, 0, c->stream>>>(
+        tmp, rendered, measured, n, w, h, render_scale, taps, lambda_ssim, grad_scale, dL, values);
+  }
+  {
+    KScope _ks(c, "K11_finish");
+    photometric_finish_kernel<<<1, 128, 0, c->stream>>>(values, n, w, h);
+  }
   dev_free(c, tmp);
   dev_free(c, fields);
   return SCT_OK;

@@ -206,35 +206,43 @@ int grid_cap(Ctx* c, long long n, int block) {
 void launch_raster_emit(Ctx* c, int64_t n_items, int64_t m, const short4* rect, const int32_t* offset,
                         int tiles_x, int tile_bits, uint32_t* keys, int32_t* vals) {
   if (n_items == 0) return;
-  raster_emit_kernel<<<grid_cap(c, n_items, 256), 256, 0, c->stream>>>(n_items, m, rect, offset, tiles_x,
-                                                                      tile_bits, keys, vals);
-  c->launches++;
+  {
+    KScope _ks(c, "K2_raster_emit");
+    raster_emit_kernel<<<grid_cap(c, n_items, 256), 256, 0, c->stream>>>(n_items, m, rect, offset, tiles_x,
+                                                                        tile_bits, keys, vals);
+  }
 }
 
 void launch_ranges(Ctx* c, int64_t n_pairs, const uint32_t* keys, int tile_bits, int64_t tiles_per_view,
                    int2* ranges) {
   if (n_pairs == 0) return;
-  ranges_kernel<<<grid_cap(c, n_pairs, 256), 256, 0, c->stream>>>(n_pairs, keys, tile_bits, tiles_per_view,
-                                                                  ranges);
-  c->launches++;
+  {
+    KScope _ks(c, "K2_ranges");
+    ranges_kernel<<<grid_cap(c, n_pairs, 256), 256, 0, c->stream>>>(n_pairs, keys, tile_bits, tiles_per_view,
+                                                                    ranges);
+  }
 }
 
 void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images) {
   const int T = s->det.tiles_x * s->det.tiles_y;
   dim3 grid(T, s->n_views);
-  composite_kernel<<<grid, kCompThreads, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
-                                                         s->det.w, s->det.h, images);
-  c->launches++;
+  {
+    KScope _ks(c, "K3_composite");
+    composite_kernel<<<grid, kCompThreads, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
+                                                           s->det.w, s->det.h, images);
+  }
 }
 
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats) {
   if (s->n_pairs == 0) return;
   const int T = s->det.tiles_x * s->det.tiles_y;
   dim3 grid(T, s->n_views);
-  backward_stats_kernel<<<grid, kBwdThreads, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
-                                                             s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h,
-                                                             dL, pair_stats);
-  c->launches++;
+  {
+    KScope _ks(c, "K4_backward_stats");
+    backward_stats_kernel<<<grid, kBwdThreads, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
+                                                               s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h,
+                                                               dL, pair_stats);
+  }
 }
 
 }  // namespace sct

@@ -70,7 +70,17 @@ struct DevBuf {
 };
 
 // ------------------------------------------------------------------ context
+struct TimingRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+
 struct Ctx {
+  // per-kernel CUDA-event timing (sct_ctx_set_timing); events bracket each
+  // engine launch on the context stream
+  bool timing = false;
+  std::vector<TimingRec> recs;
+  std::vector<cudaEvent_t> pool;
   int device = 0;
   cudaStream_t stream = nullptr;
   bool deterministic = true;
@@ -83,6 +93,15 @@ struct Ctx {
 };
 
 int ensure_cub_tmp(Ctx* c, size_t bytes);
+
+// RAII scope recording a start/stop event pair around one kernel launch when
+// timing is enabled; also counts the launch.
+struct KScope {
+  Ctx* c;
+  int idx = -1;
+  KScope(Ctx* ctx, const char* name, bool engine_kernel = true);
+  ~KScope();
+};
 int dev_alloc(Ctx* c, void** p, size_t bytes);
 void dev_free(Ctx* c, void* p);
 

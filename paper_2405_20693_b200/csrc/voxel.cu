@@ -231,17 +231,21 @@ void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, co
   if (m == 0) return;
   long long b = (m + 255) / 256;
   if (b > (long long)c->sm_count * 16) b = (long long)c->sm_count * 16;
-  voxel_emit_kernel<<<(int)b, 256, 0, c->stream>>>(m, lo, hi, offset, bricks_x, bricks_y, keys, vals);
-  c->launches++;
+  {
+    KScope _ks(c, "K6_voxel_emit");
+    voxel_emit_kernel<<<(int)b, 256, 0, c->stream>>>(m, lo, hi, offset, bricks_x, bricks_y, keys, vals);
+  }
 }
 
 void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x, int32_t bricks_y,
                        const int2* ranges, const int32_t* vals, const float4* rec, const sct_cloud&, float* vol) {
   const long long nb = (long long)bricks_x * bricks_y * (zb1 - zb0);
   if (nb <= 0) return;
-  voxel_eval_kernel<<<(unsigned)nb, kEvalThreads, 0, c->stream>>>(make_geo(g, zb0, bricks_x, bricks_y), ranges,
-                                                                   vals, rec, vol);
-  c->launches++;
+  {
+    KScope _ks(c, "K7_voxel_eval");
+    voxel_eval_kernel<<<(unsigned)nb, kEvalThreads, 0, c->stream>>>(make_geo(g, zb0, bricks_x, bricks_y), ranges,
+                                                                     vals, rec, vol);
+  }
 }
 
 void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
@@ -250,9 +254,11 @@ void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t
                                  const float* dL, float4* pair_stats) {
   const long long nb = (long long)bricks_x * bricks_y * (zb1 - zb0);
   if (nb <= 0) return;
-  voxel_backward_stats_kernel<<<(unsigned)nb, kVBwdThreads, 0, c->stream>>>(
-      make_geo(g, zb0, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL, pair_stats);
-  c->launches++;
+  {
+    KScope _ks(c, "K8_voxel_backward_stats");
+    voxel_backward_stats_kernel<<<(unsigned)nb, kVBwdThreads, 0, c->stream>>>(
+        make_geo(g, zb0, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL, pair_stats);
+  }
 }
 
 }  // namespace sct

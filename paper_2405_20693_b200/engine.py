@@ -235,15 +235,16 @@ class CloudGrads:
         self.resize(m, device)
 
     def resize(self, m: int, device="cuda"):
-        z = lambda n: torch.zeros(n, dtype=torch.float32, device=device)
-        self.rho_raw, self.pos, self.scale_raw, self.rot = z(m), z(3 * m), z(3 * m), z(4 * m)
+        # one contiguous buffer (11 floats per kernel) so a single collective
+        # can reduce all four groups; the group tensors are views into it
+        self.buffer = torch.zeros(11 * m, dtype=torch.float32, device=device)
+        self.rho_raw, self.pos, self.scale_raw, self.rot = torch.split(self.buffer, [m, 3 * m, 3 * m, 4 * m])
 
     def zero_(self):
-        for t in (self.rho_raw, self.pos, self.scale_raw, self.rot):
-            t.zero_()
+        self.buffer.zero_()
 
     def flat(self) -> torch.Tensor:
-        return torch.cat([self.rho_raw, self.pos, self.scale_raw, self.rot])
+        return self.buffer
 
     def tensors(self):
         return [self.rho_raw, self.pos, self.scale_raw, self.rot]
@@ -291,6 +292,26 @@ class Engine:
 
     def kernel_launches(self) -> int:
         return int(self.lib.sct_ctx_kernel_launches(self._h))
+
+    def set_timing(self, enable: bool):
+        """Bracket every engine launch with CUDA events on the context stream."""
+        _check(self.lib.sct_ctx_set_timing(self._h, int(enable)))
+
+    def timing_report(self) -> dict:
+        """{kernel: (total_ms, launches)} since the last report (synchronises)."""
+        import json
+        buf = C.create_string_buffer(1 << 16)
+        _check(self.lib.sct_ctx_timing_report(self._h, buf, len(buf)))
+        return {k: (float(v[0]), int(v[1])) for k, v in json.loads(buf.value.decode()).items()}
+
+    def voxel_work(self, cloud: "GaussianCloud", grid: "GridSpec", opts: Optional["VoxelizeOptions"] = None):
+        """(VGE, pairs) of a full-grid voxelize: the algorithmic work unit of K7/K8."""
+        opts = opts or VoxelizeOptions()
+        cl, g = cloud._c(), grid._c()
+        vge, n = C.c_int64(0), C.c_int64(0)
+        _check(self.lib.sct_voxel_work(self._h, C.byref(cl), C.byref(g), float(opts.cull_mahalanobis), C.byref(vge),
+                                       C.byref(n)))
+        return int(vge.value), int(n.value)
 
     # ------------------------------------------------------------- rasterizer
     def render(self, cloud: GaussianCloud, config: ScannerConfig, theta_rad: Union[float, Sequence[float]],
@@ -437,6 +458,12 @@ class RenderedProjection:
         n = C.c_int64(0)
         _check(self._engine.lib.sct_fwd_info(self._state, C.byref(n), None, None, None))
         return int(n.value)
+
+    def work(self):
+        """(GPE, pairs): Gaussian-pixel evaluations of this forward (= of its backward)."""
+        g, n = C.c_int64(0), C.c_int64(0)
+        _check(self._engine.lib.sct_fwd_work(self._state, C.byref(g), C.byref(n)))
+        return int(g.value), int(n.value)
 
     def n_visible(self) -> int:
         n = C.c_int64(0)
