@@ -42,10 +42,14 @@ __global__ void __launch_bounds__(256) raster_preprocess_kernel(
     count[item] = c;
     vis[item] = 1;
     rect[item] = make_short4((short)tx0, (short)tx1, (short)ty0, (short)ty1);
-    // exp(-1/2 d^T Q d) = exp2(A dx^2 + B dx dy + C dy^2)
-    rec[2 * item + 0] = make_float4((float)g.cx, (float)g.cy, (float)g.amp, 0.f);
-    rec[2 * item + 1] = make_float4((float)(kA * g.conic.m[0][0]), (float)(2.0 * kA * g.conic.m[0][1]),
-                                    (float)(kA * g.conic.m[1][1]), 0.f);
+    // exp(-1/2 d^T Q d) = exp2(A dx^2 + B dx dy + C dy^2). The FP32 kernels
+    // evaluate it as 2^(L + 64) along 4-pixel runs with the ratio recurrence
+    // E(dx+1) = E(dx) * 2^(2A dx + A + B dy), ratio(dx+1) = ratio(dx) * 2^(2A);
+    // the record carries amp * 2^-64 and K = 2^(2A) for that.
+    const double A = kA * g.conic.m[0][0];
+    rec[2 * item + 0] = make_float4((float)g.cx, (float)g.cy, (float)(g.amp * 0x1p-64), (float)exp2(2.0 * A));
+    rec[2 * item + 1] = make_float4((float)A, (float)(2.0 * kA * g.conic.m[0][1]), (float)(kA * g.conic.m[1][1]),
+                                    (float)(2.0 * A));
   }
 }
 

@@ -59,6 +59,37 @@ __global__ void __launch_bounds__(256) ranges_kernel(long long n_pairs, const ui
   }
 }
 
+// Gaussian-pixel evaluation along a run of 4 pixels of one row.
+// The exponent is carried with a +64 offset: E' = 2^(L + 64), L <= 0, so one
+// MUFU.EX2 gives the first pixel and one more the ratio to the next pixel,
+// R = 2^(L(dx+1) - L(dx)) = 2^(2A dx + A + B dy); later ratios follow from
+// R *= K, K = 2^(2A). Two MUFU per 4 GPE instead of four. The ratio argument
+// is clamped at 126: when it would exceed that, L(dx) < -126 already and every
+// pixel value it could feed is below 2^-29 of the amplitude;
+// likewise a run whose first E' flushes to zero (L < -190) only holds values
+// below 2^-29 * amp. The amplitude (records) or upstream gradient (backward)
+// carries the matching 2^-64.
+struct Run4 {
+  float e0, e1, e2, e3;
+};
+__device__ __forceinline__ Run4 run4(float dx, float A, float A2, float bdy, float apb, float cdy2o, float K) {
+  const float t = fmaf(A, dx, bdy);
+  const float L = fmaf(dx, t, cdy2o);
+  const float D = fmaf(A2, dx, apb);
+  float E = ex2(L);
+  float R = ex2(fminf(D, 126.f));
+  Run4 r;
+  r.e0 = E;
+  E *= R;
+  R *= K;
+  r.e1 = E;
+  E *= R;
+  R *= K;
+  r.e2 = E;
+  r.e3 = E * R;
+  return r;
+}
+
 // K3: one 64-thread CTA per (tile, view); thread = 1 row x 4 columns.
 // Records for the tile list are staged through shared memory 64 at a time
 // (coalesced float4 gathers); every thread then reads them as broadcasts.
@@ -90,17 +121,16 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(
     __syncthreads();
 #pragma unroll 4
     for (int j = 0; j < n; ++j) {
-      const float4 a = s0[j];  // cx cy amp
-      const float4 b = s1[j];  // A B C
+      const float4 a = s0[j];  // cx cy amp*2^-64 K
+      const float4 b = s1[j];  // A B C 2A
       const float dy = py - a.y;
       const float bdy = b.y * dy;
-      const float cdy2 = b.z * dy * dy;
-      const float dx = px0 - a.x;
-      float d, t;
-      d = dx;        t = fmaf(b.x, d, bdy); acc0 = fmaf(a.z, ex2(fmaf(d, t, cdy2)), acc0);
-      d = dx + 1.f;  t = fmaf(b.x, d, bdy); acc1 = fmaf(a.z, ex2(fmaf(d, t, cdy2)), acc1);
-      d = dx + 2.f;  t = fmaf(b.x, d, bdy); acc2 = fmaf(a.z, ex2(fmaf(d, t, cdy2)), acc2);
-      d = dx + 3.f;  t = fmaf(b.x, d, bdy); acc3 = fmaf(a.z, ex2(fmaf(d, t, cdy2)), acc3);
+      const float cdy2o = fmaf(b.z * dy, dy, 64.f);
+      const Run4 e = run4(px0 - a.x, b.x, b.w, bdy, b.x + bdy, cdy2o, a.w);
+      acc0 = fmaf(a.z, e.e0, acc0);
+      acc1 = fmaf(a.z, e.e1, acc1);
+      acc2 = fmaf(a.z, e.e2, acc2);
+      acc3 = fmaf(a.z, e.e3, acc3);
     }
   }
   if (v < H) {
@@ -117,78 +147,105 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(
 }
 
 // K4: Gaussian-major backward statistics. One 256-thread CTA per non-empty
-// (tile, view). Sixteen lanes share a Gaussian, one pixel row each, so the
-// sums over a row stay in registers; the 16 partials are combined with warp
-// shuffles and written once per (tile, Gaussian) pair into that pair's slot
-// (slot = item's scan offset + rank of this tile in its rectangle), which the
-// chain kernel later reduces in the reference's fixed tile order
-// (rasterizer.cpp:245-257) — deterministic, no atomics.
+// (tile, view). Eight lanes share a Gaussian; lane s owns pixel rows s and
+// s+8 with their upstream gradient in registers, so per pixel the work is the
+// run4 exponential plus three FMAs accumulating column moments
+// R0 = sum g E, R1 = sum g E c', R2 = sum g E c'^2 (c' = column - 7.5); the
+// row's s0, s1, s2 follow from them. The 8 lanes' partial statistics are
+// combined with a 3-step shuffle reduce-scatter (7 shuffles for 6 values) and
+// lanes 0..5 write the (tile, Gaussian) pair's 6 values as one 32-byte sector
+// into the pair's slot (item scan offset + rank of this tile in its
+// rectangle). The chain kernel reduces slots in the reference's fixed tile
+// order (rasterizer.cpp:245-257): deterministic, no atomics.
 constexpr int kBwdThreads = 256;
-__global__ void __launch_bounds__(kBwdThreads) backward_stats_kernel(
+__global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ rect, const int32_t* __restrict__ offset, int tiles_x, int tiles_per_view, int W,
-    int H, const float* __restrict__ dL, float4* __restrict__ pair_stats) {
+    int H, const float* __restrict__ dL, float* __restrict__ pair_stats) {
   const int tile = blockIdx.x;
   const int view = blockIdx.y;
   const int2 rg = ranges[(long long)view * tiles_per_view + tile];
   if (rg.y <= rg.x) return;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int lane16 = threadIdx.x & 15;
-  const int group = threadIdx.x >> 4;
-  const int v = ty * kTilePx + lane16;
+  const int s = threadIdx.x & 7;
+  const int group = threadIdx.x >> 3;
   const int u0 = tx * kTilePx;
-  // upstream gradient of this thread's pixel row, in registers
-  float g[kTilePx];
-  const float* drow = dL + ((long long)view * H + v) * W + u0;
+  float g[2][kTilePx];
 #pragma unroll
-  for (int c = 0; c < kTilePx; ++c) g[c] = (v < H && u0 + c < W) ? __ldg(drow + c) : 0.f;
-  const float py = (float)v + 0.5f;
+  for (int r = 0; r < 2; ++r) {
+    const int v = ty * kTilePx + s + 8 * r;
+    const float* drow = dL + ((long long)view * H + v) * W + u0;
+#pragma unroll
+    for (int c = 0; c < kTilePx; ++c) g[r][c] = (v < H && u0 + c < W) ? __ldg(drow + c) * 0x1p-64f : 0.f;
+  }
+  const float py0 = (float)(ty * kTilePx + s) + 0.5f;
   const float px0 = (float)u0 + 0.5f;
-  for (int base = rg.x; base < rg.y; base += 16) {
+  const bool b2 = s & 4, b1 = s & 2, b0 = s & 1;
+  for (int base = rg.x; base < rg.y; base += kBwdThreads / 8) {
     const int j = base + group;
     const bool valid = j < rg.y;
-    float st0 = 0.f, st1 = 0.f, st2 = 0.f, st3 = 0.f, st4 = 0.f, st5 = 0.f;
+    float st[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) st[k] = 0.f;
     long long item = 0;
     if (valid) {
       item = vals[j];
       const float4 a = __ldg(rec + 2 * item);
       const float4 b = __ldg(rec + 2 * item + 1);
-      const float dy = py - a.y;
-      const float bdy = b.y * dy;
-      const float cdy2 = b.z * dy * dy;
       const float dx0 = px0 - a.x;
-      float r0 = 0.f, rx = 0.f, rxx = 0.f;
+      const float dxm = dx0 + 7.5f;
 #pragma unroll
-      for (int c = 0; c < kTilePx; ++c) {
-        const float dx = dx0 + (float)c;
-        const float t = fmaf(b.x, dx, bdy);
-        const float ge = g[c] * ex2(fmaf(dx, t, cdy2));
-        r0 += ge;
-        const float gx = ge * dx;
-        rx += gx;
-        rxx = fmaf(gx, dx, rxx);
+      for (int r = 0; r < 2; ++r) {
+        const float dy = py0 + 8.f * r - a.y;
+        const float bdy = b.y * dy;
+        const float apb = b.x + bdy;
+        const float cdy2o = fmaf(b.z * dy, dy, 64.f);
+        float R0 = 0.f, R1 = 0.f, R2 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const Run4 e = run4(dx0 + 4.f * q, b.x, b.w, bdy, apb, cdy2o, a.w);
+          const float ev[4] = {e.e0, e.e1, e.e2, e.e3};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float cp = (float)(4 * q + k) - 7.5f;
+            const float ge = g[r][4 * q + k] * ev[k];
+            R0 += ge;
+            R1 = fmaf(ge, cp, R1);
+            R2 = fmaf(ge, cp * cp, R2);
+          }
+        }
+        // sum ge dx = dxm R0 + R1, sum ge dx^2 = dxm^2 R0 + 2 dxm R1 + R2
+        const float rx = fmaf(dxm, R0, R1);
+        const float rxx = fmaf(dxm, fmaf(dxm, R0, 2.f * R1), R2);
+        st[0] += R0;                      // s0
+        st[1] += rx;                      // s1.x
+        st[2] = fmaf(dy, R0, st[2]);      // s1.y
+        st[3] += rxx;                     // s2.xx
+        st[4] = fmaf(dy * dy, R0, st[4]); // s2.yy
+        st[5] = fmaf(dy, rx, st[5]);      // s2.xy
       }
-      st0 = r0;            // s0
-      st1 = rx;            // s1.x
-      st2 = dy * r0;       // s1.y
-      st3 = rxx;           // s2.xx
-      st4 = dy * dy * r0;  // s2.yy
-      st5 = dy * rx;       // s2.xy
+    }
+    // reduce-scatter over the 8 lanes of the group: lane s ends with total[s]
+    float w[4], x[2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float send = b2 ? st[k] : st[k + 4];
+      const float keep = b2 ? st[k + 4] : st[k];
+      w[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
     }
 #pragma unroll
-    for (int off = 8; off >= 1; off >>= 1) {
-      st0 += __shfl_xor_sync(0xffffffffu, st0, off);
-      st1 += __shfl_xor_sync(0xffffffffu, st1, off);
-      st2 += __shfl_xor_sync(0xffffffffu, st2, off);
-      st3 += __shfl_xor_sync(0xffffffffu, st3, off);
-      st4 += __shfl_xor_sync(0xffffffffu, st4, off);
-      st5 += __shfl_xor_sync(0xffffffffu, st5, off);
+    for (int k = 0; k < 2; ++k) {
+      const float send = b1 ? w[k] : w[k + 2];
+      const float keep = b1 ? w[k + 2] : w[k];
+      x[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
     }
-    if (valid && lane16 == 0) {
+    const float send = b0 ? x[0] : x[1];
+    const float keep = b0 ? x[1] : x[0];
+    const float tot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    if (valid && s < 6) {
       const short4 r = rect[item];
       const int slot = offset[item] + (ty - r.z) * (r.y - r.x + 1) + (tx - r.x);
-      pair_stats[2 * (long long)slot] = make_float4(st0, st1, st2, st3);
-      pair_stats[2 * (long long)slot + 1] = make_float4(st4, st5, 0.f, 0.f);
+      pair_stats[8 * (long long)slot + s] = tot;
     }
   }
 }
@@ -241,7 +298,7 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
     KScope _ks(c, "K4_backward_stats");
     backward_stats_kernel<<<grid, kBwdThreads, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
                                                                s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h,
-                                                               dL, pair_stats);
+                                                               dL, reinterpret_cast<float*>(pair_stats));
   }
 }
 
