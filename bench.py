@@ -342,16 +342,20 @@ def run_e2e(args, eng, ca, scanner, thetas, up_host, n_total_views, world, dev):
             gbuf.copy_(gdev)
         return float(gbuf[0])  # the step's result read on the host
 
-    for _ in range(2):
+    for _ in range(max(3, args.warmup)):
         step()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    per = []
     for _ in range(args.steps):
+        ts = time.perf_counter()
         step()
+        per.append(1e3 * (time.perf_counter() - ts))
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    print(f"[bench] e2e per-step ms: {[round(x, 2) for x in per]}", file=sys.stderr)
     if world > 1:
         t = torch.tensor([dt], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -13,12 +13,30 @@ namespace sct {
 
 namespace {
 
+// K0: view-independent per-Gaussian quantities, once per kernel: the 3D
+// covariance Sigma (all 9 entries, d_covariance order — its rounding is not
+// symmetric, so both halves are kept) and rho = act_density(rho_raw).
+// prep[i] = {S00 S01 S02 S10 S11 S12 S20 S21 S22, rho}.
+__global__ void __launch_bounds__(256) gauss_prep_kernel(long long m, double s_min, const float* __restrict__ rho_raw,
+                                                         const float* __restrict__ pos,
+                                                         const float* __restrict__ scale_raw,
+                                                         const float* __restrict__ rot, double* __restrict__ prep) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
+    const dM3 s = d_covariance(k);
+    double* o = prep + kPrepStride * i;
+#pragma unroll
+    for (int a = 0; a < 9; ++a) o[a] = s.m[a / 3][a % 3];
+    o[9] = d_act_density(k.rho_raw);
+  }
+}
+
 // One thread per (view, kernel) item; item = view * m + kernel (view-major, so
 // a stable sort on the (view, tile) key leaves each tile list ascending in
 // kernel index exactly like the reference's serial push_back, rasterizer.cpp:124-133).
 __global__ void __launch_bounds__(256) raster_preprocess_kernel(
-    long long m, long long n_items, double s_min, const float* __restrict__ rho_raw,
-    const float* __restrict__ pos, const float* __restrict__ scale_raw, const float* __restrict__ rot,
+    long long m, long long n_items, const float* __restrict__ pos, const double* __restrict__ prep,
     const ViewParams* __restrict__ views, DetParams det, RasterParams rp, float4* __restrict__ rec,
     short4* __restrict__ rect, int32_t* __restrict__ count, uint8_t* __restrict__ vis) {
   const double kA = -0.5 * kLog2e;
@@ -26,10 +44,14 @@ __global__ void __launch_bounds__(256) raster_preprocess_kernel(
        item += (long long)gridDim.x * blockDim.x) {
     const long long v = item / m;
     const long long i = item - v * m;
-    const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
+    const double p[3] = {(double)pos[3 * i], (double)pos[3 * i + 1], (double)pos[3 * i + 2]};
+    dM3 sigma;
+    const double* pr = prep + kPrepStride * i;
+#pragma unroll
+    for (int a = 0; a < 9; ++a) sigma.m[a / 3][a % 3] = pr[a];
     const ViewParams view = views[v];
     dProj g;
-    if (!d_project(k, view, det, rp, g)) {
+    if (!d_project(p, sigma, pr[9], view, det, rp, g)) {
       count[item] = 0;
       vis[item] = 0;
       rect[item] = make_short4(1, 0, 1, 0);
@@ -111,7 +133,7 @@ __global__ void project_export_kernel(long long m, double s_min, const float* __
        i += (long long)gridDim.x * blockDim.x) {
     const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
     dProj g;
-    const bool ok = d_project(k, view[0], det, rp, g);
+    const bool ok = d_project(k.p, d_covariance(k), d_act_density(k.rho_raw), view[0], det, rp, g);
     vis[i] = ok ? 1 : 0;
     double* o = out + 11 * i;
     if (!ok) {
@@ -142,17 +164,21 @@ int grid_for(Ctx* c, long long n, int block) {
 
 }  // namespace
 
-void launch_raster_preprocess(Ctx* c, const sct_cloud& cl, const ViewParams* d_views, int n_views,
-                              const DetParams& det, const RasterParams& rp, float4* rec, short4* rect,
+void launch_gauss_prep(Ctx* c, const sct_cloud& cl, double* prep) {
+  if (cl.m == 0) return;
+  KScope _ks(c, "K0_gauss_prep");
+  gauss_prep_kernel<<<grid_for(c, cl.m, 256), 256, 0, c->stream>>>(cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
+                                                                   cl.scale_raw, cl.rot, prep);
+}
+
+void launch_raster_preprocess(Ctx* c, const sct_cloud& cl, const double* prep, const ViewParams* d_views,
+                              int n_views, const DetParams& det, const RasterParams& rp, float4* rec, short4* rect,
                               int32_t* count, uint8_t* vis) {
   const long long n_items = (long long)cl.m * n_views;
   if (n_items == 0) return;
-  {
-    KScope _ks(c, "K1_raster_preprocess");
-    raster_preprocess_kernel<<<grid_for(c, n_items, 256), 256, 0, c->stream>>>(
-        cl.m, n_items, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, d_views, det, rp, rec, rect, count,
-        vis);
-  }
+  KScope _ks(c, "K1_raster_preprocess");
+  raster_preprocess_kernel<<<grid_for(c, n_items, 256), 256, 0, c->stream>>>(cl.m, n_items, cl.pos, prep, d_views,
+                                                                             det, rp, rec, rect, count, vis);
 }
 
 void launch_voxel_preprocess(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull, int32_t zb0,

@@ -85,6 +85,18 @@ int dev_alloc(Ctx* c, void** p, size_t bytes) {
 void dev_free(Ctx* c, void* p) {
   if (p) cudaFreeAsync(p, c->stream);
 }
+int stage_buf(Ctx* c, int slot, size_t bytes, void** p) {
+  if (bytes > c->stage_bytes[slot]) {
+    if (c->stage[slot]) cudaFreeAsync(c->stage[slot], c->stream);
+    c->stage[slot] = nullptr;
+    c->stage_bytes[slot] = 0;
+    SCT_CUDA_TRY(cudaMallocAsync(&c->stage[slot], bytes, c->stream));
+    c->stage_bytes[slot] = bytes;
+  }
+  *p = c->stage[slot];
+  return SCT_OK;
+}
+
 int ensure_cub_tmp(Ctx* c, size_t bytes) {
   if (bytes <= c->cub_tmp_bytes) return SCT_OK;
   if (c->cub_tmp) cudaFreeAsync(c->cub_tmp, c->stream);
@@ -262,6 +274,7 @@ static void free_state_buffers(sct_fwd* s) {
   dev_free(c, s->d_keys);
   dev_free(c, s->d_vals);
   dev_free(c, s->d_ranges);
+  dev_free(c, s->d_prep);
 }
 
 extern "C" {
@@ -299,6 +312,8 @@ int sct_ctx_destroy(sct_ctx* c) {
   if (!c) return SCT_OK;
   cudaStreamSynchronize(c->stream);
   if (c->cub_tmp) cudaFree(c->cub_tmp);
+  for (int a = 0; a < Ctx::kStageSlots; ++a)
+    if (c->stage[a]) cudaFree(c->stage[a]);
   if (c->pinned_count) cudaFreeHost(c->pinned_count);
   delete c;
   return SCT_OK;
@@ -431,14 +446,21 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
     set_error("CUDA error: memset");
     return fail(SCT_ERR_CUDA);
   }
-  launch_raster_preprocess(c, *cloud, s->d_views, n_views, s->det, s->rp, s->d_rec, s->d_rect, s->d_count,
-                           s->d_vis);
+  if ((rc = dev_alloc(c, (void**)&s->d_prep, kPrepStride * s->m * sizeof(double)))) return fail(rc);
+  launch_gauss_prep(c, *cloud, s->d_prep);
+  launch_raster_preprocess(c, *cloud, s->d_prep, s->d_views, n_views, s->det, s->rp, s->d_rec, s->d_rect,
+                           s->d_count, s->d_vis);
   if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs))) return fail(rc);
   if ((rc = dev_alloc(c, (void**)&s->d_keys, s->n_pairs * sizeof(uint32_t)))) return fail(rc);
   if ((rc = dev_alloc(c, (void**)&s->d_vals, s->n_pairs * sizeof(int32_t)))) return fail(rc);
   launch_raster_emit(c, ni, s->m, s->d_rect, s->d_offset, s->det.tiles_x, s->tile_bits, s->d_keys, s->d_vals);
-  if ((rc = sort_pairs(c, s->d_keys, s->d_vals, s->n_pairs, s->tile_bits + bits_for((uint64_t)n_views))))
-    return fail(rc);
+  // Pairs are emitted view-major (and kernel-ascending within a view), so a
+  // STABLE sort on the tile bits alone already groups them by (tile, view)
+  // with each list ascending in kernel index: one or two radix passes fewer
+  // than sorting the full (view, tile) key. The view bits stay in the keys
+  // for the range scan.
+  if (s->tile_bits > 0)
+    if ((rc = sort_pairs(c, s->d_keys, s->d_vals, s->n_pairs, s->tile_bits))) return fail(rc);
   launch_ranges(c, s->n_pairs, s->d_keys, s->tile_bits, T, s->d_ranges);
   if (images) launch_raster_composite(c, s, images);
   if (cudaGetLastError() != cudaSuccess) {
@@ -530,25 +552,21 @@ int sct_fwd_tile_lists(sct_fwd* s, int32_t view, int64_t* offsets, int32_t* kern
   SCT_CUDA_TRY(cudaMemcpyAsync(r.data(), s->d_ranges + view * T, T * sizeof(int2), cudaMemcpyDeviceToHost,
                                c->stream));
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
-  int64_t lo = -1, hi = -1;
-  for (int64_t t = 0; t < T; ++t)
-    if (r[t].y > r[t].x) {
-      if (lo < 0) lo = r[t].x;
-      hi = r[t].y;
-    }
   int64_t o = 0;
   for (int64_t t = 0; t < T; ++t) {
     offsets[t] = o;
     o += r[t].y > r[t].x ? r[t].y - r[t].x : 0;
   }
   offsets[T] = o;
-  if (kernel_idx && lo >= 0) {
-    std::vector<int32_t> v(hi - lo);
-    SCT_CUDA_TRY(cudaMemcpyAsync(v.data(), s->d_vals + lo, (hi - lo) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+  if (kernel_idx && o > 0) {
+    // pairs are sorted tile-major; gather this view's sub-range of every tile
+    std::vector<int32_t> all(s->n_pairs);
+    SCT_CUDA_TRY(cudaMemcpyAsync(all.data(), s->d_vals, s->n_pairs * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                  c->stream));
     SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
     const int64_t base = (int64_t)view * s->m;
-    for (int64_t k = 0; k < hi - lo; ++k) kernel_idx[k] = (int32_t)(v[k] - base);
+    for (int64_t t = 0; t < T; ++t)
+      for (int64_t k = r[t].x; k < r[t].y; ++k) kernel_idx[offsets[t] + (k - r[t].x)] = (int32_t)(all[k] - base);
   }
   return SCT_OK;
 }
@@ -578,6 +596,8 @@ int sct_project_kernels(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* s
 }
 
 // ---- host-buffer variants ----------------------------------------------------
+// Staging slots: 0-3 cloud arrays, 4 images, 5 upstream gradient, 6-9 grads,
+// 10-12 stats, 13 volume.
 static int upload_cloud(Ctx* c, const sct_cloud* h, sct_cloud* d) {
   *d = *h;
   const int64_t m = h->m;
@@ -585,35 +605,31 @@ static int upload_cloud(Ctx* c, const sct_cloud* h, sct_cloud* d) {
   float* src[4] = {h->rho_raw, h->pos, h->scale_raw, h->rot};
   const int64_t n[4] = {m, 3 * m, 3 * m, 4 * m};
   for (int a = 0; a < 4; ++a) {
-    SCT_TRY(dev_alloc(c, (void**)dst[a], n[a] * sizeof(float)));
+    SCT_TRY(stage_buf(c, a, n[a] * sizeof(float), (void**)dst[a]));
     SCT_CUDA_TRY(cudaMemcpyAsync(*dst[a], src[a], n[a] * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   }
   return SCT_OK;
-}
-static void free_cloud(Ctx* c, sct_cloud* d) {
-  dev_free(c, d->rho_raw);
-  dev_free(c, d->pos);
-  dev_free(c, d->scale_raw);
-  dev_free(c, d->rot);
 }
 
 int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scanner* scanner, const double* thetas,
                         int32_t n_views, const sct_raster_opts* opts, float* images_host, sct_fwd** state) {
   SCT_TRY(check_cloud(cloud_host));
   SCT_TRY(check_scanner(scanner));
+  if (n_views < 1) {
+    set_error("ConfigError: need at least one view");
+    return SCT_ERR_CONFIG;
+  }
   sct_cloud d;
   SCT_TRY(upload_cloud(c, cloud_host, &d));
   const size_t img = (size_t)n_views * scanner->det_res_px[0] * scanner->det_res_px[1];
   float* dimg = nullptr;
-  SCT_TRY(dev_alloc(c, (void**)&dimg, img * sizeof(float)));
+  SCT_TRY(stage_buf(c, 4, img * sizeof(float), (void**)&dimg));
   int rc = sct_render_fwd(c, &d, scanner, thetas, n_views, opts, dimg, state);
   if (rc == SCT_OK && images_host)
     if (cudaMemcpyAsync(images_host, dimg, img * sizeof(float), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) {
       set_error("CUDA error: image download");
       rc = SCT_ERR_CUDA;
     }
-  dev_free(c, dimg);
-  free_cloud(c, &d);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess && rc == SCT_OK) {
     set_error("CUDA error in sct_render_fwd_host");
     rc = SCT_ERR_CUDA;
@@ -623,14 +639,17 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
 
 int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, const float* dL_host,
                         sct_grads* grads_host, sct_stats* stats_host) {
-  if (!s || !grads_host) return SCT_ERR_CONFIG;
+  if (!s || !grads_host || !dL_host) {
+    set_error("ConfigError: null argument");
+    return SCT_ERR_CONFIG;
+  }
   SCT_TRY(check_cloud(cloud_host));
   sct_cloud d;
   SCT_TRY(upload_cloud(c, cloud_host, &d));
   const int64_t m = cloud_host->m;
   const size_t img = (size_t)s->n_views * s->det.w * s->det.h;
   float* ddl = nullptr;
-  SCT_TRY(dev_alloc(c, (void**)&ddl, img * sizeof(float)));
+  SCT_TRY(stage_buf(c, 5, img * sizeof(float), (void**)&ddl));
   SCT_CUDA_TRY(cudaMemcpyAsync(ddl, dL_host, img * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   // accumulate semantics: bring the caller's running sums to the device
   sct_grads dg;
@@ -638,42 +657,30 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
   float* gh[4] = {grads_host->rho_raw, grads_host->pos, grads_host->scale_raw, grads_host->rot};
   const int64_t n[4] = {m, 3 * m, 3 * m, 4 * m};
   for (int a = 0; a < 4; ++a) {
-    SCT_TRY(dev_alloc(c, (void**)gd[a], n[a] * sizeof(float)));
+    SCT_TRY(stage_buf(c, 6 + a, n[a] * sizeof(float), (void**)gd[a]));
     SCT_CUDA_TRY(cudaMemcpyAsync(*gd[a], gh[a], n[a] * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   }
   sct_stats dst{};
+  void* sh[3] = {};
+  void** sd[3] = {(void**)&dst.grad2d_norm_accum, (void**)&dst.grad_count, (void**)&dst.grad3d_accum};
+  const size_t sb[3] = {m * sizeof(float), m * sizeof(int32_t), 3 * m * sizeof(float)};
   if (stats_host) {
-    SCT_TRY(dev_alloc(c, (void**)&dst.grad2d_norm_accum, m * sizeof(float)));
-    SCT_TRY(dev_alloc(c, (void**)&dst.grad_count, m * sizeof(int32_t)));
-    SCT_TRY(dev_alloc(c, (void**)&dst.grad3d_accum, 3 * m * sizeof(float)));
-    SCT_CUDA_TRY(cudaMemcpyAsync(dst.grad2d_norm_accum, stats_host->grad2d_norm_accum, m * sizeof(float),
-                                 cudaMemcpyHostToDevice, c->stream));
-    SCT_CUDA_TRY(cudaMemcpyAsync(dst.grad_count, stats_host->grad_count, m * sizeof(int32_t),
-                                 cudaMemcpyHostToDevice, c->stream));
-    SCT_CUDA_TRY(cudaMemcpyAsync(dst.grad3d_accum, stats_host->grad3d_accum, 3 * m * sizeof(float),
-                                 cudaMemcpyHostToDevice, c->stream));
+    sh[0] = stats_host->grad2d_norm_accum;
+    sh[1] = stats_host->grad_count;
+    sh[2] = stats_host->grad3d_accum;
+    for (int a = 0; a < 3; ++a) {
+      SCT_TRY(stage_buf(c, 10 + a, sb[a], sd[a]));
+      SCT_CUDA_TRY(cudaMemcpyAsync(*sd[a], sh[a], sb[a], cudaMemcpyHostToDevice, c->stream));
+    }
   }
   int rc = sct_render_bwd(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr);
   if (rc == SCT_OK) {
     for (int a = 0; a < 4; ++a)
       SCT_CUDA_TRY(cudaMemcpyAsync(gh[a], *gd[a], n[a] * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-    if (stats_host) {
-      SCT_CUDA_TRY(cudaMemcpyAsync(stats_host->grad2d_norm_accum, dst.grad2d_norm_accum, m * sizeof(float),
-                                   cudaMemcpyDeviceToHost, c->stream));
-      SCT_CUDA_TRY(cudaMemcpyAsync(stats_host->grad_count, dst.grad_count, m * sizeof(int32_t),
-                                   cudaMemcpyDeviceToHost, c->stream));
-      SCT_CUDA_TRY(cudaMemcpyAsync(stats_host->grad3d_accum, dst.grad3d_accum, 3 * m * sizeof(float),
-                                   cudaMemcpyDeviceToHost, c->stream));
-    }
+    if (stats_host)
+      for (int a = 0; a < 3; ++a)
+        SCT_CUDA_TRY(cudaMemcpyAsync(sh[a], *sd[a], sb[a], cudaMemcpyDeviceToHost, c->stream));
   }
-  for (int a = 0; a < 4; ++a) dev_free(c, *gd[a]);
-  if (stats_host) {
-    dev_free(c, dst.grad2d_norm_accum);
-    dev_free(c, dst.grad_count);
-    dev_free(c, dst.grad3d_accum);
-  }
-  dev_free(c, ddl);
-  free_cloud(c, &d);
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return rc;
 }
@@ -790,15 +797,13 @@ int sct_voxelize_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_gri
   SCT_TRY(upload_cloud(c, cloud_host, &d));
   const size_t nv = (size_t)grid->dims[0] * grid->dims[1] * grid->dims[2];
   float* dv = nullptr;
-  SCT_TRY(dev_alloc(c, (void**)&dv, nv * sizeof(float)));
+  SCT_TRY(stage_buf(c, 13, nv * sizeof(float), (void**)&dv));
   int rc = sct_voxelize_fwd(c, &d, grid, cull, 0, INT32_MAX, dv);
   if (rc == SCT_OK)
     if (cudaMemcpyAsync(vol_host, dv, nv * sizeof(float), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) {
       set_error("CUDA error: volume download");
       rc = SCT_ERR_CUDA;
     }
-  dev_free(c, dv);
-  free_cloud(c, &d);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess && rc == SCT_OK) rc = SCT_ERR_CUDA;
   return rc;
 }

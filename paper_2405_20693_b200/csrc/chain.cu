@@ -24,39 +24,32 @@ namespace {
 
 constexpr int kItemOut = 11;  // g_rho, g_pos[3], g_sigma (xx yy zz xy xz yz), ndc_norm
 
-// d(J)/d(p_c) contracted with g_jac: sum_ab g_jac(a,b) * dJ/dp_c(a,b)
-// (rasterizer.cpp:162-191, :322-326)
-__device__ __forceinline__ double jac_contract(const dM3& gj, const DetParams& det, const double p[3], int c) {
-  const double x = p[0], y = p[1], z = p[2];
-  const double n = sqrt(x * x + y * y + z * z);
-  const double n3 = n * n * n;
-  if (c == 0)
-    return gj.m[0][2] * (-det.fx / (z * z)) + gj.m[2][0] * (1.0 / n - x * x / n3) + gj.m[2][1] * (-x * y / n3) +
-           gj.m[2][2] * (-x * z / n3);
-  if (c == 1)
-    return gj.m[1][2] * (-det.fy / (z * z)) + gj.m[2][0] * (-x * y / n3) + gj.m[2][1] * (1.0 / n - y * y / n3) +
-           gj.m[2][2] * (-y * z / n3);
-  return gj.m[0][0] * (-det.fx / (z * z)) + gj.m[0][2] * (2.0 * det.fx * x / (z * z * z)) +
-         gj.m[1][1] * (-det.fy / (z * z)) + gj.m[1][2] * (2.0 * det.fy * y / (z * z * z)) +
-         gj.m[2][0] * (-x * z / n3) + gj.m[2][1] * (-y * z / n3) + gj.m[2][2] * (1.0 / n - z * z / n3);
-}
+// Symmetric 3x3 as (xx, xy, xz, yy, yz, zz).
+struct Sym3 {
+  double xx, xy, xz, yy, yz, zz;
+};
 
+// K5 item chain. The projection chain is re-derived in FP64 as the reference
+// does (rasterizer.cpp:266-268) but written for the GPU: reciprocals computed
+// once (5 divisions instead of ~25), symmetric matrices kept as 6 values,
+// Sigma and rho read from the per-Gaussian prep record, FMAs allowed. The
+// math is the same chain as rasterizer.cpp:270-327; it does not feed binning,
+// so it need not be bit-identical to the preprocess.
 __global__ void __launch_bounds__(128) raster_chain_kernel(
-    long long m, long long n_items, double s_min, const float* __restrict__ rho_raw, const float* __restrict__ pos,
-    const float* __restrict__ scale_raw, const float* __restrict__ rot, const ViewParams* __restrict__ views,
-    DetParams det, RasterParams rp, const uint8_t* __restrict__ vis, const int32_t* __restrict__ offset,
-    const float4* __restrict__ pair_stats, float* __restrict__ out) {
+    long long m, long long n_items, const float* __restrict__ pos, const double* __restrict__ prep,
+    const ViewParams* __restrict__ views, DetParams det, RasterParams rp, const uint8_t* __restrict__ vis,
+    const int32_t* __restrict__ offset, const float4* __restrict__ pair_stats, float* __restrict__ out) {
   for (long long item = blockIdx.x * (long long)blockDim.x + threadIdx.x; item < n_items;
        item += (long long)gridDim.x * blockDim.x) {
     if (!vis[item]) continue;
     const long long v = item / m;
     const long long i = item - v * m;
-    // fixed-order reduction over the item's tiles
+    // fixed-order reduction over the item's tiles (rasterizer.cpp:245-257)
     double S0 = 0, S1x = 0, S1y = 0, Sxx = 0, Syy = 0, Sxy = 0;
     const int32_t p0 = offset[item], p1 = offset[item + 1];
     for (int32_t p = p0; p < p1; ++p) {
       const float4 a = pair_stats[2 * (long long)p];
-      const float4 b = pair_stats[2 * (long long)p + 1];
+      const float2 b = *reinterpret_cast<const float2*>(pair_stats + 2 * (long long)p + 1);
       S0 += a.x;
       S1x += a.y;
       S1y += a.z;
@@ -64,106 +57,149 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
       Syy += b.x;
       Sxy += b.y;
     }
-    const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
-    const ViewParams view = views[v];
-    dProj g;
-    d_project(k, view, det, rp, g);  // visible by construction (vis[item])
-    const dM2& q = g.conic;
-    // pixel value: amp * exp(-1/2 d^T Q d), d = x - p_hat   (rasterizer.cpp:277-281)
-    const double g_amp = S0;
-    const double gcx = g.amp * (q.m[0][0] * S1x + q.m[0][1] * S1y);
-    const double gcy = g.amp * (q.m[1][0] * S1x + q.m[1][1] * S1y);
-    dM2 gq;
-    gq.m[0][0] = -0.5 * g.amp * Sxx;
-    gq.m[0][1] = -0.5 * g.amp * Sxy;
-    gq.m[1][0] = -0.5 * g.amp * Sxy;
-    gq.m[1][1] = -0.5 * g.amp * Syy;
-    dM2 t, gs2;
+    const ViewParams& V = views[v];
+    const double* W = V.rot;
+    const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
+    const double* pr = prep + kPrepStride * i;
+    const Sym3 Sg{pr[0], pr[1], pr[2], pr[4], pr[5], pr[8]};
+    const double rho = pr[9];
+    const double x = fma(W[0], px, fma(W[1], py, W[2] * pz)) + V.t[0];
+    const double y = fma(W[3], px, fma(W[4], py, W[5] * pz)) + V.t[1];
+    const double z = fma(W[6], px, fma(W[7], py, W[8] * pz)) + V.t[2];
+    const double iz = 1.0 / z;
+    const double n = sqrt(fma(x, x, fma(y, y, z * z)));
+    const double in = 1.0 / n;
+    const double j00 = det.fx * iz, j11 = det.fy * iz;
+    const double j02 = -j00 * x * iz, j12 = -j11 * y * iz;
+    const double j20 = x * in, j21 = y * in, j22 = z * in;
+    // A = J W
+    double A[3][3];
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) t.m[a][b] = -q.m[a][0] * gq.m[0][b] + -q.m[a][1] * gq.m[1][b];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) gs2.m[a][b] = t.m[a][0] * q.m[0][b] + t.m[a][1] * q.m[1][b];
-    // low-pass (rasterizer.cpp:283-293)
-    double g_amp_pre = g_amp;
-    dM2 gs2r;
-    gs2r.m[0][0] = gs2r.m[0][1] = gs2r.m[1][0] = gs2r.m[1][1] = 0.0;
-    const dM2 inv_raw = d_inv2(g.s2r);
-    if (rp.dilation_compensation) {
-      g_amp_pre = g_amp * g.comp;
-      const double g_comp = g_amp * g.amp_pre;
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          gs2r.m[a][b] += g_comp * 0.5 * g.comp * inv_raw.m[a][b];
-          gs2.m[a][b] += g_comp * (-0.5) * g.comp * q.m[a][b];
-        }
+    for (int k = 0; k < 3; ++k) {
+      A[0][k] = fma(j00, W[k], j02 * W[6 + k]);
+      A[1][k] = fma(j11, W[3 + k], j12 * W[6 + k]);
+      A[2][k] = fma(j20, W[k], fma(j21, W[3 + k], j22 * W[6 + k]));
     }
+    // T = A Sigma, sigma_ray = T A^T (symmetric)
+    double T[3][3];
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) gs2r.m[a][b] += gs2.m[a][b];
+    for (int r = 0; r < 3; ++r) {
+      T[r][0] = fma(A[r][0], Sg.xx, fma(A[r][1], Sg.xy, A[r][2] * Sg.xz));
+      T[r][1] = fma(A[r][0], Sg.xy, fma(A[r][1], Sg.yy, A[r][2] * Sg.yz));
+      T[r][2] = fma(A[r][0], Sg.xz, fma(A[r][1], Sg.yz, A[r][2] * Sg.zz));
+    }
+    auto dot3 = [](const double* a, const double* b) { return fma(a[0], b[0], fma(a[1], b[1], a[2] * b[2])); };
+    const Sym3 R{dot3(T[0], A[0]), dot3(T[0], A[1]), dot3(T[0], A[2]), dot3(T[1], A[1]), dot3(T[1], A[2]),
+                 dot3(T[2], A[2])};
+    const double d2r = fma(R.xx, R.yy, -R.xy * R.xy);
+    const double c00 = fma(R.yy, R.zz, -R.yz * R.yz), c01 = fma(R.xz, R.yz, -R.xy * R.zz),
+                 c02 = fma(R.xy, R.yz, -R.xz * R.yy);
+    const double d3 = fma(R.xx, c00, fma(R.xy, c01, R.xz * c02));
+    const double id2r = 1.0 / d2r;
+    const double mu = sqrt(2.0 * kPi * d3 * id2r);
+    const double amp_pre = (rp.mode == SCT_MODE_RECTIFIED) ? mu * rho : rho;
+    const double s00 = R.xx + rp.eps2, s11 = R.yy + rp.eps2, s01 = R.xy;
+    const double id2 = 1.0 / fma(s00, s11, -s01 * s01);
+    const double comp = rp.dilation_compensation ? sqrt(d2r * id2) : 1.0;
+    const double amp = amp_pre * comp;
+    const double q00 = s11 * id2, q01 = -s01 * id2, q11 = s00 * id2;  // conic
+    // rasterizer.cpp:277-281
+    const double gcx = amp * fma(q00, S1x, q01 * S1y);
+    const double gcy = amp * fma(q01, S1x, q11 * S1y);
+    // g_sigma2 = -Q g_Q Q = 1/2 amp Q S2 Q
+    const double h = 0.5 * amp;
+    const double u00 = fma(q00, Sxx, q01 * Sxy), u01 = fma(q00, Sxy, q01 * Syy);
+    const double u10 = fma(q01, Sxx, q11 * Sxy), u11 = fma(q01, Sxy, q11 * Syy);
+    double g00 = h * fma(u00, q00, u01 * q01);
+    double g01 = h * fma(u00, q01, u01 * q11);
+    double g11 = h * fma(u10, q01, u11 * q11);
+    // low-pass (rasterizer.cpp:283-293)
+    const double ir00 = R.yy * id2r, ir01 = -R.xy * id2r, ir11 = R.xx * id2r;  // sigma2_raw^-1
+    double r00 = 0.0, r01 = 0.0, r11 = 0.0;
+    double g_amp_pre = S0;
+    if (rp.dilation_compensation) {
+      g_amp_pre = S0 * comp;
+      const double gc = S0 * amp_pre * comp * 0.5;
+      r00 = gc * ir00;
+      r01 = gc * ir01;
+      r11 = gc * ir11;
+      g00 -= gc * q00;
+      g01 -= gc * q01;
+      g11 -= gc * q11;
+    }
+    r00 += g00;
+    r01 += g01;
+    r11 += g11;
     // amplitude chain (rasterizer.cpp:295-306)
-    dM3 G = d_zero3();
+    Sym3 G{0, 0, 0, 0, 0, 0};
     double g_rho;
     if (rp.mode == SCT_MODE_RECTIFIED) {
-      g_rho = g_amp_pre * g.mu;
-      const double g_mu = g_amp_pre * g.rho;
-      const dM3 inv_ray = d_inv3(g.sigma_ray);
-      const double c3 = g_mu * 0.5 * g.mu, c2 = g_mu * (-0.5) * g.mu;
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) G.m[a][b] += c3 * inv_ray.m[a][b];
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) gs2r.m[a][b] += c2 * inv_raw.m[a][b];
+      g_rho = g_amp_pre * mu;
+      const double hm = 0.5 * g_amp_pre * rho * mu;
+      const double c3 = hm / d3;
+      const double c11 = fma(R.xx, R.zz, -R.xz * R.xz), c12 = fma(R.xy, R.xz, -R.xx * R.yz),
+                   c22 = fma(R.xx, R.yy, -R.xy * R.xy);
+      G = Sym3{c3 * c00, c3 * c01, c3 * c02, c3 * c11, c3 * c12, c3 * c22};
+      r00 -= hm * ir00;
+      r01 -= hm * ir01;
+      r11 -= hm * ir11;
     } else {
       g_rho = g_amp_pre;
     }
+    G.xx += r00;
+    G.xy += r01;
+    G.yy += r11;
+    // sigma_ray = A Sigma A^T (rasterizer.cpp:308-311): U = G A, g_sigma = A^T U
+    double U[3][3];
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) G.m[a][b] += gs2r.m[a][b];
-    // sigma_ray = A Sigma A^T (rasterizer.cpp:308-311)
-    const dM3 gsig = d_mul(d_mul_at(g.a, G), g.a);
-    // centre chain + dJ/dp chain (rasterizer.cpp:313-327)
-    const double zc = g.ps[2];
-    double gp[3];
-    gp[0] = (det.fx / zc) * gcx;
-    gp[1] = (det.fy / zc) * gcy;
-    gp[2] = (-det.fx * g.ps[0] / (zc * zc)) * gcx + (-det.fy * g.ps[1] / (zc * zc)) * gcy;
-    if (!rp.freeze_jacobian) {
-      const dM3 g_a = d_mul(d_mul(d_add_t(G), g.a), g.sigma);
-      dM3 W;
-#pragma unroll
-      for (int a = 0; a < 9; ++a) W.m[a / 3][a % 3] = view.rot[a];
-      const dM3 g_jac = d_mul_bt(g_a, W);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) gp[c] += jac_contract(g_jac, det, g.ps, c);
+    for (int k = 0; k < 3; ++k) {
+      U[0][k] = fma(G.xx, A[0][k], fma(G.xy, A[1][k], G.xz * A[2][k]));
+      U[1][k] = fma(G.xy, A[0][k], fma(G.yy, A[1][k], G.yz * A[2][k]));
+      U[2][k] = fma(G.xz, A[0][k], fma(G.yz, A[1][k], G.zz * A[2][k]));
     }
-    double gpos[3];
+    auto col = [&](int a, int b) { return fma(A[0][a], U[0][b], fma(A[1][a], U[1][b], A[2][a] * U[2][b])); };
+    const Sym3 gS{col(0, 0), 0.5 * (col(0, 1) + col(1, 0)), 0.5 * (col(0, 2) + col(2, 0)), col(1, 1),
+                  0.5 * (col(1, 2) + col(2, 1)), col(2, 2)};
+    // centre chain (rasterizer.cpp:313-321)
+    double gp0 = j00 * gcx, gp1 = j11 * gcy, gp2 = fma(j02, gcx, j12 * gcy);
+    if (!rp.freeze_jacobian) {
+      // g_A = (G + G^T) A Sigma = 2 U Sigma; g_J = g_A W^T (rasterizer.cpp:310,322-326)
+      double gA[3][3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-      gpos[a] = view.rot[0 * 3 + a] * gp[0] + view.rot[1 * 3 + a] * gp[1] + view.rot[2 * 3 + a] * gp[2];
+      for (int r = 0; r < 3; ++r) {
+        gA[r][0] = 2.0 * fma(U[r][0], Sg.xx, fma(U[r][1], Sg.xy, U[r][2] * Sg.xz));
+        gA[r][1] = 2.0 * fma(U[r][0], Sg.xy, fma(U[r][1], Sg.yy, U[r][2] * Sg.yz));
+        gA[r][2] = 2.0 * fma(U[r][0], Sg.xz, fma(U[r][1], Sg.yz, U[r][2] * Sg.zz));
+      }
+      double gJ[3][3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gJ[r][c] = fma(gA[r][0], W[3 * c], fma(gA[r][1], W[3 * c + 1], gA[r][2] * W[3 * c + 2]));
+      // dJ/dp contractions (jacobian_derivative, rasterizer.cpp:162-191)
+      const double in3 = in * in * in;
+      const double fz2 = det.fx * iz * iz, gz2 = det.fy * iz * iz;
+      gp0 += -gJ[0][2] * fz2 + gJ[2][0] * (in - x * x * in3) - gJ[2][1] * x * y * in3 - gJ[2][2] * x * z * in3;
+      gp1 += -gJ[1][2] * gz2 - gJ[2][0] * x * y * in3 + gJ[2][1] * (in - y * y * in3) - gJ[2][2] * y * z * in3;
+      gp2 += -gJ[0][0] * fz2 + gJ[0][2] * 2.0 * fz2 * x * iz - gJ[1][1] * gz2 + gJ[1][2] * 2.0 * gz2 * y * iz -
+             gJ[2][0] * x * z * in3 - gJ[2][1] * y * z * in3 + gJ[2][2] * (in - z * z * in3);
+    }
+    // g_pos = W^T g_ps (rasterizer.cpp:327)
+    const double gx = fma(W[0], gp0, fma(W[3], gp1, W[6] * gp2));
+    const double gy = fma(W[1], gp0, fma(W[4], gp1, W[7] * gp2));
+    const double gz = fma(W[2], gp0, fma(W[5], gp1, W[8] * gp2));
     const double nx = gcx * 0.5 * det.w, ny = gcy * 0.5 * det.h;
-    // item outputs, [kItemOut][n_items]
     out[0 * n_items + item] = (float)g_rho;
-    out[1 * n_items + item] = (float)gpos[0];
-    out[2 * n_items + item] = (float)gpos[1];
-    out[3 * n_items + item] = (float)gpos[2];
-    out[4 * n_items + item] = (float)gsig.m[0][0];
-    out[5 * n_items + item] = (float)gsig.m[1][1];
-    out[6 * n_items + item] = (float)gsig.m[2][2];
-    out[7 * n_items + item] = (float)(0.5 * (gsig.m[0][1] + gsig.m[1][0]));
-    out[8 * n_items + item] = (float)(0.5 * (gsig.m[0][2] + gsig.m[2][0]));
-    out[9 * n_items + item] = (float)(0.5 * (gsig.m[1][2] + gsig.m[2][1]));
-    out[10 * n_items + item] = (float)sqrt(nx * nx + ny * ny);
+    out[1 * n_items + item] = (float)gx;
+    out[2 * n_items + item] = (float)gy;
+    out[3 * n_items + item] = (float)gz;
+    out[4 * n_items + item] = (float)gS.xx;
+    out[5 * n_items + item] = (float)gS.yy;
+    out[6 * n_items + item] = (float)gS.zz;
+    out[7 * n_items + item] = (float)gS.xy;
+    out[8 * n_items + item] = (float)gS.xz;
+    out[9 * n_items + item] = (float)gS.yz;
+    out[10 * n_items + item] = (float)sqrt(fma(nx, nx, ny * ny));
   }
 }
 
@@ -317,8 +353,8 @@ void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const fl
   {
     KScope _ks(c, "K5_raster_chain");
     raster_chain_kernel<<<grid_cap(c, s->n_items, 128), 128, 0, c->stream>>>(
-        s->m, s->n_items, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, s->d_views, s->det, s->rp, s->d_vis,
-        s->d_offset, pair_stats, item_grads);
+        s->m, s->n_items, cl.pos, s->d_prep, s->d_views, s->det, s->rp, s->d_vis, s->d_offset, pair_stats,
+        item_grads);
   }
 }
 

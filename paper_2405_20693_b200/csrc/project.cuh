@@ -22,12 +22,14 @@ struct dProj {
   double comp, rho, amp_pre;
 };
 
-__device__ __forceinline__ bool d_project(const dKernel& k, const ViewParams& v, const DetParams& det,
-                                          const RasterParams& rp, dProj& o) {
+// p: kernel position; sigma: its 3D covariance (d_covariance, bit-identical
+// whether recomputed or read from the per-Gaussian prep buffer); rho: act_density.
+__device__ __forceinline__ bool d_project(const double p[3], const dM3& sigma, double rho, const ViewParams& v,
+                                          const DetParams& det, const RasterParams& rp, dProj& o) {
   double ps[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    ps[i] = v.rot[3 * i + 0] * k.p[0] + v.rot[3 * i + 1] * k.p[1] + v.rot[3 * i + 2] * k.p[2];
+    ps[i] = v.rot[3 * i + 0] * p[0] + v.rot[3 * i + 1] * p[1] + v.rot[3 * i + 2] * p[2];
     ps[i] = ps[i] + v.t[i];
   }
   if (ps[2] < det.near_clip) return false;
@@ -47,7 +49,6 @@ __device__ __forceinline__ bool d_project(const dKernel& k, const ViewParams& v,
 #pragma unroll
   for (int i = 0; i < 9; ++i) W.m[i / 3][i % 3] = v.rot[i];
   const dM3 a = d_mul(jac, W);
-  const dM3 sigma = d_covariance(k);
   const dM3 sigma_ray = d_mul_bt(d_mul(a, sigma), a);
   dM2 s2r;
   s2r.m[0][0] = sigma_ray.m[0][0];
@@ -56,7 +57,6 @@ __device__ __forceinline__ bool d_project(const dKernel& k, const ViewParams& v,
   s2r.m[1][1] = sigma_ray.m[1][1];
   const double d3 = d_det3(sigma_ray);
   const double d2r = d_det2(s2r);
-  const double rho = d_act_density(k.rho_raw);
   const double mu = sqrt(2.0 * kPi * d3 / d2r);
   double amp = (rp.mode == SCT_MODE_RECTIFIED) ? mu * rho : rho;
   const double amp_pre = amp;

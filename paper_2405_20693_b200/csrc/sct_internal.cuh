@@ -15,6 +15,7 @@ constexpr int kTilePx = 16;   // common.hpp:24 kImageTilePx
 constexpr int kTileVox = 8;   // common.hpp:25 kVolumeTileVox
 constexpr double kLog2e = 1.4426950408889634;
 constexpr double kPi = 3.14159265358979323846;  // M_PI
+constexpr int kPrepStride = 10;  // per-Gaussian prep record: Sigma (9 doubles) + rho
 
 // ------------------------------------------------------------------ errors
 void set_error(const std::string& msg);
@@ -90,7 +91,13 @@ struct Ctx {
   size_t cub_tmp_bytes = 0;
   int64_t* pinned_count = nullptr;  // small pinned host word for D2H of counts
   int sm_count = 148;
+  // grow-only device staging buffers of the host-buffer entry points (a
+  // context serialises its calls, so a slot is free again at the next call)
+  static constexpr int kStageSlots = 16;
+  void* stage[kStageSlots] = {};
+  size_t stage_bytes[kStageSlots] = {};
 };
+int stage_buf(Ctx* c, int slot, size_t bytes, void** p);
 
 int ensure_cub_tmp(Ctx* c, size_t bytes);
 
@@ -131,6 +138,7 @@ struct sct_fwd {
   uint32_t* d_keys = nullptr;          // [pairs] sorted (view,tile) keys
   int32_t* d_vals = nullptr;           // [pairs] sorted item index
   int2* d_ranges = nullptr;            // [V*T] [start,end) into sorted pairs
+  double* d_prep = nullptr;            // [m][kPrepStride] Sigma (9) + rho, FP64
 };
 
 struct sct_ctx : public sct::Ctx {};
@@ -138,8 +146,9 @@ struct sct_ctx : public sct::Ctx {};
 // ------------------------------------------------------------------ kernel entry points
 namespace sct {
 // binning preprocess (FP64, compiled with -fmad=false: bit-exact vs oracle)
-void launch_raster_preprocess(Ctx* c, const sct_cloud& cl, const ViewParams* d_views, int n_views,
-                              const DetParams& det, const RasterParams& rp, float4* rec, short4* rect,
+void launch_gauss_prep(Ctx* c, const sct_cloud& cl, double* prep);
+void launch_raster_preprocess(Ctx* c, const sct_cloud& cl, const double* prep, const ViewParams* d_views,
+                              int n_views, const DetParams& det, const RasterParams& rp, float4* rec, short4* rect,
                               int32_t* count, uint8_t* vis);
 void launch_voxel_preprocess(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull, int32_t zb0,
                              int32_t zb1, int32_t bricks_x, int32_t bricks_y, float4* rec, short4* rect_lo,

@@ -63,3 +63,31 @@ t0 = time.perf_counter()
 x.copy_(dL.view(-1), non_blocking=True)
 torch.cuda.synchronize()
 print(f"torch H2D 78.6MB {1e3*(time.perf_counter()-t0):.2f} ms")
+
+# long loops: per-step wall times of the host path and the device path
+import subprocess
+smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,clocks_event_reasons.active",
+                        "--format=csv,noheader", "-lms", "100"], stdout=subprocess.PIPE, text=True)
+hw = []
+for it in range(30):
+    st = C.c_void_p()
+    t0 = time.perf_counter()
+    L.sct_render_fwd_host(eng._h, C.byref(cl), C.byref(sc), th, 75, C.byref(op), C.c_void_p(imgs.data_ptr()),
+                          C.byref(st))
+    L.sct_render_bwd_host(eng._h, st, C.byref(cl), C.c_void_p(dL.data_ptr()), C.byref(g), None)
+    L.sct_fwd_free(st)
+    hw.append(round(1e3 * (time.perf_counter() - t0), 1))
+print("host path per step ms:", hw)
+dw = []
+for it in range(30):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    f = eng.render(cloud, scn, thetas)
+    eng.render_backward(cloud, f, dd, gr)
+    f.free()
+    torch.cuda.synchronize()
+    dw.append(round(1e3 * (time.perf_counter() - t0), 1))
+print("device path per step ms:", dw)
+smi.terminate()
+out = smi.communicate()[0].strip().splitlines()
+print("smi samples:", len(out), out[:3], out[-3:])
