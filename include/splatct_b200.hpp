@@ -1,0 +1,337 @@
+// splatct_b200.hpp — header-only C++ mirror of the reference's host API for
+// the hot path, implemented over the C ABI (splatct_gpu.h, host-buffer entry
+// points). Same names, argument meaning, accumulate semantics and exception
+// types as /root/reference/proj/core/include/splatct/{rasterizer,voxelizer,
+// objectives,gaussian_cloud,geometry}.hpp; Eigen vectors are replaced by
+// std::array so the header has no third-party dependency.
+//
+//   render            rasterizer.hpp:53-54      render_backward  rasterizer.hpp:61-64
+//   voxelize          voxelizer.hpp:60-61       voxelize_backward voxelizer.hpp:65-67
+//   tv3d_loss         objectives.hpp:31         grid_for_extent  voxelizer.hpp:26-27
+//
+// Link with -lsplatct_b200 (paper_2405_20693_b200/libsplatct_b200.so).
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "splatct_gpu.h"
+
+namespace splatct_b200 {
+
+// ---- exceptions (common.hpp:27-64) ------------------------------------------
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DataError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DimMismatch : DataError {
+  using DataError::DataError;
+};
+struct DivergenceDetected : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == SCT_OK) return;
+  const std::string msg = sct_last_error();
+  switch (rc) {
+    case SCT_ERR_CONFIG: throw ConfigError(msg);
+    case SCT_ERR_DATA:
+      if (msg.rfind("DimMismatch", 0) == 0) throw DimMismatch(msg);
+      throw DataError(msg);
+    case SCT_ERR_DIVERGENCE: throw DivergenceDetected(msg);
+    case SCT_ERR_CUDA: throw CudaError(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+// ---- types -------------------------------------------------------------------
+using Vec2 = std::array<double, 2>;
+using Vec3 = std::array<double, 3>;
+
+struct ScannerConfig {  // geometry.hpp:12-31
+  double l_so_mm = 8.0;
+  double l_sd_mm = 12.0;
+  Vec2 detector_size_mm{5.6, 5.6};
+  std::array<int, 2> detector_res_px{128, 128};
+  std::vector<double> angles_rad;
+  Vec3 extent_min_mm{-1.0, -1.0, -1.0};
+  Vec3 extent_max_mm{1.0, 1.0, 1.0};
+  double near_clip_mm = 0.0;
+
+  sct_scanner c() const {
+    sct_scanner s{};
+    s.l_so_mm = l_so_mm;
+    s.l_sd_mm = l_sd_mm;
+    for (int k = 0; k < 2; ++k) {
+      s.det_size_mm[k] = detector_size_mm[k];
+      s.det_res_px[k] = detector_res_px[k];
+    }
+    for (int k = 0; k < 3; ++k) {
+      s.extent_min_mm[k] = extent_min_mm[k];
+      s.extent_max_mm[k] = extent_max_mm[k];
+    }
+    s.near_clip_mm = near_clip_mm;
+    return s;
+  }
+};
+
+inline std::vector<double> full_circle_angles(int n) {  // geometry.cpp:63-67
+  std::vector<double> a(n);
+  for (int i = 0; i < n; ++i) a[i] = 2.0 * M_PI * i / n;
+  return a;
+}
+
+enum class RenderMode { kRectified, kBiased };
+
+struct RasterOptions {  // rasterizer.hpp:15-21
+  RenderMode mode = RenderMode::kRectified;
+  double lowpass_eps_px = 0.3;
+  bool dilation_compensation = true;
+  bool freeze_jacobian = false;
+  double cull_mahalanobis = 3.0348542587702925;
+
+  sct_raster_opts c() const {
+    sct_raster_opts o{};
+    o.mode = mode == RenderMode::kRectified ? SCT_MODE_RECTIFIED : SCT_MODE_BIASED;
+    o.lowpass_eps_px = lowpass_eps_px;
+    o.dilation_compensation = dilation_compensation;
+    o.freeze_jacobian = freeze_jacobian;
+    o.cull_mahalanobis = cull_mahalanobis;
+    return o;
+  }
+};
+
+// Raw parameters in the reference's SoA layout (gaussian_cloud.hpp:62-77).
+struct GaussianCloud {
+  double s_min_mm = 1e-4;
+  std::vector<double> rho_raw, pos, scale_raw, rot;
+  std::vector<double> grad2d_norm_accum;
+  std::vector<int> grad_count;
+  std::vector<double> grad3d_accum;
+  int size() const { return static_cast<int>(rho_raw.size()); }
+  double s_min() const { return s_min_mm; }
+};
+
+struct CloudGrads {  // gaussian_cloud.hpp:84-96
+  std::vector<double> rho_raw, pos, scale_raw, rot;
+  void resize(int m) {
+    rho_raw.assign(m, 0.0);
+    pos.assign(3 * static_cast<size_t>(m), 0.0);
+    scale_raw.assign(3 * static_cast<size_t>(m), 0.0);
+    rot.assign(4 * static_cast<size_t>(m), 0.0);
+  }
+};
+
+struct Image {  // common.hpp:66-79
+  int width = 0, height = 0;
+  std::vector<double> data;
+  Image() = default;
+  Image(int w, int h, double fill = 0.0) : width(w), height(h), data(static_cast<size_t>(w) * h, fill) {}
+  double at(int u, int v) const { return data[static_cast<size_t>(v) * width + u]; }
+  double& at(int u, int v) { return data[static_cast<size_t>(v) * width + u]; }
+};
+
+struct GridSpec {  // voxelizer.hpp:13-24
+  std::array<int, 3> dims{0, 0, 0};
+  Vec3 origin_mm{0, 0, 0};
+  Vec3 spacing_mm{1, 1, 1};
+  size_t voxel_count() const { return static_cast<size_t>(dims[0]) * dims[1] * dims[2]; }
+  sct_grid c() const {
+    sct_grid g{};
+    for (int k = 0; k < 3; ++k) {
+      g.dims[k] = dims[k];
+      g.origin_mm[k] = origin_mm[k];
+      g.spacing_mm[k] = spacing_mm[k];
+    }
+    return g;
+  }
+};
+
+inline GridSpec grid_for_extent(const Vec3& lo, const Vec3& hi, const std::array<int, 3>& dims) {
+  GridSpec g;  // voxelizer.cpp:8-14
+  g.dims = dims;
+  g.origin_mm = lo;
+  for (int k = 0; k < 3; ++k) g.spacing_mm[k] = (hi[k] - lo[k]) / static_cast<double>(dims[k]);
+  return g;
+}
+
+struct DensityVolume {  // voxelizer.hpp:29-48
+  std::array<int, 3> dims{0, 0, 0};
+  Vec3 origin_mm{0, 0, 0}, spacing_mm{1, 1, 1};
+  std::vector<double> data;
+  GridSpec grid() const { return {dims, origin_mm, spacing_mm}; }
+  size_t index(int x, int y, int z) const { return (static_cast<size_t>(z) * dims[1] + y) * dims[0] + x; }
+  double at(int x, int y, int z) const { return data[index(x, y, z)]; }
+};
+
+struct VoxelizeOptions {  // voxelizer.hpp:53-57
+  double cull_mahalanobis = 3.3681993876652464;
+};
+
+// ---- engine context (one per thread; the reference's calls are synchronous) --
+class Context {
+ public:
+  static Context& get() {
+    thread_local Context ctx;
+    return ctx;
+  }
+  sct_ctx* handle() { return ctx_; }
+  ~Context() {
+    if (ctx_) sct_ctx_destroy(ctx_);
+  }
+
+ private:
+  Context() { check(sct_ctx_create(0, nullptr, &ctx_)); }
+  sct_ctx* ctx_ = nullptr;
+};
+
+// fp32 staging of a cloud in the reference's field order
+struct CloudF32 {
+  std::vector<float> rho_raw, pos, scale_raw, rot;
+  sct_cloud c{};
+  explicit CloudF32(const GaussianCloud& g) {
+    auto cv = [](const std::vector<double>& v) { return std::vector<float>(v.begin(), v.end()); };
+    rho_raw = cv(g.rho_raw);
+    pos = cv(g.pos);
+    scale_raw = cv(g.scale_raw);
+    rot = cv(g.rot);
+    c.m = g.size();
+    c.s_min_mm = g.s_min_mm;
+    c.rho_raw = rho_raw.data();
+    c.pos = pos.data();
+    c.scale_raw = scale_raw.data();
+    c.rot = rot.data();
+  }
+};
+
+struct GradsF32 {
+  std::vector<float> rho_raw, pos, scale_raw, rot;
+  sct_grads c{};
+  explicit GradsF32(const CloudGrads& g) {
+    auto cv = [](const std::vector<double>& v) { return std::vector<float>(v.begin(), v.end()); };
+    rho_raw = cv(g.rho_raw);
+    pos = cv(g.pos);
+    scale_raw = cv(g.scale_raw);
+    rot = cv(g.rot);
+    c.rho_raw = rho_raw.data();
+    c.pos = pos.data();
+    c.scale_raw = scale_raw.data();
+    c.rot = rot.data();
+  }
+  void store(CloudGrads& g) const {
+    g.rho_raw.assign(rho_raw.begin(), rho_raw.end());
+    g.pos.assign(pos.begin(), pos.end());
+    g.scale_raw.assign(scale_raw.begin(), scale_raw.end());
+    g.rot.assign(rot.begin(), rot.end());
+  }
+};
+
+// RenderedProjection (rasterizer.hpp:41-51): image + the device forward state.
+struct RenderedProjection {
+  Image image;
+  int tiles_x = 0, tiles_y = 0;
+  std::shared_ptr<sct_fwd> state;
+  // tile_visible expressed in kernel indices (visible[vi].kernel_index)
+  std::vector<std::vector<int>> tile_kernels() const {
+    const int T = tiles_x * tiles_y;
+    std::vector<int64_t> off(T + 1);
+    check(sct_fwd_tile_lists(state.get(), 0, off.data(), nullptr));
+    std::vector<int32_t> idx(off[T] > 0 ? off[T] : 1);
+    check(sct_fwd_tile_lists(state.get(), 0, off.data(), idx.data()));
+    std::vector<std::vector<int>> out(T);
+    for (int t = 0; t < T; ++t) out[t].assign(idx.begin() + off[t], idx.begin() + off[t + 1]);
+    return out;
+  }
+};
+
+// ---- the hot path --------------------------------------------------------------
+inline RenderedProjection render(const GaussianCloud& cloud, const ScannerConfig& config, double theta_rad,
+                                 const RasterOptions& opts = {}) {
+  CloudF32 cf(cloud);
+  const sct_scanner sc = config.c();
+  const sct_raster_opts op = opts.c();
+  const int w = config.detector_res_px[0], h = config.detector_res_px[1];
+  std::vector<float> img(static_cast<size_t>(w) * h);
+  sct_fwd* st = nullptr;
+  check(sct_render_fwd_host(Context::get().handle(), &cf.c, &sc, &theta_rad, 1, &op, img.data(), &st));
+  RenderedProjection r;
+  r.state = std::shared_ptr<sct_fwd>(st, [](sct_fwd* p) { sct_fwd_free(p); });
+  r.image = Image(w, h);
+  r.image.data.assign(img.begin(), img.end());
+  r.tiles_x = (w + 15) / 16;
+  r.tiles_y = (h + 15) / 16;
+  return r;
+}
+
+inline void render_backward(GaussianCloud& cloud, const ScannerConfig& config, double /*theta_rad*/,
+                            const RenderedProjection& fwd, const Image& dL_dimage, CloudGrads& grads,
+                            const RasterOptions& /*opts*/ = {}, bool accumulate_stats = false) {
+  if (dL_dimage.width != config.detector_res_px[0] || dL_dimage.height != config.detector_res_px[1])
+    throw DimMismatch("render_backward: upstream gradient dims mismatch");
+  const int m = cloud.size();
+  if (static_cast<int>(grads.rho_raw.size()) != m) throw DimMismatch("render_backward: grads not sized");
+  CloudF32 cf(cloud);
+  GradsF32 gf(grads);
+  std::vector<float> dl(dL_dimage.data.begin(), dL_dimage.data.end());
+  std::vector<float> s_norm, s_3d;
+  std::vector<int32_t> s_cnt;
+  sct_stats st{};
+  if (accumulate_stats) {
+    if (cloud.grad2d_norm_accum.size() != static_cast<size_t>(m)) {
+      cloud.grad2d_norm_accum.assign(m, 0.0);
+      cloud.grad_count.assign(m, 0);
+      cloud.grad3d_accum.assign(3 * static_cast<size_t>(m), 0.0);
+    }
+    s_norm.assign(cloud.grad2d_norm_accum.begin(), cloud.grad2d_norm_accum.end());
+    s_cnt.assign(cloud.grad_count.begin(), cloud.grad_count.end());
+    s_3d.assign(cloud.grad3d_accum.begin(), cloud.grad3d_accum.end());
+    st.grad2d_norm_accum = s_norm.data();
+    st.grad_count = s_cnt.data();
+    st.grad3d_accum = s_3d.data();
+  }
+  check(sct_render_bwd_host(Context::get().handle(), fwd.state.get(), &cf.c, dl.data(), &gf.c,
+                            accumulate_stats ? &st : nullptr));
+  gf.store(grads);
+  if (accumulate_stats) {
+    cloud.grad2d_norm_accum.assign(s_norm.begin(), s_norm.end());
+    cloud.grad_count.assign(s_cnt.begin(), s_cnt.end());
+    cloud.grad3d_accum.assign(s_3d.begin(), s_3d.end());
+  }
+}
+
+inline DensityVolume voxelize(const GaussianCloud& cloud, const GridSpec& grid, const VoxelizeOptions& opts = {}) {
+  CloudF32 cf(cloud);
+  const sct_grid g = grid.c();
+  std::vector<float> vol(grid.voxel_count());
+  check(sct_voxelize_fwd_host(Context::get().handle(), &cf.c, &g, opts.cull_mahalanobis, vol.data()));
+  DensityVolume v;
+  v.dims = grid.dims;
+  v.origin_mm = grid.origin_mm;
+  v.spacing_mm = grid.spacing_mm;
+  v.data.assign(vol.begin(), vol.end());
+  return v;
+}
+
+inline void voxelize_backward(const GaussianCloud& cloud, const GridSpec& grid, const DensityVolume& dL_dV,
+                              CloudGrads& grads, const VoxelizeOptions& opts = {}) {
+  if (dL_dV.dims != grid.dims) throw DimMismatch("voxelize_backward: gradient volume dims mismatch");
+  CloudF32 cf(cloud);
+  GradsF32 gf(grads);
+  const sct_grid g = grid.c();
+  std::vector<float> dl(dL_dV.data.begin(), dL_dV.data.end());
+  check(sct_voxelize_bwd_host(Context::get().handle(), &cf.c, &g, opts.cull_mahalanobis, dl.data(), &gf.c));
+  gf.store(grads);
+}
+
+}  // namespace splatct_b200

@@ -184,6 +184,9 @@ int sct_voxel_work(sct_ctx* ctx, const sct_cloud* cloud, const sct_grid* grid, d
                    int64_t* vge, int64_t* n_pairs);
 int sct_voxelize_fwd_host(sct_ctx* ctx, const sct_cloud* cloud_host, const sct_grid* grid,
                           double cull_mahalanobis, float* vol_host);
+/* grads_host accumulate (+=), like voxelize_backward (voxelizer.cpp:140-224) */
+int sct_voxelize_bwd_host(sct_ctx* ctx, const sct_cloud* cloud_host, const sct_grid* grid,
+                          double cull_mahalanobis, const float* dL_dvol_host, sct_grads* grads_host);
 
 /* ---- objectives / optimizer -------------------------------------------- */
 /* TV value (device double [1], written) and lambda-scaled gradient (device, overwritten). */

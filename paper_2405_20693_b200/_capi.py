@@ -81,6 +81,7 @@ SIGNATURES = {
                                    P(sct_grads)]),
     "sct_voxel_bins": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, I64, I64, I32]),
     "sct_voxelize_fwd_host": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, VP]),
+    "sct_voxelize_bwd_host": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, VP, P(sct_grads)]),
     "sct_tv3d": (C.c_int, [VP, VP, I32, C.c_float, VP, VP]),
     "sct_photometric_loss": (C.c_int, [VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float,
                                        C.c_float, VP, VP]),

@@ -808,6 +808,37 @@ int sct_voxelize_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_gri
   return rc;
 }
 
+int sct_voxelize_bwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_grid* grid, double cull,
+                          const float* dL_host, sct_grads* grads_host) {
+  SCT_TRY(check_cloud(cloud_host));
+  SCT_TRY(check_grid(grid));
+  if (!dL_host || !grads_host) {
+    set_error("ConfigError: null argument");
+    return SCT_ERR_CONFIG;
+  }
+  sct_cloud d;
+  SCT_TRY(upload_cloud(c, cloud_host, &d));
+  const int64_t m = cloud_host->m;
+  const size_t nv = (size_t)grid->dims[0] * grid->dims[1] * grid->dims[2];
+  float* ddl = nullptr;
+  SCT_TRY(stage_buf(c, 13, nv * sizeof(float), (void**)&ddl));
+  SCT_CUDA_TRY(cudaMemcpyAsync(ddl, dL_host, nv * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  sct_grads dg;
+  float** gd[4] = {&dg.rho_raw, &dg.pos, &dg.scale_raw, &dg.rot};
+  float* gh[4] = {grads_host->rho_raw, grads_host->pos, grads_host->scale_raw, grads_host->rot};
+  const int64_t n[4] = {m, 3 * m, 3 * m, 4 * m};
+  for (int a = 0; a < 4; ++a) {
+    SCT_TRY(stage_buf(c, 6 + a, n[a] * sizeof(float), (void**)gd[a]));
+    SCT_CUDA_TRY(cudaMemcpyAsync(*gd[a], gh[a], n[a] * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  }
+  int rc = sct_voxelize_bwd(c, &d, grid, cull, 0, INT32_MAX, ddl, &dg);
+  if (rc == SCT_OK)
+    for (int a = 0; a < 4; ++a)
+      SCT_CUDA_TRY(cudaMemcpyAsync(gh[a], *gd[a], n[a] * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return rc;
+}
+
 // ------------------------------------------------------------------ objectives / optimizer
 int sct_tv3d(sct_ctx* c, const float* vol, const int32_t dims[3], float lambda, double* value, float* grad) {
   if (!dims || dims[0] < 2 || dims[1] < 2 || dims[2] < 2) {
