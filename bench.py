@@ -38,7 +38,8 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="engine", choices=["engine", "reference"])
-    p.add_argument("--cpu-views", type=int, default=4, help="views in the bounded CPU-oracle sample")
+    p.add_argument("--cpu-views", type=int, default=24,
+                   help="views in the bounded CPU-oracle sample (~10-30 s of host work)")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-voxel", action="store_true")
@@ -69,48 +70,60 @@ def upstream(n_views, res, views):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock / throttle reasons sampled DURING the timed region by an
+    in-process NVML thread (the same counters `nvidia-smi --query-gpu=
+    clocks.sm,clocks_event_reasons.*` reads). A looping nvidia-smi process was
+    measured to stall this process's driver calls (host syncs) for tens of ms,
+    so it is not used."""
 
-    def __init__(self, index):
+    def __init__(self, index, period_s=0.05):
         self.index = index
-        self.proc = None
+        self.period = period_s
+        self.samples = []
+        self.thread = None
+        self.stop_flag = False
+        self.max_mhz = None
 
     def start(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+            return
+        self.stop_flag = False
+
+        def loop():
+            nv = self.nv
+            while not self.stop_flag:
+                try:
+                    self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                         nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+                except Exception:  # noqa: BLE001
+                    pass
+                time.sleep(self.period)
+
+        self.thread = threading.Thread(target=loop, daemon=True)
+        self.thread.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except Exception:
-            self.proc.kill()
-            out, _ = self.proc.communicate()
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
-                "reasons": sorted(reasons)}
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: " + getattr(self, "err", "")]}
+        self.stop_flag = True
+        self.thread.join()
+        nv = self.nv
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        reasons = sorted({n for _, r in self.samples for n, b in bits.items() if r & b})
+        sm = [s for s, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz, "samples": len(sm),
+                "min_mhz": min(sm) if sm else None, "reasons": reasons, "source": "NVML, 50 ms period"}
 
 
 # ------------------------------------------------------------------ CPU oracle leg
@@ -206,6 +219,10 @@ def run_engine(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    e2e_first = None
+    if os.environ.get("BENCH_E2E_FIRST") and not args.no_e2e:
+        e2e_first = run_e2e(args, eng, ca, scanner, my_thetas, up_host, len(thetas), world, dev)
+
     sampler = ClockSampler(local)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = eng.kernel_launches()
@@ -265,8 +282,8 @@ def run_engine(args):
           "dominant_by_time": dom}
 
     # --- e2e through the host-buffer C ABI
-    e2e = None
-    if not args.no_e2e:
+    e2e = e2e_first
+    if not args.no_e2e and e2e is None:
         e2e = run_e2e(args, eng, ca, scanner, my_thetas, up_host, len(thetas), world, dev)
 
     # --- voxelizer (configs[3])
@@ -318,6 +335,8 @@ def run_e2e(args, eng, ca, scanner, thetas, up_host, n_total_views, world, dev):
     imgs = torch.empty(up_host.shape, dtype=torch.float32).pin_memory()
     gbuf = torch.zeros(11 * m, dtype=torch.float32).pin_memory()
     gparts = torch.split(gbuf, [m, 3 * m, 3 * m, 4 * m])
+    gbuf_bytes = gbuf.numel() * 4
+    gview = gbuf.numpy()
     g = _capi.sct_grads()
     for k, t in zip(("rho_raw", "pos", "scale_raw", "rot"), gparts):
         setattr(g, k, t.data_ptr())
@@ -327,20 +346,25 @@ def run_e2e(args, eng, ca, scanner, thetas, up_host, n_total_views, world, dev):
     th = (C.c_double * len(thetas))(*thetas)
     gdev = torch.empty(11 * m, dtype=torch.float32, device=dev)
 
+    calls = []
+
     def step():
-        gbuf.zero_()
+        C.memset(gbuf.data_ptr(), 0, gbuf_bytes)  # CloudGrads::resize (trainer.cpp:283), no torch CPU op
         st = C.c_void_p()
+        t0 = time.perf_counter()
         rc = L.sct_render_fwd_host(eng._h, C.byref(cl), C.byref(sc), th, len(thetas), C.byref(op),
                                    C.c_void_p(imgs.data_ptr()), C.byref(st))
         assert rc == 0, L.sct_last_error()
+        t1 = time.perf_counter()
         rc = L.sct_render_bwd_host(eng._h, st, C.byref(cl), C.c_void_p(dL.data_ptr()), C.byref(g), None)
         assert rc == 0, L.sct_last_error()
+        calls.append((round(1e3 * (t1 - t0), 1), round(1e3 * (time.perf_counter() - t1), 1)))
         L.sct_fwd_free(st)
         if world > 1:
             gdev.copy_(gbuf, non_blocking=True)
             dist.all_reduce(gdev)
             gbuf.copy_(gdev)
-        return float(gbuf[0])  # the step's result read on the host
+        return float(gview[0])  # the step's result read on the host
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -356,6 +380,7 @@ def run_e2e(args, eng, ca, scanner, thetas, up_host, n_total_views, world, dev):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     print(f"[bench] e2e per-step ms: {[round(x, 2) for x in per]}", file=sys.stderr)
+    print(f"[bench] e2e (fwd_host, bwd_host) ms: {calls[-args.steps:]}", file=sys.stderr)
     if world > 1:
         t = torch.tensor([dt], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

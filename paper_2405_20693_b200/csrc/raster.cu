@@ -90,58 +90,79 @@ __device__ __forceinline__ Run4 run4(float dx, float A, float A2, float bdy, flo
   return r;
 }
 
-// K3: one 64-thread CTA per (tile, view); thread = 1 row x 4 columns.
-// Records for the tile list are staged through shared memory 64 at a time
-// (coalesced float4 gathers); every thread then reads them as broadcasts.
-constexpr int kCompThreads = 64;
-__global__ void __launch_bounds__(kCompThreads) composite_kernel(
+// K3: one warp per (tile, view), four warps per CTA; lane = 1 row x 8
+// columns (two 4-pixel runs sharing the per-row setup). Each warp stages its
+// own tile list through shared memory 32 records at a time (one coalesced
+// gather per lane) and synchronises only itself (__syncwarp); the next
+// chunk's records are fetched into registers while the current chunk is
+// evaluated, so the gather latency overlaps the arithmetic.
+constexpr int kCompWarps = 4;
+__global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     int tiles_x, int tiles_per_view, int W, int H, float* __restrict__ images) {
-  __shared__ float4 s0[kCompThreads];
-  __shared__ float4 s1[kCompThreads];
-  const int tile = blockIdx.x;
+  __shared__ float4 sa[kCompWarps][32];
+  __shared__ float4 sb[kCompWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kCompWarps + warp;
   const int view = blockIdx.y;
+  if (tile >= tiles_per_view) return;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int row = threadIdx.x >> 2;
-  const int col0 = (threadIdx.x & 3) * 4;
-  const int u0 = tx * kTilePx + col0;
+  const int row = lane >> 1;
+  const int u0 = tx * kTilePx + (lane & 1) * 8;
   const int v = ty * kTilePx + row;
   const float py = (float)v + 0.5f;
   const float px0 = (float)u0 + 0.5f;
   const int2 rg = ranges[(long long)view * tiles_per_view + tile];
-  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-  for (int base = rg.x; base < rg.y; base += kCompThreads) {
-    const int n = min(kCompThreads, rg.y - base);
-    __syncthreads();
-    if ((int)threadIdx.x < n) {
-      const long long item = vals[base + threadIdx.x];
-      s0[threadIdx.x] = rec[2 * item];
-      s1[threadIdx.x] = rec[2 * item + 1];
+  float acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+  float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na;
+  if (rg.x + lane < rg.y) {
+    const long long item = vals[rg.x + lane];
+    na = __ldg(rec + 2 * item);
+    nb = __ldg(rec + 2 * item + 1);
+  }
+  for (int base = rg.x; base < rg.y; base += 32) {
+    const int n = min(32, rg.y - base);
+    __syncwarp();
+    sa[warp][lane] = na;
+    sb[warp][lane] = nb;
+    __syncwarp();
+    if (base + 32 + lane < rg.y) {  // prefetch the next chunk
+      const long long item = vals[base + 32 + lane];
+      na = __ldg(rec + 2 * item);
+      nb = __ldg(rec + 2 * item + 1);
     }
-    __syncthreads();
-#pragma unroll 4
+#pragma unroll 2
     for (int j = 0; j < n; ++j) {
-      const float4 a = s0[j];  // cx cy amp*2^-64 K
-      const float4 b = s1[j];  // A B C 2A
+      const float4 a = sa[warp][j];  // cx cy amp*2^-64 K
+      const float4 b = sb[warp][j];  // A B C 2A
       const float dy = py - a.y;
       const float bdy = b.y * dy;
+      const float apb = b.x + bdy;
       const float cdy2o = fmaf(b.z * dy, dy, 64.f);
-      const Run4 e = run4(px0 - a.x, b.x, b.w, bdy, b.x + bdy, cdy2o, a.w);
-      acc0 = fmaf(a.z, e.e0, acc0);
-      acc1 = fmaf(a.z, e.e1, acc1);
-      acc2 = fmaf(a.z, e.e2, acc2);
-      acc3 = fmaf(a.z, e.e3, acc3);
+      const float dx = px0 - a.x;
+      const Run4 e0 = run4(dx, b.x, b.w, bdy, apb, cdy2o, a.w);
+      const Run4 e1 = run4(dx + 4.f, b.x, b.w, bdy, apb, cdy2o, a.w);
+      acc[0] = fmaf(a.z, e0.e0, acc[0]);
+      acc[1] = fmaf(a.z, e0.e1, acc[1]);
+      acc[2] = fmaf(a.z, e0.e2, acc[2]);
+      acc[3] = fmaf(a.z, e0.e3, acc[3]);
+      acc[4] = fmaf(a.z, e1.e0, acc[4]);
+      acc[5] = fmaf(a.z, e1.e1, acc[5]);
+      acc[6] = fmaf(a.z, e1.e2, acc[6]);
+      acc[7] = fmaf(a.z, e1.e3, acc[7]);
     }
   }
   if (v < H) {
     float* out = images + ((long long)view * H + v) * W;
-    if (u0 + 3 < W && (W & 3) == 0) {
-      *reinterpret_cast<float4*>(out + u0) = make_float4(acc0, acc1, acc2, acc3);
+    if (u0 + 7 < W && (W & 3) == 0) {
+      *reinterpret_cast<float4*>(out + u0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      *reinterpret_cast<float4*>(out + u0 + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
     } else {
-      if (u0 < W) out[u0] = acc0;
-      if (u0 + 1 < W) out[u0 + 1] = acc1;
-      if (u0 + 2 < W) out[u0 + 2] = acc2;
-      if (u0 + 3 < W) out[u0 + 3] = acc3;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (u0 + k < W) out[u0 + k] = acc[k];
     }
   }
 }
@@ -181,17 +202,28 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
   const float py0 = (float)(ty * kTilePx + s) + 0.5f;
   const float px0 = (float)u0 + 0.5f;
   const bool b2 = s & 4, b1 = s & 2, b0 = s & 1;
+  // software pipeline: the next pass's record is in flight while this pass computes
+  long long nitem = 0;
+  float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na;
+  if (rg.x + group < rg.y) {
+    nitem = vals[rg.x + group];
+    na = __ldg(rec + 2 * nitem);
+    nb = __ldg(rec + 2 * nitem + 1);
+  }
   for (int base = rg.x; base < rg.y; base += kBwdThreads / 8) {
     const int j = base + group;
     const bool valid = j < rg.y;
     float st[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) st[k] = 0.f;
-    long long item = 0;
+    const long long item = nitem;
+    const float4 a = na, b = nb;
+    if (j + kBwdThreads / 8 < rg.y) {
+      nitem = vals[j + kBwdThreads / 8];
+      na = __ldg(rec + 2 * nitem);
+      nb = __ldg(rec + 2 * nitem + 1);
+    }
     if (valid) {
-      item = vals[j];
-      const float4 a = __ldg(rec + 2 * item);
-      const float4 b = __ldg(rec + 2 * item + 1);
       const float dx0 = px0 - a.x;
       const float dxm = dx0 + 7.5f;
 #pragma unroll
@@ -282,11 +314,11 @@ void launch_ranges(Ctx* c, int64_t n_pairs, const uint32_t* keys, int tile_bits,
 
 void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images) {
   const int T = s->det.tiles_x * s->det.tiles_y;
-  dim3 grid(T, s->n_views);
+  dim3 grid((T + kCompWarps - 1) / kCompWarps, s->n_views);
   {
     KScope _ks(c, "K3_composite");
-    composite_kernel<<<grid, kCompThreads, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
-                                                           s->det.w, s->det.h, images);
+    composite_kernel<<<grid, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
+                                                              s->det.w, s->det.h, images);
   }
 }
 
