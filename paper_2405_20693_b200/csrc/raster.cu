@@ -202,28 +202,17 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
   const float py0 = (float)(ty * kTilePx + s) + 0.5f;
   const float px0 = (float)u0 + 0.5f;
   const bool b2 = s & 4, b1 = s & 2, b0 = s & 1;
-  // software pipeline: the next pass's record is in flight while this pass computes
-  long long nitem = 0;
-  float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na;
-  if (rg.x + group < rg.y) {
-    nitem = vals[rg.x + group];
-    na = __ldg(rec + 2 * nitem);
-    nb = __ldg(rec + 2 * nitem + 1);
-  }
   for (int base = rg.x; base < rg.y; base += kBwdThreads / 8) {
     const int j = base + group;
     const bool valid = j < rg.y;
     float st[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) st[k] = 0.f;
-    const long long item = nitem;
-    const float4 a = na, b = nb;
-    if (j + kBwdThreads / 8 < rg.y) {
-      nitem = vals[j + kBwdThreads / 8];
-      na = __ldg(rec + 2 * nitem);
-      nb = __ldg(rec + 2 * nitem + 1);
-    }
+    long long item = 0;
     if (valid) {
+      item = vals[j];
+      const float4 a = __ldg(rec + 2 * item);
+      const float4 b = __ldg(rec + 2 * item + 1);
       const float dx0 = px0 - a.x;
       const float dxm = dx0 + 7.5f;
 #pragma unroll
@@ -232,18 +221,26 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
         const float bdy = b.y * dy;
         const float apb = b.x + bdy;
         const float cdy2o = fmaf(b.z * dy, dy, 64.f);
+        // Columns c and 15-c have opposite c' = c - 7.5, so with s = F_c + F_15-c
+        // and d = F_c - F_15-c (F = g E): R0 += s, R1 += c' d, R2 += c'^2 s —
+        // 7 instead of 8 ops per column pair. Runs 0/3 and 1/2 are paired.
         float R0 = 0.f, R1 = 0.f, R2 = 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const Run4 e = run4(dx0 + 4.f * q, b.x, b.w, bdy, apb, cdy2o, a.w);
-          const float ev[4] = {e.e0, e.e1, e.e2, e.e3};
+        for (int q = 0; q < 2; ++q) {
+          const Run4 lo = run4(dx0 + 4.f * q, b.x, b.w, bdy, apb, cdy2o, a.w);
+          const Run4 hi = run4(dx0 + 4.f * (3 - q), b.x, b.w, bdy, apb, cdy2o, a.w);
+          const float el[4] = {lo.e0, lo.e1, lo.e2, lo.e3};
+          const float eh[4] = {hi.e0, hi.e1, hi.e2, hi.e3};
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const float cp = (float)(4 * q + k) - 7.5f;
-            const float ge = g[r][4 * q + k] * ev[k];
-            R0 += ge;
-            R1 = fmaf(ge, cp, R1);
-            R2 = fmaf(ge, cp * cp, R2);
+            const int c = 4 * q + k;           // 0..7
+            const float cp = (float)c - 7.5f;  // c' of column c; column 15-c has -c'
+            const float fa = g[r][c] * el[k];
+            const float fb = g[r][15 - c] * eh[3 - k];
+            const float s = fa + fb;
+            R0 += s;
+            R1 = fmaf(fa - fb, cp, R1);
+            R2 = fmaf(s, cp * cp, R2);
           }
         }
         // sum ge dx = dxm R0 + R1, sum ge dx^2 = dxm^2 R0 + 2 dxm R1 + R2
