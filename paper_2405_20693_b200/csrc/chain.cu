@@ -41,7 +41,11 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
     const int32_t* __restrict__ offset, const float4* __restrict__ pair_stats, float* __restrict__ out) {
   for (long long item = blockIdx.x * (long long)blockDim.x + threadIdx.x; item < n_items;
        item += (long long)gridDim.x * blockDim.x) {
-    if (!vis[item]) continue;
+    if (!vis[item]) {  // culled in this view: contributes nothing to the view sums
+#pragma unroll
+      for (int a = 0; a < kItemOut; ++a) out[a * n_items + item] = 0.f;
+      continue;
+    }
     const long long v = item / m;
     const long long i = item - v * m;
     // fixed-order reduction over the item's tiles (rasterizer.cpp:245-257)
@@ -236,26 +240,39 @@ __device__ __forceinline__ void d_cov_param_grads(const dKernel& k, const dM3& G
   for (int kk = 0; kk < 4; ++kk) g_rot[kk] = (c[kk] - qn[kk] * qc) / nrm;
 }
 
+// Sum of the item outputs over the views, in view order, one thread per
+// (output, kernel) so the reads are coalesced; row kItemOut counts the views in
+// which the kernel is visible (grad_count, rasterizer.cpp:337-338).
+__global__ void __launch_bounds__(256) view_sum_kernel(long long m, int n_views, const uint8_t* __restrict__ vis,
+                                                       const float* __restrict__ item, double* __restrict__ vsum) {
+  const long long n_items = m * n_views;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (kItemOut + 1) * m;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long a = t / m, i = t - a * m;
+    double acc = 0.0;
+    if (a < kItemOut) {
+      const float* src = item + a * n_items + i;
+      for (int v = 0; v < n_views; ++v) acc += (double)src[(long long)v * m];
+    } else {
+      for (int v = 0; v < n_views; ++v) acc += (double)vis[(long long)v * m + i];
+    }
+    vsum[t] = acc;
+  }
+}
+
 __global__ void __launch_bounds__(128) raster_finalize_kernel(
-    long long m, int n_views, double s_min, const float* __restrict__ rho_raw, const float* __restrict__ pos,
-    const float* __restrict__ scale_raw, const float* __restrict__ rot, const uint8_t* __restrict__ vis,
-    const float* __restrict__ item, float* __restrict__ g_rho, float* __restrict__ g_pos,
+    long long m, double s_min, const float* __restrict__ rho_raw, const float* __restrict__ pos,
+    const float* __restrict__ scale_raw, const float* __restrict__ rot, const double* __restrict__ vsum,
+    float* __restrict__ g_rho, float* __restrict__ g_pos,
     float* __restrict__ g_scale, float* __restrict__ g_rotp, float* __restrict__ st_norm,
     int32_t* __restrict__ st_count, float* __restrict__ st_3d) {
-  const long long n_items = m * n_views;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
+    // view sums from view_sum_kernel: [kItemOut][m] + visible count at [kItemOut][m]
     double acc[kItemOut];
 #pragma unroll
-    for (int a = 0; a < kItemOut; ++a) acc[a] = 0.0;
-    int nvis = 0;
-    for (int v = 0; v < n_views; ++v) {
-      const long long it = (long long)v * m + i;
-      if (!vis[it]) continue;
-      ++nvis;
-#pragma unroll
-      for (int a = 0; a < kItemOut; ++a) acc[a] += (double)item[a * n_items + it];
-    }
+    for (int a = 0; a < kItemOut; ++a) acc[a] = vsum[a * m + i];
+    const int nvis = (int)vsum[kItemOut * m + i];
     if (nvis == 0) continue;
     const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
     g_rho[i] += (float)(acc[0] * d_act_density_grad(k.rho_raw));
@@ -361,13 +378,20 @@ void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const fl
 void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float* item_grads, sct_grads* g,
                             sct_stats* st) {
   if (s->m == 0) return;
+  double* vsum = nullptr;
+  if (dev_alloc(c, (void**)&vsum, (kItemOut + 1) * s->m * sizeof(double)) != SCT_OK) return;
+  {
+    KScope _ks(c, "K5_view_sum");
+    view_sum_kernel<<<grid_cap(c, (kItemOut + 1) * s->m, 256), 256, 0, c->stream>>>(s->m, s->n_views, s->d_vis,
+                                                                                     item_grads, vsum);
+  }
   {
     KScope _ks(c, "K5_raster_finalize");
     raster_finalize_kernel<<<grid_cap(c, s->m, 128), 128, 0, c->stream>>>(
-        s->m, s->n_views, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, s->d_vis, item_grads, g->rho_raw,
-        g->pos, g->scale_raw, g->rot, st ? st->grad2d_norm_accum : nullptr, st ? st->grad_count : nullptr,
-        st ? st->grad3d_accum : nullptr);
+        s->m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, vsum, g->rho_raw, g->pos, g->scale_raw, g->rot,
+        st ? st->grad2d_norm_accum : nullptr, st ? st->grad_count : nullptr, st ? st->grad3d_accum : nullptr);
   }
+  dev_free(c, vsum);
 }
 
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,

@@ -29,20 +29,45 @@ __global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, lon
                                                           const int32_t* __restrict__ offset, int tiles_x,
                                                           int tile_bits, uint32_t* __restrict__ keys,
                                                           int32_t* __restrict__ vals) {
-  for (long long item = blockIdx.x * (long long)blockDim.x + threadIdx.x; item < n_items;
-       item += (long long)gridDim.x * blockDim.x) {
-    const int32_t o0 = offset[item];
-    const int32_t o1 = offset[item + 1];
-    if (o1 == o0) continue;
-    const short4 r = rect[item];
-    const uint32_t vbase = (uint32_t)(item / m) << tile_bits;
-    int32_t o = o0;
-    for (int ty = r.z; ty <= r.w; ++ty)
-      for (int tx = r.x; tx <= r.y; ++tx) {
-        keys[o] = vbase | (uint32_t)(ty * tiles_x + tx);
-        vals[o] = (int32_t)item;
-        ++o;
+  // Warp-cooperative: a warp owns 32 consecutive items, whose pairs occupy one
+  // contiguous output range (exclusive-scan order); lanes stride over that
+  // range so the key/value stores are coalesced. Each output slot finds its
+  // item by a 5-step binary search over the 32 offsets held in the lanes.
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long w0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < n_items;
+       w0 += warps * 32) {
+    const long long it = w0 + lane;
+    const int32_t o_l = it < n_items ? offset[it] : offset[n_items];
+    const long long last = min(w0 + 32, n_items);
+    const int32_t o_end = offset[last];
+    short4 r = make_short4(0, -1, 0, -1);
+    if (it < n_items) r = rect[it];
+    const int rxy = ((int)(unsigned short)r.x) | ((int)r.y << 16);
+    const int rzw = ((int)(unsigned short)r.z) | ((int)r.w << 16);
+    const int32_t o_0 = __shfl_sync(0xffffffffu, o_l, 0);
+    for (int32_t p0 = o_0; p0 < o_end; p0 += 32) {
+      const int32_t p = p0 + lane;
+      // largest j with offset[w0+j] <= p
+      int j = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int32_t oj = __shfl_sync(0xffffffffu, o_l, j + step);
+        if (j + step < 32 && oj <= p) j += step;
       }
+      const int32_t oj = __shfl_sync(0xffffffffu, o_l, j);
+      const int jxy = __shfl_sync(0xffffffffu, rxy, j);
+      const int jzw = __shfl_sync(0xffffffffu, rzw, j);
+      if (p < o_end) {
+        const int x0 = (short)(jxy & 0xffff), x1 = (short)(jxy >> 16), y0 = (short)(jzw & 0xffff);
+        const int nx = x1 - x0 + 1;
+        const int rank = p - oj;
+        const int ty = y0 + rank / nx, tx = x0 + rank % nx;
+        const long long item = w0 + j;
+        keys[p] = ((uint32_t)(item / m) << tile_bits) | (uint32_t)(ty * tiles_x + tx);
+        vals[p] = (int32_t)item;
+      }
+    }
   }
 }
 
