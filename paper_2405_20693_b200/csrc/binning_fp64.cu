@@ -118,7 +118,9 @@ __global__ void __launch_bounds__(256) voxel_preprocess_kernel(
     const dM3 q = d_inv3(sigma);
     const double rho = d_act_density(k.rho_raw);
     rec[3 * i + 0] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], (float)rho);
-    rec[3 * i + 1] = make_float4((float)(kA * q.m[0][0]), (float)(kA * q.m[1][1]), (float)(kA * q.m[2][2]), 0.f);
+    // .w = K = 2^(2 Qxx sx^2): voxel-to-voxel ratio step of the x recurrence (voxel.cu)
+    rec[3 * i + 1] = make_float4((float)(kA * q.m[0][0]), (float)(kA * q.m[1][1]), (float)(kA * q.m[2][2]),
+                                 (float)exp2(2.0 * kA * q.m[0][0] * sp[0] * sp[0]));
     rec[3 * i + 2] = make_float4((float)(2.0 * kA * q.m[0][1]), (float)(2.0 * kA * q.m[0][2]),
                                  (float)(2.0 * kA * q.m[1][2]), 0.f);
   }
