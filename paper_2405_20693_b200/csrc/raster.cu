@@ -22,6 +22,25 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// Asynchronous global -> shared copies (LDGSTS): staged data never passes
+// through registers.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+constexpr int kBwdChunk = 256;  // tile-list entries staged per chunk in K4
+
 namespace {
 
 __global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, long long m,
@@ -227,17 +246,50 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
   const float py0 = (float)(ty * kTilePx + s) + 0.5f;
   const float px0 = (float)u0 + 0.5f;
   const bool b2 = s & 4, b1 = s & 2, b0 = s & 1;
-  for (int base = rg.x; base < rg.y; base += kBwdThreads / 8) {
-    const int j = base + group;
-    const bool valid = j < rg.y;
+  // The tile list is processed in chunks of kBwdChunk entries (item indices
+  // loaded coalesced into shared memory), 32 kernels per pass. Warp 0 stages
+  // the NEXT pass's records, rectangles and scan offsets with cp.async
+  // (global -> shared, no registers held) while all warps evaluate the
+  // current pass from the other buffer.
+  constexpr int kPass = kBwdThreads / 8;  // kernels per pass
+  __shared__ int s_items[kBwdChunk];
+  __shared__ float4 s_rec[2][kPass][2];
+  __shared__ short4 s_rect[2][kPass];
+  __shared__ int s_off[2][kPass];
+  const int tid = threadIdx.x;
+  const int n_list = rg.y - rg.x;
+  auto stage = [&](int buf, int p, int cn) {  // called by warp 0 only
+    const int e = p * kPass + tid;
+    if (e < cn) {
+      const long long it = s_items[e];
+      cp_async16(&s_rec[buf][tid][0], rec + 2 * it);
+      cp_async16(&s_rec[buf][tid][1], rec + 2 * it + 1);
+      cp_async8(&s_rect[buf][tid], rect + it);
+      cp_async4(&s_off[buf][tid], offset + it);
+    }
+    cp_async_commit();
+  };
+  for (int cb = 0; cb < n_list; cb += kBwdChunk) {
+    const int cn = min(kBwdChunk, n_list - cb);
+    __syncthreads();  // previous chunk finished with s_items / buffers
+    if (tid < cn) s_items[tid] = vals[rg.x + cb + tid];
+    __syncthreads();
+    if (tid < 32) {
+      stage(0, 0, cn);
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    const int npass = (cn + kPass - 1) / kPass;
+  for (int p = 0; p < npass; ++p) {
+    if (tid < 32 && p + 1 < npass) stage((p + 1) & 1, p + 1, cn);
+    const int buf = p & 1;
+    const bool valid = p * kPass + group < cn;
     float st[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) st[k] = 0.f;
-    long long item = 0;
     if (valid) {
-      item = vals[j];
-      const float4 a = __ldg(rec + 2 * item);
-      const float4 b = __ldg(rec + 2 * item + 1);
+      const float4 a = s_rec[buf][group][0];
+      const float4 b = s_rec[buf][group][1];
       const float dx0 = px0 - a.x;
       const float dxm = dx0 + 7.5f;
 #pragma unroll
@@ -297,10 +349,13 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
     const float keep = b0 ? x[1] : x[0];
     const float tot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
     if (valid && s < 6) {
-      const short4 r = rect[item];
-      const int slot = offset[item] + (ty - r.z) * (r.y - r.x + 1) + (tx - r.x);
+      const short4 r = s_rect[buf][group];
+      const int slot = s_off[buf][group] + (ty - r.z) * (r.y - r.x + 1) + (tx - r.x);
       pair_stats[8 * (long long)slot + s] = tot;
     }
+    if (tid < 32) cp_async_wait_all();
+    __syncthreads();  // next buffer visible; this buffer free for re-staging
+  }
   }
 }
 
