@@ -41,6 +41,7 @@
 #ifndef SPLATCT_GPU_H
 #define SPLATCT_GPU_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -203,6 +204,14 @@ int sct_photometric_loss(sct_ctx* ctx, const float* rendered, const float* measu
 int sct_adam_step(sct_ctx* ctx, sct_cloud* params, sct_adam_state* state, const sct_grads* grads, int32_t t,
                   const double lr[4], double beta1, double beta2, double eps);
 double sct_lr_at(double lr_init, double final_ratio, int32_t t, int32_t iters);
+
+/* ---- host memory --------------------------------------------------------- */
+/* page-locked host buffers for the _host entry points (full-bandwidth,
+ * asynchronous copies); sct_debug_pointer_type reports how the engine's CUDA
+ * runtime classifies a pointer (0 unregistered, 1 host, 2 device, 3 managed). */
+int sct_host_alloc(void** p, size_t bytes);
+int sct_host_free(void* p);
+int sct_debug_pointer_type(const void* p);
 
 #ifdef __cplusplus
 }

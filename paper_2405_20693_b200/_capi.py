@@ -88,6 +88,9 @@ SIGNATURES = {
     "sct_adam_step": (C.c_int, [VP, P(sct_cloud), P(sct_adam_state), P(sct_grads), C.c_int32, D, C.c_double,
                                 C.c_double, C.c_double]),
     "sct_lr_at": (C.c_double, [C.c_double, C.c_double, C.c_int32, C.c_int32]),
+    "sct_host_alloc": (C.c_int, [P(VP), C.c_size_t]),
+    "sct_host_free": (C.c_int, [VP]),
+    "sct_debug_pointer_type": (C.c_int, [VP]),
 }
 
 _lib = None

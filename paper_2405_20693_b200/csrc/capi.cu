@@ -299,10 +299,15 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  if (cudaMallocHost((void**)&c->pinned_count, 64) != cudaSuccess) {
+  if (cudaMallocHost((void**)&c->pinned_count, 64) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
-    set_error("CUDA error: cudaMallocHost failed");
+    set_error("CUDA error: context host allocations failed");
     return SCT_ERR_CUDA;
+  }
+  for (int a = 0; a < Ctx::kChunkEvents; ++a) {
+    cudaEventCreateWithFlags(&c->ev_compute[a], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_copy[a], cudaEventDisableTiming);
   }
   *out = c;
   return SCT_OK;
@@ -315,6 +320,11 @@ int sct_ctx_destroy(sct_ctx* c) {
   for (int a = 0; a < Ctx::kStageSlots; ++a)
     if (c->stage[a]) cudaFree(c->stage[a]);
   if (c->pinned_count) cudaFreeHost(c->pinned_count);
+  for (int a = 0; a < Ctx::kChunkEvents; ++a) {
+    if (c->ev_compute[a]) cudaEventDestroy(c->ev_compute[a]);
+    if (c->ev_copy[a]) cudaEventDestroy(c->ev_copy[a]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   delete c;
   return SCT_OK;
 }
@@ -471,8 +481,10 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   return SCT_OK;
 }
 
-int sct_render_bwd(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
-                   sct_stats* stats) {
+// chunks > 0: the upstream gradient arrives in `chunks` view chunks, chunk k
+// signalled by ctx->ev_copy[k]; K4 for chunk k waits only for its own copy.
+static int render_bwd_impl(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
+                           sct_stats* stats, int chunks) {
   if (!c || !s || !grads || !dL) {
     set_error("ConfigError: null argument");
     return SCT_ERR_CONFIG;
@@ -487,13 +499,26 @@ int sct_render_bwd(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* 
   float* item_grads = nullptr;
   SCT_TRY(dev_alloc(c, (void**)&pair_stats, 2 * s->n_pairs * sizeof(float4)));
   SCT_TRY(dev_alloc(c, (void**)&item_grads, 11 * s->n_items * sizeof(float)));
-  launch_raster_backward_stats(c, s, dL, pair_stats);
+  if (chunks <= 0) {
+    launch_raster_backward_stats(c, s, dL, pair_stats);
+  } else {
+    for (int k = 0; k < chunks; ++k) {
+      const int v0 = (int)((int64_t)s->n_views * k / chunks), v1 = (int)((int64_t)s->n_views * (k + 1) / chunks);
+      SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_copy[k], 0));
+      launch_raster_backward_stats(c, s, dL, pair_stats, v0, v1 - v0);
+    }
+  }
   launch_raster_chain(c, s, *cloud, pair_stats, item_grads);
   launch_raster_finalize(c, s, *cloud, item_grads, grads, stats);
   dev_free(c, pair_stats);
   dev_free(c, item_grads);
   SCT_CUDA_TRY(cudaGetLastError());
   return SCT_OK;
+}
+
+int sct_render_bwd(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
+                   sct_stats* stats) {
+  return render_bwd_impl(c, s, cloud, dL, grads, stats, 0);
 }
 
 int sct_fwd_free(sct_fwd* s) {
@@ -596,6 +621,17 @@ int sct_project_kernels(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* s
 }
 
 // ---- host-buffer variants ----------------------------------------------------
+// Number of view chunks for overlapping the image/upstream copies with compute:
+// ~8 MB per chunk, at most Ctx::kChunkEvents.
+static int host_chunks(size_t bytes) {
+  if (const char* e = std::getenv("SCT_HOST_CHUNKS")) return std::max(1, std::min(atoi(e), Ctx::kChunkEvents));
+  const size_t per = 20u << 20;
+  size_t k = (bytes + per - 1) / per;
+  if (k < 1) k = 1;
+  if (k > (size_t)Ctx::kChunkEvents) k = Ctx::kChunkEvents;
+  return (int)k;
+}
+
 // Staging slots: 0-3 cloud arrays, 4 images, 5 upstream gradient, 6-9 grads,
 // 10-12 stats, 13 volume.
 static int upload_cloud(Ctx* c, const sct_cloud* h, sct_cloud* d) {
@@ -621,19 +657,27 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
   }
   sct_cloud d;
   SCT_TRY(upload_cloud(c, cloud_host, &d));
-  const size_t img = (size_t)n_views * scanner->det_res_px[0] * scanner->det_res_px[1];
+  const size_t px = (size_t)scanner->det_res_px[0] * scanner->det_res_px[1];
   float* dimg = nullptr;
-  SCT_TRY(stage_buf(c, 4, img * sizeof(float), (void**)&dimg));
-  int rc = sct_render_fwd(c, &d, scanner, thetas, n_views, opts, dimg, state);
-  if (rc == SCT_OK && images_host)
-    if (cudaMemcpyAsync(images_host, dimg, img * sizeof(float), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) {
-      set_error("CUDA error: image download");
-      rc = SCT_ERR_CUDA;
+  SCT_TRY(stage_buf(c, 4, n_views * px * sizeof(float), (void**)&dimg));
+  // binning for all views, then the composite in view chunks whose D2H copy
+  // (copy stream) overlaps the next chunk's composite
+  int rc = sct_render_fwd(c, &d, scanner, thetas, n_views, opts, nullptr, state);
+  if (rc != SCT_OK) return rc;
+  const int chunks = std::min(n_views, host_chunks(n_views * px * sizeof(float)));
+  for (int k = 0; k < chunks; ++k) {
+    const int v0 = (int)((int64_t)n_views * k / chunks), v1 = (int)((int64_t)n_views * (k + 1) / chunks);
+    launch_raster_composite(c, *state, dimg, v0, v1 - v0);
+    if (images_host) {
+      SCT_CUDA_TRY(cudaEventRecord(c->ev_compute[k], c->stream));
+      SCT_CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev_compute[k], 0));
+      SCT_CUDA_TRY(cudaMemcpyAsync(images_host + v0 * px, dimg + v0 * px, (v1 - v0) * px * sizeof(float),
+                                   cudaMemcpyDeviceToHost, c->copy_stream));
     }
-  if (cudaStreamSynchronize(c->stream) != cudaSuccess && rc == SCT_OK) {
-    set_error("CUDA error in sct_render_fwd_host");
-    rc = SCT_ERR_CUDA;
   }
+  SCT_CUDA_TRY(cudaGetLastError());
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return rc;
 }
 
@@ -647,10 +691,18 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
   sct_cloud d;
   SCT_TRY(upload_cloud(c, cloud_host, &d));
   const int64_t m = cloud_host->m;
-  const size_t img = (size_t)s->n_views * s->det.w * s->det.h;
+  const size_t px = (size_t)s->det.w * s->det.h;
   float* ddl = nullptr;
-  SCT_TRY(stage_buf(c, 5, img * sizeof(float), (void**)&ddl));
-  SCT_CUDA_TRY(cudaMemcpyAsync(ddl, dL_host, img * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  SCT_TRY(stage_buf(c, 5, s->n_views * px * sizeof(float), (void**)&ddl));
+  // upstream gradient in view chunks on the copy stream; K4 for chunk k starts
+  // as soon as chunk k has landed
+  const int chunks = std::min<int>(s->n_views, host_chunks(s->n_views * px * sizeof(float)));
+  for (int k = 0; k < chunks; ++k) {
+    const int v0 = (int)((int64_t)s->n_views * k / chunks), v1 = (int)((int64_t)s->n_views * (k + 1) / chunks);
+    SCT_CUDA_TRY(cudaMemcpyAsync(ddl + v0 * px, dL_host + v0 * px, (v1 - v0) * px * sizeof(float),
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+    SCT_CUDA_TRY(cudaEventRecord(c->ev_copy[k], c->copy_stream));
+  }
   // accumulate semantics: bring the caller's running sums to the device
   sct_grads dg;
   float** gd[4] = {&dg.rho_raw, &dg.pos, &dg.scale_raw, &dg.rot};
@@ -673,7 +725,7 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
       SCT_CUDA_TRY(cudaMemcpyAsync(*sd[a], sh[a], sb[a], cudaMemcpyHostToDevice, c->stream));
     }
   }
-  int rc = sct_render_bwd(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr);
+  int rc = render_bwd_impl(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, chunks);
   if (rc == SCT_OK) {
     for (int a = 0; a < 4; ++a)
       SCT_CUDA_TRY(cudaMemcpyAsync(gh[a], *gd[a], n[a] * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
@@ -681,6 +733,7 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
       for (int a = 0; a < 3; ++a)
         SCT_CUDA_TRY(cudaMemcpyAsync(sh[a], *sd[a], sb[a], cudaMemcpyDeviceToHost, c->stream));
   }
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return rc;
 }
@@ -878,3 +931,26 @@ int sct_adam_step(sct_ctx* c, sct_cloud* p, sct_adam_state* st, const sct_grads*
 }
 
 }  // extern "C"
+
+extern "C" {
+// Diagnostics: cudaPointerGetAttributes(ptr).type as seen by the engine's
+// runtime (0 unregistered, 1 host/pinned, 2 device, 3 managed).
+int sct_debug_pointer_type(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return (int)a.type;
+}
+// Page-locked host allocation through the engine's runtime (for callers that
+// want the host-buffer entry points to run at full copy bandwidth).
+int sct_host_alloc(void** p, size_t bytes) {
+  SCT_CUDA_TRY(cudaMallocHost(p, bytes));
+  return SCT_OK;
+}
+int sct_host_free(void* p) {
+  SCT_CUDA_TRY(cudaFreeHost(p));
+  return SCT_OK;
+}
+}

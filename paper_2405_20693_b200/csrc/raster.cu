@@ -143,12 +143,12 @@ __device__ __forceinline__ Run4 run4(float dx, float A, float A2, float bdy, flo
 constexpr int kCompWarps = 4;
 __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
-    int tiles_x, int tiles_per_view, int W, int H, float* __restrict__ images) {
+    int tiles_x, int tiles_per_view, int W, int H, int view0, float* __restrict__ images) {
   __shared__ float4 sa[kCompWarps][32];
   __shared__ float4 sb[kCompWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x * kCompWarps + warp;
-  const int view = blockIdx.y;
+  const int view = view0 + blockIdx.y;
   if (tile >= tiles_per_view) return;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int row = lane >> 1;
@@ -226,9 +226,9 @@ constexpr int kBwdThreads = 256;
 __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ rect, const int32_t* __restrict__ offset, int tiles_x, int tiles_per_view, int W,
-    int H, const float* __restrict__ dL, float* __restrict__ pair_stats) {
+    int H, int view0, const float* __restrict__ dL, float* __restrict__ pair_stats) {
   const int tile = blockIdx.x;
-  const int view = blockIdx.y;
+  const int view = view0 + blockIdx.y;
   const int2 rg = ranges[(long long)view * tiles_per_view + tile];
   if (rg.y <= rg.x) return;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -389,26 +389,27 @@ void launch_ranges(Ctx* c, int64_t n_pairs, const uint32_t* keys, int tile_bits,
   }
 }
 
-void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images) {
+// Views [v0, v0 + nv) of the forward state (nv <= 0: all views).
+void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, int nv) {
+  if (nv <= 0) nv = s->n_views - v0;
+  if (nv <= 0) return;
   const int T = s->det.tiles_x * s->det.tiles_y;
-  dim3 grid((T + kCompWarps - 1) / kCompWarps, s->n_views);
-  {
-    KScope _ks(c, "K3_composite");
-    composite_kernel<<<grid, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
-                                                              s->det.w, s->det.h, images);
-  }
+  dim3 grid((T + kCompWarps - 1) / kCompWarps, nv);
+  KScope _ks(c, "K3_composite");
+  composite_kernel<<<grid, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
+                                                            s->det.w, s->det.h, v0, images);
 }
 
-void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats) {
+void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0, int nv) {
   if (s->n_pairs == 0) return;
+  if (nv <= 0) nv = s->n_views - v0;
+  if (nv <= 0) return;
   const int T = s->det.tiles_x * s->det.tiles_y;
-  dim3 grid(T, s->n_views);
-  {
-    KScope _ks(c, "K4_backward_stats");
-    backward_stats_kernel<<<grid, kBwdThreads, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
-                                                               s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h,
-                                                               dL, reinterpret_cast<float*>(pair_stats));
-  }
+  dim3 grid(T, nv);
+  KScope _ks(c, "K4_backward_stats");
+  backward_stats_kernel<<<grid, kBwdThreads, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
+                                                             s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0,
+                                                             dL, reinterpret_cast<float*>(pair_stats));
 }
 
 }  // namespace sct

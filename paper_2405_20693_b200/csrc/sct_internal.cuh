@@ -91,6 +91,12 @@ struct Ctx {
   size_t cub_tmp_bytes = 0;
   int64_t* pinned_count = nullptr;  // small pinned host word for D2H of counts
   int sm_count = 148;
+  // copy stream + events for the host-buffer entry points (H2D/D2H of view
+  // chunks overlap the compute of neighbouring chunks)
+  cudaStream_t copy_stream = nullptr;
+  static constexpr int kChunkEvents = 16;
+  cudaEvent_t ev_compute[kChunkEvents] = {};
+  cudaEvent_t ev_copy[kChunkEvents] = {};
   // grow-only device staging buffers of the host-buffer entry points (a
   // context serialises its calls, so a slot is free again at the next call)
   static constexpr int kStageSlots = 16;
@@ -158,8 +164,9 @@ void launch_raster_emit(Ctx* c, int64_t n_items, int64_t m, const short4* rect, 
                         int tiles_x, int tile_bits, uint32_t* keys, int32_t* vals);
 void launch_ranges(Ctx* c, int64_t n_pairs, const uint32_t* keys, int tile_bits, int64_t tiles_per_view,
                    int2* ranges);
-void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images);
-void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats);
+void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0 = 0, int nv = 0);
+void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0 = 0,
+                                  int nv = 0);
 void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, const int32_t* offset,
                        int32_t bricks_x, int32_t bricks_y, uint32_t* keys, int32_t* vals);
 void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
