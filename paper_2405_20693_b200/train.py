@@ -1,0 +1,108 @@
+"""Device-resident training iteration of the reference trainer (BASELINE
+configs[1], "full train step"): trainer.cpp:268-319 without adaptive control.
+
+One iteration = render the selected view(s) (rasterizer.cpp:112-157), form
+L1 + lambda_ssim * D-SSIM on projections normalised by the dataset maximum and
+the matching dL/dI (objectives.cpp:113-167, trainer.cpp:277-287),
+render_backward with adaptive statistics (trainer.cpp:288), the TV term on a D^3
+sub-grid at the output spacing (voxelize -> tv3d_loss -> lambda_tv-scaled
+voxelize_backward, trainer.cpp:290-300), the non-finite check
+(trainer.cpp:302-308) and the four Adam groups with the exponential learning
+rate followed by quaternion renormalisation (trainer.cpp:310-319) — all on the
+GPU through the C ABI; the host only picks the view and the sub-grid origin.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from .engine import (CloudGrads, DivergenceDetected, Engine, GaussianCloud, GridSpec, RasterOptions, ScannerConfig,
+                     lr_at)
+
+
+@dataclass
+class TrainConfig:  # trainer.hpp:13-44 (the fields the iteration uses)
+    iters: int = 30000
+    lr_position: float = 0.0002
+    lr_density: float = 0.01
+    lr_scale: float = 0.005
+    lr_rotation: float = 0.001
+    lr_final_ratio: float = 0.1
+    lambda_ssim: float = 0.25
+    lambda_tv: float = 0.05
+    tv_grid_dim: int = 32
+    output_dims: tuple = (64, 64, 64)
+    seed: int = 0
+    mode: int = 0
+    check_every: int = 1  # iterations between host-side non-finite checks
+
+
+def random_subvolume_origin(lo, hi, spacing, d, u):
+    """voxelizer.cpp:226-239 with the uniform draws u[3] supplied by the caller."""
+    out = []
+    for k in range(3):
+        span = (hi[k] - lo[k]) - d * spacing[k]
+        out.append(lo[k] + u[k] * span if span > 0.0 else 0.5 * (lo[k] + hi[k]) - 0.5 * d * spacing[k])
+    return tuple(out)
+
+
+class Trainer:
+    def __init__(self, engine: Engine, cloud: GaussianCloud, scanner: ScannerConfig, angles: Sequence[float],
+                 projections: torch.Tensor, cfg: TrainConfig):
+        self.eng, self.cloud, self.scanner, self.cfg = engine, cloud, scanner, cfg
+        self.angles = list(angles)
+        proj = projections.to(engine.device, torch.float32).contiguous()
+        norm = float(proj.max().item())  # trainer.cpp:243-246
+        if not norm > 0.0:
+            norm = 1.0
+        self.inv_norm = 1.0 / norm
+        self.measured_norm = proj * self.inv_norm  # trainer.cpp:248-252
+        self.grads = CloudGrads(cloud.size(), device=engine.device)
+        ext = [scanner.extent_max_mm[k] - scanner.extent_min_mm[k] for k in range(3)]
+        self.output_spacing = tuple(ext[k] / cfg.output_dims[k] for k in range(3))
+        self.opts = RasterOptions(mode=cfg.mode)
+        self.t = 0
+        self.rng = np.random.default_rng(cfg.seed)
+        self.order: list = []
+
+    def next_view(self) -> int:
+        """Shuffled epochs (trainer.cpp:269-273)."""
+        if not self.order:
+            self.order = list(self.rng.permutation(len(self.angles)))
+        return int(self.order.pop(0))
+
+    def step(self, view: Optional[int] = None, sub_origin: Optional[tuple] = None) -> dict:
+        cfg, eng, cloud = self.cfg, self.eng, self.cloud
+        self.t += 1
+        t = self.t
+        if view is None:
+            view = self.next_view()
+        fwd = eng.render(cloud, self.scanner, self.angles[view], self.opts)
+        vals, dL = eng.photometric_loss(fwd.images, self.measured_norm[view:view + 1], render_scale=self.inv_norm,
+                                        lambda_ssim=cfg.lambda_ssim, grad_scale=self.inv_norm)
+        self.grads.zero_()  # grads.resize(M), trainer.cpp:283
+        eng.render_backward(cloud, fwd, dL, self.grads, accumulate_stats=True)
+        fwd.free()
+        tv = torch.zeros((), dtype=torch.float64, device=eng.device)
+        if cfg.lambda_tv > 0.0:
+            if sub_origin is None:
+                sub_origin = random_subvolume_origin(self.scanner.extent_min_mm, self.scanner.extent_max_mm,
+                                                     self.output_spacing, cfg.tv_grid_dim, self.rng.random(3))
+            d = cfg.tv_grid_dim
+            sub = GridSpec((d, d, d), sub_origin, self.output_spacing)
+            vol = eng.voxelize(cloud, sub)
+            tv, g_tv = eng.tv3d_loss(vol, cfg.lambda_tv)
+            eng.voxelize_backward(cloud, sub, g_tv, self.grads)
+        total = vals[0, 0] + cfg.lambda_ssim * vals[0, 1] + cfg.lambda_tv * tv  # trainer.cpp:302-303
+        if cfg.check_every and t % cfg.check_every == 0 and not math.isfinite(float(total.item())):
+            raise DivergenceDetected(f"non-finite loss at iteration {t}")
+        lrs = [lr_at(cfg.lr_position, cfg.lr_final_ratio, t, cfg.iters),
+               lr_at(cfg.lr_density, cfg.lr_final_ratio, t, cfg.iters),
+               lr_at(cfg.lr_scale, cfg.lr_final_ratio, t, cfg.iters),
+               lr_at(cfg.lr_rotation, cfg.lr_final_ratio, t, cfg.iters)]
+        eng.adam_step(cloud, self.grads, t, lrs)  # trainer.cpp:310-319
+        return {"iter": t, "view": view, "l1": vals[0, 0], "dssim": vals[0, 1], "tv": tv, "total": total}
