@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-voxel", action="store_true")
     p.add_argument("--no-train", action="store_true")
+    p.add_argument("--reduction", default="deterministic", choices=["deterministic", "atomic"],
+                   help="backward reduction: fixed-order per-pair slots, or the parallel-atomic mode")
     return p.parse_args()
 
 
@@ -190,7 +192,7 @@ def run_engine(args):
     w, ca, thetas, vol = make_workload()
     my_views = pdist.shard_views(len(thetas), rank, world)
     my_thetas = [thetas[v] for v in my_views]
-    eng = P.Engine(local)
+    eng = P.Engine(local, deterministic=(args.reduction == "deterministic"))
     stream = eng.stream
     cloud = P.GaussianCloud(ca.s_min, ca.rho_raw, ca.pos, ca.scale_raw, ca.rot, device=dev)
     scanner = P.ScannerConfig(detector_res_px=(w.res, w.res))

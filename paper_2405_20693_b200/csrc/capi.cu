@@ -497,21 +497,34 @@ static int render_bwd_impl(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
   if (s->n_items == 0) return SCT_OK;
   float4* pair_stats = nullptr;
   float* item_grads = nullptr;
-  SCT_TRY(dev_alloc(c, (void**)&pair_stats, 2 * s->n_pairs * sizeof(float4)));
-  SCT_TRY(dev_alloc(c, (void**)&item_grads, 11 * s->n_items * sizeof(float)));
+  // deterministic (default): per-(tile, kernel) slots reduced in the
+  // reference's fixed tile order; otherwise the parallel-atomic mode of
+  // SPEC.md:224-226 accumulates straight into 8-float per-item records.
+  // (grow-only context buffers: slot 14 statistics, slot 15 item outputs)
+  const bool atomic = !c->deterministic;
+  float* item_stats = nullptr;
+  if (atomic) {
+    SCT_TRY(stage_buf(c, 14, 8 * s->n_items * sizeof(float), (void**)&item_stats));
+    SCT_CUDA_TRY(cudaMemsetAsync(item_stats, 0, 8 * s->n_items * sizeof(float), c->stream));
+  } else {
+    SCT_TRY(stage_buf(c, 14, 2 * s->n_pairs * sizeof(float4), (void**)&pair_stats));
+  }
+  SCT_TRY(stage_buf(c, 15, 11 * s->n_items * sizeof(float), (void**)&item_grads));
   if (chunks <= 0) {
-    launch_raster_backward_stats(c, s, dL, pair_stats);
+    launch_raster_backward_stats(c, s, dL, pair_stats, 0, 0, item_stats);
   } else {
     for (int k = 0; k < chunks; ++k) {
       const int v0 = (int)((int64_t)s->n_views * k / chunks), v1 = (int)((int64_t)s->n_views * (k + 1) / chunks);
       SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_copy[k], 0));
-      launch_raster_backward_stats(c, s, dL, pair_stats, v0, v1 - v0);
+      launch_raster_backward_stats(c, s, dL, pair_stats, v0, v1 - v0, item_stats);
     }
   }
-  launch_raster_chain(c, s, *cloud, pair_stats, item_grads);
+  if (atomic) {
+    launch_raster_chain(c, s, *cloud, reinterpret_cast<const float4*>(item_stats), item_grads, true);
+  } else {
+    launch_raster_chain(c, s, *cloud, pair_stats, item_grads);
+  }
   launch_raster_finalize(c, s, *cloud, item_grads, grads, stats);
-  dev_free(c, pair_stats);
-  dev_free(c, item_grads);
   SCT_CUDA_TRY(cudaGetLastError());
   return SCT_OK;
 }

@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
     const long long i = item - v * m;
     // fixed-order reduction over the item's tiles (rasterizer.cpp:245-257)
     double S0 = 0, S1x = 0, S1y = 0, Sxx = 0, Syy = 0, Sxy = 0;
-    const int32_t p0 = offset[item], p1 = offset[item + 1];
+    // offset == nullptr: parallel-atomic mode, one pre-summed record per item
+    const int32_t p0 = offset ? offset[item] : (int32_t)item, p1 = offset ? offset[item + 1] : (int32_t)item + 1;
     for (int32_t p = p0; p < p1; ++p) {
       const float4 a = pair_stats[2 * (long long)p];
       const float2 b = *reinterpret_cast<const float2*>(pair_stats + 2 * (long long)p + 1);
@@ -365,13 +366,13 @@ int grid_cap(Ctx* c, long long n, int block) {
 }  // namespace
 
 void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float4* pair_stats,
-                         float* item_grads) {
+                         float* item_grads, bool per_item) {
   if (s->n_items == 0) return;
   {
     KScope _ks(c, "K5_raster_chain");
     raster_chain_kernel<<<grid_cap(c, s->n_items, 128), 128, 0, c->stream>>>(
-        s->m, s->n_items, cl.pos, s->d_prep, s->d_views, s->det, s->rp, s->d_vis, s->d_offset, pair_stats,
-        item_grads);
+        s->m, s->n_items, cl.pos, s->d_prep, s->d_views, s->det, s->rp, s->d_vis, per_item ? nullptr : s->d_offset,
+        pair_stats, item_grads);
   }
 }
 

@@ -226,7 +226,7 @@ constexpr int kBwdThreads = 256;
 __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ rect, const int32_t* __restrict__ offset, int tiles_x, int tiles_per_view, int W,
-    int H, int view0, const float* __restrict__ dL, float* __restrict__ pair_stats) {
+    int H, int view0, const float* __restrict__ dL, float* __restrict__ pair_stats, float* __restrict__ item_stats) {
   const int tile = blockIdx.x;
   const int view = view0 + blockIdx.y;
   const int2 rg = ranges[(long long)view * tiles_per_view + tile];
@@ -349,9 +349,15 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
     const float keep = b0 ? x[1] : x[0];
     const float tot = keep + __shfl_xor_sync(0xffffffffu, send, 1);
     if (valid && s < 6) {
-      const short4 r = s_rect[buf][group];
-      const int slot = s_off[buf][group] + (ty - r.z) * (r.y - r.x + 1) + (tx - r.x);
-      pair_stats[8 * (long long)slot + s] = tot;
+      if (item_stats) {
+        // parallel-atomic mode: the shuffle-reduced pair
+        // statistics go straight into the item's 6 accumulators
+        atomicAdd(item_stats + 8 * (long long)s_items[p * kPass + group] + s, tot);
+      } else {
+        const short4 r = s_rect[buf][group];
+        const int slot = s_off[buf][group] + (ty - r.z) * (r.y - r.x + 1) + (tx - r.x);
+        pair_stats[8 * (long long)slot + s] = tot;
+      }
     }
     if (tid < 32) cp_async_wait_all();
     __syncthreads();  // next buffer visible; this buffer free for re-staging
@@ -400,7 +406,8 @@ void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, in
                                                             s->det.w, s->det.h, v0, images);
 }
 
-void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0, int nv) {
+void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0, int nv,
+                                  float* item_stats) {
   if (s->n_pairs == 0) return;
   if (nv <= 0) nv = s->n_views - v0;
   if (nv <= 0) return;
@@ -409,7 +416,7 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
   KScope _ks(c, "K4_backward_stats");
   backward_stats_kernel<<<grid, kBwdThreads, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
                                                              s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0,
-                                                             dL, reinterpret_cast<float*>(pair_stats));
+                                                             dL, reinterpret_cast<float*>(pair_stats), item_stats);
 }
 
 }  // namespace sct

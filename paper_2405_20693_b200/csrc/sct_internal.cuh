@@ -99,7 +99,7 @@ struct Ctx {
   cudaEvent_t ev_copy[kChunkEvents] = {};
   // grow-only device staging buffers of the host-buffer entry points (a
   // context serialises its calls, so a slot is free again at the next call)
-  static constexpr int kStageSlots = 16;
+  static constexpr int kStageSlots = 20;
   void* stage[kStageSlots] = {};
   size_t stage_bytes[kStageSlots] = {};
 };
@@ -165,8 +165,10 @@ void launch_raster_emit(Ctx* c, int64_t n_items, int64_t m, const short4* rect, 
 void launch_ranges(Ctx* c, int64_t n_pairs, const uint32_t* keys, int tile_bits, int64_t tiles_per_view,
                    int2* ranges);
 void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0 = 0, int nv = 0);
+// item_stats != nullptr: parallel-atomic mode, 8 floats per item accumulated
+// with atomics instead of per-pair slots
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0 = 0,
-                                  int nv = 0);
+                                  int nv = 0, float* item_stats = nullptr);
 void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, const int32_t* offset,
                        int32_t bricks_x, int32_t bricks_y, uint32_t* keys, int32_t* vals);
 void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
@@ -178,8 +180,9 @@ void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t
                                  const int32_t* offset, const sct_cloud& cl, const float* dL,
                                  float4* pair_stats);
 // FP64 chain rules
+// per_item: pair_stats holds one pre-summed 8-float record per item (atomic mode)
 void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float4* pair_stats,
-                         float* item_grads);
+                         float* item_grads, bool per_item = false);
 void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float* item_grads,
                             sct_grads* g, sct_stats* st);
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,

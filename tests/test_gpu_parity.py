@@ -422,3 +422,21 @@ def test_photometric_loss(eng):
         assert vals[i, 0] == pytest.approx(l1, rel=1e-5)
         assert vals[i, 1] == pytest.approx(ds, rel=1e-4, abs=1e-6)
         assert rel_l2(dL[i], (g1 + 0.25 * g2) * 0.5) <= 1e-4
+
+
+def test_render_backward_atomic_mode():
+    """Parallel-atomic reduction mode against the oracle."""
+    import paper_2405_20693_b200 as P
+    eng_a = P.Engine(0, deterministic=False)
+    oc = O.random_cloud(O.Rng(22), 1500, 0.85, 0.02, 0.08)
+    ec, oc = to_engine(P, oc)
+    thetas = [0.37, 3.3]
+    up = np.random.default_rng(2).uniform(-1, 1, (2, 129, 129)).astype(np.float32)
+    fwd = eng_a.render(ec, escan(P, 129), thetas)
+    g = P.CloudGrads(ec.size())
+    eng_a.render_backward(ec, fwd, torch.from_numpy(up).cuda(), g, accumulate_stats=True)
+    og = O.Grads.zeros(oc.m)
+    for v, th in enumerate(thetas):
+        r = O.render(oc, O.test_scanner(129), th)
+        O.render_backward(oc, O.test_scanner(129), th, r, up[v].astype(np.float64), og)
+    check_grads(g, og, what="atomic")
