@@ -458,7 +458,10 @@ def run_voxel(args, eng, vol, world, rank, dev):
     cloud = P.GaussianCloud(ca.s_min, ca.rho_raw, ca.pos, ca.scale_raw, ca.rot, device=dev)
     grid = P.grid_for_extent((-1, -1, -1), (1, 1, 1), (w.n_vox,) * 3)
     nl = (w.n_vox + 7) // 8
-    zb = pdist.shard_z_bricks(nl, rank, world)
+    # balance the slabs by kernel count per brick layer (the phantom occupancy is ellipsoidal)
+    zc = ca.pos.reshape(-1, 3)[:, 2]
+    layer = np.clip(((zc - grid.origin_mm[2]) / grid.spacing_mm[2] // 8).astype(np.int64), 0, nl - 1)
+    zb = pdist.shard_z_bricks(nl, rank, world, list(np.bincount(layer, minlength=nl).astype(float) + 1.0))
     vge, pairs = eng.voxel_work(cloud, grid)
     out = torch.zeros(grid.shape_zyx, dtype=torch.float32, device=dev)
     up = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, grid.shape_zyx).astype(np.float32)).to(dev)

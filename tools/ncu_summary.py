@@ -41,14 +41,14 @@ def main(rep):
         if r[mi] in DETAILS and r[mi] not in d:
             d[r[mi]] = f"{r[vi]} {r[ui]}"
     raw = run(rep, "raw")
-    rh = raw[0]
+    rh, ru = raw[0], raw[1]
     rawper = {}
     for r in raw[2:]:
         rid = r[rh.index("ID")]
         d = {}
         for j, name in enumerate(rh):
             if name in RAW or name.startswith(STALLS):
-                d[name] = r[j]
+                d[name] = f"{r[j]} {ru[j]}".strip()
         rawper[rid] = d
     for (rid, name), d in per.items():
         print(f"=== [{rid}] {name}")
@@ -59,8 +59,8 @@ def main(rep):
         for k in RAW:
             if k in rd:
                 print(f"  {k:70s} {rd[k]}")
-        st = sorted(((float(v.replace(',', '') or 0), k) for k, v in rd.items() if k.startswith(STALLS)
-                     and v not in ("", "n/a")), reverse=True)[:6]
+        st = sorted(((float(v.split()[0].replace(',', '') or 0), k) for k, v in rd.items()
+                     if k.startswith(STALLS) and v.split() and v.split()[0] not in ("", "n/a")), reverse=True)[:6]
         if st:
             print("  top stall reasons (avg warp latency, cycles):")
             for v, k in st:
