@@ -24,11 +24,26 @@ __global__ void __launch_bounds__(256) gauss_prep_kernel(long long m, double s_m
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
-    const dM3 s = d_covariance(k);
+    dM3 r;
+    const dM3 s = d_covariance(k, &r);
     double* o = prep + kPrepStride * i;
 #pragma unroll
     for (int a = 0; a < 9; ++a) o[a] = s.m[a / 3][a % 3];
     o[9] = d_act_density(k.rho_raw);
+    // Sigma^-1 = R diag(1/s^2) R^T (well conditioned: no inversion of Sigma)
+    // and det Sigma = prod s_k^2, for the chain kernel's identities
+    double is2[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) is2[a] = 1.0 / (k.s[a] * k.s[a]);
+    const int ij[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      const int a = ij[e][0], b = ij[e][1];
+      o[10 + e] = __fma_rn(r.m[a][0] * is2[0], r.m[b][0],
+                           __fma_rn(r.m[a][1] * is2[1], r.m[b][1], r.m[a][2] * is2[2] * r.m[b][2]));
+    }
+    o[16] = (k.s[0] * k.s[0]) * (k.s[1] * k.s[1]) * (k.s[2] * k.s[2]);
+    o[17] = 0.0;
   }
 }
 

@@ -68,42 +68,48 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
     const double* pr = prep + kPrepStride * i;
     const Sym3 Sg{pr[0], pr[1], pr[2], pr[4], pr[5], pr[8]};
     const double rho = pr[9];
+    const Sym3 Si{pr[10], pr[11], pr[12], pr[13], pr[14], pr[15]};  // Sigma^-1
+    const double detS = pr[16];
     const double x = fma(W[0], px, fma(W[1], py, W[2] * pz)) + V.t[0];
     const double y = fma(W[3], px, fma(W[4], py, W[5] * pz)) + V.t[1];
     const double z = fma(W[6], px, fma(W[7], py, W[8] * pz)) + V.t[2];
     const double iz = 1.0 / z;
     const double n = sqrt(fma(x, x, fma(y, y, z * z)));
     const double in = 1.0 / n;
-    const double j00 = det.fx * iz, j11 = det.fy * iz;
-    const double j02 = -j00 * x * iz, j12 = -j11 * y * iz;
-    const double j20 = x * in, j21 = y * in, j22 = z * in;
-    // A = J W
-    double A[3][3];
+    // J (geometry.cpp:111-123): rows (a 0 b), (0 c d), (e f g)
+    const double ja = det.fx * iz, jc = det.fy * iz;
+    const double jb = -ja * x * iz, jd = -jc * y * iz;
+    const double je = x * in, jf = y * in, jg = z * in;
+    // A2 = first two rows of A = J W (only they reach the 2D covariance)
+    double A[2][3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      A[0][k] = fma(j00, W[k], j02 * W[6 + k]);
-      A[1][k] = fma(j11, W[3 + k], j12 * W[6 + k]);
-      A[2][k] = fma(j20, W[k], fma(j21, W[3 + k], j22 * W[6 + k]));
+      A[0][k] = fma(ja, W[k], jb * W[6 + k]);
+      A[1][k] = fma(jc, W[3 + k], jd * W[6 + k]);
     }
-    // T = A Sigma, sigma_ray = T A^T (symmetric)
-    double T[3][3];
+    // T2 = A2 Sigma; sigma2_raw = T2 A2^T
+    double T[2][3];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
+    for (int r = 0; r < 2; ++r) {
       T[r][0] = fma(A[r][0], Sg.xx, fma(A[r][1], Sg.xy, A[r][2] * Sg.xz));
       T[r][1] = fma(A[r][0], Sg.xy, fma(A[r][1], Sg.yy, A[r][2] * Sg.yz));
       T[r][2] = fma(A[r][0], Sg.xz, fma(A[r][1], Sg.yz, A[r][2] * Sg.zz));
     }
     auto dot3 = [](const double* a, const double* b) { return fma(a[0], b[0], fma(a[1], b[1], a[2] * b[2])); };
-    const Sym3 R{dot3(T[0], A[0]), dot3(T[0], A[1]), dot3(T[0], A[2]), dot3(T[1], A[1]), dot3(T[1], A[2]),
-                 dot3(T[2], A[2])};
-    const double d2r = fma(R.xx, R.yy, -R.xy * R.xy);
-    const double c00 = fma(R.yy, R.zz, -R.yz * R.yz), c01 = fma(R.xz, R.yz, -R.xy * R.zz),
-                 c02 = fma(R.xy, R.yz, -R.xz * R.yy);
-    const double d3 = fma(R.xx, c00, fma(R.xy, c01, R.xz * c02));
+    const double Rxx = dot3(T[0], A[0]), Rxy = dot3(T[0], A[1]), Ryy = dot3(T[1], A[1]);
+    const double d2r = fma(Rxx, Ryy, -Rxy * Rxy);
+    // cofactors of J: J^-T = C / det J; det(sigma_ray) = det(J)^2 det(Sigma)
+    // (det W = 1) — exact identities that avoid inverting the ill-conditioned
+    // sigma_ray (cond ~1e5)
+    const double C00 = fma(jc, jg, -jd * jf), C01 = jd * je, C02 = -jc * je;
+    const double C10 = jb * jf, C11 = fma(ja, jg, -jb * je), C12 = -ja * jf;
+    const double C20 = -jb * jc, C21 = -ja * jd, C22 = ja * jc;
+    const double detJ = fma(ja, C00, jb * C02);
+    const double d3 = detJ * detJ * detS;
     const double id2r = 1.0 / d2r;
     const double mu = sqrt(2.0 * kPi * d3 * id2r);
     const double amp_pre = (rp.mode == SCT_MODE_RECTIFIED) ? mu * rho : rho;
-    const double s00 = R.xx + rp.eps2, s11 = R.yy + rp.eps2, s01 = R.xy;
+    const double s00 = Rxx + rp.eps2, s11 = Ryy + rp.eps2, s01 = Rxy;
     const double id2 = 1.0 / fma(s00, s11, -s01 * s01);
     const double comp = rp.dilation_compensation ? sqrt(d2r * id2) : 1.0;
     const double amp = amp_pre * comp;
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
     double g01 = h * fma(u00, q01, u01 * q11);
     double g11 = h * fma(u10, q01, u11 * q11);
     // low-pass (rasterizer.cpp:283-293)
-    const double ir00 = R.yy * id2r, ir01 = -R.xy * id2r, ir11 = R.xx * id2r;  // sigma2_raw^-1
+    const double ir00 = Ryy * id2r, ir01 = -Rxy * id2r, ir11 = Rxx * id2r;  // sigma2_raw^-1
     double r00 = 0.0, r01 = 0.0, r11 = 0.0;
     double g_amp_pre = S0;
     if (rp.dilation_compensation) {
@@ -135,52 +141,57 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
     r00 += g00;
     r01 += g01;
     r11 += g11;
-    // amplitude chain (rasterizer.cpp:295-306)
-    Sym3 G{0, 0, 0, 0, 0, 0};
-    double g_rho;
+    // amplitude chain (rasterizer.cpp:295-306): dL/dsigma_ray = hm sigma_ray^-1 + [r 0; 0 0]
+    double g_rho, hm = 0.0;
     if (rp.mode == SCT_MODE_RECTIFIED) {
       g_rho = g_amp_pre * mu;
-      const double hm = 0.5 * g_amp_pre * rho * mu;
-      const double c3 = hm / d3;
-      const double c11 = fma(R.xx, R.zz, -R.xz * R.xz), c12 = fma(R.xy, R.xz, -R.xx * R.yz),
-                   c22 = fma(R.xx, R.yy, -R.xy * R.xy);
-      G = Sym3{c3 * c00, c3 * c01, c3 * c02, c3 * c11, c3 * c12, c3 * c22};
+      hm = 0.5 * g_amp_pre * rho * mu;
       r00 -= hm * ir00;
       r01 -= hm * ir01;
       r11 -= hm * ir11;
     } else {
       g_rho = g_amp_pre;
     }
-    G.xx += r00;
-    G.xy += r01;
-    G.yy += r11;
-    // sigma_ray = A Sigma A^T (rasterizer.cpp:308-311): U = G A, g_sigma = A^T U
-    double U[3][3];
+    // g_Sigma = A^T G A (rasterizer.cpp:311) = hm Sigma^-1 + A2^T r A2
+    double Vr[2][3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      U[0][k] = fma(G.xx, A[0][k], fma(G.xy, A[1][k], G.xz * A[2][k]));
-      U[1][k] = fma(G.xy, A[0][k], fma(G.yy, A[1][k], G.yz * A[2][k]));
-      U[2][k] = fma(G.xz, A[0][k], fma(G.yz, A[1][k], G.zz * A[2][k]));
+      Vr[0][k] = fma(r00, A[0][k], r01 * A[1][k]);
+      Vr[1][k] = fma(r01, A[0][k], r11 * A[1][k]);
     }
-    auto col = [&](int a, int b) { return fma(A[0][a], U[0][b], fma(A[1][a], U[1][b], A[2][a] * U[2][b])); };
-    const Sym3 gS{col(0, 0), 0.5 * (col(0, 1) + col(1, 0)), 0.5 * (col(0, 2) + col(2, 0)), col(1, 1),
-                  0.5 * (col(1, 2) + col(2, 1)), col(2, 2)};
+    auto arA = [&](int a, int b) { return fma(A[0][a], Vr[0][b], A[1][a] * Vr[1][b]); };
+    const Sym3 gS{fma(hm, Si.xx, arA(0, 0)), fma(hm, Si.xy, 0.5 * (arA(0, 1) + arA(1, 0))),
+                  fma(hm, Si.xz, 0.5 * (arA(0, 2) + arA(2, 0))), fma(hm, Si.yy, arA(1, 1)),
+                  fma(hm, Si.yz, 0.5 * (arA(1, 2) + arA(2, 1))), fma(hm, Si.zz, arA(2, 2))};
     // centre chain (rasterizer.cpp:313-321)
-    double gp0 = j00 * gcx, gp1 = j11 * gcy, gp2 = fma(j02, gcx, j12 * gcy);
+    double gp0 = ja * gcx, gp1 = jc * gcy, gp2 = fma(jb, gcx, jd * gcy);
     if (!rp.freeze_jacobian) {
-      // g_A = (G + G^T) A Sigma = 2 U Sigma; g_J = g_A W^T (rasterizer.cpp:310,322-326)
-      double gA[3][3];
+      // g_A = (G + G^T) A Sigma and g_J = g_A W^T (rasterizer.cpp:310,322-326);
+      // with sigma_ray^-1 A Sigma = A^-T and A^-T W^T = J^-T:
+      // g_J = 2 hm J^-T + 2 [r A2 Sigma W^T ; 0]
+      double X[2][3];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        gA[r][0] = 2.0 * fma(U[r][0], Sg.xx, fma(U[r][1], Sg.xy, U[r][2] * Sg.xz));
-        gA[r][1] = 2.0 * fma(U[r][0], Sg.xy, fma(U[r][1], Sg.yy, U[r][2] * Sg.yz));
-        gA[r][2] = 2.0 * fma(U[r][0], Sg.xz, fma(U[r][1], Sg.yz, U[r][2] * Sg.zz));
+      for (int r = 0; r < 2; ++r) {
+        X[r][0] = fma(Vr[r][0], Sg.xx, fma(Vr[r][1], Sg.xy, Vr[r][2] * Sg.xz));
+        X[r][1] = fma(Vr[r][0], Sg.xy, fma(Vr[r][1], Sg.yy, Vr[r][2] * Sg.yz));
+        X[r][2] = fma(Vr[r][0], Sg.xz, fma(Vr[r][1], Sg.yz, Vr[r][2] * Sg.zz));
       }
+      const double k2 = 2.0 * hm / detJ;
       double gJ[3][3];
 #pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) gJ[r][c] = fma(gA[r][0], W[3 * c], fma(gA[r][1], W[3 * c + 1], gA[r][2] * W[3 * c + 2]));
+      for (int c = 0; c < 3; ++c) {
+        gJ[0][c] = 2.0 * fma(X[0][0], W[3 * c], fma(X[0][1], W[3 * c + 1], X[0][2] * W[3 * c + 2]));
+        gJ[1][c] = 2.0 * fma(X[1][0], W[3 * c], fma(X[1][1], W[3 * c + 1], X[1][2] * W[3 * c + 2]));
+      }
+      gJ[0][0] = fma(k2, C00, gJ[0][0]);
+      gJ[0][1] = fma(k2, C01, gJ[0][1]);
+      gJ[0][2] = fma(k2, C02, gJ[0][2]);
+      gJ[1][0] = fma(k2, C10, gJ[1][0]);
+      gJ[1][1] = fma(k2, C11, gJ[1][1]);
+      gJ[1][2] = fma(k2, C12, gJ[1][2]);
+      gJ[2][0] = k2 * C20;
+      gJ[2][1] = k2 * C21;
+      gJ[2][2] = k2 * C22;
       // dJ/dp contractions (jacobian_derivative, rasterizer.cpp:162-191)
       const double in3 = in * in * in;
       const double fz2 = det.fx * iz * iz, gz2 = det.fy * iz * iz;

@@ -15,7 +15,9 @@ constexpr int kTilePx = 16;   // common.hpp:24 kImageTilePx
 constexpr int kTileVox = 8;   // common.hpp:25 kVolumeTileVox
 constexpr double kLog2e = 1.4426950408889634;
 constexpr double kPi = 3.14159265358979323846;  // M_PI
-constexpr int kPrepStride = 10;  // per-Gaussian prep record: Sigma (9 doubles) + rho
+// per-Gaussian prep record (doubles): Sigma (9, d_covariance order) | rho |
+// Sigma^-1 (xx xy xz yy yz zz) | det Sigma | pad
+constexpr int kPrepStride = 18;
 
 // ------------------------------------------------------------------ errors
 void set_error(const std::string& msg);
