@@ -55,7 +55,8 @@ RasterParams make_raster(const sct_raster_opts& o) {
   return r;
 }
 
-KScope::KScope(Ctx* ctx, const char* name, bool engine_kernel) : c(ctx) {
+KScope::KScope(Ctx* ctx, const char* name, bool engine_kernel, cudaStream_t stream)
+    : c(ctx), st(stream ? stream : ctx->stream) {
   if (engine_kernel) c->launches++;
   if (!c->timing) return;
   TimingRec r;
@@ -68,12 +69,12 @@ KScope::KScope(Ctx* ctx, const char* name, bool engine_kernel) : c(ctx) {
       cudaEventCreate(e);
     }
   }
-  cudaEventRecord(r.a, c->stream);
+  cudaEventRecord(r.a, st);
   idx = (int)c->recs.size();
   c->recs.push_back(r);
 }
 KScope::~KScope() {
-  if (idx >= 0) cudaEventRecord(c->recs[idx].b, c->stream);
+  if (idx >= 0) cudaEventRecord(c->recs[idx].b, st);
 }
 
 int dev_alloc(Ctx* c, void** p, size_t bytes) {
@@ -300,7 +301,8 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   if (cudaMallocHost((void**)&c->pinned_count, 64) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     set_error("CUDA error: context host allocations failed");
     return SCT_ERR_CUDA;
@@ -309,6 +311,7 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
     cudaEventCreateWithFlags(&c->ev_compute[a], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_copy[a], cudaEventDisableTiming);
   }
+  cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
   *out = c;
   return SCT_OK;
 }
@@ -325,6 +328,8 @@ int sct_ctx_destroy(sct_ctx* c) {
     if (c->ev_copy[a]) cudaEventDestroy(c->ev_copy[a]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
   return SCT_OK;
 }
@@ -510,19 +515,33 @@ static int render_bwd_impl(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
     SCT_TRY(stage_buf(c, 14, 2 * s->n_pairs * sizeof(float4), (void**)&pair_stats));
   }
   SCT_TRY(stage_buf(c, 15, 11 * s->n_items * sizeof(float), (void**)&item_grads));
-  if (chunks <= 0) {
-    launch_raster_backward_stats(c, s, dL, pair_stats, 0, 0, item_stats);
-  } else {
-    for (int k = 0; k < chunks; ++k) {
-      const int v0 = (int)((int64_t)s->n_views * k / chunks), v1 = (int)((int64_t)s->n_views * (k + 1) / chunks);
-      SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_copy[k], 0));
-      launch_raster_backward_stats(c, s, dL, pair_stats, v0, v1 - v0, item_stats);
+  // View chunks pipeline the two backward stages: the statistics kernel of
+  // chunk k+1 (FP32, issue-bound) runs on the main stream while the FP64
+  // chain of chunk k (latency-bound) runs on the aux stream; items of view v
+  // only receive statistics from tiles of view v, so chunk k's chain needs
+  // nothing from later chunks.
+  // (measured on B200 at cfg3: the overlap is neutral when the upstream
+  // gradient is already resident — the issue-bound K4 yields the slots K5
+  // takes — and pays off on the host-buffer path, where it also hides the
+  // chunked H2D copies; so it is used there only)
+  const int nch = chunks > 0 ? chunks : 1;
+  const float4* chain_src = atomic ? reinterpret_cast<const float4*>(item_stats) : pair_stats;
+  for (int k = 0; k < nch; ++k) {
+    const int v0 = (int)((int64_t)s->n_views * k / nch), v1 = (int)((int64_t)s->n_views * (k + 1) / nch);
+    if (chunks > 0) SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_copy[k], 0));
+    launch_raster_backward_stats(c, s, dL, pair_stats, v0, v1 - v0, item_stats);
+    if (nch > 1) {
+      SCT_CUDA_TRY(cudaEventRecord(c->ev_compute[k], c->stream));
+      SCT_CUDA_TRY(cudaStreamWaitEvent(c->aux_stream, c->ev_compute[k], 0));
+      launch_raster_chain(c, s, *cloud, chain_src, item_grads, atomic, (int64_t)v0 * s->m, (int64_t)v1 * s->m,
+                          c->aux_stream);
+    } else {
+      launch_raster_chain(c, s, *cloud, chain_src, item_grads, atomic);
     }
   }
-  if (atomic) {
-    launch_raster_chain(c, s, *cloud, reinterpret_cast<const float4*>(item_stats), item_grads, true);
-  } else {
-    launch_raster_chain(c, s, *cloud, pair_stats, item_grads);
+  if (nch > 1) {
+    SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->aux_stream));
+    SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   }
   launch_raster_finalize(c, s, *cloud, item_grads, grads, stats);
   SCT_CUDA_TRY(cudaGetLastError());

@@ -36,10 +36,11 @@ struct Sym3 {
 // math is the same chain as rasterizer.cpp:270-327; it does not feed binning,
 // so it need not be bit-identical to the preprocess.
 __global__ void __launch_bounds__(128) raster_chain_kernel(
-    long long m, long long n_items, const float* __restrict__ pos, const double* __restrict__ prep,
-    const ViewParams* __restrict__ views, DetParams det, RasterParams rp, const uint8_t* __restrict__ vis,
-    const int32_t* __restrict__ offset, const float4* __restrict__ pair_stats, float* __restrict__ out) {
-  for (long long item = blockIdx.x * (long long)blockDim.x + threadIdx.x; item < n_items;
+    long long m, long long n_items, long long item0, long long item1, const float* __restrict__ pos,
+    const double* __restrict__ prep, const ViewParams* __restrict__ views, DetParams det, RasterParams rp,
+    const uint8_t* __restrict__ vis, const int32_t* __restrict__ offset, const float4* __restrict__ pair_stats,
+    float* __restrict__ out) {
+  for (long long item = item0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; item < item1;
        item += (long long)gridDim.x * blockDim.x) {
     if (!vis[item]) {  // culled in this view: contributes nothing to the view sums
 #pragma unroll
@@ -377,14 +378,14 @@ int grid_cap(Ctx* c, long long n, int block) {
 }  // namespace
 
 void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float4* pair_stats,
-                         float* item_grads, bool per_item) {
-  if (s->n_items == 0) return;
-  {
-    KScope _ks(c, "K5_raster_chain");
-    raster_chain_kernel<<<grid_cap(c, s->n_items, 128), 128, 0, c->stream>>>(
-        s->m, s->n_items, cl.pos, s->d_prep, s->d_views, s->det, s->rp, s->d_vis, per_item ? nullptr : s->d_offset,
-        pair_stats, item_grads);
-  }
+                         float* item_grads, bool per_item, int64_t item0, int64_t item1, cudaStream_t stream) {
+  if (item1 < 0) item1 = s->n_items;
+  if (item1 <= item0) return;
+  cudaStream_t st = stream ? stream : c->stream;
+  KScope _ks(c, "K5_raster_chain", true, st);
+  raster_chain_kernel<<<grid_cap(c, item1 - item0, 128), 128, 0, st>>>(
+      s->m, s->n_items, item0, item1, cl.pos, s->d_prep, s->d_views, s->det, s->rp, s->d_vis,
+      per_item ? nullptr : s->d_offset, pair_stats, item_grads);
 }
 
 void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float* item_grads, sct_grads* g,

@@ -96,6 +96,10 @@ struct Ctx {
   // copy stream + events for the host-buffer entry points (H2D/D2H of view
   // chunks overlap the compute of neighbouring chunks)
   cudaStream_t copy_stream = nullptr;
+  // second compute stream: the FP64 chain of view chunk k runs on it while
+  // the statistics kernel of chunk k+1 runs on the main stream
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t ev_join = nullptr;
   static constexpr int kChunkEvents = 16;
   cudaEvent_t ev_compute[kChunkEvents] = {};
   cudaEvent_t ev_copy[kChunkEvents] = {};
@@ -114,7 +118,8 @@ int ensure_cub_tmp(Ctx* c, size_t bytes);
 struct KScope {
   Ctx* c;
   int idx = -1;
-  KScope(Ctx* ctx, const char* name, bool engine_kernel = true);
+  cudaStream_t st;
+  KScope(Ctx* ctx, const char* name, bool engine_kernel = true, cudaStream_t stream = nullptr);
   ~KScope();
 };
 int dev_alloc(Ctx* c, void** p, size_t bytes);
@@ -184,7 +189,8 @@ void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t
 // FP64 chain rules
 // per_item: pair_stats holds one pre-summed 8-float record per item (atomic mode)
 void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float4* pair_stats,
-                         float* item_grads, bool per_item = false);
+                         float* item_grads, bool per_item = false, int64_t item0 = 0, int64_t item1 = -1,
+                         cudaStream_t stream = nullptr);
 void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float* item_grads,
                             sct_grads* g, sct_stats* st);
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,
