@@ -205,6 +205,27 @@ int sct_adam_step(sct_ctx* ctx, sct_cloud* params, sct_adam_state* state, const 
                   const double lr[4], double beta1, double beta2, double eps);
 double sct_lr_at(double lr_init, double final_ratio, int32_t t, int32_t iters);
 
+/* ---- adaptive density control (trainer.cpp:167-230) ---------------------- */
+/* Two phases so the caller can size the new cloud: sct_adaptive_plan classifies
+ * every kernel (prune rho < prune_density_threshold; clone or split kernels whose
+ * mean accumulated screen-space gradient exceeds densify_grad_threshold, split
+ * when max scale > split_scale_threshold_frac * max(extent_size_mm)) and reports
+ * the new size, the number of split kernels and counts = {pruned, cloned, split}
+ * (synchronises the context stream). sct_adaptive_apply writes the compacted
+ * survivors (Adam state carried) followed by the new kernels in parent order
+ * (zero Adam state) into out / out_adam (device buffers of new_m kernels).
+ * gauss: device float [6 * n_split] standard-normal draws, per split kernel and
+ * child in the order (z, y, x) — the reference's consumption order — may be
+ * NULL when n_split == 0. The caller resets the gradient statistics. */
+typedef struct sct_ac_plan sct_ac_plan;
+int sct_adaptive_plan(sct_ctx* ctx, const sct_cloud* cloud, const sct_stats* stats, double prune_density_threshold,
+                      double densify_grad_threshold, double split_scale_threshold_frac, double split_factor,
+                      const double extent_size_mm[3], sct_ac_plan** plan, int64_t* new_m, int64_t* n_split,
+                      int32_t counts[3]);
+int sct_adaptive_apply(sct_ctx* ctx, sct_ac_plan* plan, const sct_cloud* cloud, const sct_adam_state* adam,
+                       const float* grad3d_accum, const float* gauss, sct_cloud* out, sct_adam_state* out_adam);
+int sct_adaptive_free(sct_ac_plan* plan);
+
 /* ---- host memory --------------------------------------------------------- */
 /* page-locked host buffers for the _host entry points (full-bandwidth,
  * asynchronous copies); sct_debug_pointer_type reports how the engine's CUDA

@@ -83,6 +83,13 @@ def lib():
             "orc_tv3d": (C.c_int, [I32, D, D, D]),
             "orc_l1": (C.c_int, [C.c_int, D, D, D, D]),
             "orc_dssim": (C.c_int, [C.c_int, C.c_int, D, D, D, D]),
+            "orc_adaptive_control": (VP, [VP, C.c_int, C.c_double, C.POINTER(D), D, I32, D, C.c_double,
+                                          C.c_double, C.c_double, C.c_double, D]),
+            "orc_ac_size": (C.c_int, [VP]),
+            "orc_ac_counts": (None, [VP, C.POINTER(C.c_int)]),
+            "orc_ac_get": (None, [VP, C.c_int, D]),
+            "orc_ac_free": (None, [VP]),
+            "orc_normal_draws": (None, [VP, C.c_int, D]),
             "orc_lr_at": (C.c_double, [C.c_double, C.c_double, C.c_int, C.c_int]),
             "orc_adam_step": (None, [C.c_int64, D, D, D, D, C.c_double, C.c_int, C.c_double, C.c_double,
                                      C.c_double]),
@@ -543,6 +550,41 @@ def dssim_loss(rendered, measured):
     val = C.c_double(0.0)
     _check(lib().orc_dssim(r.shape[1], r.shape[0], _d(r), _d(m), C.byref(val), _d(g)))
     return val.value, g
+
+
+# ----------------------------------------------------------------- adaptive control
+ADAM_KEYS = ("m_rho", "v_rho", "m_pos", "v_pos", "m_scale", "v_scale", "m_rot", "v_rot")
+
+
+def adaptive_control(rng: Rng, cloud: Cloud, adam: dict, stats: Stats, prune_thr=0.005, densify_thr=0.00005,
+                     split_frac=0.01, split_factor=1.6, extent_size=(2.0, 2.0, 2.0)):
+    """trainer.cpp:167-230. Returns (new Cloud, new adam dict, (pruned, cloned, split))."""
+    arrs = [cloud.rho_raw, cloud.pos, cloud.scale_raw, cloud.rot] + [np.ascontiguousarray(adam[k], dtype=np.float64)
+                                                                   for k in ADAM_KEYS]
+    ptrs = (D * 12)(*[_d(a) for a in arrs])
+    ext = np.array(extent_size, dtype=np.float64)
+    h = lib().orc_adaptive_control(rng._h, cloud.m, cloud.s_min, ptrs, _d(stats.grad2d_norm_accum),
+                                   _i32(stats.grad_count), _d(stats.grad3d_accum), prune_thr, densify_thr,
+                                   split_frac, split_factor, _d(ext))
+    try:
+        n = lib().orc_ac_size(h)
+        cnt = (C.c_int * 3)()
+        lib().orc_ac_counts(h, cnt)
+        strides = (1, 3, 3, 4, 1, 1, 3, 3, 3, 3, 4, 4)
+        out = []
+        for a in range(12):
+            buf = np.zeros(max(1, strides[a] * n))
+            lib().orc_ac_get(h, a, _d(buf))
+            out.append(buf[: strides[a] * n])
+    finally:
+        lib().orc_ac_free(h)
+    return Cloud(cloud.s_min, *out[:4]), dict(zip(ADAM_KEYS, out[4:])), tuple(cnt)
+
+
+def normal_draws(rng: Rng, n: int) -> np.ndarray:
+    out = np.zeros(max(n, 1))
+    lib().orc_normal_draws(rng._h, n, _d(out))
+    return out[:n]
 
 
 # ----------------------------------------------------------------- optimizer

@@ -1429,6 +1429,124 @@ int orc_dssim(int w, int h, const double* a, const double* b, double* value, dou
   return 0;
 }
 
+// --- adaptive control: trainer.cpp:167-230 (prune / clone / split), with
+// GaussianCloud::remove_kernels (gaussian_cloud.cpp:89-110, order-preserving
+// compaction) and add_kernel (:48-72, fresh zero Adam state), reset_grad_stats.
+// arrays: 0 rho_raw, 1 pos, 2 scale_raw, 3 rot, 4..11 Adam m/v (rho, pos, scale, rot).
+struct ACResult {
+  std::vector<double> a[12];
+  int pruned = 0, cloned = 0, split = 0;
+};
+void* orc_adaptive_control(void* rp, int m, double s_min, const double* const* arrays, const double* norm_acc,
+                           const int32_t* count, const double* g3d, double prune_thr, double densify_thr,
+                           double split_frac, double split_factor, const double* extent_size) {
+  auto& rng = *static_cast<std::mt19937_64*>(rp);
+  const int stride[12] = {1, 3, 3, 4, 1, 1, 3, 3, 3, 3, 4, 4};
+  Cloud c = make_cloud(m, s_min, arrays[0], arrays[1], arrays[2], arrays[3]);
+  auto* res = new ACResult();
+  std::vector<double> rho_raw(arrays[0], arrays[0] + m);
+  std::vector<char> keep(m, 1);
+  for (int i = 0; i < m; ++i)
+    if (c.rho(i) < prune_thr) {
+      keep[i] = 0;
+      ++res->pruned;
+    }
+  struct NK {
+    double rho, pos[3], scale[3], q[4];
+  };
+  std::vector<NK> added;
+  const double size_thr = split_frac * std::max({extent_size[0], extent_size[1], extent_size[2]});
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  for (int i = 0; i < m; ++i) {
+    if (!keep[i]) continue;
+    if (count[i] == 0) continue;
+    const double mean_grad = norm_acc[i] / count[i];
+    if (mean_grad <= densify_thr) continue;
+    const V3 s = c.scalev(i);
+    const double rho_half = 0.5 * c.rho(i);
+    if (rho_half <= 0.0) continue;
+    double qn[4];
+    normalize4(c.rot + 4 * i, qn);  // kernel(i).rotation = quat_raw(i).normalized()
+    if (std::max({s[0], s[1], s[2]}) <= size_thr) {
+      NK ch{};
+      ch.rho = rho_half;
+      for (int k = 0; k < 3; ++k) {
+        ch.pos[k] = c.pos[3 * i + k];
+        ch.scale[k] = s[k];
+      }
+      for (int k = 0; k < 4; ++k) ch.q[k] = qn[k];
+      const double gd[3] = {g3d[3 * i], g3d[3 * i + 1], g3d[3 * i + 2]};
+      const double norm = std::sqrt(gd[0] * gd[0] + gd[1] * gd[1] + gd[2] * gd[2]);
+      if (norm > 0.0) {
+        const double smean = (s[0] + s[1] + s[2]) / 3.0;
+        for (int k = 0; k < 3; ++k) ch.pos[k] -= (smean / norm) * gd[k];
+      }
+      rho_raw[i] = act_density_inv(rho_half);
+      added.push_back(ch);
+      ++res->cloned;
+    } else {
+      keep[i] = 0;
+      const M3 rot = rotation_matrix(c.rot + 4 * i);
+      for (int cc = 0; cc < 2; ++cc) {
+        NK ch{};
+        ch.rho = rho_half;
+        for (int k = 0; k < 3; ++k) {
+          ch.pos[k] = c.pos[3 * i + k];
+          ch.scale[k] = std::max(s[k] / split_factor, s_min * (1.0 + 1e-6));
+        }
+        for (int k = 0; k < 4; ++k) ch.q[k] = qn[k];
+        // Vec3 local(gauss*s.x, gauss*s.y, gauss*s.z): GCC evaluates the
+        // constructor arguments right to left (z draw first)
+        V3 local;
+        local[2] = gauss(rng) * s[2];
+        local[1] = gauss(rng) * s[1];
+        local[0] = gauss(rng) * s[0];
+        const V3 d = mulv(rot, local);
+        for (int k = 0; k < 3; ++k) ch.pos[k] += d[k];
+        added.push_back(ch);
+      }
+      ++res->split;
+    }
+  }
+  // remove_kernels(keep): compaction in order; parent clones keep halved rho_raw
+  for (int a = 0; a < 12; ++a) {
+    const double* src = a == 0 ? rho_raw.data() : arrays[a];
+    for (int i = 0; i < m; ++i)
+      if (keep[i])
+        for (int k = 0; k < stride[a]; ++k) res->a[a].push_back(src[stride[a] * i + k]);
+  }
+  // add_kernel for every new kernel (activated values -> raw, zero Adam state)
+  for (const NK& n : added) {
+    res->a[0].push_back(act_density_inv(n.rho));
+    for (int k = 0; k < 3; ++k) res->a[1].push_back(n.pos[k]);
+    for (int k = 0; k < 3; ++k) res->a[2].push_back(act_scale_inv(n.scale[k], s_min));
+    double q2[4];
+    normalize4(n.q, q2);
+    for (int k = 0; k < 4; ++k) res->a[3].push_back(q2[k]);
+    for (int a = 4; a < 12; ++a)
+      for (int k = 0; k < stride[a]; ++k) res->a[a].push_back(0.0);
+  }
+  return res;
+}
+int orc_ac_size(void* h) { return static_cast<int>(static_cast<ACResult*>(h)->a[0].size()); }
+void orc_ac_counts(void* h, int* out3) {
+  auto* r = static_cast<ACResult*>(h);
+  out3[0] = r->pruned;
+  out3[1] = r->cloned;
+  out3[2] = r->split;
+}
+void orc_ac_get(void* h, int a, double* out) {
+  auto* r = static_cast<ACResult*>(h);
+  std::memcpy(out, r->a[a].data(), r->a[a].size() * sizeof(double));
+}
+void orc_ac_free(void* h) { delete static_cast<ACResult*>(h); }
+// n consecutive draws of one std::normal_distribution(0,1) object
+void orc_normal_draws(void* rp, int n, double* out) {
+  auto& rng = *static_cast<std::mt19937_64*>(rp);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  for (int i = 0; i < n; ++i) out[i] = gauss(rng);
+}
+
 // --- optimizer: trainer.cpp:34-36 lr_at, :144-163 Adam::step
 double orc_lr_at(double lr_init, double ratio, int t, int iters) {
   return lr_init * std::pow(ratio, static_cast<double>(t) / iters);

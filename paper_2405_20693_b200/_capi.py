@@ -88,6 +88,11 @@ SIGNATURES = {
     "sct_adam_step": (C.c_int, [VP, P(sct_cloud), P(sct_adam_state), P(sct_grads), C.c_int32, D, C.c_double,
                                 C.c_double, C.c_double]),
     "sct_lr_at": (C.c_double, [C.c_double, C.c_double, C.c_int32, C.c_int32]),
+    "sct_adaptive_plan": (C.c_int, [VP, P(sct_cloud), P(sct_stats), C.c_double, C.c_double, C.c_double, C.c_double,
+                                    D, P(VP), I64, I64, I32]),
+    "sct_adaptive_apply": (C.c_int, [VP, VP, P(sct_cloud), P(sct_adam_state), VP, VP, P(sct_cloud),
+                                     P(sct_adam_state)]),
+    "sct_adaptive_free": (C.c_int, [VP]),
     "sct_host_alloc": (C.c_int, [P(VP), C.c_size_t]),
     "sct_host_free": (C.c_int, [VP]),
     "sct_debug_pointer_type": (C.c_int, [VP]),

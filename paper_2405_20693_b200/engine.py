@@ -429,6 +429,42 @@ class Engine:
         lrs = (C.c_double * 4)(*[float(x) for x in lr])
         _check(self.lib.sct_adam_step(self._h, C.byref(cl), C.byref(st), C.byref(g), int(t), lrs, beta1, beta2, eps))
 
+    def adaptive_control(self, cloud: GaussianCloud, extent_size_mm: Sequence[float],
+                         prune_density_threshold: float = 0.005, densify_grad_threshold: float = 0.00005,
+                         split_scale_threshold_frac: float = 0.01, split_factor: float = 1.6,
+                         gauss: Optional[torch.Tensor] = None, generator: Optional[torch.Generator] = None):
+        """trainer.cpp:167-230 on the device: prune, clone, split; returns (new cloud with carried /
+        zeroed Adam state and reset statistics, (pruned, cloned, split)). The split positions use
+        6 standard-normal draws per split kernel (z, y, x per child); pass ``gauss`` to supply them
+        (e.g. a reference std::mt19937_64 stream), otherwise they come from torch.randn."""
+        if not split_factor > 1.0:
+            raise ConfigError("train: split_factor must be > 1")
+        cl, st = cloud._c(), cloud._stats_c()
+        ext = (C.c_double * 3)(*[float(x) for x in extent_size_mm])
+        plan, new_m, n_split = C.c_void_p(), C.c_int64(), C.c_int64()
+        counts = (C.c_int32 * 3)()
+        _check(self.lib.sct_adaptive_plan(self._h, C.byref(cl), C.byref(st), float(prune_density_threshold),
+                                          float(densify_grad_threshold), float(split_scale_threshold_frac),
+                                          float(split_factor), ext, C.byref(plan), C.byref(new_m),
+                                          C.byref(n_split), counts))
+        try:
+            n, ns = int(new_m.value), int(n_split.value)
+            e = lambda k: torch.empty(k * n, dtype=torch.float32, device=self.device)
+            out = GaussianCloud(cloud.s_min, e(1), e(3), e(3), e(4), device=self.device)
+            if ns > 0:
+                if gauss is None:
+                    gauss = torch.randn(6 * ns, dtype=torch.float32, device=self.device, generator=generator)
+                gauss = gauss.to(device=self.device, dtype=torch.float32).contiguous()
+                if gauss.numel() < 6 * ns:
+                    raise ConfigError(f"adaptive control: need {6 * ns} normal draws, got {gauss.numel()}")
+            ocl, ost, ast = out._c(), out._adam_c(), cloud._adam_c()
+            _check(self.lib.sct_adaptive_apply(self._h, plan, C.byref(cl), C.byref(ast),
+                                               _ptr(cloud.grad3d_accum), _ptr(gauss) if ns > 0 else None,
+                                               C.byref(ocl), C.byref(ost)))
+        finally:
+            self.lib.sct_adaptive_free(plan)
+        return out, tuple(int(x) for x in counts)
+
 
 class RenderedProjection:
     """rasterizer.hpp:41-51: images + the forward state (tile lists) for the backward."""

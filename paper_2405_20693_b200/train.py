@@ -35,6 +35,13 @@ class TrainConfig:  # trainer.hpp:13-44 (the fields the iteration uses)
     lambda_ssim: float = 0.25
     lambda_tv: float = 0.05
     tv_grid_dim: int = 32
+    adaptive_start: int = 500
+    adaptive_end: int = 15000
+    densify_interval: int = 100
+    densify_grad_threshold: float = 0.00005
+    prune_density_threshold: float = 0.005
+    split_scale_threshold_frac: float = 0.01  # of the max extent side
+    split_factor: float = 1.6
     output_dims: tuple = (64, 64, 64)
     seed: int = 0
     mode: int = 0
@@ -105,4 +112,21 @@ class Trainer:
                lr_at(cfg.lr_scale, cfg.lr_final_ratio, t, cfg.iters),
                lr_at(cfg.lr_rotation, cfg.lr_final_ratio, t, cfg.iters)]
         eng.adam_step(cloud, self.grads, t, lrs)  # trainer.cpp:310-319
-        return {"iter": t, "view": view, "l1": vals[0, 0], "dssim": vals[0, 1], "tv": tv, "total": total}
+        adapted = None
+        if (cfg.adaptive_start <= t <= cfg.adaptive_end and t > cfg.adaptive_start
+                and (t - cfg.adaptive_start) % cfg.densify_interval == 0):  # trainer.cpp:321-323
+            adapted = self.adaptive_control()
+        return {"iter": t, "view": view, "l1": vals[0, 0], "dssim": vals[0, 1], "tv": tv, "total": total,
+                "kernels": self.cloud.size(), "adaptive": adapted}
+
+    def adaptive_control(self, gauss: Optional[torch.Tensor] = None):
+        """trainer.cpp:167-230 on the device; replaces self.cloud (new size, carried Adam state,
+        reset statistics) and resizes the gradient buffer. Returns (pruned, cloned, split)."""
+        cfg = self.cfg
+        ext = [self.scanner.extent_max_mm[k] - self.scanner.extent_min_mm[k] for k in range(3)]
+        self.cloud, counts = self.eng.adaptive_control(
+            self.cloud, ext, prune_density_threshold=cfg.prune_density_threshold,
+            densify_grad_threshold=cfg.densify_grad_threshold,
+            split_scale_threshold_frac=cfg.split_scale_threshold_frac, split_factor=cfg.split_factor, gauss=gauss)
+        self.grads.resize(self.cloud.size(), device=self.eng.device)
+        return counts

@@ -69,3 +69,50 @@ def test_train_steps_match_oracle():
         upd_ref = getattr(oc, k) - p0[k]
         assert rel_l2(upd_gpu, upd_ref) < 2e-2, k
     assert ec.grad_count.sum().item() > 0  # adaptive statistics accumulated (trainer.cpp:288)
+
+
+def test_train_with_adaptive_control():
+    """Iterations with densification inside the loop (trainer.cpp:321-323): the device
+    adaptive-control pass applied to the trainer's own accumulated statistics matches the
+    oracle on the same state, and training continues on the resized cloud."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_2405_20693_b200 as P
+    from paper_2405_20693_b200.train import TrainConfig, Trainer
+
+    res, n_views = 64, 6
+    scanner_o = O.test_scanner(res)
+    angles = O.full_circle_angles(n_views)
+    target = O.random_cloud(O.Rng(5), 80, 0.6, 0.05, 0.15)
+    meas = np.stack([O.render(target, scanner_o, th).image for th in angles]).astype(np.float32)
+    oc = O.random_cloud(O.Rng(7), 300, 0.6, 0.01, 0.12)
+    f32 = [np.asarray(a, dtype=np.float32) for a in (oc.rho_raw, oc.pos, oc.scale_raw, oc.rot)]
+    cfg = TrainConfig(iters=100, output_dims=(32, 32, 32), tv_grid_dim=8, adaptive_start=2, densify_interval=3,
+                      densify_grad_threshold=1e-6, prune_density_threshold=0.05)
+    eng = P.Engine(0)
+    tr = Trainer(eng, P.GaussianCloud(oc.s_min, *f32), P.ScannerConfig(detector_res_px=(res, res)), angles,
+                 torch.from_numpy(meas), cfg)
+    sizes = []
+    for _ in range(4):  # t = 1..4; t = 5 is the first densification step
+        sizes.append(tr.step()["kernels"])
+    # state before the densification pass, as the oracle sees it
+    c = tr.cloud
+    h = lambda t: t.detach().cpu().numpy().astype(np.float64)
+    ocl = O.Cloud(c.s_min, h(c.rho_raw), h(c.pos), h(c.scale_raw), h(c.rot))
+    st = O.Stats(h(c.grad2d_norm_accum), c.grad_count.cpu().numpy().copy(), h(c.grad3d_accum))
+    onc, oad, ocnt = O.adaptive_control(O.Rng(17), ocl, {k: h(v) for k, v in c.adam.items()}, st,
+                                        cfg.prune_density_threshold, cfg.densify_grad_threshold,
+                                        cfg.split_scale_threshold_frac, cfg.split_factor, (2.0, 2.0, 2.0))
+    draws = torch.from_numpy(O.normal_draws(O.Rng(17), 6 * ocnt[2]).astype(np.float32))
+    counts = tr.adaptive_control(gauss=draws)
+    assert counts == tuple(ocnt) and sum(counts) > 0
+    assert tr.cloud.size() == onc.m
+    np.testing.assert_allclose(h(tr.cloud.pos), onc.pos, atol=2e-6, rtol=0)
+    for k in O.ADAM_KEYS:
+        np.testing.assert_array_equal(tr.cloud.adam[k].cpu().numpy(), oad[k].astype(np.float32))
+    for _ in range(6):  # keeps training (and densifying at t = 5, 8) on the resized cloud
+        out = tr.step()
+        assert np.isfinite(float(out["total"]))
+        sizes.append(out["kernels"])
+    assert tr.grads.flat().numel() == 11 * tr.cloud.size()
+    assert len(set(sizes)) > 1, sizes

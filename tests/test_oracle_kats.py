@@ -417,3 +417,39 @@ def test_clone_halving_mass():  # test_trainer.cpp:213-230
     cloned = cloned.concat(raw_half)
     after = O.render(cloned, cfg, 0.7).image
     assert np.abs(after - before).max() < 1e-6
+
+
+# ----------------------------------------------------------- adaptive control (test_trainer.cpp:150-231)
+def _stats(m):
+    return O.Stats.zeros(m)
+
+
+def _adam(m):
+    return {k: np.zeros(n) for k, n in zip(O.ADAM_KEYS, (m, m, 3 * m, 3 * m, 3 * m, 3 * m, 4 * m, 4 * m))}
+
+
+def test_adaptive_control_prune_only():
+    rng = O.Rng(223)
+    c = O.random_cloud(rng, 5, 0.3, 0.05, 0.15)
+    faint = O.kernels_to_cloud(c.s_min, [1e-4], [[0.5, 0.5, 0.5]], [[0.1, 0.1, 0.1]], [[1, 0, 0, 0]])
+    c = c.concat(faint)
+    nc, _, cnt = O.adaptive_control(rng, c, _adam(6), _stats(6))
+    assert cnt == (1, 0, 0) and nc.m == 5
+
+
+def test_adaptive_control_clone_and_split():
+    c = O.kernels_to_cloud(2e-4, [0.8], [[0.1, 0.2, 0.3]], [[0.01, 0.01, 0.01]], [[1, 0, 0, 0]])
+    st = _stats(1)
+    st.grad2d_norm_accum[0], st.grad_count[0], st.grad3d_accum[0] = 1.0, 1, 1.0
+    nc, na, cnt = O.adaptive_control(O.Rng(223), c, _adam(1), st)
+    assert cnt == (0, 1, 0) and nc.m == 2
+    np.testing.assert_allclose(nc.rho(), [0.4, 0.4], rtol=1e-9)
+    assert np.linalg.norm(nc.pos[:3] - nc.pos[3:]) > 0.0
+    assert na["m_rho"][1] == 0.0
+    c = O.kernels_to_cloud(2e-4, [0.8], [[0.1, 0.2, 0.3]], [[0.1, 0.1, 0.1]], [[1, 0, 0, 0]])
+    st = _stats(1)
+    st.grad2d_norm_accum[0], st.grad_count[0] = 1.0, 1
+    nc, _, cnt = O.adaptive_control(O.Rng(223), c, _adam(1), st)
+    assert cnt == (0, 0, 1) and nc.m == 2
+    np.testing.assert_allclose(nc.rho(), [0.4, 0.4], rtol=1e-9)
+    np.testing.assert_allclose(nc.scale()[:, 0], [0.1 / 1.6] * 2, rtol=1e-9)
