@@ -265,12 +265,12 @@ def run_engine(args):
     rf = None
     for name in ("K3_composite", "K4_backward_stats"):
         ms, n = kt[name]
-        ach = flops_per_gpe[name] * gpe / (ms / n / 1000.0) / 1e12
+        ach = flops_per_gpe[name] * gpe / (ms / args.steps / 1000.0) / 1e12  # all launches of a step
         kernels[name]["achieved_tflops"] = ach
         kernels[name]["frac_fp32_peak"] = ach / fp32_peak
     dname = dom if dom in flops_per_gpe else max(flops_per_gpe, key=lambda k: kt[k][0])
     ms, n = kt[dname]
-    ach = flops_per_gpe[dname] * gpe / (ms / n / 1000.0) / 1e12
+    ach = flops_per_gpe[dname] * gpe / (ms / args.steps / 1000.0) / 1e12
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
@@ -281,7 +281,7 @@ def run_engine(args):
           "frac": ach / fp32_peak, "traffic": traffic,
           "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json); "
                          "non-tensor path, so neither the copy nor the bf16 GEMM peak applies",
-          "algorithmic": f"{flops_per_gpe[dname]} FLOP/GPE x {gpe} GPE per launch (SURVEY.md §8d)",
+          "algorithmic": f"{flops_per_gpe[dname]} FLOP/GPE x {gpe} GPE per step, all launches of the kernel in a step (SURVEY.md §8d)",
           "dominant_by_time": dom}
 
     # --- e2e through the host-buffer C ABI
@@ -505,7 +505,7 @@ def run_voxel(args, eng, vol, world, rank, dev):
     for name, fl in (("K7_voxel_eval", 27), ("K8_voxel_backward_stats", 51)):
         if name in kt and world == 1:
             ms, n = kt[name]
-            ach = fl * vge / (ms / n / 1000.0) / 1e12
+            ach = fl * vge / (ms / args.steps / 1000.0) / 1e12
             kern[name]["achieved_tflops"] = ach
             kern[name]["frac_fp32_peak"] = ach / fp32_peak
     return {"metric": "voxelized voxels/sec (fwd+bwd)", "value": grid.voxel_count() * args.steps / (total_ms / 1e3),
