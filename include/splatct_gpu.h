@@ -226,6 +226,28 @@ int sct_adaptive_apply(sct_ctx* ctx, sct_ac_plan* plan, const sct_cloud* cloud, 
                        const float* grad3d_accum, const float* gauss, sct_cloud* out, sct_adam_state* out_adam);
 int sct_adaptive_free(sct_ac_plan* plan);
 
+/* ---- multi-GPU exchange (NCCL) ------------------------ */
+/* Views are sharded across ranks, each rank holding the whole cloud; the only
+ * exchange is a sum over ranks of the per-kernel gradients (and adaptive
+ * statistics). NCCL is resolved at run time (libnccl.so.2); these return
+ * SCT_ERR_CUDA if it is absent and SCT_ERR_CONFIG without a communicator.
+ * sct_nccl_unique_id: rank 0 makes the id, the caller broadcasts it.
+ * sct_ctx_comm_init: context-owned communicator (destroyed with the context).
+ * sct_ctx_set_comm: caller-owned ncclComm_t (NULL detaches).
+ * sct_allreduce_grads: in-place sum of grads (and stats when non-NULL).
+ * sct_render_bwd_allreduce / sct_voxelize_bwd_allreduce: as sct_render_bwd /
+ * sct_voxelize_bwd, but every rank gets grads += sum over ranks of the ranks'
+ * contributions (one contiguous 11*M-float collective on the context stream). */
+int sct_nccl_unique_id(uint8_t id[128]);
+int sct_ctx_comm_init(sct_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id[128]);
+int sct_ctx_set_comm(sct_ctx* ctx, void* nccl_comm);
+int sct_ctx_comm_info(sct_ctx* ctx, int32_t* nranks, int32_t* rank);
+int sct_allreduce_grads(sct_ctx* ctx, int64_t m, sct_grads* grads, sct_stats* stats);
+int sct_render_bwd_allreduce(sct_ctx* ctx, sct_fwd* state, const sct_cloud* cloud, const float* dL_dimages,
+                             sct_grads* grads, sct_stats* stats);
+int sct_voxelize_bwd_allreduce(sct_ctx* ctx, const sct_cloud* cloud, const sct_grid* grid, double cull_mahalanobis,
+                               int32_t z_brick_begin, int32_t z_brick_end, const float* dL_dvol, sct_grads* grads);
+
 /* ---- host memory --------------------------------------------------------- */
 /* page-locked host buffers for the _host entry points (full-bandwidth,
  * asynchronous copies); sct_debug_pointer_type reports how the engine's CUDA

@@ -93,6 +93,14 @@ SIGNATURES = {
     "sct_adaptive_apply": (C.c_int, [VP, VP, P(sct_cloud), P(sct_adam_state), VP, VP, P(sct_cloud),
                                      P(sct_adam_state)]),
     "sct_adaptive_free": (C.c_int, [VP]),
+    "sct_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "sct_ctx_comm_init": (C.c_int, [VP, C.c_int32, C.c_int32, C.POINTER(C.c_uint8)]),
+    "sct_ctx_set_comm": (C.c_int, [VP, VP]),
+    "sct_ctx_comm_info": (C.c_int, [VP, I32, I32]),
+    "sct_allreduce_grads": (C.c_int, [VP, C.c_int64, P(sct_grads), P(sct_stats)]),
+    "sct_render_bwd_allreduce": (C.c_int, [VP, VP, P(sct_cloud), VP, P(sct_grads), P(sct_stats)]),
+    "sct_voxelize_bwd_allreduce": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, C.c_int32, C.c_int32, VP,
+                                             P(sct_grads)]),
     "sct_host_alloc": (C.c_int, [P(VP), C.c_size_t]),
     "sct_host_free": (C.c_int, [VP]),
     "sct_debug_pointer_type": (C.c_int, [VP]),

@@ -319,6 +319,7 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
 int sct_ctx_destroy(sct_ctx* c) {
   if (!c) return SCT_OK;
   cudaStreamSynchronize(c->stream);
+  comm_release(c);
   if (c->cub_tmp) cudaFree(c->cub_tmp);
   for (int a = 0; a < Ctx::kStageSlots; ++a)
     if (c->stage[a]) cudaFree(c->stage[a]);
@@ -488,8 +489,8 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
 
 // chunks > 0: the upstream gradient arrives in `chunks` view chunks, chunk k
 // signalled by ctx->ev_copy[k]; K4 for chunk k waits only for its own copy.
-static int render_bwd_impl(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
-                           sct_stats* stats, int chunks) {
+int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
+                         sct_stats* stats, int chunks) {
   if (!c || !s || !grads || !dL) {
     set_error("ConfigError: null argument");
     return SCT_ERR_CONFIG;
@@ -550,7 +551,7 @@ static int render_bwd_impl(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
 
 int sct_render_bwd(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
                    sct_stats* stats) {
-  return render_bwd_impl(c, s, cloud, dL, grads, stats, 0);
+  return sct_render_bwd_chunked(c, s, cloud, dL, grads, stats, 0);
 }
 
 int sct_fwd_free(sct_fwd* s) {
@@ -757,7 +758,7 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
       SCT_CUDA_TRY(cudaMemcpyAsync(*sd[a], sh[a], sb[a], cudaMemcpyHostToDevice, c->stream));
     }
   }
-  int rc = render_bwd_impl(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, chunks);
+  int rc = sct_render_bwd_chunked(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, chunks);
   if (rc == SCT_OK) {
     for (int a = 0; a < 4; ++a)
       SCT_CUDA_TRY(cudaMemcpyAsync(gh[a], *gd[a], n[a] * sizeof(float), cudaMemcpyDeviceToHost, c->stream));

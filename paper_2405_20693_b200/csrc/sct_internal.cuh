@@ -108,7 +108,12 @@ struct Ctx {
   static constexpr int kStageSlots = 20;
   void* stage[kStageSlots] = {};
   size_t stage_bytes[kStageSlots] = {};
+  // NCCL communicator of the *_allreduce entry points (comm.cu): an
+  // ncclComm_t, owned by the context when made by sct_ctx_comm_init
+  void* comm = nullptr;
+  bool comm_owned = false;
 };
+void comm_release(Ctx* c);
 int stage_buf(Ctx* c, int slot, size_t bytes, void** p);
 
 int ensure_cub_tmp(Ctx* c, size_t bytes);
@@ -155,6 +160,11 @@ struct sct_fwd {
 };
 
 struct sct_ctx : public sct::Ctx {};
+
+// render backward with optional view-chunk pipelining (capi.cu; chunks = 0:
+// the device-resident path); shared by the plain and the NCCL entry points
+extern "C" int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL,
+                                      sct_grads* grads, sct_stats* stats, int chunks);
 
 // ------------------------------------------------------------------ kernel entry points
 namespace sct {

@@ -331,17 +331,20 @@ class Engine:
 
     def render_backward(self, cloud: GaussianCloud, fwd: "RenderedProjection", dL_dimage: torch.Tensor,
                         grads: CloudGrads, accumulate_stats: bool = False):
+        dl = self._check_upstream(fwd, dL_dimage)
+        cl, g = cloud._c(), grads._c()
+        st = cloud._stats_c() if accumulate_stats else None
+        _check(self.lib.sct_render_bwd(self._h, fwd._state, C.byref(cl), _ptr(dl), C.byref(g),
+                                       C.byref(st) if st is not None else None))
+
+    def _check_upstream(self, fwd: "RenderedProjection", dL_dimage: torch.Tensor) -> torch.Tensor:
         dl = dL_dimage
         expect = (len(fwd.thetas), fwd.config.height, fwd.config.width)
         if dl.dim() == 2:
             dl = dl.unsqueeze(0)
         if tuple(dl.shape) != expect:
             raise DimMismatch("render_backward: upstream gradient dims mismatch")
-        dl = dl.to(device=self.device, dtype=torch.float32).contiguous()
-        cl, g = cloud._c(), grads._c()
-        st = cloud._stats_c() if accumulate_stats else None
-        _check(self.lib.sct_render_bwd(self._h, fwd._state, C.byref(cl), _ptr(dl), C.byref(g),
-                                       C.byref(st) if st is not None else None))
+        return dl.to(device=self.device, dtype=torch.float32).contiguous()
 
     def project_kernels(self, cloud: GaussianCloud, config: ScannerConfig, theta_rad: float,
                         opts: Optional[RasterOptions] = None):
@@ -378,6 +381,19 @@ class Engine:
         cl, g, gr = cloud._c(), grid._c(), grads._c()
         _check(self.lib.sct_voxelize_bwd(self._h, C.byref(cl), C.byref(g), float(opts.cull_mahalanobis), zb0, zb1,
                                          _ptr(dl), C.byref(gr)))
+
+    def voxelize_backward_allreduce(self, cloud: GaussianCloud, grid: GridSpec, dL_dV: torch.Tensor,
+                                    grads: CloudGrads, opts: Optional[VoxelizeOptions] = None,
+                                    z_bricks: Optional[tuple] = None):
+        """voxelize_backward over this rank's z-slab, summed over all ranks before the += into grads."""
+        opts = opts or VoxelizeOptions()
+        if tuple(dL_dV.shape) != grid.shape_zyx:
+            raise DimMismatch("voxelize_backward: gradient volume dims mismatch")
+        dl = dL_dV.to(device=self.device, dtype=torch.float32).contiguous()
+        zb0, zb1 = z_bricks if z_bricks is not None else (0, 2 ** 31 - 1)
+        cl, g, gr = cloud._c(), grid._c(), grads._c()
+        _check(self.lib.sct_voxelize_bwd_allreduce(self._h, C.byref(cl), C.byref(g), float(opts.cull_mahalanobis),
+                                                   zb0, zb1, _ptr(dl), C.byref(gr)))
 
     def voxel_bins(self, cloud: GaussianCloud, grid: GridSpec, opts: Optional[VoxelizeOptions] = None):
         opts = opts or VoxelizeOptions()
@@ -428,6 +444,45 @@ class Engine:
         cl, st, g = cloud._c(), cloud._adam_c(), grads._c()
         lrs = (C.c_double * 4)(*[float(x) for x in lr])
         _check(self.lib.sct_adam_step(self._h, C.byref(cl), C.byref(st), C.byref(g), int(t), lrs, beta1, beta2, eps))
+
+    # ------------------------------------------------------------- multi-GPU exchange (comm.cu)
+    def comm_init(self, rank: int, world: int, unique_id: Optional[bytes] = None):
+        """Context-owned NCCL communicator over `world` ranks. Without ``unique_id`` the id is
+        made on rank 0 and broadcast over the default torch.distributed group."""
+        if unique_id is None:
+            buf = (C.c_uint8 * 128)()
+            if rank == 0:
+                _check(self.lib.sct_nccl_unique_id(buf))
+            if world > 1:
+                import torch.distributed as dist
+                obj = [bytes(buf)]
+                dist.broadcast_object_list(obj, src=0)
+                unique_id = obj[0]
+            else:
+                unique_id = bytes(buf)
+        uid = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(self.lib.sct_ctx_comm_init(self._h, int(world), int(rank), uid))
+
+    def comm_info(self):
+        n, r = C.c_int32(), C.c_int32()
+        _check(self.lib.sct_ctx_comm_info(self._h, C.byref(n), C.byref(r)))
+        return int(n.value), int(r.value)
+
+    def allreduce_grads(self, grads: CloudGrads, cloud: Optional[GaussianCloud] = None):
+        """In-place sum over ranks of grads (and of cloud's adaptive statistics when given)."""
+        g = grads._c()
+        st = cloud._stats_c() if cloud is not None else None
+        _check(self.lib.sct_allreduce_grads(self._h, int(grads.rho_raw.numel()), C.byref(g),
+                                            C.byref(st) if st is not None else None))
+
+    def render_backward_allreduce(self, cloud: GaussianCloud, fwd: "RenderedProjection", dL_dimage: torch.Tensor,
+                                  grads: CloudGrads, accumulate_stats: bool = False):
+        """render_backward whose contribution is summed over all ranks before the += into grads."""
+        dl = self._check_upstream(fwd, dL_dimage)
+        cl, g = cloud._c(), grads._c()
+        st = cloud._stats_c() if accumulate_stats else None
+        _check(self.lib.sct_render_bwd_allreduce(self._h, fwd._state, C.byref(cl), _ptr(dl), C.byref(g),
+                                                 C.byref(st) if st is not None else None))
 
     def adaptive_control(self, cloud: GaussianCloud, extent_size_mm: Sequence[float],
                          prune_density_threshold: float = 0.005, densify_grad_threshold: float = 0.00005,
