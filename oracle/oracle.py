@@ -28,8 +28,8 @@ VP = C.c_void_p
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(_HERE, "splatct_oracle.cpp")
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+    newest = max(os.path.getmtime(os.path.join(_HERE, s)) for s in ("splatct_oracle.cpp", "fixtures_oracle.cpp"))
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < newest:
         subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return _LIB_PATH
 
