@@ -226,6 +226,34 @@ int sct_adaptive_apply(sct_ctx* ctx, sct_ac_plan* plan, const sct_cloud* cloud, 
                        const float* grad3d_accum, const float* gauss, sct_cloud* out, sct_adam_state* out_adam);
 int sct_adaptive_free(sct_ac_plan* plan);
 
+/* ---- fixture generation (simulator.cpp, fdk.cpp) ------- */
+/* Analytic ellipsoid phantom (simulator.cpp:31-65): ellipsoids [n][8] host
+ * {intensity, a, b, c, x0, y0, z0, phi_rad} in coordinates normalised to the
+ * box [lo, hi]; vol device [Z][Y][X] on grid_for_extent(lo, hi, dims); dims >= 16. */
+int sct_phantom(sct_ctx* ctx, int32_t n_ellipsoids, const double* ellipsoids, const double lo_mm[3],
+                const double hi_mm[3], const int32_t dims[3], float* vol);
+/* Quadrature projector project_volume (simulator.cpp:109-132), FP64 per ray:
+ * images device [n_views][H][W] (clean log-domain line integrals). */
+int sct_project_volume(sct_ctx* ctx, const float* vol, const sct_grid* grid, const sct_scanner* scanner,
+                       const double* thetas, int32_t n_views, double step_mm, float* images);
+/* add_noise (simulator.cpp:143-157) in place on HOST images [n_views][H][W]; view v uses
+ * the reference stream view_rng(seed, view0 + v) (simulator.cpp:134-141), so results equal
+ * simulate_projections bit-for-bit up to the fp32 storage. Views run in parallel threads. */
+int sct_add_noise_host(float* images, int32_t n_views, int32_t w, int32_t h, double i0, double gauss_sigma,
+                       uint64_t seed, int32_t view0);
+/* fdk_reconstruct (fdk.cpp:53-134): images device [n_views][H][W]; window 0 ramp, 1 Hann,
+ * 2 auto (Hann when n_views < 100); vol device [Z][Y][X]. n_views < 2 -> SCT_ERR_DATA. */
+int sct_fdk(sct_ctx* ctx, const float* images, int32_t n_views, const sct_scanner* scanner, const double* thetas,
+            const sct_grid* grid, int32_t window, float* vol);
+/* exact nearest-neighbour distances (fdk.cpp:136-201): points/out device double [n][3] / [n]. */
+int sct_nn_distances(sct_ctx* ctx, int64_t n, const double* points, double* out);
+/* sample_init_cloud (fdk.cpp:203-247) with std::mt19937_64(seed): out = device cloud with
+ * out->m == count (raw parameters as add_kernel stores them). Too few voxels above the
+ * threshold -> SCT_ERR_DATA (TooFewOccupiedVoxels). Synchronises the context stream. */
+int sct_sample_init_cloud(sct_ctx* ctx, const float* vol, const sct_grid* grid, int32_t count,
+                          double density_threshold, double density_scale, double s_min_mm, uint64_t seed,
+                          sct_cloud* out);
+
 /* ---- multi-GPU exchange (NCCL) ------------------------ */
 /* Views are sharded across ranks, each rank holding the whole cloud; the only
  * exchange is a sum over ranks of the per-kernel gradients (and adaptive

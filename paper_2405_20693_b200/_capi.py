@@ -93,6 +93,14 @@ SIGNATURES = {
     "sct_adaptive_apply": (C.c_int, [VP, VP, P(sct_cloud), P(sct_adam_state), VP, VP, P(sct_cloud),
                                      P(sct_adam_state)]),
     "sct_adaptive_free": (C.c_int, [VP]),
+    "sct_phantom": (C.c_int, [VP, C.c_int32, D, D, D, I32, VP]),
+    "sct_project_volume": (C.c_int, [VP, VP, P(sct_grid), P(sct_scanner), D, C.c_int32, C.c_double, VP]),
+    "sct_add_noise_host": (C.c_int, [VP, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64,
+                                     C.c_int32]),
+    "sct_fdk": (C.c_int, [VP, VP, C.c_int32, P(sct_scanner), D, P(sct_grid), C.c_int32, VP]),
+    "sct_nn_distances": (C.c_int, [VP, C.c_int64, VP, VP]),
+    "sct_sample_init_cloud": (C.c_int, [VP, VP, P(sct_grid), C.c_int32, C.c_double, C.c_double, C.c_double,
+                                        C.c_uint64, P(sct_cloud)]),
     "sct_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "sct_ctx_comm_init": (C.c_int, [VP, C.c_int32, C.c_int32, C.POINTER(C.c_uint8)]),
     "sct_ctx_set_comm": (C.c_int, [VP, VP]),
