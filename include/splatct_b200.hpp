@@ -68,6 +68,7 @@ struct ScannerConfig {  // geometry.hpp:12-31
   Vec3 extent_min_mm{-1.0, -1.0, -1.0};
   Vec3 extent_max_mm{1.0, 1.0, 1.0};
   double near_clip_mm = 0.0;
+  bool parallel_beam = false;  // extension; the reference is cone-beam only
 
   sct_scanner c() const {
     sct_scanner s{};
@@ -82,6 +83,7 @@ struct ScannerConfig {  // geometry.hpp:12-31
       s.extent_max_mm[k] = extent_max_mm[k];
     }
     s.near_clip_mm = near_clip_mm;
+    s.parallel_beam = parallel_beam ? 1 : 0;
     return s;
   }
 };

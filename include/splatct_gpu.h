@@ -69,6 +69,9 @@ typedef struct {
   double extent_min_mm[3];
   double extent_max_mm[3];
   double near_clip_mm;     /* <= 0 selects 1% of l_so_mm (geometry.hpp:24-28) */
+  int32_t parallel_beam;   /* 0: cone beam (the reference); 1: parallel beam, an extension
+                              (orthographic: detector mm = scanner mm, J = diag(fx, fy, 1),
+                              no near-clip cull); zero-initialise for the reference behaviour */
 } sct_scanner;
 
 typedef struct {

@@ -53,9 +53,12 @@ Grid make_grid(const int* dims, const double* origin, const double* spacing) {
 // geo = [l_so, l_sd, det_w_mm, det_h_mm, ext_min(3), ext_max(3), near_clip]
 struct Scan {
   double l_so, l_sd, dw, dh;
-  int w, h;
+  int w, h, parallel;
 };
-Scan make_scan(const double* geo, const int* res) { return Scan{geo[0], geo[1], geo[2], geo[3], res[0], res[1]}; }
+// res = {W, H, parallel_beam}
+Scan make_scan(const double* geo, const int* res) {
+  return Scan{geo[0], geo[1], geo[2], geo[3], res[0], res[1], res[2]};
+}
 
 struct Rot {
   double m[3][3];
@@ -85,10 +88,15 @@ void pixel_ray(const Scan& s, double theta, int u, int v, V3d& origin, V3d& dir)
   const double du = s.dw / s.w, dv = s.dh / s.h;
   const double xd = (u + 0.5) * du - 0.5 * s.dw;
   const double yd = (v + 0.5) * dv - 0.5 * s.dh;
+  const Rot r = view_rot(theta);
+  if (s.parallel) {  // parallel-beam extension: ray through (xd, yd) along the view axis
+    origin = mul_t(r, V3d{{xd, yd, -s.l_so}});
+    dir = mul_t(r, V3d{{0.0, 0.0, 1.0}});
+    return;
+  }
   V3d d{{xd, yd, s.l_sd}};
   const double n = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
   for (int k = 0; k < 3; ++k) d[k] = d[k] / n;
-  const Rot r = view_rot(theta);
   const V3d t{{0.0, 0.0, s.l_so}};
   const V3d src = mul_t(r, t);
   for (int k = 0; k < 3; ++k) origin[k] = -src[k];

@@ -148,11 +148,12 @@ class ScannerConfig:  # geometry.hpp:12-31 (angles passed per call)
     extent_min_mm: tuple = (-1.0, -1.0, -1.0)
     extent_max_mm: tuple = (1.0, 1.0, 1.0)
     near_clip_mm: float = 0.0
+    parallel_beam: bool = False  # extension: orthographic projection (no reference code)
 
     def _geo(self):
         g = np.array([self.l_so_mm, self.l_sd_mm, *self.detector_size_mm, *self.extent_min_mm,
                       *self.extent_max_mm, self.near_clip_mm], dtype=np.float64)
-        r = np.array(self.detector_res_px, dtype=np.int32)
+        r = np.array([*self.detector_res_px, int(self.parallel_beam)], dtype=np.int32)
         return g, r
 
 

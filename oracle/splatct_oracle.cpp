@@ -166,6 +166,7 @@ struct Scanner {
   int det_res_px[2] = {128, 128};
   double extent_min_mm[3] = {-1, -1, -1}, extent_max_mm[3] = {1, 1, 1};
   double near_clip_mm = 0.0;
+  int parallel = 0;  // parallel-beam extension (not in the reference)
   double near_clip() const { return near_clip_mm > 0.0 ? near_clip_mm : 0.01 * l_so_mm; }
 };
 struct View {
@@ -176,6 +177,7 @@ struct Det {
   double fx = 0, fy = 0, cx = 0, cy = 0;
   int w = 0, h = 0;
   double near = 0;
+  bool parallel = false;
 };
 
 // geometry.cpp:76-86
@@ -193,8 +195,10 @@ static Det detector_model(const Scanner& c) {
   Det d;
   d.w = c.det_res_px[0];
   d.h = c.det_res_px[1];
-  d.fx = c.l_sd_mm * d.w / c.det_size_mm[0];
-  d.fy = c.l_sd_mm * d.h / c.det_size_mm[1];
+  // parallel beam: orthographic, detector mm == scanner mm (no magnification)
+  d.parallel = c.parallel != 0;
+  d.fx = d.parallel ? d.w / c.det_size_mm[0] : c.l_sd_mm * d.w / c.det_size_mm[0];
+  d.fy = d.parallel ? d.h / c.det_size_mm[1] : c.l_sd_mm * d.h / c.det_size_mm[1];
   d.cx = 0.5 * d.w;
   d.cy = 0.5 * d.h;
   d.near = c.near_clip();
@@ -203,6 +207,12 @@ static Det detector_model(const Scanner& c) {
 // geometry.cpp:105-109
 static V3 ray_space_point(const Det& d, const V3& p) {
   V3 r;
+  if (d.parallel) {  // affine map: phi(p) = (fx x + cx, fy y + cy, z)
+    r[0] = d.fx * p[0] + d.cx;
+    r[1] = d.fy * p[1] + d.cy;
+    r[2] = p[2];
+    return r;
+  }
   r[0] = d.fx * p[0] / p[2] + d.cx;
   r[1] = d.fy * p[1] / p[2] + d.cy;
   r[2] = norm3(p);
@@ -213,6 +223,12 @@ static M3 local_jacobian(const Det& d, const V3& p) {
   const double z = p[2], x = p[0], y = p[1];
   const double n = norm3(p);
   M3 j;
+  if (d.parallel) {  // constant: diag(fx, fy, 1)
+    j.m[0][0] = d.fx; j.m[0][1] = 0.0; j.m[0][2] = 0.0;
+    j.m[1][0] = 0.0; j.m[1][1] = d.fy; j.m[1][2] = 0.0;
+    j.m[2][0] = 0.0; j.m[2][1] = 0.0; j.m[2][2] = 1.0;
+    return j;
+  }
   j.m[0][0] = d.fx / z; j.m[0][1] = 0.0; j.m[0][2] = -d.fx * x / (z * z);
   j.m[1][0] = 0.0; j.m[1][1] = d.fy / z; j.m[1][2] = -d.fy * y / (z * z);
   j.m[2][0] = x / n; j.m[2][1] = y / n; j.m[2][2] = z / n;
@@ -382,7 +398,7 @@ static bool project_impl(const Cloud& c, int i, const View& view, const Det& det
   const V3 p = c.position(i);
   V3 p_s = mulv(view.rot, p);
   for (int k = 0; k < 3; ++k) p_s[k] = p_s[k] + view.t[k];
-  if (p_s[2] < det.near) return false;
+  if (!det.parallel && p_s[2] < det.near) return false;  // no source plane for parallel rays
 
   const M3 jac = local_jacobian(det, p_s);
   const M3 a = mul(jac, view.rot);
@@ -520,6 +536,7 @@ static M3 jacobian_derivative(const Det& det, const V3& p, int c) {
   const double n = norm3(p);
   const double n3 = n * n * n;
   M3 d;
+  if (det.parallel) return d;  // J is constant
   switch (c) {
     case 0:
       d.m[0][2] = -det.fx / (z * z);
@@ -619,8 +636,10 @@ static void raster_chain(const Cloud& c, const View& view, const Det& det, const
   V3 g_ps;
   {
     const double zc = ch.p_s[2];
-    const double d00 = det.fx / zc, d02 = -det.fx * ch.p_s[0] / (zc * zc);
-    const double d11 = det.fy / zc, d12 = -det.fy * ch.p_s[1] / (zc * zc);
+    const double d00 = det.parallel ? det.fx : det.fx / zc;
+    const double d02 = det.parallel ? 0.0 : -det.fx * ch.p_s[0] / (zc * zc);
+    const double d11 = det.parallel ? det.fy : det.fy / zc;
+    const double d12 = det.parallel ? 0.0 : -det.fy * ch.p_s[1] / (zc * zc);
     g_ps[0] += d00 * g_center.x;
     g_ps[1] += d11 * g_center.y;
     g_ps[2] += d02 * g_center.x + d12 * g_center.y;
@@ -1011,6 +1030,7 @@ Scanner make_scanner(const double* geo, const int* res) {
   s.near_clip_mm = geo[10];
   s.det_res_px[0] = res[0];
   s.det_res_px[1] = res[1];
+  s.parallel = res[2];  // res = {W, H, parallel_beam}
   return s;
 }
 RasterOptions make_opts(const double* o) {
@@ -1154,6 +1174,20 @@ void orc_pixel_ray(const double* geo, const int* res, double theta, int u, int v
   const double xd = (u + 0.5) * du - 0.5 * c.det_size_mm[0];
   const double yd = (v + 0.5) * dv - 0.5 * c.det_size_mm[1];
   V3 ds;
+  if (c.parallel) {  // parallel beam: ray through the detector point along the view axis
+    const View view = view_transform(c, theta);
+    V3 os;
+    os[0] = xd; os[1] = yd; os[2] = -view.t[2];
+    const V3 o = mulv_t(view.rot, os);
+    V3 dz;
+    dz[0] = 0.0; dz[1] = 0.0; dz[2] = 1.0;
+    const V3 d = mulv_t(view.rot, dz);
+    for (int k = 0; k < 3; ++k) {
+      origin[k] = o[k];
+      dir[k] = d[k];
+    }
+    return;
+  }
   ds[0] = xd; ds[1] = yd; ds[2] = c.l_sd_mm;
   const double n = norm3(ds);
   for (int k = 0; k < 3; ++k) ds[k] = ds[k] / n;

@@ -22,7 +22,7 @@ VP = C.c_void_p
 class sct_scanner(C.Structure):
     _fields_ = [("l_so_mm", C.c_double), ("l_sd_mm", C.c_double), ("det_size_mm", C.c_double * 2),
                 ("det_res_px", C.c_int32 * 2), ("extent_min_mm", C.c_double * 3),
-                ("extent_max_mm", C.c_double * 3), ("near_clip_mm", C.c_double)]
+                ("extent_max_mm", C.c_double * 3), ("near_clip_mm", C.c_double), ("parallel_beam", C.c_int32)]
 
 
 class sct_raster_opts(C.Structure):

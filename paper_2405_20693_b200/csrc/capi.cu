@@ -24,8 +24,9 @@ DetParams make_det(const sct_scanner& s) {  // geometry.cpp:88-98
   DetParams d;
   d.w = s.det_res_px[0];
   d.h = s.det_res_px[1];
-  d.fx = s.l_sd_mm * d.w / s.det_size_mm[0];
-  d.fy = s.l_sd_mm * d.h / s.det_size_mm[1];
+  d.parallel = s.parallel_beam != 0;
+  d.fx = d.parallel ? d.w / s.det_size_mm[0] : s.l_sd_mm * d.w / s.det_size_mm[0];
+  d.fy = d.parallel ? d.h / s.det_size_mm[1] : s.l_sd_mm * d.h / s.det_size_mm[1];
   d.cx = 0.5 * d.w;
   d.cy = 0.5 * d.h;
   d.near_clip = s.near_clip_mm > 0.0 ? s.near_clip_mm : 0.01 * s.l_so_mm;

@@ -78,9 +78,11 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
     const double n = sqrt(fma(x, x, fma(y, y, z * z)));
     const double in = 1.0 / n;
     // J (geometry.cpp:111-123): rows (a 0 b), (0 c d), (e f g)
-    const double ja = det.fx * iz, jc = det.fy * iz;
-    const double jb = -ja * x * iz, jd = -jc * y * iz;
-    const double je = x * in, jf = y * in, jg = z * in;
+    // parallel beam: J = diag(fx, fy, 1), constant
+    const bool par = det.parallel != 0;
+    const double ja = par ? det.fx : det.fx * iz, jc = par ? det.fy : det.fy * iz;
+    const double jb = par ? 0.0 : -ja * x * iz, jd = par ? 0.0 : -jc * y * iz;
+    const double je = par ? 0.0 : x * in, jf = par ? 0.0 : y * in, jg = par ? 1.0 : z * in;
     // A2 = first two rows of A = J W (only they reach the 2D covariance)
     double A[2][3];
 #pragma unroll
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
                   fma(hm, Si.yz, 0.5 * (arA(1, 2) + arA(2, 1))), fma(hm, Si.zz, arA(2, 2))};
     // centre chain (rasterizer.cpp:313-321)
     double gp0 = ja * gcx, gp1 = jc * gcy, gp2 = fma(jb, gcx, jd * gcy);
-    if (!rp.freeze_jacobian) {
+    if (!rp.freeze_jacobian && !par) {  // dJ/dp = 0 for parallel beam
       // g_A = (G + G^T) A Sigma and g_J = g_A W^T (rasterizer.cpp:310,322-326);
       // with sigma_ray^-1 A Sigma = A^-T and A^-T W^T = J^-T:
       // g_J = 2 hm J^-T + 2 [r A2 Sigma W^T ; 0]

@@ -103,7 +103,7 @@ struct ViewRot {
 
 struct ScanGeo {
   double l_so, l_sd, dw, dh;
-  int w, h;
+  int w, h, parallel;
 };
 
 __device__ __forceinline__ void view_rot(double s, double c, double m[9]) {
@@ -129,15 +129,23 @@ __global__ void project_volume_kernel(const float* __restrict__ vol, VolGeo g, S
     const double du = sc.dw / sc.w, dv = sc.dh / sc.h;
     const double xd = (u + 0.5) * du - 0.5 * sc.dw;
     const double yd = (v + 0.5) * dv - 0.5 * sc.dh;
-    const double nrm = sqrt(xd * xd + yd * yd + sc.l_sd * sc.l_sd);
-    const double ds[3] = {xd / nrm, yd / nrm, sc.l_sd / nrm};
     double m[9];
     view_rot(sincos_v[view].x, sincos_v[view].y, m);
     double o[3], d[3];
+    if (sc.parallel) {  // parallel-beam extension: ray through (xd, yd) along the view axis
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      o[k] = -(m[0 * 3 + k] * 0.0 + m[1 * 3 + k] * 0.0 + m[2 * 3 + k] * sc.l_so);
-      d[k] = m[0 * 3 + k] * ds[0] + m[1 * 3 + k] * ds[1] + m[2 * 3 + k] * ds[2];
+      for (int k = 0; k < 3; ++k) {
+        o[k] = m[0 * 3 + k] * xd + m[1 * 3 + k] * yd + m[2 * 3 + k] * -sc.l_so;
+        d[k] = m[0 * 3 + k] * 0.0 + m[1 * 3 + k] * 0.0 + m[2 * 3 + k] * 1.0;
+      }
+    } else {
+      const double nrm = sqrt(xd * xd + yd * yd + sc.l_sd * sc.l_sd);
+      const double ds[3] = {xd / nrm, yd / nrm, sc.l_sd / nrm};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        o[k] = -(m[0 * 3 + k] * 0.0 + m[1 * 3 + k] * 0.0 + m[2 * 3 + k] * sc.l_so);
+        d[k] = m[0 * 3 + k] * ds[0] + m[1 * 3 + k] * ds[1] + m[2 * 3 + k] * ds[2];
+      }
     }
     // simulator.cpp:90-107 box_clip
     double t0 = 0.0, t1 = INFINITY;
@@ -397,7 +405,7 @@ int sct_project_volume(sct_ctx* c, const float* vol, const sct_grid* grid, const
   double2* sc = nullptr;
   SCT_TRY(upload_sincos(c, thetas, n_views, &sc));
   const ScanGeo g{scanner->l_so_mm, scanner->l_sd_mm, scanner->det_size_mm[0], scanner->det_size_mm[1],
-                  scanner->det_res_px[0], scanner->det_res_px[1]};
+                  scanner->det_res_px[0], scanner->det_res_px[1], scanner->parallel_beam != 0};
   const int64_t n = (int64_t)g.w * g.h * n_views;
   {
     KScope _ks(c, "K13_project_volume");
@@ -451,6 +459,10 @@ int sct_fdk(sct_ctx* c, const float* images, int32_t n_views, const sct_scanner*
   }
   SCT_TRY(check_vol_grid(grid));
   SCT_TRY(check_scan(scanner));
+  if (scanner->parallel_beam) {
+    set_error("ConfigError: fdk: cone-beam geometry only (fdk.cpp is Feldkamp-Davis-Kress)");
+    return SCT_ERR_CONFIG;
+  }
   if (n_views < 2) {  // fdk.cpp:55
     set_error("DataError: fdk: need at least 2 views");
     return SCT_ERR_DATA;
@@ -480,7 +492,7 @@ int sct_fdk(sct_ctx* c, const float* images, int32_t n_views, const sct_scanner*
   SCT_TRY(stage_buf(c, 19, gk.size() * sizeof(double), (void**)&d_gk));
   SCT_CUDA_TRY(cudaMemcpyAsync(d_gk, gk.data(), gk.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   SCT_TRY(dev_alloc(c, (void**)&filt, (size_t)n_views * w * h * sizeof(double)));
-  const ScanGeo sg{scanner->l_so_mm, scanner->l_sd_mm, scanner->det_size_mm[0], scanner->det_size_mm[1], w, h};
+  const ScanGeo sg{scanner->l_so_mm, scanner->l_sd_mm, scanner->det_size_mm[0], scanner->det_size_mm[1], w, h, 0};
   const size_t smem = (3 * (size_t)w - 1) * sizeof(double);
   if (smem > 48 * 1024) SCT_CUDA_TRY(cudaFuncSetAttribute(fdk_filter_kernel,
                                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -32,19 +32,32 @@ __device__ __forceinline__ bool d_project(const double p[3], const dM3& sigma, d
     ps[i] = v.rot[3 * i + 0] * p[0] + v.rot[3 * i + 1] * p[1] + v.rot[3 * i + 2] * p[2];
     ps[i] = ps[i] + v.t[i];
   }
-  if (ps[2] < det.near_clip) return false;
+  const bool par = det.parallel != 0;  // parallel beam: affine map, no source plane
+  if (!par && ps[2] < det.near_clip) return false;
   const double x = ps[0], y = ps[1], z = ps[2];
   const double n = sqrt(x * x + y * y + z * z);
   dM3 jac;
-  jac.m[0][0] = det.fx / z;
-  jac.m[0][1] = 0.0;
-  jac.m[0][2] = -det.fx * x / (z * z);
-  jac.m[1][0] = 0.0;
-  jac.m[1][1] = det.fy / z;
-  jac.m[1][2] = -det.fy * y / (z * z);
-  jac.m[2][0] = x / n;
-  jac.m[2][1] = y / n;
-  jac.m[2][2] = z / n;
+  if (par) {
+    jac.m[0][0] = det.fx;
+    jac.m[0][1] = 0.0;
+    jac.m[0][2] = 0.0;
+    jac.m[1][0] = 0.0;
+    jac.m[1][1] = det.fy;
+    jac.m[1][2] = 0.0;
+    jac.m[2][0] = 0.0;
+    jac.m[2][1] = 0.0;
+    jac.m[2][2] = 1.0;
+  } else {
+    jac.m[0][0] = det.fx / z;
+    jac.m[0][1] = 0.0;
+    jac.m[0][2] = -det.fx * x / (z * z);
+    jac.m[1][0] = 0.0;
+    jac.m[1][1] = det.fy / z;
+    jac.m[1][2] = -det.fy * y / (z * z);
+    jac.m[2][0] = x / n;
+    jac.m[2][1] = y / n;
+    jac.m[2][2] = z / n;
+  }
   dM3 W;
 #pragma unroll
   for (int i = 0; i < 9; ++i) W.m[i / 3][i % 3] = v.rot[i];
@@ -68,8 +81,8 @@ __device__ __forceinline__ bool d_project(const double p[3], const dM3& sigma, d
     comp = sqrt(d2r / d_det2(s2));
     amp *= comp;
   }
-  const double cx = det.fx * x / z + det.cx;
-  const double cy = det.fy * y / z + det.cy;
+  const double cx = par ? det.fx * x + det.cx : det.fx * x / z + det.cx;
+  const double cy = par ? det.fy * y + det.cy : det.fy * y / z + det.cy;
   const double rx = rp.cull * sqrt(s2.m[0][0]);
   const double ry = rp.cull * sqrt(s2.m[1][1]);
   if (cx + rx < 0.0 || cx - rx > (double)det.w || cy + ry < 0.0 || cy - ry > (double)det.h) return false;
@@ -79,7 +92,7 @@ __device__ __forceinline__ bool d_project(const double p[3], const dM3& sigma, d
   o.conic = d_inv2(s2);
   o.amp = amp;
   o.mu = mu;
-  o.depth = n;
+  o.depth = par ? z : n;
   o.ps[0] = x;
   o.ps[1] = y;
   o.ps[2] = z;

@@ -50,6 +50,7 @@ struct DetParams {
   int32_t w, h;
   double near_clip;
   int32_t tiles_x, tiles_y;
+  int32_t parallel;  // parallel-beam extension: phi(p) = (fx x + cx, fy y + cy, z)
 };
 DetParams make_det(const sct_scanner& s);
 ViewParams make_view(const sct_scanner& s, double theta);

@@ -82,6 +82,7 @@ class ScannerConfig:
     extent_min_mm: tuple = (-1.0, -1.0, -1.0)
     extent_max_mm: tuple = (1.0, 1.0, 1.0)
     near_clip_mm: float = 0.0
+    parallel_beam: bool = False  # extension (no reference code): orthographic projection
 
     def near_clip(self):
         return self.near_clip_mm if self.near_clip_mm > 0.0 else 0.01 * self.l_so_mm
@@ -103,6 +104,7 @@ class ScannerConfig:
         s.extent_min_mm[:] = [float(x) for x in self.extent_min_mm]
         s.extent_max_mm[:] = [float(x) for x in self.extent_max_mm]
         s.near_clip_mm = self.near_clip_mm
+        s.parallel_beam = int(bool(self.parallel_beam))
         return s
 
 
