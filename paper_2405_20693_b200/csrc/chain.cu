@@ -35,6 +35,7 @@ struct Sym3 {
 // Sigma and rho read from the per-Gaussian prep record, FMAs allowed. The
 // math is the same chain as rasterizer.cpp:270-327; it does not feed binning,
 // so it need not be bit-identical to the preprocess.
+template <bool kParallel>
 __global__ void __launch_bounds__(128) raster_chain_kernel(
     long long m, long long n_items, long long item0, long long item1, const float* __restrict__ pos,
     const double* __restrict__ prep, const ViewParams* __restrict__ views, DetParams det, RasterParams rp,
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
     const double in = 1.0 / n;
     // J (geometry.cpp:111-123): rows (a 0 b), (0 c d), (e f g)
     // parallel beam: J = diag(fx, fy, 1), constant
-    const bool par = det.parallel != 0;
+    constexpr bool par = kParallel;
     const double ja = par ? det.fx : det.fx * iz, jc = par ? det.fy : det.fy * iz;
     const double jb = par ? 0.0 : -ja * x * iz, jd = par ? 0.0 : -jc * y * iz;
     const double je = par ? 0.0 : x * in, jf = par ? 0.0 : y * in, jg = par ? 1.0 : z * in;
@@ -385,9 +386,10 @@ void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const fl
   if (item1 <= item0) return;
   cudaStream_t st = stream ? stream : c->stream;
   KScope _ks(c, "K5_raster_chain", true, st);
-  raster_chain_kernel<<<grid_cap(c, item1 - item0, 128), 128, 0, st>>>(
-      s->m, s->n_items, item0, item1, cl.pos, s->d_prep, s->d_views, s->det, s->rp, s->d_vis,
-      per_item ? nullptr : s->d_offset, pair_stats, item_grads);
+  auto kern = s->det.parallel ? raster_chain_kernel<true> : raster_chain_kernel<false>;
+  kern<<<grid_cap(c, item1 - item0, 128), 128, 0, st>>>(s->m, s->n_items, item0, item1, cl.pos, s->d_prep,
+                                                        s->d_views, s->det, s->rp, s->d_vis,
+                                                        per_item ? nullptr : s->d_offset, pair_stats, item_grads);
 }
 
 void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float* item_grads, sct_grads* g,
