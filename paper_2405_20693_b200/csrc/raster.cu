@@ -13,6 +13,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -138,79 +139,87 @@ __device__ __forceinline__ Run4 run4(float dx, float A, float A2, float bdy, flo
   return r;
 }
 
-// K3: one warp per (tile, view), four warps per CTA; lane = 1 row x 8
-// columns (two 4-pixel runs sharing the per-row setup). Each warp stages its
-// own tile list through shared memory 32 records at a time (one coalesced
+// K3: one warp per (tile, view); lane = 1 row x 8 columns (two 4-pixel runs
+// sharing the per-row setup). Persistent: each warp takes the next (view,
+// tile) from a global counter, so no warp waits for sibling warps with longer
+// lists and residency stays at the register limit until the tail. Each warp
+// stages its list through shared memory 32 records at a time (one coalesced
 // gather per lane) and synchronises only itself (__syncwarp); the next
 // chunk's records are fetched into registers while the current chunk is
 // evaluated, so the gather latency overlaps the arithmetic.
 constexpr int kCompWarps = 4;
 __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
-    int tiles_x, int tiles_per_view, int W, int H, int view0, float* __restrict__ images) {
+    int tiles_x, int tiles_per_view, int W, int H, int view0, int total, int* __restrict__ work,
+    float* __restrict__ images) {
   __shared__ float4 sa[kCompWarps][32];
   __shared__ float4 sb[kCompWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kCompWarps + warp;
-  const int view = view0 + blockIdx.y;
-  if (tile >= tiles_per_view) return;
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int row = lane >> 1;
-  const int u0 = tx * kTilePx + (lane & 1) * 8;
-  const int v = ty * kTilePx + row;
-  const float py = (float)v + 0.5f;
-  const float px0 = (float)u0 + 0.5f;
-  const int2 rg = ranges[(long long)view * tiles_per_view + tile];
-  float acc[8];
+  for (;;) {
+    int w = 0;
+    if (lane == 0) w = atomicAdd(work, 1);
+    w = __shfl_sync(0xffffffffu, w, 0);
+    if (w >= total) break;
+    const int view = view0 + w / tiles_per_view;
+    const int tile = w % tiles_per_view;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int u0 = tx * kTilePx + (lane & 1) * 8;
+    const int v = ty * kTilePx + row;
+    const float py = (float)v + 0.5f;
+    const float px0 = (float)u0 + 0.5f;
+    const int2 rg = ranges[(long long)view * tiles_per_view + tile];
+    float acc[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-  float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na;
-  if (rg.x + lane < rg.y) {
-    const long long item = vals[rg.x + lane];
-    na = __ldg(rec + 2 * item);
-    nb = __ldg(rec + 2 * item + 1);
-  }
-  for (int base = rg.x; base < rg.y; base += 32) {
-    const int n = min(32, rg.y - base);
-    __syncwarp();
-    sa[warp][lane] = na;
-    sb[warp][lane] = nb;
-    __syncwarp();
-    if (base + 32 + lane < rg.y) {  // prefetch the next chunk
-      const long long item = vals[base + 32 + lane];
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+    float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na;
+    if (rg.x + lane < rg.y) {
+      const long long item = vals[rg.x + lane];
       na = __ldg(rec + 2 * item);
       nb = __ldg(rec + 2 * item + 1);
     }
+    for (int base = rg.x; base < rg.y; base += 32) {
+      const int n = min(32, rg.y - base);
+      __syncwarp();
+      sa[warp][lane] = na;
+      sb[warp][lane] = nb;
+      __syncwarp();
+      if (base + 32 + lane < rg.y) {  // prefetch the next chunk
+        const long long item = vals[base + 32 + lane];
+        na = __ldg(rec + 2 * item);
+        nb = __ldg(rec + 2 * item + 1);
+      }
 #pragma unroll 2
-    for (int j = 0; j < n; ++j) {
-      const float4 a = sa[warp][j];  // cx cy amp*2^-64 K
-      const float4 b = sb[warp][j];  // A B C 2A
-      const float dy = py - a.y;
-      const float bdy = b.y * dy;
-      const float apb = b.x + bdy;
-      const float cdy2o = fmaf(b.z * dy, dy, 64.f);
-      const float dx = px0 - a.x;
-      const Run4 e0 = run4(dx, b.x, b.w, bdy, apb, cdy2o, a.w);
-      const Run4 e1 = run4(dx + 4.f, b.x, b.w, bdy, apb, cdy2o, a.w);
-      acc[0] = fmaf(a.z, e0.e0, acc[0]);
-      acc[1] = fmaf(a.z, e0.e1, acc[1]);
-      acc[2] = fmaf(a.z, e0.e2, acc[2]);
-      acc[3] = fmaf(a.z, e0.e3, acc[3]);
-      acc[4] = fmaf(a.z, e1.e0, acc[4]);
-      acc[5] = fmaf(a.z, e1.e1, acc[5]);
-      acc[6] = fmaf(a.z, e1.e2, acc[6]);
-      acc[7] = fmaf(a.z, e1.e3, acc[7]);
+      for (int j = 0; j < n; ++j) {
+        const float4 a = sa[warp][j];  // cx cy amp*2^-64 K
+        const float4 b = sb[warp][j];  // A B C 2A
+        const float dy = py - a.y;
+        const float bdy = b.y * dy;
+        const float apb = b.x + bdy;
+        const float cdy2o = fmaf(b.z * dy, dy, 64.f);
+        const float dx = px0 - a.x;
+        const Run4 e0 = run4(dx, b.x, b.w, bdy, apb, cdy2o, a.w);
+        const Run4 e1 = run4(dx + 4.f, b.x, b.w, bdy, apb, cdy2o, a.w);
+        acc[0] = fmaf(a.z, e0.e0, acc[0]);
+        acc[1] = fmaf(a.z, e0.e1, acc[1]);
+        acc[2] = fmaf(a.z, e0.e2, acc[2]);
+        acc[3] = fmaf(a.z, e0.e3, acc[3]);
+        acc[4] = fmaf(a.z, e1.e0, acc[4]);
+        acc[5] = fmaf(a.z, e1.e1, acc[5]);
+        acc[6] = fmaf(a.z, e1.e2, acc[6]);
+        acc[7] = fmaf(a.z, e1.e3, acc[7]);
+      }
     }
-  }
-  if (v < H) {
-    float* out = images + ((long long)view * H + v) * W;
-    if (u0 + 7 < W && (W & 3) == 0) {
-      *reinterpret_cast<float4*>(out + u0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      *reinterpret_cast<float4*>(out + u0 + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
-    } else {
+    if (v < H) {
+      float* out = images + ((long long)view * H + v) * W;
+      if (u0 + 7 < W && (W & 3) == 0) {
+        *reinterpret_cast<float4*>(out + u0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        *reinterpret_cast<float4*>(out + u0 + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      } else {
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (u0 + k < W) out[u0 + k] = acc[k];
+        for (int k = 0; k < 8; ++k)
+          if (u0 + k < W) out[u0 + k] = acc[k];
+      }
     }
   }
 }
@@ -657,10 +666,19 @@ void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, in
   if (nv <= 0) nv = s->n_views - v0;
   if (nv <= 0) return;
   const int T = s->det.tiles_x * s->det.tiles_y;
-  dim3 grid((T + kCompWarps - 1) / kCompWarps, nv);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, composite_kernel, 32 * kCompWarps, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const long long total = (long long)T * nv;
+  const int blocks = (int)std::min<long long>((long long)c->sm_count * per_sm, (total + kCompWarps - 1) / kCompWarps);
+  int* work = nullptr;
+  if (stage_buf(c, 20, sizeof(int) * 4, (void**)&work) != SCT_OK) return;
+  cudaMemsetAsync(work, 0, sizeof(int), c->stream);
   KScope _ks(c, "K3_composite");
-  composite_kernel<<<grid, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
-                                                            s->det.w, s->det.h, v0, images);
+  composite_kernel<<<blocks, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
+                                                              s->det.w, s->det.h, v0, (int)total, work, images);
 }
 
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0, int nv,

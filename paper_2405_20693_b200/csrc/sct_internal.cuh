@@ -106,7 +106,7 @@ struct Ctx {
   cudaEvent_t ev_copy[kChunkEvents] = {};
   // grow-only device staging buffers of the host-buffer entry points (a
   // context serialises its calls, so a slot is free again at the next call)
-  static constexpr int kStageSlots = 20;
+  static constexpr int kStageSlots = 24;  // 20: K3 work counter
   void* stage[kStageSlots] = {};
   size_t stage_bytes[kStageSlots] = {};
   // NCCL communicator of the *_allreduce entry points (comm.cu): an
