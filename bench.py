@@ -89,6 +89,9 @@ class ClockSampler:
 
     def start(self):
         import threading
+        if os.environ.get("BENCH_NO_CLOCKS"):  # diagnosis only: no sampling thread
+            self.err = "disabled by BENCH_NO_CLOCKS"
+            return
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -243,7 +246,9 @@ def run_engine(args):
     kt = eng.timing_report()
     eng.set_timing(False)
     launches = eng.kernel_launches() - launches0
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    print(f"[bench] device per-step ms: {[round(x, 3) for x in step_ms]}", file=sys.stderr)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

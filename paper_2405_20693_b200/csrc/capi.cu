@@ -139,11 +139,12 @@ static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64
 }
 
 // stable LSD radix sort of (key, value) pairs on key bits [0, end_bit)
-static int sort_pairs(Ctx* c, uint32_t*& keys, int32_t*& vals, int64_t n, int end_bit) {
+template <typename KeyT>
+static int sort_pairs(Ctx* c, KeyT*& keys, int32_t*& vals, int64_t n, int end_bit) {
   if (n == 0) return SCT_OK;
-  uint32_t* k2 = nullptr;
+  KeyT* k2 = nullptr;
   int32_t* v2 = nullptr;
-  SCT_TRY(dev_alloc(c, (void**)&k2, n * sizeof(uint32_t)));
+  SCT_TRY(dev_alloc(c, (void**)&k2, n * sizeof(KeyT)));
   SCT_TRY(dev_alloc(c, (void**)&v2, n * sizeof(int32_t)));
   size_t tmp = 0;
   SCT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, k2, vals, v2, (int)n, 0, end_bit, c->stream));
@@ -432,9 +433,9 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   s->thetas.assign(thetas, thetas + n_views);
   const int64_t T = (int64_t)s->det.tiles_x * s->det.tiles_y;
   s->tile_bits = bits_for((uint64_t)T);
-  if (s->tile_bits + bits_for((uint64_t)n_views) > 32) {
+  if (s->tile_bits > 31 || s->m * (int64_t)n_views > INT32_MAX) {
     delete s;
-    set_error("ConfigError: (view, tile) key exceeds 32 bits; split the views into batches");
+    set_error("ConfigError: more than 2^31 (view, kernel) items or tiles; split the views into batches");
     return SCT_ERR_CONFIG;
   }
   s->n_items = s->m * n_views;
@@ -468,17 +469,28 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   launch_raster_preprocess(c, *cloud, s->d_prep, s->d_views, n_views, s->det, s->rp, s->d_rec, s->d_rect,
                            s->d_count, s->d_vis);
   if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs))) return fail(rc);
-  if ((rc = dev_alloc(c, (void**)&s->d_keys, s->n_pairs * sizeof(uint32_t)))) return fail(rc);
-  if ((rc = dev_alloc(c, (void**)&s->d_vals, s->n_pairs * sizeof(int32_t)))) return fail(rc);
-  launch_raster_emit(c, ni, s->m, s->d_rect, s->d_offset, s->det.tiles_x, s->tile_bits, s->d_keys, s->d_vals);
   // Pairs are emitted view-major (and kernel-ascending within a view), so a
   // STABLE sort on the tile bits alone already groups them by (tile, view)
-  // with each list ascending in kernel index: one or two radix passes fewer
-  // than sorting the full (view, tile) key. The view bits stay in the keys
-  // for the range scan.
-  if (s->tile_bits > 0)
-    if ((rc = sort_pairs(c, s->d_keys, s->d_vals, s->n_pairs, s->tile_bits))) return fail(rc);
-  launch_ranges(c, s->n_pairs, s->d_keys, s->tile_bits, T, s->d_ranges);
+  // with each list ascending in kernel index: fewer radix passes than the
+  // full (view, tile) key, and 16-bit keys whenever the tile index fits.
+  const bool k16 = s->tile_bits <= 16;
+  const size_t ksz = k16 ? sizeof(uint16_t) : sizeof(uint32_t);
+  if ((rc = dev_alloc(c, &s->d_keys, s->n_pairs * ksz))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&s->d_vals, s->n_pairs * sizeof(int32_t)))) return fail(rc);
+  launch_raster_emit(c, ni, s->d_rect, s->d_offset, s->det.tiles_x, s->d_keys, k16, s->d_vals);
+  if (s->tile_bits > 0) {
+    if (k16) {
+      uint16_t* kp = static_cast<uint16_t*>(s->d_keys);
+      rc = sort_pairs(c, kp, s->d_vals, s->n_pairs, s->tile_bits);
+      s->d_keys = kp;
+    } else {
+      uint32_t* kp = static_cast<uint32_t*>(s->d_keys);
+      rc = sort_pairs(c, kp, s->d_vals, s->n_pairs, s->tile_bits);
+      s->d_keys = kp;
+    }
+    if (rc) return fail(rc);
+  }
+  launch_raster_ranges(c, s->n_pairs, s->d_keys, k16, s->d_vals, s->m, T, s->d_ranges);
   if (images) launch_raster_composite(c, s, images);
   if (cudaGetLastError() != cudaSuccess) {
     set_error("CUDA error: kernel launch in sct_render_fwd");

@@ -48,11 +48,13 @@ constexpr int kBwdChunk = 256;  // tile-list entries staged per chunk in K4
 
 namespace {
 
-__global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, long long m,
-                                                          const short4* __restrict__ rect,
+// Keys are the tile index only (16-bit when it fits): pairs are emitted
+// view-major, so a stable sort on the tile groups them by (tile, view) and the
+// view is recovered from the item (value) in the range scan.
+template <typename KeyT>
+__global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, const short4* __restrict__ rect,
                                                           const int32_t* __restrict__ offset, int tiles_x,
-                                                          int tile_bits, uint32_t* __restrict__ keys,
-                                                          int32_t* __restrict__ vals) {
+                                                          KeyT* __restrict__ keys, int32_t* __restrict__ vals) {
   // Warp-cooperative: a warp owns 32 consecutive items, whose pairs occupy one
   // contiguous output range (exclusive-scan order); lanes stride over that
   // range so the key/value stores are coalesced. Each output slot finds its
@@ -88,7 +90,7 @@ __global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, lon
         const int rank = p - oj;
         const int ty = y0 + rank / nx, tx = x0 + rank % nx;
         const long long item = w0 + j;
-        keys[p] = ((uint32_t)(item / m) << tile_bits) | (uint32_t)(ty * tiles_x + tx);
+        keys[p] = (KeyT)(ty * tiles_x + tx);
         vals[p] = (int32_t)item;
       }
     }
@@ -105,6 +107,36 @@ __global__ void __launch_bounds__(256) ranges_kernel(long long n_pairs, const ui
     const long long slot = (long long)(k >> tile_bits) * tiles_per_view + (k & mask);
     if (p == 0 || keys[p - 1] != k) ranges[slot].x = (int)p;
     if (p == n_pairs - 1 || keys[p + 1] != k) ranges[slot].y = (int)(p + 1);
+  }
+}
+
+// (view, tile) ranges of the sorted raster pairs: tile from the key, view
+// from the item (item = view * m + kernel; quotient by a float reciprocal
+// with an exact integer correction). Thread p closes the range at p and opens
+// the one at p + 1 when the slot changes.
+__device__ __forceinline__ int div_m(int x, int m, float inv_m) {
+  int q = (int)((float)x * inv_m);
+  if ((long long)q * m > x) --q;
+  if ((long long)(q + 1) * m <= x) ++q;
+  return q;
+}
+template <typename KeyT>
+__global__ void __launch_bounds__(256) raster_ranges_kernel(long long n_pairs, const KeyT* __restrict__ keys,
+                                                            const int32_t* __restrict__ vals, int m, float inv_m,
+                                                            long long tiles_per_view, int2* __restrict__ ranges) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_pairs;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long slot = (long long)div_m(vals[p], m, inv_m) * tiles_per_view + keys[p];
+    if (p == 0) ranges[slot].x = 0;
+    if (p == n_pairs - 1) {
+      ranges[slot].y = (int)n_pairs;
+    } else {
+      const long long next = (long long)div_m(vals[p + 1], m, inv_m) * tiles_per_view + keys[p + 1];
+      if (next != slot) {
+        ranges[slot].y = (int)(p + 1);
+        ranges[next].x = (int)(p + 1);
+      }
+    }
   }
 }
 
@@ -596,14 +628,28 @@ int grid_cap(Ctx* c, long long n, int block) {
 
 }  // namespace
 
-void launch_raster_emit(Ctx* c, int64_t n_items, int64_t m, const short4* rect, const int32_t* offset,
-                        int tiles_x, int tile_bits, uint32_t* keys, int32_t* vals) {
+void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32_t* offset, int tiles_x,
+                        void* keys, bool keys16, int32_t* vals) {
   if (n_items == 0) return;
-  {
-    KScope _ks(c, "K2_raster_emit");
-    raster_emit_kernel<<<grid_cap(c, n_items, 256), 256, 0, c->stream>>>(n_items, m, rect, offset, tiles_x,
-                                                                        tile_bits, keys, vals);
-  }
+  KScope _ks(c, "K2_raster_emit");
+  if (keys16)
+    raster_emit_kernel<uint16_t><<<grid_cap(c, n_items, 256), 256, 0, c->stream>>>(
+        n_items, rect, offset, tiles_x, static_cast<uint16_t*>(keys), vals);
+  else
+    raster_emit_kernel<uint32_t><<<grid_cap(c, n_items, 256), 256, 0, c->stream>>>(
+        n_items, rect, offset, tiles_x, static_cast<uint32_t*>(keys), vals);
+}
+
+void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,
+                          int64_t tiles_per_view, int2* ranges) {
+  if (n_pairs == 0) return;
+  KScope _ks(c, "K2_ranges");
+  if (keys16)
+    raster_ranges_kernel<uint16_t><<<grid_cap(c, n_pairs, 256), 256, 0, c->stream>>>(
+        n_pairs, static_cast<const uint16_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
+  else
+    raster_ranges_kernel<uint32_t><<<grid_cap(c, n_pairs, 256), 256, 0, c->stream>>>(
+        n_pairs, static_cast<const uint32_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
 }
 
 void launch_ranges(Ctx* c, int64_t n_pairs, const uint32_t* keys, int tile_bits, int64_t tiles_per_view,

@@ -154,7 +154,7 @@ struct sct_fwd {
   int32_t* d_count = nullptr;          // [items] tiles covered
   int32_t* d_offset = nullptr;         // [items+1] exclusive scan of count
   uint8_t* d_vis = nullptr;            // [items] visible flag
-  uint32_t* d_keys = nullptr;          // [pairs] sorted (view,tile) keys
+  void* d_keys = nullptr;              // [pairs] sorted tile keys (uint16 if tile_bits <= 16, else uint32)
   int32_t* d_vals = nullptr;           // [pairs] sorted item index
   int2* d_ranges = nullptr;            // [V*T] [start,end) into sorted pairs
   double* d_prep = nullptr;            // [m][kPrepStride] Sigma (9) + rho, FP64
@@ -178,8 +178,10 @@ void launch_voxel_preprocess(Ctx* c, const sct_cloud& cl, const sct_grid& g, dou
                              int32_t zb1, int32_t bricks_x, int32_t bricks_y, float4* rec, short4* rect_lo,
                              short4* rect_hi, int32_t* count);
 // FP32 hot kernels
-void launch_raster_emit(Ctx* c, int64_t n_items, int64_t m, const short4* rect, const int32_t* offset,
-                        int tiles_x, int tile_bits, uint32_t* keys, int32_t* vals);
+void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32_t* offset, int tiles_x,
+                        void* keys, bool keys16, int32_t* vals);
+void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,
+                          int64_t tiles_per_view, int2* ranges);
 void launch_ranges(Ctx* c, int64_t n_pairs, const uint32_t* keys, int tile_bits, int64_t tiles_per_view,
                    int2* ranges);
 void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0 = 0, int nv = 0);
