@@ -19,7 +19,11 @@
 // DESIGN.md §K3, a run can only lose values below 2^-29 of rho) and narrow
 // kernels take the direct one-MUFU-per-voxel path. The branch is uniform
 // across the CTA (all lanes evaluate the same kernel at the same time).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <string>
 
 #include "sct_internal.cuh"
 
@@ -291,6 +295,201 @@ __global__ void __launch_bounds__(kVBwdThreads, 3) voxel_backward_stats_kernel(
   }
 }
 
+// K8 (tensor-core form), the voxel analogue of the rasterizer's moment GEMM
+// (raster.cu, K4): with brick-centred voxel coordinates c' = index - 3.5 and
+// the kernel's offset o = brick centre - kernel position, d = s*c' + o per
+// axis, so the 10 statistics follow from the moments
+// M[kernel][n] = sum_voxels E * g * {1, cx, cy, cz, cx^2, cy^2, cz^2, cxcy, cxcz, cycz}
+// by a binomial shift. E comes from the x-recurrence (row8, +15 exponent
+// offset so it fits binary16; values below 2^-29 of a kernel's peak lose
+// precision) written straight into m16n8k16 A fragments; G (per brick: the
+// upstream gradient times the 10 monomials, two n8 tiles) is split into hi + lo
+// binary16 parts after a per-brick power-of-two scale. Lane t of a quad owns
+// the x-row 4q + t (y = row & 7, z = row >> 3) of row quad q for kernels gq and
+// gq + 8; slice 2q + h maps k = 2t, 2t+1 to x = 4h + {0, 1} and k = 2t+8, 2t+9
+// to x = 4h + {2, 3}.
+constexpr int kVMmaWarps = 4;
+
+__device__ __forceinline__ void vmma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo_k, float hi_k) {
+  const __half2 h = __floats2half2_rn(lo_k, hi_k);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(32 * kVMmaWarps, 6) voxel_backward_mma_kernel(
+    BrickGeo G, const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
+    const short4* __restrict__ lo, const short4* __restrict__ hi, const int32_t* __restrict__ offset,
+    const float* __restrict__ dL, float* __restrict__ pair_stats) {
+  __shared__ uint4 s_g[32][32][2];  // [slice][lane][n tile] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}
+  __shared__ float s_gmax[kVMmaWarps];
+  int tx, ty, tz;
+  brick_of(G, blockIdx.x, tx, ty, tz);
+  const int brick = (tz * G.by + ty) * G.bx + tx;
+  const int2 rg = ranges[brick];
+  if (rg.y <= rg.x) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane & 3, gq = lane >> 2;
+  const int x0 = tx * kTileVox, y0 = ty * kTileVox, z0 = tz * kTileVox;
+  auto grad = [&](int x, int y, int z) -> float {
+    const int X = x0 + x, Y = y0 + y, Z = z0 + z;
+    return (X < G.dims.x && Y < G.dims.y && Z < G.dims.z)
+               ? __ldg(dL + ((long long)Z * G.dims.y + Y) * G.dims.x + X)
+               : 0.f;
+  };
+  // --- per-brick scale: largest |G| = gmax * 12.25 * 2^-15 * S <= 2^14
+  float gm = 0.f;
+  for (int v = threadIdx.x; v < 512; v += 32 * kVMmaWarps) gm = fmaxf(gm, fabsf(grad(v & 7, (v >> 3) & 7, v >> 6)));
+  gm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gm)));
+  if (lane == 0) s_gmax[warp] = gm;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kVMmaWarps; ++k) gm = fmaxf(gm, s_gmax[k]);
+  const float S = gm > 0.f ? exp2f(floorf(log2f(16384.f / (gm * 12.25f * 0x1p-15f)))) : 1.f;
+  const float gscale = 0x1p-15f * S, inv_s = 1.f / S;
+  // --- G fragments: each thread produces voxel pairs (adjacent k) for all 16 moments
+  for (int pp = threadIdx.x; pp < 256; pp += 32 * kVMmaWarps) {
+    const int s = pp >> 3, j = pp & 7;
+    const int tp = j >> 1, part = j & 1;
+    const int q = s >> 1, h = s & 1;
+    const int r = 4 * q + tp;
+    const int y = r & 7, z = r >> 3;
+    const int xa = 4 * h + 2 * part;
+    float ph[2][16];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float g = grad(xa + e, y, z) * gscale;
+      const float cx = (float)(xa + e) - 3.5f, cy = (float)y - 3.5f, cz = (float)z - 3.5f;
+      ph[e][0] = g;
+      ph[e][1] = g * cx;
+      ph[e][2] = g * cy;
+      ph[e][3] = g * cz;
+      ph[e][4] = g * cx * cx;
+      ph[e][5] = g * cy * cy;
+      ph[e][6] = g * cz * cz;
+      ph[e][7] = g * cx * cy;
+      ph[e][8] = g * cx * cz;
+      ph[e][9] = g * cy * cz;
+#pragma unroll
+      for (int n = 10; n < 16; ++n) ph[e][n] = 0.f;
+    }
+#pragma unroll
+    for (int n = 0; n < 16; ++n) {
+      const __half2 hv = __floats2half2_rn(ph[0][n], ph[1][n]);
+      const float2 f = __half22float2(hv);
+      const uint32_t hb = *reinterpret_cast<const uint32_t*>(&hv);
+      const uint32_t lb = pack_h2(ph[0][n] - f.x, ph[1][n] - f.y);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(&s_g[s][(n & 7) * 4 + tp][n >> 3]);
+      dst[part] = hb;
+      dst[2 + part] = lb;
+    }
+  }
+  __syncthreads();
+  const double c0x = G.origin.x + ((double)x0 + 0.5) * G.spacing.x;
+  const double c0y = G.origin.y + ((double)y0 + 0.5) * G.spacing.y;
+  const double c0z = G.origin.z + ((double)z0 + 0.5) * G.spacing.z;
+  const float sx = G.spf.x, sy = G.spf.y, sz = G.spf.z;
+  const int n_list = rg.y - rg.x;
+  for (int cb = 16 * warp; cb < n_list; cb += 16 * kVMmaWarps) {
+    float bxk[2], byk[2], bzk[2];
+    float4 qk[2], okk[2];
+    bool valid[2], rec_ok[2];
+    long long itk[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int e = cb + gq + 8 * k;
+      valid[k] = e < n_list;
+      itk[k] = valid[k] ? vals[rg.x + e] : 0;
+      const float4 a = __ldg(rec + 3 * itk[k]);
+      qk[k] = __ldg(rec + 3 * itk[k] + 1);
+      okk[k] = __ldg(rec + 3 * itk[k] + 2);
+      bxk[k] = (float)(c0x - (double)a.x);
+      byk[k] = (float)(c0y - (double)a.y);
+      bzk[k] = (float)(c0z - (double)a.z);
+      rec_ok[k] = qk[k].x * sx * sx >= -8.f;
+    }
+    float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+    for (int q = 0; q < 16; ++q) {
+      const int r = 4 * q + t;
+      const float fy = (float)(r & 7) * sy, fz = (float)(r >> 3) * sz;
+      float E[2][8];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float dy = byk[k] + fy, dz = bzk[k] + fz;
+        const float4 qq = qk[k], oo = okk[k];
+        const float c0o = valid[k] ? fmaf(qq.y * dy, dy, fmaf(qq.z * dz, dz, fmaf(oo.z * dy, dz, 15.f))) : -1e30f;
+        const float c1 = fmaf(oo.x, dy, oo.y * dz);
+        row8(E[k], rec_ok[k], bxk[k], sx, qq.x, c1, c0o, qq.w);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t a0 = pack_h2(E[0][4 * h], E[0][4 * h + 1]);
+        const uint32_t a1 = pack_h2(E[1][4 * h], E[1][4 * h + 1]);
+        const uint32_t a2 = pack_h2(E[0][4 * h + 2], E[0][4 * h + 3]);
+        const uint32_t a3 = pack_h2(E[1][4 * h + 2], E[1][4 * h + 3]);
+        const uint4 g0 = s_g[2 * q + h][lane][0], g1 = s_g[2 * q + h][lane][1];
+        vmma_f16(acc0, a0, a1, a2, a3, g0.x, g0.y);
+        vmma_f16(acc0, a0, a1, a2, a3, g0.z, g0.w);
+        vmma_f16(acc1, a0, a1, a2, a3, g1.x, g1.y);
+        vmma_f16(acc1, a0, a1, a2, a3, g1.z, g1.w);
+      }
+    }
+    // acc0: moments 2t, 2t+1 (c0,c1: kernel gq; c2,c3: kernel gq + 8); acc1: moments 8 + 2t, 9 + 2t
+    const int base = lane & ~3;
+    const bool second = t == 1;
+    float m[10];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float x0v = __shfl_sync(0xffffffffu, acc0[0], base + k);
+      const float x1v = __shfl_sync(0xffffffffu, acc0[1], base + k);
+      const float y0v = __shfl_sync(0xffffffffu, acc0[2], base + k);
+      const float y1v = __shfl_sync(0xffffffffu, acc0[3], base + k);
+      m[2 * k] = (second ? y0v : x0v) * inv_s;
+      m[2 * k + 1] = (second ? y1v : x1v) * inv_s;
+    }
+    {
+      const float x0v = __shfl_sync(0xffffffffu, acc1[0], base);
+      const float x1v = __shfl_sync(0xffffffffu, acc1[1], base);
+      const float y0v = __shfl_sync(0xffffffffu, acc1[2], base);
+      const float y1v = __shfl_sync(0xffffffffu, acc1[3], base);
+      m[8] = (second ? y0v : x0v) * inv_s;
+      m[9] = (second ? y1v : x1v) * inv_s;
+    }
+    const int kk = second ? 1 : 0;
+    if (t < 2 && (kk ? valid[1] : valid[0])) {
+      const float ox = fmaf(3.5f, sx, kk ? bxk[1] : bxk[0]);
+      const float oy = fmaf(3.5f, sy, kk ? byk[1] : byk[0]);
+      const float oz = fmaf(3.5f, sz, kk ? bzk[1] : bzk[0]);
+      const long long i = kk ? itk[1] : itk[0];
+      float v[10];
+      v[0] = m[0];
+      v[1] = fmaf(ox, m[0], sx * m[1]);
+      v[2] = fmaf(oy, m[0], sy * m[2]);
+      v[3] = fmaf(oz, m[0], sz * m[3]);
+      v[4] = fmaf(ox, fmaf(ox, m[0], 2.f * sx * m[1]), sx * sx * m[4]);
+      v[5] = fmaf(oy, fmaf(oy, m[0], 2.f * sy * m[2]), sy * sy * m[5]);
+      v[6] = fmaf(oz, fmaf(oz, m[0], 2.f * sz * m[3]), sz * sz * m[6]);
+      v[7] = fmaf(ox, fmaf(oy, m[0], sy * m[2]), fmaf(oy * sx, m[1], sx * sy * m[7]));
+      v[8] = fmaf(ox, fmaf(oz, m[0], sz * m[3]), fmaf(oz * sx, m[1], sx * sz * m[8]));
+      v[9] = fmaf(oy, fmaf(oz, m[0], sz * m[3]), fmaf(oz * sy, m[2], sy * sz * m[9]));
+      const short4 l = lo[i], hh = hi[i];
+      const int nx = hh.x - l.x + 1, ny = hh.y - l.y + 1;
+      const long long slot = offset[i] + ((tz - l.z) * ny + (ty - l.y)) * nx + (tx - l.x);
+      float4* dst = reinterpret_cast<float4*>(pair_stats + 12 * slot);
+      dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+      dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+      *reinterpret_cast<float2*>(dst + 2) = make_float2(v[8], v[9]);
+    }
+  }
+}
+
 BrickGeo make_geo(const sct_grid& g, int zb0, int zb1, int bx, int by) {
   BrickGeo G;
   G.dims = make_int3(g.dims[0], g.dims[1], g.dims[2]);
@@ -330,10 +529,20 @@ void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t
                                  const float* dL, float4* pair_stats) {
   const long long nb = (long long)bricks_x * bricks_y * (zb1 - zb0);
   if (nb <= 0) return;
+  // SCT_K8=simt selects the FP32 SIMT statistics kernel; default: tensor-core moments
+  static const bool simt = [] {
+    const char* e = std::getenv("SCT_K8");
+    return e && std::string(e) == "simt";
+  }();
   KScope _ks(c, "K8_voxel_backward_stats");
-  voxel_backward_stats_kernel<<<(unsigned)nb, kVBwdThreads, 0, c->stream>>>(
-      make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL,
-      reinterpret_cast<float*>(pair_stats));
+  if (simt)
+    voxel_backward_stats_kernel<<<(unsigned)nb, kVBwdThreads, 0, c->stream>>>(
+        make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL,
+        reinterpret_cast<float*>(pair_stats));
+  else
+    voxel_backward_mma_kernel<<<(unsigned)nb, 32 * kVMmaWarps, 0, c->stream>>>(
+        make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL,
+        reinterpret_cast<float*>(pair_stats));
 }
 
 }  // namespace sct
