@@ -323,11 +323,14 @@ __device__ __forceinline__ uint32_t pack_h2(float lo_k, float hi_k) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-__global__ void __launch_bounds__(32 * kVMmaWarps, 6) voxel_backward_mma_kernel(
+__global__ void __launch_bounds__(32 * kVMmaWarps, 7) voxel_backward_mma_kernel(
     BrickGeo G, const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ lo, const short4* __restrict__ hi, const int32_t* __restrict__ offset,
     const float* __restrict__ dL, float* __restrict__ pair_stats) {
-  __shared__ uint4 s_g[32][32][2];  // [slice][lane][n tile] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}
+  // B fragments [slice][lane] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}: n tile 0
+  // (moments 0-7) for all lanes; n tile 1 holds moments 8, 9 only (lanes 0-7)
+  __shared__ uint4 s_g[32][32];
+  __shared__ uint4 s_g1[32][8];
   __shared__ float s_gmax[kVMmaWarps];
   int tx, ty, tz;
   brick_of(G, blockIdx.x, tx, ty, tz);
@@ -380,12 +383,12 @@ __global__ void __launch_bounds__(32 * kVMmaWarps, 6) voxel_backward_mma_kernel(
       for (int n = 10; n < 16; ++n) ph[e][n] = 0.f;
     }
 #pragma unroll
-    for (int n = 0; n < 16; ++n) {
+    for (int n = 0; n < 10; ++n) {  // moments 10..15 are zero: not stored
       const __half2 hv = __floats2half2_rn(ph[0][n], ph[1][n]);
       const float2 f = __half22float2(hv);
       const uint32_t hb = *reinterpret_cast<const uint32_t*>(&hv);
       const uint32_t lb = pack_h2(ph[0][n] - f.x, ph[1][n] - f.y);
-      uint32_t* dst = reinterpret_cast<uint32_t*>(&s_g[s][(n & 7) * 4 + tp][n >> 3]);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(n < 8 ? &s_g[s][n * 4 + tp] : &s_g1[s][(n - 8) * 4 + tp]);
       dst[part] = hb;
       dst[2 + part] = lb;
     }
@@ -434,7 +437,8 @@ __global__ void __launch_bounds__(32 * kVMmaWarps, 6) voxel_backward_mma_kernel(
         const uint32_t a1 = pack_h2(E[1][4 * h], E[1][4 * h + 1]);
         const uint32_t a2 = pack_h2(E[0][4 * h + 2], E[0][4 * h + 3]);
         const uint32_t a3 = pack_h2(E[1][4 * h + 2], E[1][4 * h + 3]);
-        const uint4 g0 = s_g[2 * q + h][lane][0], g1 = s_g[2 * q + h][lane][1];
+        const uint4 g0 = s_g[2 * q + h][lane];
+        const uint4 g1 = lane < 8 ? s_g1[2 * q + h][lane] : make_uint4(0u, 0u, 0u, 0u);
         vmma_f16(acc0, a0, a1, a2, a3, g0.x, g0.y);
         vmma_f16(acc0, a0, a1, a2, a3, g0.z, g0.w);
         vmma_f16(acc1, a0, a1, a2, a3, g1.x, g1.y);
