@@ -214,7 +214,7 @@ struct VoxelBins {
   short4* hi = nullptr;
   int32_t* count = nullptr;
   int32_t* offset = nullptr;
-  uint32_t* keys = nullptr;
+  void* keys = nullptr;  // brick ids, uint16 when they fit
   int32_t* vals = nullptr;
   int2* ranges = nullptr;
   void release(Ctx* c) {
@@ -253,11 +253,23 @@ static int voxel_bin(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull
   SCT_CUDA_TRY(cudaMemsetAsync(b.ranges, 0, nbr * sizeof(int2), c->stream));
   launch_voxel_preprocess(c, cl, g, cull, b.zb0, b.zb1, b.bx, b.by, b.rec, b.lo, b.hi, b.count);
   SCT_TRY(scan_counts(c, b.count, b.offset, m, &b.n_pairs));
-  SCT_TRY(dev_alloc(c, (void**)&b.keys, b.n_pairs * sizeof(uint32_t)));
+  const int bits = bits_for((uint64_t)nbr);
+  const bool k16 = bits <= 16;
+  SCT_TRY(dev_alloc(c, &b.keys, b.n_pairs * (k16 ? sizeof(uint16_t) : sizeof(uint32_t))));
   SCT_TRY(dev_alloc(c, (void**)&b.vals, b.n_pairs * sizeof(int32_t)));
-  launch_voxel_emit(c, m, b.lo, b.hi, b.offset, b.bx, b.by, b.keys, b.vals);
-  SCT_TRY(sort_pairs(c, b.keys, b.vals, b.n_pairs, bits_for((uint64_t)nbr)));
-  launch_ranges(c, b.n_pairs, b.keys, 31, nbr, b.ranges);
+  launch_voxel_emit(c, m, b.lo, b.hi, b.offset, b.bx, b.by, b.keys, k16, b.vals);
+  if (bits > 0) {
+    if (k16) {
+      uint16_t* kp = static_cast<uint16_t*>(b.keys);
+      SCT_TRY(sort_pairs(c, kp, b.vals, b.n_pairs, bits));
+      b.keys = kp;
+    } else {
+      uint32_t* kp = static_cast<uint32_t*>(b.keys);
+      SCT_TRY(sort_pairs(c, kp, b.vals, b.n_pairs, bits));
+      b.keys = kp;
+    }
+  }
+  launch_key_ranges(c, b.n_pairs, b.keys, k16, b.ranges);
   SCT_CUDA_TRY(cudaGetLastError());
   return SCT_OK;
 }

@@ -97,18 +97,6 @@ __global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, con
   }
 }
 
-__global__ void __launch_bounds__(256) ranges_kernel(long long n_pairs, const uint32_t* __restrict__ keys,
-                                                     int tile_bits, long long tiles_per_view,
-                                                     int2* __restrict__ ranges) {
-  const uint32_t mask = (1u << tile_bits) - 1u;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_pairs;
-       p += (long long)gridDim.x * blockDim.x) {
-    const uint32_t k = keys[p];
-    const long long slot = (long long)(k >> tile_bits) * tiles_per_view + (k & mask);
-    if (p == 0 || keys[p - 1] != k) ranges[slot].x = (int)p;
-    if (p == n_pairs - 1 || keys[p + 1] != k) ranges[slot].y = (int)(p + 1);
-  }
-}
 
 // (view, tile) ranges of the sorted raster pairs: tile from the key, view
 // from the item (item = view * m + kernel; quotient by a float reciprocal
@@ -650,16 +638,6 @@ void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16
   else
     raster_ranges_kernel<uint32_t><<<grid_cap(c, n_pairs, 256), 256, 0, c->stream>>>(
         n_pairs, static_cast<const uint32_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
-}
-
-void launch_ranges(Ctx* c, int64_t n_pairs, const uint32_t* keys, int tile_bits, int64_t tiles_per_view,
-                   int2* ranges) {
-  if (n_pairs == 0) return;
-  {
-    KScope _ks(c, "K2_ranges");
-    ranges_kernel<<<grid_cap(c, n_pairs, 256), 256, 0, c->stream>>>(n_pairs, keys, tile_bits, tiles_per_view,
-                                                                    ranges);
-  }
 }
 
 // Views [v0, v0 + nv) of the forward state (nv <= 0: all views).

@@ -182,15 +182,14 @@ void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32
                         void* keys, bool keys16, int32_t* vals);
 void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,
                           int64_t tiles_per_view, int2* ranges);
-void launch_ranges(Ctx* c, int64_t n_pairs, const uint32_t* keys, int tile_bits, int64_t tiles_per_view,
-                   int2* ranges);
 void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0 = 0, int nv = 0);
 // item_stats != nullptr: parallel-atomic mode, 8 floats per item accumulated
 // with atomics instead of per-pair slots
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0 = 0,
                                   int nv = 0, float* item_stats = nullptr);
 void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, const int32_t* offset,
-                       int32_t bricks_x, int32_t bricks_y, uint32_t* keys, int32_t* vals);
+                       int32_t bricks_x, int32_t bricks_y, void* keys, bool keys16, int32_t* vals);
+void launch_key_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, int2* ranges);
 void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
                        int32_t bricks_y, const int2* ranges, const int32_t* vals, const float4* rec,
                        const sct_cloud& cl, float* vol);

@@ -37,22 +37,76 @@ __device__ __forceinline__ float ex2v(float x) {
 
 namespace {
 
+// Warp-cooperative emission (as raster_emit): a warp owns 32 consecutive
+// kernels, whose pairs form one contiguous output range; lanes stride over it
+// (coalesced stores) and find their kernel by a 5-step binary search over the
+// 32 offsets held in the lanes. Bricks of a kernel in z, y, x order
+// (voxelizer.cpp:82-85), i.e. ascending brick id; 16-bit keys when they fit.
+template <typename KeyT>
 __global__ void __launch_bounds__(256) voxel_emit_kernel(long long m, const short4* __restrict__ lo,
                                                          const short4* __restrict__ hi,
                                                          const int32_t* __restrict__ offset, int bx, int by,
-                                                         uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
-       i += (long long)gridDim.x * blockDim.x) {
-    int32_t o = offset[i];
-    if (offset[i + 1] == o) continue;
-    const short4 a = lo[i], b = hi[i];
-    for (int tz = a.z; tz <= b.z; ++tz)
-      for (int ty = a.y; ty <= b.y; ++ty)
-        for (int tx = a.x; tx <= b.x; ++tx) {
-          keys[o] = (uint32_t)((tz * by + ty) * bx + tx);
-          vals[o] = (int32_t)i;
-          ++o;
-        }
+                                                         KeyT* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long w0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < m;
+       w0 += warps * 32) {
+    const long long it = w0 + lane;
+    const int32_t o_l = it < m ? offset[it] : offset[m];
+    const long long last = min(w0 + 32, m);
+    const int32_t o_end = offset[last];
+    short4 a = make_short4(0, 0, 0, 0), b = make_short4(-1, -1, -1, -1);
+    if (it < m) {
+      a = lo[it];
+      b = hi[it];
+    }
+    const int axy = ((int)(unsigned short)a.x) | ((int)a.y << 16);
+    const int nxy = ((b.x - a.x + 1) & 0xffff) | ((b.y - a.y + 1) << 16);
+    const int az = a.z;
+    const int32_t o_0 = __shfl_sync(0xffffffffu, o_l, 0);
+    for (int32_t p0 = o_0; p0 < o_end; p0 += 32) {
+      const int32_t p = p0 + lane;
+      int j = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int32_t oj = __shfl_sync(0xffffffffu, o_l, j + step);
+        if (j + step < 32 && oj <= p) j += step;
+      }
+      const int32_t oj = __shfl_sync(0xffffffffu, o_l, j);
+      const int jxy = __shfl_sync(0xffffffffu, axy, j);
+      const int jn = __shfl_sync(0xffffffffu, nxy, j);
+      const int jz = __shfl_sync(0xffffffffu, az, j);
+      if (p < o_end) {
+        const int x0 = (short)(jxy & 0xffff), y0 = (short)(jxy >> 16);
+        const int nx = jn & 0xffff, ny = jn >> 16;
+        const int rank = p - oj;
+        const int tx = x0 + rank % nx;
+        const int r2 = rank / nx;
+        const int ty = y0 + r2 % ny, tz = jz + r2 / ny;
+        keys[p] = (KeyT)((tz * by + ty) * bx + tx);
+        vals[p] = (int32_t)(w0 + j);
+      }
+    }
+  }
+}
+
+// [start, end) of each key's run in the sorted pairs (key = slot)
+template <typename KeyT>
+__global__ void __launch_bounds__(256) key_ranges_kernel(long long n_pairs, const KeyT* __restrict__ keys,
+                                                         int2* __restrict__ ranges) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_pairs;
+       p += (long long)gridDim.x * blockDim.x) {
+    const KeyT k = keys[p];
+    if (p == 0) ranges[k].x = 0;
+    if (p == n_pairs - 1) {
+      ranges[k].y = (int)n_pairs;
+    } else {
+      const KeyT k2 = keys[p + 1];
+      if (k2 != k) {
+        ranges[k].y = (int)(p + 1);
+        ranges[k2].x = (int)(p + 1);
+      }
+    }
   }
 }
 
@@ -510,12 +564,28 @@ BrickGeo make_geo(const sct_grid& g, int zb0, int zb1, int bx, int by) {
 }  // namespace
 
 void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, const int32_t* offset,
-                       int32_t bricks_x, int32_t bricks_y, uint32_t* keys, int32_t* vals) {
+                       int32_t bricks_x, int32_t bricks_y, void* keys, bool keys16, int32_t* vals) {
   if (m == 0) return;
   long long b = (m + 255) / 256;
   if (b > (long long)c->sm_count * 16) b = (long long)c->sm_count * 16;
   KScope _ks(c, "K6_voxel_emit");
-  voxel_emit_kernel<<<(int)b, 256, 0, c->stream>>>(m, lo, hi, offset, bricks_x, bricks_y, keys, vals);
+  if (keys16)
+    voxel_emit_kernel<uint16_t><<<(int)b, 256, 0, c->stream>>>(m, lo, hi, offset, bricks_x, bricks_y,
+                                                               static_cast<uint16_t*>(keys), vals);
+  else
+    voxel_emit_kernel<uint32_t><<<(int)b, 256, 0, c->stream>>>(m, lo, hi, offset, bricks_x, bricks_y,
+                                                               static_cast<uint32_t*>(keys), vals);
+}
+
+void launch_key_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, int2* ranges) {
+  if (n_pairs == 0) return;
+  long long b = (n_pairs + 255) / 256;
+  if (b > (long long)c->sm_count * 16) b = (long long)c->sm_count * 16;
+  KScope _ks(c, "K2_ranges");
+  if (keys16)
+    key_ranges_kernel<uint16_t><<<(int)b, 256, 0, c->stream>>>(n_pairs, static_cast<const uint16_t*>(keys), ranges);
+  else
+    key_ranges_kernel<uint32_t><<<(int)b, 256, 0, c->stream>>>(n_pairs, static_cast<const uint32_t*>(keys), ranges);
 }
 
 void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x, int32_t bricks_y,
