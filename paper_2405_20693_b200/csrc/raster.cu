@@ -13,6 +13,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -171,14 +173,18 @@ constexpr int kCompWarps = 4;
 __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     int tiles_x, int tiles_per_view, int W, int H, int view0, int total, int* __restrict__ work,
-    float* __restrict__ images) {
+    const int* __restrict__ order, float* __restrict__ images) {
   __shared__ float4 sa[kCompWarps][32];
   __shared__ float4 sb[kCompWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = lane >> 1;
   for (;;) {
     int w = 0;
-    if (lane == 0) w = atomicAdd(work, 1);
+    if (lane == 0) {
+      w = atomicAdd(work, 1);
+      if (w < total) w = order[w];  // longest lists first (tile_order)
+      else w = total;
+    }
     w = __shfl_sync(0xffffffffu, w, 0);
     if (w >= total) break;
     const int view = view0 + w / tiles_per_view;
@@ -455,7 +461,8 @@ __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cas
 __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats_mma_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ rect, const int32_t* __restrict__ offset, int tiles_x, int tiles_per_view, int W,
-    int H, int view0, const float* __restrict__ dL, float* __restrict__ pair_stats, float* __restrict__ item_stats) {
+    int H, int view0, const int* __restrict__ order, const float* __restrict__ dL, float* __restrict__ pair_stats,
+    float* __restrict__ item_stats) {
   __shared__ uint4 s_g[16][32];  // [slice][lane] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}
   __shared__ float s_gmax[kMmaWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -463,8 +470,9 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
   const float px_off = (float)(8 * (t & 1)) + 0.5f;
   const float py_off = (float)(t >> 1) + 0.5f;
   {
-    const int tile = blockIdx.x;
-    const int view = view0 + blockIdx.y;
+    const int w = order[blockIdx.x];  // blocks dispatched longest lists first (tile_order)
+    const int tile = w % tiles_per_view;
+    const int view = view0 + w / tiles_per_view;
     const int2 rg = ranges[(long long)view * tiles_per_view + tile];
     if (rg.y <= rg.x) return;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -640,6 +648,52 @@ void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16
         n_pairs, static_cast<const uint32_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
 }
 
+// Longest-processing-time order of the (view, tile) lists of views
+// [v0, v0 + nv): local indices sorted by descending list length, so that K3's
+// persistent warps and K4's blocks start the long lists first and the kernels'
+// tails consist of short lists. Cached in the context for the last range.
+__global__ void __launch_bounds__(256) tile_order_keys_kernel(const int2* __restrict__ ranges, long long base,
+                                                              int n, uint32_t* __restrict__ keys,
+                                                              int32_t* __restrict__ idx) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
+    const int2 r = ranges[base + w];
+    // descending octave of the list length; the stable sort keeps the natural
+    // (view-major, spatially coherent) order inside an octave for L2 locality
+    keys[w] = 31u - (uint32_t)(32 - __clz(max(r.y - r.x, 0)));
+    idx[w] = w;
+  }
+}
+
+static const int* tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
+  const int T = s->det.tiles_x * s->det.tiles_y;
+  const int n = T * nv;
+  char* buf = nullptr;
+  if (stage_buf(c, 22, (size_t)4 * n * sizeof(uint32_t), (void**)&buf) != SCT_OK) return nullptr;
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(buf);
+  uint32_t* k1 = k0 + n;
+  int32_t* i0 = reinterpret_cast<int32_t*>(k1 + n);
+  int32_t* i1 = i0 + n;
+  KScope _ks(c, "K2_tile_order");
+  tile_order_keys_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, k0, i0);
+  cub::DoubleBuffer<uint32_t> keys(k0, k1);
+  cub::DoubleBuffer<int32_t> vals(i0, i1);
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, n, 0, 5, c->stream);
+  if (ensure_cub_tmp(c, tmp) != SCT_OK) return nullptr;
+  tmp = c->cub_tmp_bytes;
+  cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, vals, n, 0, 5, c->stream);
+  return vals.Current();
+}
+
+static const int* cached_tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
+  if (c->order_id == s->id && c->order_v0 == v0 && c->order_nv == nv && c->order_ptr) return c->order_ptr;
+  c->order_ptr = tile_order(c, s, v0, nv);
+  c->order_id = s->id;
+  c->order_v0 = v0;
+  c->order_nv = nv;
+  return c->order_ptr;
+}
+
 // Views [v0, v0 + nv) of the forward state (nv <= 0: all views).
 void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, int nv) {
   if (nv <= 0) nv = s->n_views - v0;
@@ -652,12 +706,14 @@ void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, in
   }
   const long long total = (long long)T * nv;
   const int blocks = (int)std::min<long long>((long long)c->sm_count * per_sm, (total + kCompWarps - 1) / kCompWarps);
+  const int* order = cached_tile_order(c, s, v0, nv);
   int* work = nullptr;
-  if (stage_buf(c, 20, sizeof(int) * 4, (void**)&work) != SCT_OK) return;
+  if (!order || stage_buf(c, 20, sizeof(int) * 4, (void**)&work) != SCT_OK) return;
   cudaMemsetAsync(work, 0, sizeof(int), c->stream);
   KScope _ks(c, "K3_composite");
   composite_kernel<<<blocks, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
-                                                              s->det.w, s->det.h, v0, (int)total, work, images);
+                                                              s->det.w, s->det.h, v0, (int)total, work, order,
+                                                              images);
 }
 
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0, int nv,
@@ -681,9 +737,11 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
                                                                v0, dL, ps, item_stats);
     return;
   }
-  backward_stats_mma_kernel<<<grid, 32 * kMmaWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
-                                                                    s->d_offset, s->det.tiles_x, T, s->det.w,
-                                                                    s->det.h, v0, dL, ps, item_stats);
+  const int* order = cached_tile_order(c, s, v0, nv);
+  if (!order) return;
+  backward_stats_mma_kernel<<<T * nv, 32 * kMmaWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
+                                                                      s->d_offset, s->det.tiles_x, T, s->det.w,
+                                                                      s->det.h, v0, order, dL, ps, item_stats);
 }
 
 }  // namespace sct

@@ -106,9 +106,15 @@ struct Ctx {
   cudaEvent_t ev_copy[kChunkEvents] = {};
   // grow-only device staging buffers of the host-buffer entry points (a
   // context serialises its calls, so a slot is free again at the next call)
-  static constexpr int kStageSlots = 24;  // 20: K3 work counter
+  static constexpr int kStageSlots = 24;  // 20: K3 work counter, 22: tile order
   void* stage[kStageSlots] = {};
   size_t stage_bytes[kStageSlots] = {};
+  // longest-first (view, tile) order of the last forward state / view range
+  // (raster.cu tile_order), keyed by the state's id
+  uint64_t next_fwd_id = 1;
+  uint64_t order_id = 0;
+  int order_v0 = -1, order_nv = -1;
+  const int* order_ptr = nullptr;
   // NCCL communicator of the *_allreduce entry points (comm.cu): an
   // ncclComm_t, owned by the context when made by sct_ctx_comm_init
   void* comm = nullptr;
@@ -136,6 +142,7 @@ void dev_free(Ctx* c, void* p);
 // Forward state (opaque to callers).
 struct sct_fwd {
   sct::Ctx* ctx = nullptr;
+  uint64_t id = 0;  // unique per context (tile-order cache key)
   int32_t n_views = 0;
   int64_t m = 0;
   sct::DetParams det{};
