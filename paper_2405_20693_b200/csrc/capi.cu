@@ -823,7 +823,8 @@ int sct_voxelize_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_grid* grid, d
   SCT_TRY(check_grid(grid));
   VoxelBins b;
   int rc = voxel_bin(c, *cloud, *grid, cull, zb0, zb1, b);
-  if (rc == SCT_OK) launch_voxel_eval(c, *grid, b.zb0, b.zb1, b.bx, b.by, b.ranges, b.vals, b.rec, *cloud, vol);
+  if (rc == SCT_OK)
+    launch_voxel_eval(c, *grid, b.zb0, b.zb1, b.bx, b.by, b.ranges, b.vals, b.rec, *cloud, b.n_pairs, vol);
   b.release(c);
   if (rc == SCT_OK && cudaGetLastError() != cudaSuccess) {
     set_error("CUDA error: kernel launch in sct_voxelize_fwd");

@@ -9,6 +9,7 @@
 //                        trainer.cpp:277-287
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "sct_internal.cuh"
@@ -165,18 +166,35 @@ __global__ void ssim_h_kernel(const float* __restrict__ r, const float* __restri
   }
 }
 
+// Deterministic per-block sum: block b of image img writes partial[img][b];
+// photometric_finish_kernel adds the partials in block order.
+__device__ __forceinline__ void block_sum_to(double v, double* __restrict__ dst) {
+  __shared__ double s_red[8];
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += s_red[w];
+    *dst = s;
+  }
+}
+
 // vertical valid pass + per-window SSIM partials (objectives.cpp:93-149):
-// fields[img][5][Hv][Wv] = g1, g2, g2*mu1, g3, g3*mu2; ssim sum per image.
-__global__ void ssim_v_kernel(const float* __restrict__ tmp, int n, int W, int H, Taps taps,
-                              float* __restrict__ fields, double* __restrict__ values) {
+// fields[img][5][Hv][Wv] = g1, g2, g2*mu1, g3, g3*mu2; SSIM-map sum per image
+// as per-block partials (grid: blocks per image x images).
+__global__ void __launch_bounds__(256) ssim_v_kernel(const float* __restrict__ tmp, int n, int W, int H, Taps taps,
+                                                     float* __restrict__ fields, double* __restrict__ partial) {
   const float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
   const int Wv = W - kWin + 1, Hv = H - kWin + 1;
-  const long long total = (long long)n * Hv * Wv;
+  const long long img = blockIdx.y;
+  const long long total = (long long)Hv * Wv;
+  double acc = 0.0;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const int x = (int)(t % Wv);
-    const int y = (int)((t / Wv) % Hv);
-    const long long img = t / ((long long)Wv * Hv);
+    const int y = (int)(t / Wv);
     const long long plane = (long long)H * Wv;
     const float* src = tmp + img * 5 * plane + (long long)y * Wv + x;
     float f[5] = {0, 0, 0, 0, 0};
@@ -195,8 +213,9 @@ __global__ void ssim_v_kernel(const float* __restrict__ tmp, int n, int W, int H
     const long long vplane = (long long)Hv * Wv;
     float* o = fields + img * 5 * vplane + (long long)y * Wv + x;
     o[0] = g1; o[vplane] = g2; o[2 * vplane] = g2 * mu1; o[3 * vplane] = g3; o[4 * vplane] = g3 * mu2;
-    atomicAdd(values + 2 * img + 1, (double)(l * cs));
+    acc += (double)(l * cs);
   }
+  block_sum_to(acc, partial + img * gridDim.x + blockIdx.x);
 }
 
 // adjoint vertical pass: atmp[img][5][H][Wv]
@@ -226,19 +245,21 @@ __global__ void ssim_adj_v_kernel(const float* __restrict__ fields, int n, int W
 }
 
 // adjoint horizontal pass + dL/dI assembly (objectives.cpp:151-166, trainer.cpp:284-287)
-__global__ void ssim_adj_h_kernel(const float* __restrict__ atmp, const float* __restrict__ r,
-                                  const float* __restrict__ mm, int n, int W, int H, float rscale, Taps taps,
-                                  float lambda_ssim, float grad_scale, float* __restrict__ dL,
-                                  double* __restrict__ values) {
+__global__ void __launch_bounds__(256) ssim_adj_h_kernel(const float* __restrict__ atmp, const float* __restrict__ r,
+                                                         const float* __restrict__ mm, int n, int W, int H,
+                                                         float rscale, Taps taps, float lambda_ssim, float grad_scale,
+                                                         float* __restrict__ dL, double* __restrict__ partial) {
   const int Wv = W - kWin + 1, Hv = H - kWin + 1;
   const float inv_p = 1.f / ((float)Wv * (float)Hv);
   const float inv_n = 1.f / ((float)W * (float)H);
-  const long long total = (long long)n * H * W;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int x = (int)(t % W);
-    const int y = (int)((t / W) % H);
-    const long long img = t / ((long long)W * H);
+  const long long img = blockIdx.y;
+  const long long total = (long long)H * W;
+  double acc = 0.0;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < total;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(p % W);
+    const int y = (int)(p / W);
+    const long long t = img * total + p;
     const long long plane = (long long)H * Wv;
     float f[5] = {0, 0, 0, 0, 0};
 #pragma unroll
@@ -255,15 +276,31 @@ __global__ void ssim_adj_h_kernel(const float* __restrict__ atmp, const float* _
     const float d = a - b;
     const float g_l1 = d > 0.f ? inv_n : (d < 0.f ? -inv_n : 0.f);
     dL[t] = (g_l1 + lambda_ssim * g_dssim) * grad_scale;
-    atomicAdd(values + 2 * img, (double)fabsf(d));
+    acc += (double)fabsf(d);
   }
+  block_sum_to(acc, partial + img * gridDim.x + blockIdx.x);
 }
 
-__global__ void photometric_finish_kernel(double* values, int n, int W, int H) {
+// values[i] = {L1 mean, D-SSIM}: the per-block partials added in block order
+__global__ void photometric_finish_kernel(const double* __restrict__ l1_part, int nb_l1,
+                                          const double* __restrict__ ssim_part, int nb_ssim, double* values, int n,
+                                          int W, int H) {
+  // one warp per image: lane-strided partial sums, then a fixed shuffle tree
   const int Wv = W - kWin + 1, Hv = H - kWin + 1;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    values[2 * i] = values[2 * i] / ((double)W * H);
-    values[2 * i + 1] = 0.5 * (1.0 - values[2 * i + 1] / ((double)Wv * Hv));
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x >> 5; i < n; i += blockDim.x >> 5) {
+    double a = 0.0, b = 0.0;
+    for (int k = lane; k < nb_l1; k += 32) a += l1_part[(long long)i * nb_l1 + k];
+    for (int k = lane; k < nb_ssim; k += 32) b += ssim_part[(long long)i * nb_ssim + k];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+      values[2 * i] = a / ((double)W * H);
+      values[2 * i + 1] = 0.5 * (1.0 - b / ((double)Wv * Hv));
+    }
   }
 }
 
@@ -327,7 +364,17 @@ int photometric_loss(Ctx* c, const float* rendered, const float* measured, int n
   float* fields = nullptr;
   SCT_TRY(dev_alloc(c, (void**)&tmp, tmp_elems * sizeof(float)));
   SCT_TRY(dev_alloc(c, (void**)&fields, field_elems * sizeof(float)));
-  SCT_CUDA_TRY(cudaMemsetAsync(values, 0, sizeof(double) * 2 * n, c->stream));
+  // blocks per image for the two reducing passes (deterministic partials)
+  auto per_img = [&](long long px) {
+    long long b = (px + 255) / 256;
+    const long long cap = std::max<long long>(1, (long long)c->sm_count * 8 / n);
+    return (int)std::max<long long>(1, std::min(b, cap));
+  };
+  const int nb_ssim = per_img((long long)Hv * Wv), nb_l1 = per_img((long long)h * w);
+  double* part = nullptr;
+  SCT_TRY(stage_buf(c, 23, sizeof(double) * (size_t)n * (nb_ssim + nb_l1), (void**)&part));
+  double* ssim_part = part;
+  double* l1_part = part + (size_t)n * nb_ssim;
   {
     KScope _ks(c, "K11_ssim_h");
     ssim_h_kernel<<<grid_cap(c, (long long)n * h * Wv, 256), 256, 0, c->stream>>>(rendered, measured, n, w, h,
@@ -335,8 +382,7 @@ int photometric_loss(Ctx* c, const float* rendered, const float* measured, int n
   }
   {
     KScope _ks(c, "K11_ssim_v");
-    ssim_v_kernel<<<grid_cap(c, (long long)n * Hv * Wv, 256), 256, 0, c->stream>>>(tmp, n, w, h, taps, fields,
-                                                                                    values);
+    ssim_v_kernel<<<dim3(nb_ssim, n), 256, 0, c->stream>>>(tmp, n, w, h, taps, fields, ssim_part);
   }
   {
     KScope _ks(c, "K11_ssim_adj_v");
@@ -344,12 +390,12 @@ int photometric_loss(Ctx* c, const float* rendered, const float* measured, int n
   }
   {
     KScope _ks(c, "K11_ssim_adj_h");
-    ssim_adj_h_kernel<<<grid_cap(c, (long long)n * h * w, 256), 256, 0, c->stream>>>(
-        tmp, rendered, measured, n, w, h, render_scale, taps, lambda_ssim, grad_scale, dL, values);
+    ssim_adj_h_kernel<<<dim3(nb_l1, n), 256, 0, c->stream>>>(tmp, rendered, measured, n, w, h, render_scale, taps,
+                                                             lambda_ssim, grad_scale, dL, l1_part);
   }
   {
     KScope _ks(c, "K11_finish");
-    photometric_finish_kernel<<<1, 128, 0, c->stream>>>(values, n, w, h);
+    photometric_finish_kernel<<<1, 128, 0, c->stream>>>(l1_part, nb_l1, ssim_part, nb_ssim, values, n, w, h);
   }
   dev_free(c, tmp);
   dev_free(c, fields);

@@ -173,19 +173,24 @@ constexpr int kCompWarps = 4;
 __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     int tiles_x, int tiles_per_view, int W, int H, int view0, int total, int* __restrict__ work,
-    const int* __restrict__ order, float* __restrict__ images) {
+    const int* __restrict__ order, int splits, float* __restrict__ partial, float* __restrict__ images) {
   __shared__ float4 sa[kCompWarps][32];
   __shared__ float4 sb[kCompWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = lane >> 1;
   for (;;) {
-    int w = 0;
+    int w = 0, part = 0;
     if (lane == 0) {
       w = atomicAdd(work, 1);
-      if (w < total) w = order[w];  // longest lists first (tile_order)
-      else w = total;
+      if (w < total * splits) {
+        part = w % splits;
+        w = order[w / splits];  // longest lists first (tile_order)
+      } else {
+        w = total;
+      }
     }
     w = __shfl_sync(0xffffffffu, w, 0);
+    part = __shfl_sync(0xffffffffu, part, 0);
     if (w >= total) break;
     const int view = view0 + w / tiles_per_view;
     const int tile = w % tiles_per_view;
@@ -194,7 +199,12 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     const int v = ty * kTilePx + row;
     const float py = (float)v + 0.5f;
     const float px0 = (float)u0 + 0.5f;
-    const int2 rg = ranges[(long long)view * tiles_per_view + tile];
+    int2 rg = ranges[(long long)view * tiles_per_view + tile];
+    if (splits > 1) {  // small workloads: the list is split into `splits` parts, summed by composite_reduce
+      const int len = rg.y - rg.x, s0 = rg.x;
+      rg.x = s0 + (int)((long long)len * part / splits);
+      rg.y = s0 + (int)((long long)len * (part + 1) / splits);
+    }
     float acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.f;
@@ -237,7 +247,9 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
       }
     }
     if (v < H) {
-      float* out = images + ((long long)view * H + v) * W;
+      float* out = splits > 1
+                       ? partial + (((long long)part * (total / tiles_per_view) + (view - view0)) * H + v) * W
+                       : images + ((long long)view * H + v) * W;
       if (u0 + 7 < W && (W & 3) == 0) {
         *reinterpret_cast<float4*>(out + u0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
         *reinterpret_cast<float4*>(out + u0 + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
@@ -461,7 +473,8 @@ __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cas
 __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats_mma_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ rect, const int32_t* __restrict__ offset, int tiles_x, int tiles_per_view, int W,
-    int H, int view0, const int* __restrict__ order, const float* __restrict__ dL, float* __restrict__ pair_stats,
+    int H, int view0, const int* __restrict__ order, int parts, const float* __restrict__ dL,
+    float* __restrict__ pair_stats,
     float* __restrict__ item_stats) {
   __shared__ uint4 s_g[16][32];  // [slice][lane] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}
   __shared__ float s_gmax[kMmaWarps];
@@ -470,10 +483,16 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
   const float px_off = (float)(8 * (t & 1)) + 0.5f;
   const float py_off = (float)(t >> 1) + 0.5f;
   {
-    const int w = order[blockIdx.x];  // blocks dispatched longest lists first (tile_order)
+    const int w = order[blockIdx.x / parts];  // blocks dispatched longest lists first (tile_order)
+    const int part = blockIdx.x % parts;
     const int tile = w % tiles_per_view;
     const int view = view0 + w / tiles_per_view;
-    const int2 rg = ranges[(long long)view * tiles_per_view + tile];
+    int2 rg = ranges[(long long)view * tiles_per_view + tile];
+    if (parts > 1) {  // small workloads: several CTAs share a list (pair statistics are independent)
+      const int len = rg.y - rg.x, s0 = rg.x;
+      rg.x = s0 + (int)((long long)len * part / parts);
+      rg.y = s0 + (int)((long long)len * (part + 1) / parts);
+    }
     if (rg.y <= rg.x) return;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int u0 = tx * kTilePx, v0 = ty * kTilePx;
@@ -648,6 +667,17 @@ void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16
         n_pairs, static_cast<const uint32_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
 }
 
+// images = sum over parts (in part order) of the split composite's partials
+__global__ void __launch_bounds__(256) composite_reduce_kernel(const float* __restrict__ partial, int splits,
+                                                               long long n, float* __restrict__ images) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < splits; ++p) s += partial[(long long)p * n + i];
+    images[i] = s;
+  }
+}
+
 // Longest-processing-time order of the (view, tile) lists of views
 // [v0, v0 + nv): local indices sorted by descending list length, so that K3's
 // persistent warps and K4's blocks start the long lists first and the kernels'
@@ -705,15 +735,34 @@ void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, in
     if (per_sm < 1) per_sm = 1;
   }
   const long long total = (long long)T * nv;
-  const int blocks = (int)std::min<long long>((long long)c->sm_count * per_sm, (total + kCompWarps - 1) / kCompWarps);
+  // Small workloads (few views / tiles: the train step renders one view) have
+  // fewer lists than the GPU has warp slots: split each list into parts
+  // (>= 32 kernels each) written to partial images and summed in part order.
+  const long long slots = (long long)c->sm_count * per_sm * kCompWarps;
+  const double avg_len = total > 0 ? (double)s->n_pairs / (double)total : 0.0;
+  int splits = 1;
+  while (splits < 16 && total * splits * 2 <= slots && avg_len / (2 * splits) >= 32.0) splits *= 2;
+  const size_t px = (size_t)s->det.w * s->det.h;
+  float* partial = nullptr;
+  if (splits > 1 && stage_buf(c, 24, sizeof(float) * px * nv * splits, (void**)&partial) != SCT_OK) return;
+  const int blocks =
+      (int)std::min<long long>((long long)c->sm_count * per_sm, (total * splits + kCompWarps - 1) / kCompWarps);
   const int* order = cached_tile_order(c, s, v0, nv);
   int* work = nullptr;
   if (!order || stage_buf(c, 20, sizeof(int) * 4, (void**)&work) != SCT_OK) return;
   cudaMemsetAsync(work, 0, sizeof(int), c->stream);
-  KScope _ks(c, "K3_composite");
-  composite_kernel<<<blocks, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
-                                                              s->det.w, s->det.h, v0, (int)total, work, order,
-                                                              images);
+  {
+    KScope _ks(c, "K3_composite");
+    composite_kernel<<<blocks, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
+                                                                s->det.w, s->det.h, v0, (int)total, work, order,
+                                                                splits, partial, images);
+  }
+  if (splits > 1) {
+    KScope _ks(c, "K3_reduce");
+    const long long n = (long long)px * nv;
+    composite_reduce_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(partial, splits, n,
+                                                                        images + (size_t)v0 * px);
+  }
 }
 
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0, int nv,
@@ -739,9 +788,15 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
   }
   const int* order = cached_tile_order(c, s, v0, nv);
   if (!order) return;
-  backward_stats_mma_kernel<<<T * nv, 32 * kMmaWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
-                                                                      s->d_offset, s->det.tiles_x, T, s->det.w,
-                                                                      s->det.h, v0, order, dL, ps, item_stats);
+  // small workloads: several CTAs per list (>= 64 kernels each) until the
+  // grid fills the CTA slots (8 per SM)
+  const long long total = (long long)T * nv;
+  const double avg_len = total > 0 ? (double)s->n_pairs / (double)total : 0.0;
+  int parts = 1;
+  while (parts < 16 && total * parts * 2 <= (long long)c->sm_count * 8 && avg_len / (2 * parts) >= 64.0) parts *= 2;
+  backward_stats_mma_kernel<<<(unsigned)(total * parts), 32 * kMmaWarps, 0, c->stream>>>(
+      s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
+      parts, dL, ps, item_stats);
 }
 
 }  // namespace sct

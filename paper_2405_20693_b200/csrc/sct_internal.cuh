@@ -106,7 +106,10 @@ struct Ctx {
   cudaEvent_t ev_copy[kChunkEvents] = {};
   // grow-only device staging buffers of the host-buffer entry points (a
   // context serialises its calls, so a slot is free again at the next call)
-  static constexpr int kStageSlots = 24;  // 20: K3 work counter, 22: tile order
+  // slots: 0-13 host-path staging, 14/15 backward statistics, 16/17 NCCL
+  // scratch, 18/19 fixtures, 20 K3 work counter, 22 tile order, 23 photometric
+  // partials, 24 split-composite partial images
+  static constexpr int kStageSlots = 28;
   void* stage[kStageSlots] = {};
   size_t stage_bytes[kStageSlots] = {};
   // longest-first (view, tile) order of the last forward state / view range
@@ -199,7 +202,7 @@ void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, co
 void launch_key_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, int2* ranges);
 void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
                        int32_t bricks_y, const int2* ranges, const int32_t* vals, const float4* rec,
-                       const sct_cloud& cl, float* vol);
+                       const sct_cloud& cl, int64_t n_pairs, float* vol);
 void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
                                  int32_t bricks_y, const int2* ranges, const int32_t* vals,
                                  const float4* rec, const short4* lo, const short4* hi,

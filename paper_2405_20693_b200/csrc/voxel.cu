@@ -163,18 +163,27 @@ __device__ __forceinline__ void row8(float e[8], bool rec_ok, float dx0, float s
 constexpr int kEvalWarps = 4;
 __global__ void __launch_bounds__(32 * kEvalWarps) voxel_eval_kernel(BrickGeo G, const int2* __restrict__ ranges,
                                                                      const int32_t* __restrict__ vals,
-                                                                     const float4* __restrict__ rec,
+                                                                     const float4* __restrict__ rec, int splits,
+                                                                     float* __restrict__ partial,
                                                                      float* __restrict__ vol) {
   __shared__ float4 sA[kEvalWarps][32];  // base offset xyz, rho*2^-64
   __shared__ float4 sB[kEvalWarps][32];  // Qxx Qyy Qzz K
   __shared__ float4 sC[kEvalWarps][32];  // Qxy Qxz Qyz
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long b = (long long)blockIdx.x * kEvalWarps + warp;
+  const long long gw = (long long)blockIdx.x * kEvalWarps + warp;
+  const long long b = gw / splits;
+  const int part = (int)(gw % splits);
   if (b >= G.n_bricks) return;
   int tx, ty, tz;
   brick_of(G, b, tx, ty, tz);
   const int brick = (tz * G.by + ty) * G.bx + tx;
-  const int2 rg = ranges[brick];
+  int2 rg = ranges[brick];
+  if (splits > 1) {  // small grids: several warps per brick list, summed by voxel_reduce
+    const int len = rg.y - rg.x, s0 = rg.x;
+    rg.x = s0 + (int)((long long)len * part / splits);
+    rg.y = s0 + (int)((long long)len * (part + 1) / splits);
+    vol = partial + (long long)part * G.dims.x * G.dims.y * G.dims.z;
+  }
   const double c0x = G.origin.x + ((double)(tx * kTileVox) + 0.5) * G.spacing.x;
   const double c0y = G.origin.y + ((double)(ty * kTileVox) + 0.5) * G.spacing.y;
   const double c0z = G.origin.z + ((double)(tz * kTileVox) + 0.5) * G.spacing.z;
@@ -548,6 +557,17 @@ __global__ void __launch_bounds__(32 * kVMmaWarps, 7) voxel_backward_mma_kernel(
   }
 }
 
+// vol[i] = sum over parts (in part order) of the split evaluation's partials
+__global__ void __launch_bounds__(256) voxel_reduce_kernel(const float* __restrict__ partial, int splits,
+                                                           long long stride, long long n, float* __restrict__ vol) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < splits; ++p) s += partial[(long long)p * stride + i];
+    vol[i] = s;
+  }
+}
+
 BrickGeo make_geo(const sct_grid& g, int zb0, int zb1, int bx, int by) {
   BrickGeo G;
   G.dims = make_int3(g.dims[0], g.dims[1], g.dims[2]);
@@ -589,12 +609,39 @@ void launch_key_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, i
 }
 
 void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x, int32_t bricks_y,
-                       const int2* ranges, const int32_t* vals, const float4* rec, const sct_cloud&, float* vol) {
+                       const int2* ranges, const int32_t* vals, const float4* rec, const sct_cloud&,
+                       int64_t n_pairs, float* vol) {
   const long long nb = (long long)bricks_x * bricks_y * (zb1 - zb0);
   if (nb <= 0) return;
-  KScope _ks(c, "K7_voxel_eval");
-  voxel_eval_kernel<<<(unsigned)((nb + kEvalWarps - 1) / kEvalWarps), 32 * kEvalWarps, 0, c->stream>>>(
-      make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, vol);
+  // small grids (the train step's 32^3 TV sub-volume has 64 bricks): split
+  // each brick list over several warps, then sum. The split depends on the
+  // full grid only, so z-slab calls compute every brick exactly as the
+  // full-grid call does (slab volumes compose bit-exactly).
+  (void)n_pairs;
+  const long long nb_full =
+      (long long)bricks_x * bricks_y * (((long long)g.dims[2] + kTileVox - 1) / kTileVox);
+  int splits = 1;
+  while (splits < 16 && nb_full * splits * 2 <= (long long)c->sm_count * 32) splits *= 2;
+  if (const char* e = std::getenv("SCT_K7_SPLITS")) splits = std::max(1, std::min(16, atoi(e)));
+  const long long nvox = (long long)g.dims[0] * g.dims[1] * g.dims[2];
+  float* partial = nullptr;
+  // (every part writes every voxel of its slab bricks, so no clearing is needed)
+  if (splits > 1 && stage_buf(c, 25, sizeof(float) * (size_t)nvox * splits, (void**)&partial) != SCT_OK) return;
+  {
+    KScope _ks(c, "K7_voxel_eval");
+    const long long warps = nb * splits;
+    voxel_eval_kernel<<<(unsigned)((warps + kEvalWarps - 1) / kEvalWarps), 32 * kEvalWarps, 0, c->stream>>>(
+        make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, splits, partial, vol);
+  }
+  if (splits > 1) {
+    KScope _ks(c, "K7_reduce");
+    const long long z0 = (long long)zb0 * kTileVox, z1 = std::min<long long>((long long)zb1 * kTileVox, g.dims[2]);
+    const long long plane = (long long)g.dims[0] * g.dims[1];
+    const long long n = (z1 - z0) * plane;
+    if (n > 0)
+      voxel_reduce_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, (long long)c->sm_count * 16), 256, 0,
+                            c->stream>>>(partial + z0 * plane, splits, nvox, n, vol + z0 * plane);
+  }
 }
 
 void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
