@@ -699,11 +699,13 @@ int sct_project_kernels(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* s
 }
 
 // ---- host-buffer variants ----------------------------------------------------
-// Number of view chunks for overlapping the image/upstream copies with compute:
-// ~8 MB per chunk, at most Ctx::kChunkEvents.
-static int host_chunks(size_t bytes) {
+// Number of view chunks for overlapping the image/upstream copies with compute,
+// at most Ctx::kChunkEvents. Measured at cfg3 (78.6 MB of images either way):
+// the forward composite pays a tail per chunk, so ~40 MB chunks (2) are best
+// there; the backward hides its slower H2D best with ~20 MB chunks (4).
+static int host_chunks(size_t bytes, bool forward) {
   if (const char* e = std::getenv("SCT_HOST_CHUNKS")) return std::max(1, std::min(atoi(e), Ctx::kChunkEvents));
-  const size_t per = 20u << 20;
+  const size_t per = forward ? 40u << 20 : 20u << 20;
   size_t k = (bytes + per - 1) / per;
   if (k < 1) k = 1;
   if (k > (size_t)Ctx::kChunkEvents) k = Ctx::kChunkEvents;
@@ -742,7 +744,7 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
   // (copy stream) overlaps the next chunk's composite
   int rc = sct_render_fwd(c, &d, scanner, thetas, n_views, opts, nullptr, state);
   if (rc != SCT_OK) return rc;
-  const int chunks = std::min(n_views, host_chunks(n_views * px * sizeof(float)));
+  const int chunks = std::min(n_views, host_chunks(n_views * px * sizeof(float), true));
   for (int k = 0; k < chunks; ++k) {
     const int v0 = (int)((int64_t)n_views * k / chunks), v1 = (int)((int64_t)n_views * (k + 1) / chunks);
     launch_raster_composite(c, *state, dimg, v0, v1 - v0);
@@ -774,7 +776,7 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
   SCT_TRY(stage_buf(c, 5, s->n_views * px * sizeof(float), (void**)&ddl));
   // upstream gradient in view chunks on the copy stream; K4 for chunk k starts
   // as soon as chunk k has landed
-  const int chunks = std::min<int>(s->n_views, host_chunks(s->n_views * px * sizeof(float)));
+  const int chunks = std::min<int>(s->n_views, host_chunks(s->n_views * px * sizeof(float), false));
   for (int k = 0; k < chunks; ++k) {
     const int v0 = (int)((int64_t)s->n_views * k / chunks), v1 = (int)((int64_t)s->n_views * (k + 1) / chunks);
     SCT_CUDA_TRY(cudaMemcpyAsync(ddl + v0 * px, dL_host + v0 * px, (v1 - v0) * px * sizeof(float),
