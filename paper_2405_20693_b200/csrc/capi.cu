@@ -700,12 +700,11 @@ int sct_project_kernels(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* s
 
 // ---- host-buffer variants ----------------------------------------------------
 // Number of view chunks for overlapping the image/upstream copies with compute,
-// at most Ctx::kChunkEvents. Measured at cfg3 (78.6 MB of images either way):
-// the forward composite pays a tail per chunk, so ~40 MB chunks (2) are best
-// there; the backward hides its slower H2D best with ~20 MB chunks (4).
-static int host_chunks(size_t bytes, bool forward) {
+// at most Ctx::kChunkEvents: ~20 MB per chunk (4 at cfg3, measured best for
+// both directions once the forward chunks run on alternating streams).
+static int host_chunks(size_t bytes, bool /*forward*/) {
   if (const char* e = std::getenv("SCT_HOST_CHUNKS")) return std::max(1, std::min(atoi(e), Ctx::kChunkEvents));
-  const size_t per = forward ? 40u << 20 : 20u << 20;
+  const size_t per = 20u << 20;
   size_t k = (bytes + per - 1) / per;
   if (k < 1) k = 1;
   if (k > (size_t)Ctx::kChunkEvents) k = Ctx::kChunkEvents;
@@ -745,18 +744,21 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
   int rc = sct_render_fwd(c, &d, scanner, thetas, n_views, opts, nullptr, state);
   if (rc != SCT_OK) return rc;
   const int chunks = std::min(n_views, host_chunks(n_views * px * sizeof(float), true));
-  for (int k = 0; k < chunks; ++k) {
+  if ((*state)->n_pairs > 0) {
+    SCT_TRY(launch_raster_composite_chunks(c, *state, dimg, chunks, c->ev_compute));
+  } else {
+    SCT_CUDA_TRY(cudaMemsetAsync(dimg, 0, n_views * px * sizeof(float), c->stream));
+    for (int k = 0; k < chunks; ++k) SCT_CUDA_TRY(cudaEventRecord(c->ev_compute[k], c->stream));
+  }
+  for (int k = 0; k < chunks && images_host; ++k) {
     const int v0 = (int)((int64_t)n_views * k / chunks), v1 = (int)((int64_t)n_views * (k + 1) / chunks);
-    launch_raster_composite(c, *state, dimg, v0, v1 - v0);
-    if (images_host) {
-      SCT_CUDA_TRY(cudaEventRecord(c->ev_compute[k], c->stream));
-      SCT_CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev_compute[k], 0));
-      SCT_CUDA_TRY(cudaMemcpyAsync(images_host + v0 * px, dimg + v0 * px, (v1 - v0) * px * sizeof(float),
-                                   cudaMemcpyDeviceToHost, c->copy_stream));
-    }
+    SCT_CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev_compute[k], 0));
+    SCT_CUDA_TRY(cudaMemcpyAsync(images_host + v0 * px, dimg + v0 * px, (v1 - v0) * px * sizeof(float),
+                                 cudaMemcpyDeviceToHost, c->copy_stream));
   }
   SCT_CUDA_TRY(cudaGetLastError());
   SCT_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->aux_stream));
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return rc;
 }

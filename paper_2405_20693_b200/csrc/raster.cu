@@ -173,7 +173,8 @@ constexpr int kCompWarps = 4;
 __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     int tiles_x, int tiles_per_view, int W, int H, int view0, int total, int* __restrict__ work,
-    const int* __restrict__ order, int splits, float* __restrict__ partial, float* __restrict__ images) {
+    const int* __restrict__ order, int splits, float* __restrict__ partial, int pviews,
+    float* __restrict__ images) {
   __shared__ float4 sa[kCompWarps][32];
   __shared__ float4 sb[kCompWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -184,14 +185,14 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
       w = atomicAdd(work, 1);
       if (w < total * splits) {
         part = w % splits;
-        w = order[w / splits];  // longest lists first (tile_order)
+        w = order[w / splits];  // longest lists first (tile_order); may index views from view0
       } else {
-        w = total;
+        w = -1;
       }
     }
     w = __shfl_sync(0xffffffffu, w, 0);
     part = __shfl_sync(0xffffffffu, part, 0);
-    if (w >= total) break;
+    if (w < 0) break;
     const int view = view0 + w / tiles_per_view;
     const int tile = w % tiles_per_view;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     }
     if (v < H) {
       float* out = splits > 1
-                       ? partial + (((long long)part * (total / tiles_per_view) + (view - view0)) * H + v) * W
+                       ? partial + (((long long)part * pviews + (view - view0)) * H + v) * W
                        : images + ((long long)view * H + v) * W;
       if (u0 + 7 < W && (W & 3) == 0) {
         *reinterpret_cast<float4*>(out + u0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
@@ -678,6 +679,18 @@ __global__ void __launch_bounds__(256) composite_reduce_kernel(const float* __re
   }
 }
 
+// as composite_reduce_kernel, with a part stride independent of the range size
+__global__ void __launch_bounds__(256) composite_reduce_chunk_kernel(const float* __restrict__ partial, int splits,
+                                                                     long long stride, long long n,
+                                                                     float* __restrict__ images) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < splits; ++p) s += partial[(long long)p * stride + i];
+    images[i] = s;
+  }
+}
+
 // Longest-processing-time order of the (view, tile) lists of views
 // [v0, v0 + nv): local indices sorted by descending list length, so that K3's
 // persistent warps and K4's blocks start the long lists first and the kernels'
@@ -690,6 +703,21 @@ __global__ void __launch_bounds__(256) tile_order_keys_kernel(const int2* __rest
     // descending octave of the list length; the stable sort keeps the natural
     // (view-major, spatially coherent) order inside an octave for L2 locality
     keys[w] = 31u - (uint32_t)(32 - __clz(max(r.y - r.x, 0)));
+    idx[w] = w;
+  }
+}
+
+// keys for the chunked order: (chunk of the view, descending length octave)
+__global__ void __launch_bounds__(256) tile_order_chunk_keys_kernel(const int2* __restrict__ ranges, int n,
+                                                                    int tiles_per_view, int n_views, int chunks,
+                                                                    uint32_t* __restrict__ keys,
+                                                                    int32_t* __restrict__ idx) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
+    const int2 r = ranges[w];
+    const int v = w / tiles_per_view;
+    int k = 0;  // chunk k holds views [V k / chunks, V (k + 1) / chunks)
+    while (k + 1 < chunks && (long long)n_views * (k + 1) / chunks <= v) ++k;
+    keys[w] = ((uint32_t)k << 5) | (31u - (uint32_t)(32 - __clz(max(r.y - r.x, 0))));
     idx[w] = w;
   }
 }
@@ -725,23 +753,36 @@ static const int* cached_tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
 }
 
 // Views [v0, v0 + nv) of the forward state (nv <= 0: all views).
-void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, int nv) {
-  if (nv <= 0) nv = s->n_views - v0;
-  if (nv <= 0) return;
-  const int T = s->det.tiles_x * s->det.tiles_y;
+static int composite_per_sm() {
   static int per_sm = 0;
   if (!per_sm) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, composite_kernel, 32 * kCompWarps, 0);
     if (per_sm < 1) per_sm = 1;
   }
-  const long long total = (long long)T * nv;
-  // Small workloads (few views / tiles: the train step renders one view) have
-  // fewer lists than the GPU has warp slots: split each list into parts
-  // (>= 32 kernels each) written to partial images and summed in part order.
-  const long long slots = (long long)c->sm_count * per_sm * kCompWarps;
+  return per_sm;
+}
+
+// Small workloads (few views / tiles: the train step renders one view) have
+// fewer lists than the GPU has warp slots: split each list into parts
+// (>= 32 kernels each) written to partial images and summed in part order.
+// Decided per forward state (all its views), so the device path and the
+// chunked host path compose every tile identically.
+static int composite_splits(Ctx* c, const sct_fwd* s) {
+  const long long total = (long long)s->det.tiles_x * s->det.tiles_y * s->n_views;
+  const long long slots = (long long)c->sm_count * composite_per_sm() * kCompWarps;
   const double avg_len = total > 0 ? (double)s->n_pairs / (double)total : 0.0;
   int splits = 1;
   while (splits < 16 && total * splits * 2 <= slots && avg_len / (2 * splits) >= 32.0) splits *= 2;
+  return splits;
+}
+
+void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, int nv) {
+  if (nv <= 0) nv = s->n_views - v0;
+  if (nv <= 0) return;
+  const int T = s->det.tiles_x * s->det.tiles_y;
+  const int per_sm = composite_per_sm();
+  const long long total = (long long)T * nv;
+  const int splits = composite_splits(c, s);
   const size_t px = (size_t)s->det.w * s->det.h;
   float* partial = nullptr;
   if (splits > 1 && stage_buf(c, 24, sizeof(float) * px * nv * splits, (void**)&partial) != SCT_OK) return;
@@ -755,7 +796,7 @@ void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, in
     KScope _ks(c, "K3_composite");
     composite_kernel<<<blocks, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
                                                                 s->det.w, s->det.h, v0, (int)total, work, order,
-                                                                splits, partial, images);
+                                                                splits, partial, nv, images);
   }
   if (splits > 1) {
     KScope _ks(c, "K3_reduce");
@@ -763,6 +804,73 @@ void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, in
     composite_reduce_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(partial, splits, n,
                                                                         images + (size_t)v0 * px);
   }
+}
+
+// Host-buffer forward: the composite in `chunks` view chunks on alternating
+// streams (main / aux), so one chunk's tail overlaps the next chunk's start
+// and each chunk's D2H copy can begin as soon as the chunk is done
+// (done[k] is recorded after chunk k). One sort orders all chunks (chunk,
+// then longest lists first); each chunk has its own work counter.
+int launch_raster_composite_chunks(Ctx* c, const sct_fwd* s, float* images, int chunks, cudaEvent_t* done) {
+  const int V = s->n_views;
+  const int T = s->det.tiles_x * s->det.tiles_y;
+  const int n = T * V;
+  const int per_sm = composite_per_sm();
+  const int splits = composite_splits(c, s);
+  const size_t px = (size_t)s->det.w * s->det.h;
+  float* partial = nullptr;
+  if (splits > 1) SCT_TRY(stage_buf(c, 24, sizeof(float) * px * V * splits, (void**)&partial));
+  char* buf = nullptr;
+  int* work = nullptr;
+  SCT_TRY(stage_buf(c, 22, (size_t)4 * n * sizeof(uint32_t), (void**)&buf));
+  SCT_TRY(stage_buf(c, 26, sizeof(int) * Ctx::kChunkEvents, (void**)&work));
+  c->order_id = 0;  // slot 22 now holds the chunked order
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(buf);
+  uint32_t* k1 = k0 + n;
+  int32_t* i0 = reinterpret_cast<int32_t*>(k1 + n);
+  int32_t* i1 = i0 + n;
+  {
+    KScope _ks(c, "K2_tile_order");
+    tile_order_chunk_keys_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(s->d_ranges, n, T, V, chunks, k0, i0);
+  }
+  cub::DoubleBuffer<uint32_t> keys(k0, k1);
+  cub::DoubleBuffer<int32_t> vals(i0, i1);
+  size_t tmp = 0;
+  int bits = 5;
+  while ((1 << (bits - 5)) < chunks) ++bits;
+  SCT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, n, 0, bits, c->stream));
+  SCT_TRY(ensure_cub_tmp(c, tmp));
+  tmp = c->cub_tmp_bytes;
+  SCT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, vals, n, 0, bits, c->stream));
+  const int* order = vals.Current();
+  SCT_CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(int) * chunks, c->stream));
+  SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->stream));
+  SCT_CUDA_TRY(cudaStreamWaitEvent(c->aux_stream, c->ev_join, 0));
+  for (int k = 0; k < chunks; ++k) {
+    const int v0 = (int)((int64_t)V * k / chunks), v1 = (int)((int64_t)V * (k + 1) / chunks);
+    const long long total = (long long)T * (v1 - v0);
+    cudaStream_t st = (k & 1) ? c->aux_stream : c->stream;
+    const int blocks = (int)std::min<long long>((long long)c->sm_count * per_sm,
+                                                (total * splits + kCompWarps - 1) / kCompWarps);
+    {
+      KScope _ks(c, "K3_composite", true, st);
+      // global (view, tile) indices: view0 = 0, this chunk's slice of the order
+      composite_kernel<<<blocks, 32 * kCompWarps, 0, st>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
+                                                           s->det.w, s->det.h, 0, (int)total, work + k,
+                                                           order + (size_t)T * v0, splits, partial, V, images);
+    }
+    if (splits > 1) {
+      KScope _ks(c, "K3_reduce", true, st);
+      const long long nn = (long long)px * (v1 - v0);
+      // partial[p][view] for this chunk's views, summed in part order
+      composite_reduce_chunk_kernel<<<grid_cap(c, nn, 256), 256, 0, st>>>(partial + (size_t)v0 * px, splits,
+                                                                          (long long)px * V, nn,
+                                                                          images + (size_t)v0 * px);
+    }
+    SCT_CUDA_TRY(cudaEventRecord(done[k], st));
+  }
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
 }
 
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0, int nv,

@@ -193,6 +193,7 @@ void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32
 void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,
                           int64_t tiles_per_view, int2* ranges);
 void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0 = 0, int nv = 0);
+int launch_raster_composite_chunks(Ctx* c, const sct_fwd* s, float* images, int chunks, cudaEvent_t* done);
 // item_stats != nullptr: parallel-atomic mode, 8 floats per item accumulated
 // with atomics instead of per-pair slots
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0 = 0,
