@@ -161,6 +161,43 @@ __device__ __forceinline__ Run4 run4(float dx, float A, float A2, float bdy, flo
   return r;
 }
 
+// Eight pixels from one pair of MUFU ops (19 instead of 22 + 1 instructions
+// for two runs). Along a row L(x) = -a (x - x*)^2 + L*, a = |A|; a pixel that
+// matters (L >= -24: 2^-24 of the kernel's amplitude) sits within sqrt(24 / a)
+// of x*, so the run's first pixel is at most 49 a + 14 sqrt(24 a) below it.
+// It must stay above the ftz floor: -190 with K3's +64 offset (a <= 1.6);
+// narrower kernels take two 4-runs (a warp-uniform branch in K3).
+constexpr float kRun8MaxA_K3 = 1.5f;
+__device__ __forceinline__ void run8(float e[8], float dx, float A, float A2, float bdy, float apb, float cdy2o,
+                                     float K) {
+  const float t = fmaf(A, dx, bdy);
+  const float L = fmaf(dx, t, cdy2o);
+  const float D = fmaf(A2, dx, apb);
+  float E = ex2(L);
+  float R = ex2(fminf(D, 126.f));
+  e[0] = E;
+#pragma unroll
+  for (int k = 1; k < 8; ++k) {
+    E *= R;
+    if (k < 7) R *= K;
+    e[k] = E;
+  }
+}
+
+// the 8 pixels of a row at dx, dx+1, ..., dx+7: one 8-run when the kernel is
+// wide enough, else two 4-runs
+__device__ __forceinline__ void row8px(float e[8], float dx, float A, float A2, float bdy, float apb, float cdy2o,
+                                       float K, float amax) {
+  if (fabsf(A) <= amax) {
+    run8(e, dx, A, A2, bdy, apb, cdy2o, K);
+  } else {
+    const Run4 a = run4(dx, A, A2, bdy, apb, cdy2o, K);
+    const Run4 b = run4(dx + 4.f, A, A2, bdy, apb, cdy2o, K);
+    e[0] = a.e0; e[1] = a.e1; e[2] = a.e2; e[3] = a.e3;
+    e[4] = b.e0; e[5] = b.e1; e[6] = b.e2; e[7] = b.e3;
+  }
+}
+
 // K3: one warp per (tile, view); lane = 1 row x 8 columns (two 4-pixel runs
 // sharing the per-row setup). Persistent: each warp takes the next (view,
 // tile) from a global counter, so no warp waits for sibling warps with longer
@@ -235,16 +272,10 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
         const float apb = b.x + bdy;
         const float cdy2o = fmaf(b.z * dy, dy, 64.f);
         const float dx = px0 - a.x;
-        const Run4 e0 = run4(dx, b.x, b.w, bdy, apb, cdy2o, a.w);
-        const Run4 e1 = run4(dx + 4.f, b.x, b.w, bdy, apb, cdy2o, a.w);
-        acc[0] = fmaf(a.z, e0.e0, acc[0]);
-        acc[1] = fmaf(a.z, e0.e1, acc[1]);
-        acc[2] = fmaf(a.z, e0.e2, acc[2]);
-        acc[3] = fmaf(a.z, e0.e3, acc[3]);
-        acc[4] = fmaf(a.z, e1.e0, acc[4]);
-        acc[5] = fmaf(a.z, e1.e1, acc[5]);
-        acc[6] = fmaf(a.z, e1.e2, acc[6]);
-        acc[7] = fmaf(a.z, e1.e3, acc[7]);
+        float e[8];
+        row8px(e, dx, b.x, b.w, bdy, apb, cdy2o, a.w, kRun8MaxA_K3);  // warp-uniform branch
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = fmaf(a.z, e[k], acc[k]);
       }
     }
     if (v < H) {
@@ -576,13 +607,15 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
           const float apb = b.x + bdy;
           const float cdy2o = ok[k] ? fmaf(b.z * dy, dy, 15.f) : -1e30f;
           const float dx = px0 - a.x;
+          // (always two 4-runs here: the 8-run's per-thread branch diverges
+          // across the 16 kernels of a chunk and measured 19 % slower)
           const Run4 e0 = run4(dx, b.x, b.w, bdy, apb, cdy2o, a.w);
           const Run4 e1 = run4(dx + 4.f, b.x, b.w, bdy, apb, cdy2o, a.w);
           E[k][0] = e0.e0; E[k][1] = e0.e1; E[k][2] = e0.e2; E[k][3] = e0.e3;
           E[k][4] = e1.e0; E[k][5] = e1.e1; E[k][6] = e1.e2; E[k][7] = e1.e3;
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {  // two m16n8k16 slices per row pair, one 4-pixel run each
+        for (int h = 0; h < 2; ++h) {  // two m16n8k16 slices per row pair, four pixels each
           const uint4 gb = s_g[2 * q + h][lane];
           const __half2 a0 = __floats2half2_rn(E[0][4 * h], E[0][4 * h + 1]);
           const __half2 a1 = __floats2half2_rn(E[1][4 * h], E[1][4 * h + 1]);
