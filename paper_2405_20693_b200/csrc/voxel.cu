@@ -128,9 +128,24 @@ __device__ __forceinline__ void brick_of(const BrickGeo& G, long long b, int& tx
 
 // 8 voxel values along x for one row: E'(c) = 2^(L(dx0 + c*sx) + 64), c = 0..7.
 // rec_ok: use two 4-voxel ratio runs; otherwise one MUFU per voxel.
+// kRun8: a single 8-voxel run when Qxx sx^2 >= -1.5 (the bound of raster.cu's
+// run8 with the +64 offset; used by the forward, whose branch is warp-uniform).
+template <bool kRun8 = false>
 __device__ __forceinline__ void row8(float e[8], bool rec_ok, float dx0, float sx, float qxx, float c1, float c0o,
                                      float K) {
-  if (rec_ok) {
+  if (kRun8 && qxx * sx * sx >= -1.5f) {
+    const float qs = qxx * sx;
+    const float t = fmaf(qxx, dx0, c1);
+    float E = ex2v(fmaf(dx0, t, c0o));
+    float R = ex2v(fminf(fmaf(2.f * qs, dx0, fmaf(c1, sx, qs * sx)), 126.f));
+    e[0] = E;
+#pragma unroll
+    for (int c = 1; c < 8; ++c) {
+      E *= R;
+      if (c < 7) R *= K;
+      e[c] = E;
+    }
+  } else if (rec_ok) {
     const float qs = qxx * sx;
     const float dbase = fmaf(c1, sx, qs * sx);  // D(dx) = 2 qxx sx dx + c1 sx + qxx sx^2
 #pragma unroll
@@ -225,7 +240,7 @@ __global__ void __launch_bounds__(32 * kEvalWarps) voxel_eval_kernel(BrickGeo G,
         const float c0o = fmaf(q.y * dy, dy, fmaf(q.z * dz, dz, fmaf(o.z * dy, dz, 64.f)));
         const float c1 = fmaf(o.x, dy, o.y * dz);
         float e[8];
-        row8(e, rec_ok, a.x, G.spf.x, q.x, c1, c0o, q.w);
+        row8<true>(e, rec_ok, a.x, G.spf.x, q.x, c1, c0o, q.w);
 #pragma unroll
         for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(a.w, e[c], acc[r][c]);
       }
