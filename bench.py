@@ -514,8 +514,10 @@ def run_voxel(args, eng, vol, world, rank, dev):
 
     def step():
         grads.zero_()
-        eng.voxelize(cloud, grid, z_bricks=zb, out=out)
-        eng.voxelize_backward(cloud, grid, up, grads, z_bricks=zb)
+        # one binning shared by the forward and the backward (VoxelState)
+        _, vs = eng.voxelize(cloud, grid, z_bricks=zb, out=out, keep_state=True)
+        eng.voxelize_backward(cloud, grid, up, grads, z_bricks=zb, state=vs)
+        vs.free()
         if world > 1:
             pdist.allreduce_grads(grads)
 

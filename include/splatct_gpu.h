@@ -192,6 +192,18 @@ int sct_voxelize_fwd_host(sct_ctx* ctx, const sct_cloud* cloud_host, const sct_g
 int sct_voxelize_bwd_host(sct_ctx* ctx, const sct_cloud* cloud_host, const sct_grid* grid,
                           double cull_mahalanobis, const float* dL_dvol_host, sct_grads* grads_host);
 
+/* Forward + backward sharing one binning: sct_voxelize_fwd_state bins the
+ * kernels (as sct_voxelize_fwd; vol may be NULL to bin only) and keeps the brick
+ * lists in *state; sct_voxelize_bwd_state reuses them (the cloud must not change
+ * in between, as for sct_render_bwd); sct_vox_free releases the state. Results
+ * equal sct_voxelize_fwd / sct_voxelize_bwd, which re-bin like the reference. */
+typedef struct sct_vox_state sct_vox_state;
+int sct_voxelize_fwd_state(sct_ctx* ctx, const sct_cloud* cloud, const sct_grid* grid, double cull_mahalanobis,
+                           int32_t z_brick_begin, int32_t z_brick_end, float* vol, sct_vox_state** state);
+int sct_voxelize_bwd_state(sct_ctx* ctx, sct_vox_state* state, const sct_cloud* cloud, const float* dL_dvol,
+                           sct_grads* grads);
+int sct_vox_free(sct_vox_state* state);
+
 /* ---- objectives / optimizer -------------------------------------------- */
 /* TV value (device double [1], written) and lambda-scaled gradient (device, overwritten). */
 int sct_tv3d(sct_ctx* ctx, const float* vol, const int32_t dims[3], float lambda, double* value_dev,

@@ -82,6 +82,10 @@ SIGNATURES = {
     "sct_voxel_bins": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, I64, I64, I32]),
     "sct_voxelize_fwd_host": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, VP]),
     "sct_voxelize_bwd_host": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, VP, P(sct_grads)]),
+    "sct_voxelize_fwd_state": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, C.c_int32, C.c_int32, VP,
+                                         P(VP)]),
+    "sct_voxelize_bwd_state": (C.c_int, [VP, VP, P(sct_cloud), VP, P(sct_grads)]),
+    "sct_vox_free": (C.c_int, [VP]),
     "sct_tv3d": (C.c_int, [VP, VP, I32, C.c_float, VP, VP]),
     "sct_photometric_loss": (C.c_int, [VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float,
                                        C.c_float, VP, VP]),

@@ -863,6 +863,78 @@ int sct_voxelize_bwd(sct_ctx* c, const sct_cloud* cloud, const sct_grid* grid, d
   return rc;
 }
 
+// Forward + backward sharing one binning (the reference re-bins in
+// voxelize_backward, voxelizer.cpp:145, because it keeps no state; the brick
+// lists depend only on the cloud, grid, cull and slab, so they are reused).
+struct sct_vox_state {
+  sct_ctx* ctx = nullptr;
+  VoxelBins b;
+  sct_grid grid{};
+  double cull = 0.0;
+  int64_t m = 0;
+};
+
+int sct_voxelize_fwd_state(sct_ctx* c, const sct_cloud* cloud, const sct_grid* grid, double cull, int32_t zb0,
+                           int32_t zb1, float* vol, sct_vox_state** state) {
+  SCT_TRY(check_cloud(cloud));
+  SCT_TRY(check_grid(grid));
+  if (!state) {
+    set_error("ConfigError: null state pointer");
+    return SCT_ERR_CONFIG;
+  }
+  auto* s = new sct_vox_state();
+  s->ctx = c;
+  s->grid = *grid;
+  s->cull = cull;
+  s->m = cloud->m;
+  int rc = voxel_bin(c, *cloud, *grid, cull, zb0, zb1, s->b);
+  if (rc == SCT_OK && vol)
+    launch_voxel_eval(c, *grid, s->b.zb0, s->b.zb1, s->b.bx, s->b.by, s->b.ranges, s->b.vals, s->b.rec, *cloud,
+                      s->b.n_pairs, vol);
+  if (rc == SCT_OK && cudaGetLastError() != cudaSuccess) {
+    set_error("CUDA error: kernel launch in sct_voxelize_fwd_state");
+    rc = SCT_ERR_CUDA;
+  }
+  if (rc != SCT_OK) {
+    s->b.release(c);
+    delete s;
+    return rc;
+  }
+  *state = s;
+  return SCT_OK;
+}
+
+int sct_voxelize_bwd_state(sct_ctx* c, sct_vox_state* s, const sct_cloud* cloud, const float* dL,
+                           sct_grads* grads) {
+  SCT_TRY(check_cloud(cloud));
+  if (!s || !grads || !dL) {
+    set_error("ConfigError: null argument");
+    return SCT_ERR_CONFIG;
+  }
+  if (cloud->m != s->m) {
+    set_error("DimMismatch: voxelize_backward: cloud size differs from the forward state");
+    return SCT_ERR_DATA;
+  }
+  float4* ps = nullptr;
+  SCT_TRY(dev_alloc(c, (void**)&ps, 3 * s->b.n_pairs * sizeof(float4)));
+  launch_voxel_backward_stats(c, s->grid, s->b.zb0, s->b.zb1, s->b.bx, s->b.by, s->b.ranges, s->b.vals, s->b.rec,
+                              s->b.lo, s->b.hi, s->b.offset, *cloud, dL, ps);
+  launch_voxel_chain(c, *cloud, s->b.offset, s->b.count, ps, grads);
+  dev_free(c, ps);
+  if (cudaGetLastError() != cudaSuccess) {
+    set_error("CUDA error: kernel launch in sct_voxelize_bwd_state");
+    return SCT_ERR_CUDA;
+  }
+  return SCT_OK;
+}
+
+int sct_vox_free(sct_vox_state* s) {
+  if (!s) return SCT_OK;
+  s->b.release(s->ctx);
+  delete s;
+  return SCT_OK;
+}
+
 int sct_voxel_bins(sct_ctx* c, const sct_cloud* cloud, const sct_grid* grid, double cull, int64_t* n_pairs,
                    int64_t* offsets, int32_t* kernel_idx) {
   SCT_TRY(check_cloud(cloud));

@@ -362,25 +362,40 @@ class Engine:
 
     # ------------------------------------------------------------- voxelizer
     def voxelize(self, cloud: GaussianCloud, grid: GridSpec, opts: Optional[VoxelizeOptions] = None,
-                 z_bricks: Optional[tuple] = None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                 z_bricks: Optional[tuple] = None, out: Optional[torch.Tensor] = None, keep_state: bool = False):
+        """voxelizer.cpp:108-138. keep_state=True returns (volume, VoxelState): the brick lists
+        stay alive for voxelize_backward(state=...) instead of being rebuilt (the cloud must
+        not change in between)."""
         opts = opts or VoxelizeOptions()
         if out is None:
             out = (torch.empty if z_bricks is None else torch.zeros)(grid.shape_zyx, dtype=torch.float32,
                                                                       device=self.device)
         zb0, zb1 = z_bricks if z_bricks is not None else (0, 2 ** 31 - 1)
         cl, g = cloud._c(), grid._c()
+        if keep_state:
+            h = C.c_void_p()
+            _check(self.lib.sct_voxelize_fwd_state(self._h, C.byref(cl), C.byref(g), float(opts.cull_mahalanobis),
+                                                   zb0, zb1, _ptr(out), C.byref(h)))
+            return out, VoxelState(self, h, grid)
         _check(self.lib.sct_voxelize_fwd(self._h, C.byref(cl), C.byref(g), float(opts.cull_mahalanobis), zb0, zb1,
                                          _ptr(out)))
         return out
 
     def voxelize_backward(self, cloud: GaussianCloud, grid: GridSpec, dL_dV: torch.Tensor, grads: CloudGrads,
-                          opts: Optional[VoxelizeOptions] = None, z_bricks: Optional[tuple] = None):
+                          opts: Optional[VoxelizeOptions] = None, z_bricks: Optional[tuple] = None,
+                          state: Optional["VoxelState"] = None):
+        """voxelizer.cpp:140-224; accumulates into grads. With `state` (from voxelize(keep_state=True))
+        the forward's brick lists are reused (grid / cull / slab are the state's)."""
         opts = opts or VoxelizeOptions()
         if tuple(dL_dV.shape) != grid.shape_zyx:
             raise DimMismatch("voxelize_backward: gradient volume dims mismatch")
         dl = dL_dV.to(device=self.device, dtype=torch.float32).contiguous()
+        cl, gr = cloud._c(), grads._c()
+        if state is not None:
+            _check(self.lib.sct_voxelize_bwd_state(self._h, state._h, C.byref(cl), _ptr(dl), C.byref(gr)))
+            return
         zb0, zb1 = z_bricks if z_bricks is not None else (0, 2 ** 31 - 1)
-        cl, g, gr = cloud._c(), grid._c(), grads._c()
+        g = grid._c()
         _check(self.lib.sct_voxelize_bwd(self._h, C.byref(cl), C.byref(g), float(opts.cull_mahalanobis), zb0, zb1,
                                          _ptr(dl), C.byref(gr)))
 
@@ -521,6 +536,24 @@ class Engine:
         finally:
             self.lib.sct_adaptive_free(plan)
         return out, tuple(int(x) for x in counts)
+
+
+class VoxelState:
+    """Brick lists of one voxelize call, reused by voxelize_backward(state=...)."""
+
+    def __init__(self, engine: Engine, handle, grid: GridSpec):
+        self._engine, self._h, self.grid = engine, handle, grid
+
+    def free(self):
+        if getattr(self, "_h", None):
+            self._engine.lib.sct_vox_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # noqa: BLE001 (interpreter shutdown)
+            pass
 
 
 class RenderedProjection:

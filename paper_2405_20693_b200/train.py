@@ -101,9 +101,10 @@ class Trainer:
                                                      self.output_spacing, cfg.tv_grid_dim, self.rng.random(3))
             d = cfg.tv_grid_dim
             sub = GridSpec((d, d, d), sub_origin, self.output_spacing)
-            vol = eng.voxelize(cloud, sub)
+            vol, vstate = eng.voxelize(cloud, sub, keep_state=True)  # bins once for fwd + bwd
             tv, g_tv = eng.tv3d_loss(vol, cfg.lambda_tv)
-            eng.voxelize_backward(cloud, sub, g_tv, self.grads)
+            eng.voxelize_backward(cloud, sub, g_tv, self.grads, state=vstate)
+            vstate.free()
         total = vals[0, 0] + cfg.lambda_ssim * vals[0, 1] + cfg.lambda_tv * tv  # trainer.cpp:302-303
         if cfg.check_every and t % cfg.check_every == 0 and not math.isfinite(float(total.item())):
             raise DivergenceDetected(f"non-finite loss at iteration {t}")
