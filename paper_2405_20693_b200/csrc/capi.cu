@@ -1,5 +1,6 @@
 // C ABI (include/splatct_gpu.h): contexts, forward state, binning pipeline
 // (scan -> emit -> stable radix sort -> ranges) and the host-buffer entry points.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -345,6 +346,19 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
     cudaEventCreateWithFlags(&c->ev_copy[a], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  // unit signal words: 3 flag arrays, 2 counter arrays, the error word
+  // (device memory: kernel-side polls of mapped host words cost a PCIe read
+  // each, measured 50x slower for K4)
+  char* u = nullptr;
+  if (cudaMalloc((void**)&u, 6 * Ctx::kMaxUnits * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemset(u, 0, 6 * Ctx::kMaxUnits * sizeof(uint32_t)) != cudaSuccess) {
+    sct_ctx_destroy(c);
+    set_error("CUDA error: context signal allocation failed");
+    return SCT_ERR_CUDA;
+  }
+  c->unit_flags = reinterpret_cast<uint32_t*>(u);
+  c->unit_done = reinterpret_cast<int*>(c->unit_flags + 3 * Ctx::kMaxUnits);
+  c->unit_err = c->unit_done + 2 * Ctx::kMaxUnits;
   *out = c;
   return SCT_OK;
 }
@@ -364,6 +378,7 @@ int sct_ctx_destroy(sct_ctx* c) {
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->unit_flags) cudaFree(c->unit_flags);
   delete c;
   return SCT_OK;
 }
@@ -594,6 +609,135 @@ int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
   return SCT_OK;
 }
 
+// ------------------------------------------------------------------ view units
+// Stream memory operations (driver entry points, resolved through the
+// runtime): a stream waits until a device word reaches the call's epoch, or
+// writes it. Used by the host-buffer entry points so that one kernel over all
+// views overlaps the per-unit copies; SCT_HOST_UNITS=0 selects the chunked
+// multi-launch path instead.
+typedef CUresult (*PfnStreamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct StreamMemOps {
+  PfnStreamValue32 wait = nullptr, write = nullptr;
+};
+static const StreamMemOps& memops() {
+  static const StreamMemOps m = [] {
+    StreamMemOps r;
+    if (const char* e = std::getenv("SCT_HOST_UNITS"))
+      if (atoi(e) == 0) return r;
+    void* w = nullptr;
+    void* x = nullptr;
+    cudaDriverEntryPointQueryResult q1 = cudaDriverEntryPointSymbolNotFound, q2 = q1;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWriteValue32", &x, cudaEnableDefault, &q2) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && w && x) {
+      r.wait = reinterpret_cast<PfnStreamValue32>(w);
+      r.write = reinterpret_cast<PfnStreamValue32>(x);
+    }
+    cudaGetLastError();
+    return r;
+  }();
+  return m;
+}
+
+static int stream_wait_flag(cudaStream_t st, const uint32_t* flag, uint32_t epoch) {
+  if (memops().wait((CUstream)st, (CUdeviceptr)flag, epoch, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+    set_error("CUDA error: cuStreamWaitValue32");
+    return SCT_ERR_CUDA;
+  }
+  return SCT_OK;
+}
+
+static int stream_write_flag(cudaStream_t st, uint32_t* flag, uint32_t epoch) {
+  if (memops().write((CUstream)st, (CUdeviceptr)flag, epoch, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+    set_error("CUDA error: cuStreamWriteValue32");
+    return SCT_ERR_CUDA;
+  }
+  return SCT_OK;
+}
+
+// view units of a host transfer of `bytes` over n_views views: ~4 MB each
+static int host_units(int n_views, size_t bytes) {
+  if (const char* e = std::getenv("SCT_UNIT_KB")) {
+    const size_t per = (size_t)std::max(1, atoi(e)) << 10;
+    return (int)std::max<size_t>(1, std::min<size_t>({(bytes + per - 1) / per, (size_t)n_views,
+                                                       (size_t)Ctx::kMaxUnits}));
+  }
+  const size_t per = 4u << 20;
+  return (int)std::max<size_t>(1, std::min<size_t>({(bytes + per - 1) / per, (size_t)n_views,
+                                                     (size_t)Ctx::kMaxUnits}));
+}
+
+// the error word of a kernel-side unit wait (read after the call's stream sync)
+static int check_unit_err(Ctx* c) {
+  int32_t* h = reinterpret_cast<int32_t*>(c->pinned_count) + 8;
+  if (*h) {
+    *h = 0;
+    cudaMemsetAsync(c->unit_err, 0, sizeof(int), c->stream);
+    cudaStreamSynchronize(c->stream);
+    set_error("CUDA error: a view-unit wait timed out (host-buffer backward)");
+    return SCT_ERR_CUDA;
+  }
+  return SCT_OK;
+}
+
+// Backward with the upstream gradient landing in view units (unit_flags[1][u]
+// written by the copy stream): one K4 over all views waits per unit and
+// publishes unit_flags[2][u]; the FP64 chain runs on the aux stream in groups
+// of units, each group starting when its units' statistics are published.
+static int render_bwd_units(Ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
+                            sct_stats* stats, int units, uint32_t epoch) {
+  SCT_TRY(check_cloud(cloud));
+  if (cloud->m != s->m) {
+    set_error("DimMismatch: render_backward: cloud size differs from the forward state");
+    return SCT_ERR_DATA;
+  }
+  if (s->n_items == 0) return SCT_OK;
+  const bool atomic = !c->deterministic;
+  float4* pair_stats = nullptr;
+  float* item_stats = nullptr;
+  float* item_grads = nullptr;
+  if (atomic) {
+    SCT_TRY(stage_buf(c, 14, 8 * s->n_items * sizeof(float), (void**)&item_stats));
+    SCT_CUDA_TRY(cudaMemsetAsync(item_stats, 0, 8 * s->n_items * sizeof(float), c->stream));
+  } else {
+    SCT_TRY(stage_buf(c, 14, 2 * s->n_pairs * sizeof(float4), (void**)&pair_stats));
+  }
+  SCT_TRY(stage_buf(c, 15, 11 * s->n_items * sizeof(float), (void**)&item_grads));
+  uint32_t* ready = c->unit_flags + Ctx::kMaxUnits;
+  uint32_t* k4_done = c->unit_flags + 2 * Ctx::kMaxUnits;
+  int* counters = c->unit_done + Ctx::kMaxUnits;
+  SCT_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(int) * units, c->stream));
+  SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->stream));  // the chain stream sees the uploads and zeroing
+  SCT_CUDA_TRY(cudaStreamWaitEvent(c->aux_stream, c->ev_join, 0));
+  UnitSync us;
+  us.ready = ready;
+  us.done_flag = k4_done;
+  us.done = counters;
+  us.err = c->unit_err;
+  us.epoch = epoch;
+  us.units = units;
+  us.n_views = s->n_views;
+  launch_raster_backward_stats(c, s, dL, pair_stats, 0, 0, item_stats, &us);
+  SCT_CUDA_TRY(cudaGetLastError());
+  // a lost kernel-side signal only delays the chain to the end of K4
+  for (int u = 0; u < units; ++u) SCT_TRY(stream_write_flag(c->stream, k4_done + u, epoch));
+  const float4* chain_src = atomic ? reinterpret_cast<const float4*>(item_stats) : pair_stats;
+  const int groups = std::min(units, 4);
+  for (int g = 0; g < groups; ++g) {
+    const int u0 = units * g / groups, u1 = units * (g + 1) / groups;
+    for (int u = u0; u < u1; ++u) SCT_TRY(stream_wait_flag(c->aux_stream, k4_done + u, epoch));
+    const int64_t v0 = (int64_t)s->n_views * u0 / units, v1 = (int64_t)s->n_views * u1 / units;
+    launch_raster_chain(c, s, *cloud, chain_src, item_grads, atomic, v0 * s->m, v1 * s->m, c->aux_stream);
+  }
+  SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->aux_stream));
+  SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  launch_raster_finalize(c, s, *cloud, item_grads, grads, stats);
+  SCT_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int32_t*>(c->pinned_count) + 8, c->unit_err, sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, c->stream));
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
+
 int sct_render_bwd(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
                    sct_stats* stats) {
   return sct_render_bwd_chunked(c, s, cloud, dL, grads, stats, 0);
@@ -699,9 +843,9 @@ int sct_project_kernels(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* s
 }
 
 // ---- host-buffer variants ----------------------------------------------------
-// Number of view chunks for overlapping the image/upstream copies with compute,
-// at most Ctx::kChunkEvents: ~20 MB per chunk (4 at cfg3, measured best for
-// both directions once the forward chunks run on alternating streams).
+// Number of view chunks of the backward's upstream-gradient copy when stream
+// memory operations are unavailable, at most Ctx::kChunkEvents: ~20 MB per
+// chunk (4 at cfg3, measured best).
 static int host_chunks(size_t bytes, bool /*forward*/) {
   if (const char* e = std::getenv("SCT_HOST_CHUNKS")) return std::max(1, std::min(atoi(e), Ctx::kChunkEvents));
   const size_t per = 20u << 20;
@@ -739,26 +883,87 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
   const size_t px = (size_t)scanner->det_res_px[0] * scanner->det_res_px[1];
   float* dimg = nullptr;
   SCT_TRY(stage_buf(c, 4, n_views * px * sizeof(float), (void**)&dimg));
-  // binning for all views, then the composite in view chunks whose D2H copy
-  // (copy stream) overlaps the next chunk's composite
+  // binning for all views, then one composite whose view units are copied
+  // to the host (copy stream) as they complete
   int rc = sct_render_fwd(c, &d, scanner, thetas, n_views, opts, nullptr, state);
   if (rc != SCT_OK) return rc;
-  const int chunks = std::min(n_views, host_chunks(n_views * px * sizeof(float), true));
-  if ((*state)->n_pairs > 0) {
-    SCT_TRY(launch_raster_composite_chunks(c, *state, dimg, chunks, c->ev_compute));
-  } else {
+  if (memops().wait && images_host && (*state)->n_pairs > 0 && raster_units_supported(c, *state)) {
+    // one composite over all views; unit u's D2H copy starts when the
+    // composite publishes unit_flags[0][u] (and at the latest after the
+    // kernel, which re-publishes every unit)
+    const int units = host_units(n_views, n_views * px * sizeof(float));
+    const uint32_t epoch = ++c->epoch;
+    SCT_CUDA_TRY(cudaMemsetAsync(c->unit_done, 0, sizeof(int) * units, c->stream));
+    UnitSync us;
+    us.done_flag = c->unit_flags;
+    us.done = c->unit_done;
+    us.epoch = epoch;
+    us.units = units;
+    us.n_views = n_views;
+    static const bool dbg = std::getenv("SCT_UNIT_DEBUG") != nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr, ec[Ctx::kMaxUnits] = {};
+    unsigned long long* stamp = nullptr;
+    if (dbg) {
+      cudaMalloc((void**)&stamp, (4 * Ctx::kMaxUnits + 1) * sizeof(unsigned long long));
+      cudaMemset(stamp, 0xff, (2 * Ctx::kMaxUnits + 1) * sizeof(unsigned long long));
+      cudaMemset(stamp + 2 * Ctx::kMaxUnits + 1, 0, 2 * Ctx::kMaxUnits * sizeof(unsigned long long));
+      us.stamp = stamp;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      for (int u = 0; u < units; ++u) cudaEventCreate(&ec[u]);
+      cudaEventRecord(e0, c->stream);
+    }
+    SCT_TRY(launch_raster_composite_units(c, *state, dimg, us));
+    if (dbg) cudaEventRecord(e1, c->stream);
+    for (int u = 0; u < units; ++u) SCT_TRY(stream_write_flag(c->stream, c->unit_flags + u, epoch));
+    for (int u = 0; u < units; ++u) {
+      const int v0 = (int)((int64_t)n_views * u / units), v1 = (int)((int64_t)n_views * (u + 1) / units);
+      SCT_TRY(stream_wait_flag(c->copy_stream, c->unit_flags + u, epoch));
+      SCT_CUDA_TRY(cudaMemcpyAsync(images_host + v0 * px, dimg + v0 * px, (v1 - v0) * px * sizeof(float),
+                                   cudaMemcpyDeviceToHost, c->copy_stream));
+      if (dbg) cudaEventRecord(ec[u], c->copy_stream);
+    }
+    SCT_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+    SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (dbg) {
+      float k = 0.f;
+      cudaEventElapsedTime(&k, e0, e1);
+      std::fprintf(stderr, "[units] composite %.3f ms; copies done at", k);
+      for (int u = 0; u < units; ++u) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e0, ec[u]);
+        std::fprintf(stderr, " %.3f", t);
+        cudaEventDestroy(ec[u]);
+      }
+      std::fprintf(stderr, "\n");
+      unsigned long long hs[4 * Ctx::kMaxUnits + 1];
+      cudaMemcpy(hs, stamp, sizeof(hs), cudaMemcpyDeviceToHost);
+      std::fprintf(stderr, "[units] longest item (ms)");
+      for (int u = 0; u < units; ++u) std::fprintf(stderr, " %.3f", 1e-6 * (double)hs[3 * Ctx::kMaxUnits + 1 + u]);
+      std::fprintf(stderr, "\n");
+      const char* what[3] = {"published", "first claim", "last claim"};
+      const int off[3] = {0, Ctx::kMaxUnits + 1, 2 * Ctx::kMaxUnits + 1};
+      for (int k = 0; k < 3; ++k) {
+        std::fprintf(stderr, "[units] %s at (ms after first claim)", what[k]);
+        for (int u = 0; u < units; ++u)
+          std::fprintf(stderr, " %.3f", 1e-6 * (double)(hs[off[k] + u] - hs[Ctx::kMaxUnits]));
+        std::fprintf(stderr, "\n");
+      }
+      cudaFree(stamp);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    return SCT_OK;
+  }
+  // without stream memory operations: one composite, then one copy
+  if ((*state)->n_pairs > 0)
+    launch_raster_composite(c, *state, dimg);
+  else
     SCT_CUDA_TRY(cudaMemsetAsync(dimg, 0, n_views * px * sizeof(float), c->stream));
-    for (int k = 0; k < chunks; ++k) SCT_CUDA_TRY(cudaEventRecord(c->ev_compute[k], c->stream));
-  }
-  for (int k = 0; k < chunks && images_host; ++k) {
-    const int v0 = (int)((int64_t)n_views * k / chunks), v1 = (int)((int64_t)n_views * (k + 1) / chunks);
-    SCT_CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev_compute[k], 0));
-    SCT_CUDA_TRY(cudaMemcpyAsync(images_host + v0 * px, dimg + v0 * px, (v1 - v0) * px * sizeof(float),
-                                 cudaMemcpyDeviceToHost, c->copy_stream));
-  }
+  if (images_host)
+    SCT_CUDA_TRY(cudaMemcpyAsync(images_host, dimg, n_views * px * sizeof(float), cudaMemcpyDeviceToHost,
+                                 c->stream));
   SCT_CUDA_TRY(cudaGetLastError());
-  SCT_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
-  SCT_CUDA_TRY(cudaStreamSynchronize(c->aux_stream));
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return rc;
 }
@@ -776,9 +981,19 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
   const size_t px = (size_t)s->det.w * s->det.h;
   float* ddl = nullptr;
   SCT_TRY(stage_buf(c, 5, s->n_views * px * sizeof(float), (void**)&ddl));
-  // upstream gradient in view chunks on the copy stream; K4 for chunk k starts
-  // as soon as chunk k has landed
-  const int chunks = std::min<int>(s->n_views, host_chunks(s->n_views * px * sizeof(float), false));
+  // upstream gradient in view units (one K4 waits per unit, unit_flags[1])
+  // or in view chunks (K4 for chunk k starts once chunk k has landed)
+  const bool units_path = memops().wait && s->n_items > 0 && raster_units_supported(c, s);
+  const int units = units_path ? host_units(s->n_views, s->n_views * px * sizeof(float)) : 0;
+  const uint32_t epoch = units_path ? ++c->epoch : 0;
+  for (int u = 0; u < units; ++u) {
+    const int v0 = (int)((int64_t)s->n_views * u / units), v1 = (int)((int64_t)s->n_views * (u + 1) / units);
+    SCT_CUDA_TRY(cudaMemcpyAsync(ddl + v0 * px, dL_host + v0 * px, (v1 - v0) * px * sizeof(float),
+                                 cudaMemcpyHostToDevice, c->copy_stream));
+    SCT_TRY(stream_write_flag(c->copy_stream, c->unit_flags + Ctx::kMaxUnits + u, epoch));
+  }
+  const int chunks =
+      units_path ? 0 : std::min<int>(s->n_views, host_chunks(s->n_views * px * sizeof(float), false));
   for (int k = 0; k < chunks; ++k) {
     const int v0 = (int)((int64_t)s->n_views * k / chunks), v1 = (int)((int64_t)s->n_views * (k + 1) / chunks);
     SCT_CUDA_TRY(cudaMemcpyAsync(ddl + v0 * px, dL_host + v0 * px, (v1 - v0) * px * sizeof(float),
@@ -807,7 +1022,8 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
       SCT_CUDA_TRY(cudaMemcpyAsync(*sd[a], sh[a], sb[a], cudaMemcpyHostToDevice, c->stream));
     }
   }
-  int rc = sct_render_bwd_chunked(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, chunks);
+  int rc = units_path ? render_bwd_units(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, units, epoch)
+                      : sct_render_bwd_chunked(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, chunks);
   if (rc == SCT_OK) {
     for (int a = 0; a < 4; ++a)
       SCT_CUDA_TRY(cudaMemcpyAsync(gh[a], *gd[a], n[a] * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
@@ -817,6 +1033,7 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
   }
   SCT_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (rc == SCT_OK && units_path) rc = check_unit_err(c);
   return rc;
 }
 

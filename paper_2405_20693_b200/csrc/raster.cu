@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstdlib>
@@ -198,51 +199,55 @@ __device__ __forceinline__ void row8px(float e[8], float dx, float A, float A2, 
   }
 }
 
-// K3: one warp per (tile, view); lane = 1 row x 8 columns (two 4-pixel runs
-// sharing the per-row setup). Persistent: each warp takes the next (view,
-// tile) from a global counter, so no warp waits for sibling warps with longer
-// lists and residency stays at the register limit until the tail. Each warp
-// stages its list through shared memory 32 records at a time (one coalesced
-// gather per lane) and synchronises only itself (__syncwarp); the next
-// chunk's records are fetched into registers while the current chunk is
-// evaluated, so the gather latency overlaps the arithmetic.
+// K3: one warp per work item = one part of one (view, tile) list; lane = 1
+// row x 8 columns (two 4-pixel runs sharing the per-row setup). Lists longer
+// than kPart kernels are cut into parts of kPart (K3Work): every work item is
+// short, so the persistent warps stay balanced and finish the items in claim
+// order (which the host-buffer path relies on to publish view units early).
+// A one-part list is accumulated straight into the image; a part of a longer
+// list writes its 16x16 partial tile, and the last part to finish sums the
+// parts in part order (fixed, so the result does not depend on timing) and
+// writes the image tile. Persistent: each warp takes the next item from a
+// global counter and stages the list through shared memory 32 records at a
+// time (one coalesced gather per lane), synchronising only itself; the next
+// chunk's records are fetched while the current chunk is evaluated.
 constexpr int kCompWarps = 4;
 __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
-    int tiles_x, int tiles_per_view, int W, int H, int view0, int total, int* __restrict__ work,
-    const int* __restrict__ order, int splits, float* __restrict__ partial, int pviews,
-    float* __restrict__ images) {
+    int tiles_x, int tiles_per_view, int W, int H, const int4* __restrict__ items, const int* __restrict__ n_items,
+    int part_len, int* __restrict__ work, int* __restrict__ tile_cnt, float* __restrict__ partial,
+    float* __restrict__ images, UnitSync us) {
   __shared__ float4 sa[kCompWarps][32];
   __shared__ float4 sb[kCompWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = lane >> 1;
+  const int total = *n_items;
   for (;;) {
-    int w = 0, part = 0;
-    if (lane == 0) {
-      w = atomicAdd(work, 1);
-      if (w < total * splits) {
-        part = w % splits;
-        w = order[w / splits];  // longest lists first (tile_order); may index views from view0
-      } else {
-        w = -1;
-      }
+    int c = 0;
+    if (lane == 0) c = atomicAdd(work, 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= total) break;
+    const int4 it = items[c];  // (view * T + tile, part, parts, first item of the list)
+    unsigned long long t_claim = 0;
+    if (us.stamp && lane == 0) {
+      const unsigned long long now = global_ns();
+      t_claim = now;
+      const int uu = unit_of_view(it.x / tiles_per_view, us.n_views, us.units);
+      atomicMin(us.stamp + Ctx::kMaxUnits, now);
+      atomicMin(us.stamp + Ctx::kMaxUnits + 1 + uu, now);
+      atomicMax(us.stamp + 2 * Ctx::kMaxUnits + 1 + uu, now);
     }
-    w = __shfl_sync(0xffffffffu, w, 0);
-    part = __shfl_sync(0xffffffffu, part, 0);
-    if (w < 0) break;
-    const int view = view0 + w / tiles_per_view;
+    const int w = it.x, part = it.y, parts = it.z;
+    const int view = w / tiles_per_view;
     const int tile = w % tiles_per_view;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int u0 = tx * kTilePx + (lane & 1) * 8;
     const int v = ty * kTilePx + row;
     const float py = (float)v + 0.5f;
     const float px0 = (float)u0 + 0.5f;
-    int2 rg = ranges[(long long)view * tiles_per_view + tile];
-    if (splits > 1) {  // small workloads: the list is split into `splits` parts, summed by composite_reduce
-      const int len = rg.y - rg.x, s0 = rg.x;
-      rg.x = s0 + (int)((long long)len * part / splits);
-      rg.y = s0 + (int)((long long)len * (part + 1) / splits);
-    }
+    int2 rg = ranges[w];
+    rg.x += part * part_len;
+    rg.y = min(rg.y, rg.x + part_len);
     float acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.f;
@@ -278,10 +283,41 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
         for (int k = 0; k < 8; ++k) acc[k] = fmaf(a.z, e[k], acc[k]);
       }
     }
+    if (parts > 1) {
+      // partial tile of this part (lane: row, 8 columns), then the last part sums all parts in order
+      float4* mine = reinterpret_cast<float4*>(partial + (long long)(it.w + part) * 256) + 2 * lane;
+      mine[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      mine[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      __threadfence();
+      __syncwarp();
+      int done = 0;
+      if (lane == 0) {
+        done = atomicAdd(tile_cnt + it.w, 1) == parts - 1;
+        if (done) tile_cnt[it.w] = 0;  // ready for the next launch
+      }
+      done = __shfl_sync(0xffffffffu, done, 0);
+      if (us.stamp && lane == 0)
+        atomicMax(us.stamp + 3 * Ctx::kMaxUnits + 1 + unit_of_view(view, us.n_views, us.units),
+                  global_ns() - t_claim);
+      if (!done) continue;
+      __threadfence();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+      for (int q = 0; q < parts; ++q) {
+        const float4* src = reinterpret_cast<const float4*>(partial + (long long)(it.w + q) * 256) + 2 * lane;
+        const float4 p0 = __ldcg(src), p1 = __ldcg(src + 1);
+        acc[0] += p0.x;
+        acc[1] += p0.y;
+        acc[2] += p0.z;
+        acc[3] += p0.w;
+        acc[4] += p1.x;
+        acc[5] += p1.y;
+        acc[6] += p1.z;
+        acc[7] += p1.w;
+      }
+    }
     if (v < H) {
-      float* out = splits > 1
-                       ? partial + (((long long)part * pviews + (view - view0)) * H + v) * W
-                       : images + ((long long)view * H + v) * W;
+      float* out = images + ((long long)view * H + v) * W;
       if (u0 + 7 < W && (W & 3) == 0) {
         *reinterpret_cast<float4*>(out + u0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
         *reinterpret_cast<float4*>(out + u0 + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
@@ -291,6 +327,34 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
           if (u0 + k < W) out[u0 + k] = acc[k];
       }
     }
+    if (us.done) {  // host path: publish the view unit once all its tiles are written
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) unit_signal(us, unit_of_view(view, us.n_views, us.units));
+      if (us.stamp && lane == 0)
+        atomicMax(us.stamp + 3 * Ctx::kMaxUnits + 1 + unit_of_view(view, us.n_views, us.units),
+                  global_ns() - t_claim);
+    }
+  }
+}
+
+// Work items of K3 in the given (view, tile) order: list i of length n gets
+// max(1, ceil(n / part_len)) consecutive items (exclusive scan `first`).
+__global__ void __launch_bounds__(256) k3_parts_kernel(const int2* __restrict__ ranges, const int* __restrict__ order,
+                                                       int n, int part_len, int* __restrict__ count) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int2 r = ranges[order[i]];
+    count[i] = max(1, (r.y - r.x + part_len - 1) / part_len);
+  }
+}
+
+__global__ void __launch_bounds__(256) k3_items_kernel(const int* __restrict__ order, const int* __restrict__ count,
+                                                       const int* __restrict__ first, int n,
+                                                       int4* __restrict__ items, int* __restrict__ n_items) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int k = count[i], f = first[i], w = order[i];
+    for (int p = 0; p < k; ++p) items[f + p] = make_int4(w, p, k, f);
+    if (i == n - 1) *n_items = f + k;
   }
 }
 
@@ -507,7 +571,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
     const short4* __restrict__ rect, const int32_t* __restrict__ offset, int tiles_x, int tiles_per_view, int W,
     int H, int view0, const int* __restrict__ order, int parts, const float* __restrict__ dL,
     float* __restrict__ pair_stats,
-    float* __restrict__ item_stats) {
+    float* __restrict__ item_stats, UnitSync us) {
   __shared__ uint4 s_g[16][32];  // [slice][lane] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}
   __shared__ float s_gmax[kMmaWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -519,13 +583,22 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
     const int part = blockIdx.x % parts;
     const int tile = w % tiles_per_view;
     const int view = view0 + w / tiles_per_view;
+    // host path: wait for this view unit's upstream gradient (H2D copy on the copy stream)
+    const int unit = (us.ready || us.done) ? unit_of_view(view, us.n_views, us.units) : 0;
+    if (us.ready) {
+      if (threadIdx.x == 0) unit_wait(us, unit);
+      __syncthreads();
+    }
     int2 rg = ranges[(long long)view * tiles_per_view + tile];
     if (parts > 1) {  // small workloads: several CTAs share a list (pair statistics are independent)
       const int len = rg.y - rg.x, s0 = rg.x;
       rg.x = s0 + (int)((long long)len * part / parts);
       rg.y = s0 + (int)((long long)len * (part + 1) / parts);
     }
-    if (rg.y <= rg.x) return;
+    if (rg.y <= rg.x) {
+      if (threadIdx.x == 0) unit_signal(us, unit);
+      return;
+    }
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int u0 = tx * kTilePx, v0 = ty * kTilePx;
     const float* dtile = dL + ((long long)view * H + v0) * W + u0;
@@ -664,6 +737,11 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
         }
       }
     }
+    if (us.done) {  // host path: publish the unit to the chain stream once all its lists are done
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) unit_signal(us, unit);
+    }
   }
 }
 
@@ -699,29 +777,6 @@ void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16
   else
     raster_ranges_kernel<uint32_t><<<grid_cap(c, n_pairs, 256), 256, 0, c->stream>>>(
         n_pairs, static_cast<const uint32_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
-}
-
-// images = sum over parts (in part order) of the split composite's partials
-__global__ void __launch_bounds__(256) composite_reduce_kernel(const float* __restrict__ partial, int splits,
-                                                               long long n, float* __restrict__ images) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int p = 0; p < splits; ++p) s += partial[(long long)p * n + i];
-    images[i] = s;
-  }
-}
-
-// as composite_reduce_kernel, with a part stride independent of the range size
-__global__ void __launch_bounds__(256) composite_reduce_chunk_kernel(const float* __restrict__ partial, int splits,
-                                                                     long long stride, long long n,
-                                                                     float* __restrict__ images) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int p = 0; p < splits; ++p) s += partial[(long long)p * stride + i];
-    images[i] = s;
-  }
 }
 
 // Longest-processing-time order of the (view, tile) lists of views
@@ -785,7 +840,55 @@ static const int* cached_tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
   return c->order_ptr;
 }
 
-// Views [v0, v0 + nv) of the forward state (nv <= 0: all views).
+// (view unit, then longest lists first) order of all views: unit u holds
+// views [V u / units, V (u + 1) / units) and precedes unit u + 1, so the
+// kernels of the host-buffer path finish (and publish) units in order while
+// each unit's own tail stays short. Cached like cached_tile_order
+// (order_v0 = -1 marks a unit order of order_nv units).
+static const int* unit_tile_order(Ctx* c, const sct_fwd* s, int units) {
+  if (c->order_id == s->id && c->order_v0 == -1 && c->order_nv == units && c->order_ptr) return c->order_ptr;
+  const int V = s->n_views;
+  const int T = s->det.tiles_x * s->det.tiles_y;
+  const int n = T * V;
+  char* buf = nullptr;
+  c->order_id = 0;
+  if (stage_buf(c, 22, (size_t)4 * n * sizeof(uint32_t), (void**)&buf) != SCT_OK) return nullptr;
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(buf);
+  uint32_t* k1 = k0 + n;
+  int32_t* i0 = reinterpret_cast<int32_t*>(k1 + n);
+  int32_t* i1 = i0 + n;
+  {
+    KScope _ks(c, "K2_tile_order");
+    tile_order_chunk_keys_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(s->d_ranges, n, T, V, units, k0, i0);
+  }
+  cub::DoubleBuffer<uint32_t> keys(k0, k1);
+  cub::DoubleBuffer<int32_t> vals(i0, i1);
+  size_t tmp = 0;
+  int bits = 5;
+  while ((1 << (bits - 5)) < units) ++bits;
+  if (cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, n, 0, bits, c->stream) != cudaSuccess ||
+      ensure_cub_tmp(c, tmp) != SCT_OK)
+    return nullptr;
+  tmp = c->cub_tmp_bytes;
+  if (cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, vals, n, 0, bits, c->stream) != cudaSuccess)
+    return nullptr;
+  c->order_ptr = vals.Current();
+  c->order_id = s->id;
+  c->order_v0 = -1;
+  c->order_nv = units;
+  return c->order_ptr;
+}
+
+// SCT_K4=simt selects the FP32 SIMT statistics kernel (the reference-order
+// arithmetic without tensor cores); default: the tensor-core kernel
+static bool k4_simt() {
+  static const bool simt = [] {
+    const char* e = std::getenv("SCT_K4");
+    return e && std::string(e) == "simt";
+  }();
+  return simt;
+}
+
 static int composite_per_sm() {
   static int per_sm = 0;
   if (!per_sm) {
@@ -795,130 +898,111 @@ static int composite_per_sm() {
   return per_sm;
 }
 
-// Small workloads (few views / tiles: the train step renders one view) have
-// fewer lists than the GPU has warp slots: split each list into parts
-// (>= 32 kernels each) written to partial images and summed in part order.
-// Decided per forward state (all its views), so the device path and the
-// chunked host path compose every tile identically.
-static int composite_splits(Ctx* c, const sct_fwd* s) {
-  const long long total = (long long)s->det.tiles_x * s->det.tiles_y * s->n_views;
+// Part length of K3's work items, decided per forward state (so the device
+// and host-buffer paths cut, and therefore sum, every list identically):
+// 256 kernels, halved (down to 32) while the state has fewer items than twice
+// the GPU's warp slots (small workloads: the train step renders one view).
+// Measured at cfg3 (B200): K3 1.37 ms at 256 and 512, 1.40 at 128, 1.47 at
+// 64, 1.54 uncut; the longest item of the unit-ordered host path takes
+// 0.2 ms at 256 vs 0.4 at 512, which sets when the first D2H copy can start.
+static int composite_part_len(Ctx* c, const sct_fwd* s) {
+  if (const char* e = std::getenv("SCT_K3_PART")) return std::max(32, atoi(e));
+  const long long lists = (long long)s->det.tiles_x * s->det.tiles_y * s->n_views;
   const long long slots = (long long)c->sm_count * composite_per_sm() * kCompWarps;
-  const double avg_len = total > 0 ? (double)s->n_pairs / (double)total : 0.0;
-  int splits = 1;
-  while (splits < 16 && total * splits * 2 <= slots && avg_len / (2 * splits) >= 32.0) splits *= 2;
-  return splits;
+  int len = 256;
+  while (len > 32 && lists + s->n_pairs / len < 2 * slots) len /= 2;
+  return len;
 }
 
-void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0, int nv) {
-  if (nv <= 0) nv = s->n_views - v0;
-  if (nv <= 0) return;
-  const int T = s->det.tiles_x * s->det.tiles_y;
-  const int per_sm = composite_per_sm();
-  const long long total = (long long)T * nv;
-  const int splits = composite_splits(c, s);
-  const size_t px = (size_t)s->det.w * s->det.h;
+// K3 work items of a (view, tile) order: per list max(1, ceil(n / part_len))
+// items (scan of the counts), plus the partial tiles and the per-list
+// counters of the last-part reduction (slot 27: counts, firsts, items, the
+// item count, counters; slot 24: partial tiles).
+struct K3Work {
+  const int4* items = nullptr;
+  const int* n_items = nullptr;
+  int* tile_cnt = nullptr;
   float* partial = nullptr;
-  if (splits > 1 && stage_buf(c, 24, sizeof(float) * px * nv * splits, (void**)&partial) != SCT_OK) return;
-  const int blocks =
-      (int)std::min<long long>((long long)c->sm_count * per_sm, (total * splits + kCompWarps - 1) / kCompWarps);
-  const int* order = cached_tile_order(c, s, v0, nv);
-  int* work = nullptr;
-  if (!order || stage_buf(c, 20, sizeof(int) * 4, (void**)&work) != SCT_OK) return;
-  cudaMemsetAsync(work, 0, sizeof(int), c->stream);
-  {
-    KScope _ks(c, "K3_composite");
-    composite_kernel<<<blocks, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
-                                                                s->det.w, s->det.h, v0, (int)total, work, order,
-                                                                splits, partial, nv, images);
-  }
-  if (splits > 1) {
-    KScope _ks(c, "K3_reduce");
-    const long long n = (long long)px * nv;
-    composite_reduce_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(partial, splits, n,
-                                                                        images + (size_t)v0 * px);
-  }
-}
+  int part_len = 0;
+};
 
-// Host-buffer forward: the composite in `chunks` view chunks on alternating
-// streams (main / aux), so one chunk's tail overlaps the next chunk's start
-// and each chunk's D2H copy can begin as soon as the chunk is done
-// (done[k] is recorded after chunk k). One sort orders all chunks (chunk,
-// then longest lists first); each chunk has its own work counter.
-int launch_raster_composite_chunks(Ctx* c, const sct_fwd* s, float* images, int chunks, cudaEvent_t* done) {
-  const int V = s->n_views;
-  const int T = s->det.tiles_x * s->det.tiles_y;
-  const int n = T * V;
-  const int per_sm = composite_per_sm();
-  const int splits = composite_splits(c, s);
-  const size_t px = (size_t)s->det.w * s->det.h;
-  float* partial = nullptr;
-  if (splits > 1) SCT_TRY(stage_buf(c, 24, sizeof(float) * px * V * splits, (void**)&partial));
+static int k3_work(Ctx* c, const sct_fwd* s, const int* order, int n, K3Work& kw) {
+  kw.part_len = composite_part_len(c, s);
+  const long long max_items = (long long)n + s->n_pairs / kw.part_len + 1;
   char* buf = nullptr;
-  int* work = nullptr;
-  SCT_TRY(stage_buf(c, 22, (size_t)4 * n * sizeof(uint32_t), (void**)&buf));
-  SCT_TRY(stage_buf(c, 26, sizeof(int) * Ctx::kChunkEvents, (void**)&work));
-  c->order_id = 0;  // slot 22 now holds the chunked order
-  uint32_t* k0 = reinterpret_cast<uint32_t*>(buf);
-  uint32_t* k1 = k0 + n;
-  int32_t* i0 = reinterpret_cast<int32_t*>(k1 + n);
-  int32_t* i1 = i0 + n;
+  const size_t n4 = ((size_t)n + 3) & ~(size_t)3;  // int4 alignment of the item array
+  const size_t bytes = sizeof(int) * (2 * n4 + 4) + sizeof(int4) * max_items + sizeof(int) * max_items;
+  SCT_TRY(stage_buf(c, 27, bytes, (void**)&buf));
+  int* count = reinterpret_cast<int*>(buf);
+  int* first = count + n4;
+  int* n_items = first + n4;
+  int4* items = reinterpret_cast<int4*>(n_items + 4);
+  int* tile_cnt = reinterpret_cast<int*>(items + max_items);
+  SCT_TRY(stage_buf(c, 24, sizeof(float) * 256 * (size_t)max_items, (void**)&kw.partial));
   {
     KScope _ks(c, "K2_tile_order");
-    tile_order_chunk_keys_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(s->d_ranges, n, T, V, chunks, k0, i0);
+    k3_parts_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(s->d_ranges, order, n, kw.part_len, count);
+    size_t tmp = 0;
+    SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, first, n, c->stream));
+    SCT_TRY(ensure_cub_tmp(c, tmp));
+    tmp = c->cub_tmp_bytes;
+    SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, first, n, c->stream));
+    k3_items_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(order, count, first, n, items, n_items);
+    SCT_CUDA_TRY(cudaMemsetAsync(tile_cnt, 0, sizeof(int) * max_items, c->stream));
   }
-  cub::DoubleBuffer<uint32_t> keys(k0, k1);
-  cub::DoubleBuffer<int32_t> vals(i0, i1);
-  size_t tmp = 0;
-  int bits = 5;
-  while ((1 << (bits - 5)) < chunks) ++bits;
-  SCT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, n, 0, bits, c->stream));
-  SCT_TRY(ensure_cub_tmp(c, tmp));
-  tmp = c->cub_tmp_bytes;
-  SCT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, vals, n, 0, bits, c->stream));
-  const int* order = vals.Current();
-  SCT_CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(int) * chunks, c->stream));
-  SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->stream));
-  SCT_CUDA_TRY(cudaStreamWaitEvent(c->aux_stream, c->ev_join, 0));
-  for (int k = 0; k < chunks; ++k) {
-    const int v0 = (int)((int64_t)V * k / chunks), v1 = (int)((int64_t)V * (k + 1) / chunks);
-    const long long total = (long long)T * (v1 - v0);
-    cudaStream_t st = (k & 1) ? c->aux_stream : c->stream;
-    const int blocks = (int)std::min<long long>((long long)c->sm_count * per_sm,
-                                                (total * splits + kCompWarps - 1) / kCompWarps);
-    {
-      KScope _ks(c, "K3_composite", true, st);
-      // global (view, tile) indices: view0 = 0, this chunk's slice of the order
-      composite_kernel<<<blocks, 32 * kCompWarps, 0, st>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
-                                                           s->det.w, s->det.h, 0, (int)total, work + k,
-                                                           order + (size_t)T * v0, splits, partial, V, images);
-    }
-    if (splits > 1) {
-      KScope _ks(c, "K3_reduce", true, st);
-      const long long nn = (long long)px * (v1 - v0);
-      // partial[p][view] for this chunk's views, summed in part order
-      composite_reduce_chunk_kernel<<<grid_cap(c, nn, 256), 256, 0, st>>>(partial + (size_t)v0 * px, splits,
-                                                                          (long long)px * V, nn,
-                                                                          images + (size_t)v0 * px);
-    }
-    SCT_CUDA_TRY(cudaEventRecord(done[k], st));
+  kw.items = items;
+  kw.n_items = n_items;
+  kw.tile_cnt = tile_cnt;
+  return SCT_OK;
+}
+
+static int composite_launch(Ctx* c, const sct_fwd* s, const int* order, float* images, const UnitSync& us) {
+  const int T = s->det.tiles_x * s->det.tiles_y;
+  const int n = T * s->n_views;
+  if (!order) {
+    set_error("CUDA error: tile order");
+    return SCT_ERR_CUDA;
   }
+  K3Work kw;
+  SCT_TRY(k3_work(c, s, order, n, kw));
+  int* work = nullptr;
+  SCT_TRY(stage_buf(c, 20, sizeof(int) * 4, (void**)&work));
+  SCT_CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(int), c->stream));
+  const long long max_items = (long long)n + s->n_pairs / kw.part_len + 1;
+  const int blocks = (int)std::min<long long>((long long)c->sm_count * composite_per_sm(),
+                                              (max_items + kCompWarps - 1) / kCompWarps);
+  KScope _ks(c, "K3_composite");
+  composite_kernel<<<blocks, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
+                                                              s->det.w, s->det.h, kw.items, kw.n_items, kw.part_len,
+                                                              work, kw.tile_cnt, kw.partial, images, us);
   SCT_CUDA_TRY(cudaGetLastError());
   return SCT_OK;
 }
 
+// All views of the forward state, longest lists first.
+void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images) {
+  if (s->n_views <= 0) return;
+  composite_launch(c, s, cached_tile_order(c, s, 0, s->n_views), images, UnitSync{});
+}
+
+bool raster_units_supported(Ctx* c, const sct_fwd* s) { return !k4_simt(); }
+
+// Host-buffer forward: one composite over all views in unit order; the last
+// finished tile of unit u publishes unit_flags[u] (the copy stream waits on
+// it), so the D2H copies overlap the composite.
+int launch_raster_composite_units(Ctx* c, const sct_fwd* s, float* images, UnitSync us) {
+  us.per_view = s->det.tiles_x * s->det.tiles_y;
+  return composite_launch(c, s, unit_tile_order(c, s, us.units), images, us);
+}
+
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0, int nv,
-                                  float* item_stats) {
+                                  float* item_stats, const UnitSync* us) {
   if (s->n_pairs == 0) return;
   if (nv <= 0) nv = s->n_views - v0;
   if (nv <= 0) return;
   const int T = s->det.tiles_x * s->det.tiles_y;
   dim3 grid(T, nv);
-  // SCT_K4=simt selects the FP32 SIMT statistics kernel (the reference-order
-  // arithmetic without tensor cores); default: the tensor-core kernel above
-  static const bool simt = [] {
-    const char* e = std::getenv("SCT_K4");
-    return e && std::string(e) == "simt";
-  }();
+  const bool simt = k4_simt();
   KScope _ks(c, "K4_backward_stats");
   float* ps = reinterpret_cast<float*>(pair_stats);
   if (simt) {
@@ -927,7 +1011,11 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
                                                                v0, dL, ps, item_stats);
     return;
   }
-  const int* order = cached_tile_order(c, s, v0, nv);
+  if (us) {  // host path: all views in unit order, each unit waiting for its H2D copy
+    v0 = 0;
+    nv = s->n_views;
+  }
+  const int* order = us ? unit_tile_order(c, s, us->units) : cached_tile_order(c, s, v0, nv);
   if (!order) return;
   // small workloads: several CTAs per list (>= 64 kernels each) until the
   // grid fills the CTA slots (8 per SM)
@@ -935,9 +1023,11 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
   const double avg_len = total > 0 ? (double)s->n_pairs / (double)total : 0.0;
   int parts = 1;
   while (parts < 16 && total * parts * 2 <= (long long)c->sm_count * 8 && avg_len / (2 * parts) >= 64.0) parts *= 2;
+  UnitSync ks = us ? *us : UnitSync{};
+  ks.per_view = T * parts;
   backward_stats_mma_kernel<<<(unsigned)(total * parts), 32 * kMmaWarps, 0, c->stream>>>(
       s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
-      parts, dL, ps, item_stats);
+      parts, dL, ps, item_stats, ks);
 }
 
 }  // namespace sct

@@ -122,7 +122,76 @@ struct Ctx {
   // ncclComm_t, owned by the context when made by sct_ctx_comm_init
   void* comm = nullptr;
   bool comm_owned = false;
+  // view-unit signals of the host-buffer entry points (stream memory
+  // operations, see UnitSync): epoch-stamped flags in device memory, written
+  // by kernels or by the copy stream and waited on by streams or kernels.
+  // Flags are never reset: a wait compares against the call's epoch.
+  static constexpr int kMaxUnits = 64;
+  uint32_t* unit_flags = nullptr;  // [3][kMaxUnits] mapped host: composite done, dL landed, K4 done
+  int* unit_done = nullptr;        // [2][kMaxUnits] finished-list counters
+  int* unit_err = nullptr;         // a kernel-side wait timed out
+  uint32_t epoch = 0;
 };
+
+// Per-unit (contiguous view range) wait / signal of one kernel launch.
+// Unit u holds views [V u / units, V (u + 1) / units).
+struct UnitSync {
+  const uint32_t* ready = nullptr;  // wait until ready[u] >= epoch before reading unit u's input
+  uint32_t* done_flag = nullptr;    // done_flag[u] = epoch once all of unit u's lists are finished
+  int* done = nullptr;              // finished-list counters (zeroed before the launch)
+  int* err = nullptr;
+  uint32_t epoch = 0;
+  int units = 0, n_views = 0;
+  int per_view = 0;  // lists (x parts) per view
+  unsigned long long* stamp = nullptr;  // diagnostics (SCT_UNIT_DEBUG): [u] publish time, [kMaxUnits] first claim
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ int unit_of_view(int v, int n_views, int units) {
+  int k = 0;
+  while (k + 1 < units && (long long)n_views * (k + 1) / units <= v) ++k;
+  return k;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// one thread: spin until unit u's input has landed (bounded: after 2 s the
+// error word is set and the kernel proceeds, so a lost signal cannot hang)
+__device__ __forceinline__ void unit_wait(const UnitSync& us, int u) {
+  if (!us.ready) return;
+  const uint64_t t0 = global_ns();
+  while ((int)(ld_acquire_sys(us.ready + u) - us.epoch) < 0) {
+    __nanosleep(128);
+    if (global_ns() - t0 > 2000000000ull) {
+      atomicExch(us.err, 1);
+      break;
+    }
+  }
+}
+
+// one thread, after every writer of the finished list fenced and met it at a
+// barrier: count the list; the last list of the unit publishes the flag
+__device__ __forceinline__ void unit_signal(const UnitSync& us, int u) {
+  if (!us.done) return;
+  const int v0 = (int)((long long)us.n_views * u / us.units);
+  const int v1 = (int)((long long)us.n_views * (u + 1) / us.units);
+  if (atomicAdd(us.done + u, 1) == us.per_view * (v1 - v0) - 1) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(us.done_flag + u), "r"(us.epoch) : "memory");
+    if (us.stamp) us.stamp[u] = global_ns();
+  }
+}
+#endif
 void comm_release(Ctx* c);
 int stage_buf(Ctx* c, int slot, size_t bytes, void** p);
 
@@ -192,12 +261,15 @@ void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32
                         void* keys, bool keys16, int32_t* vals);
 void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,
                           int64_t tiles_per_view, int2* ranges);
-void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images, int v0 = 0, int nv = 0);
-int launch_raster_composite_chunks(Ctx* c, const sct_fwd* s, float* images, int chunks, cudaEvent_t* done);
+void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images);
+// unit-signalled host path (UnitSync): one composite / one K4 over all views
+bool raster_units_supported(Ctx* c, const sct_fwd* s);
+int launch_raster_composite_units(Ctx* c, const sct_fwd* s, float* images, UnitSync us);
 // item_stats != nullptr: parallel-atomic mode, 8 floats per item accumulated
-// with atomics instead of per-pair slots
+// with atomics instead of per-pair slots; us != nullptr: all views, waiting
+// for and publishing view units
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0 = 0,
-                                  int nv = 0, float* item_stats = nullptr);
+                                  int nv = 0, float* item_stats = nullptr, const UnitSync* us = nullptr);
 void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, const int32_t* offset,
                        int32_t bricks_x, int32_t bricks_y, void* keys, bool keys16, int32_t* vals);
 void launch_key_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, int2* ranges);

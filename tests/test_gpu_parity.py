@@ -440,3 +440,47 @@ def test_render_backward_atomic_mode():
         r = O.render(oc, O.test_scanner(129), th)
         O.render_backward(oc, O.test_scanner(129), th, r, up[v].astype(np.float64), og)
     check_grads(g, og, what="atomic")
+
+
+@pytest.mark.parametrize("unit_kb", [None, "96"])
+def test_host_entry_points_units(eng, monkeypatch, unit_kb):
+    """Many-view host-buffer calls (one composite / one K4 over all views, the
+    D2H / H2D copies of view units overlapped through device flags) == device path."""
+    import ctypes as C
+    import paper_2405_20693_b200 as P
+    from paper_2405_20693_b200 import _capi
+    if unit_kb:
+        monkeypatch.setenv("SCT_UNIT_KB", unit_kb)  # 64 KB views: ~1.5 views per unit
+    oc = O.random_cloud(O.Rng(9), 3000, 0.8, 0.02, 0.1)
+    ec, _ = to_engine(P, oc)
+    host = {k: np.ascontiguousarray(v, dtype=np.float32) for k, v in ec.host_arrays().items()}
+    cl = _capi.sct_cloud()
+    cl.m = ec.size()
+    cl.s_min_mm = ec.s_min
+    for k in ("rho_raw", "pos", "scale_raw", "rot"):
+        setattr(cl, k, host[k].ctypes.data)
+    V, R = 37, 128
+    thetas = [2 * np.pi * i / V for i in range(V)]
+    sc = escan(P, R)._c()
+    op = P.RasterOptions()._c()
+    th = (C.c_double * V)(*thetas)
+    imgs = np.zeros((V, R, R), dtype=np.float32)
+    st = C.c_void_p()
+    L = _capi.load()
+    for rep in range(2):  # second call: next epoch on the same flags
+        assert L.sct_render_fwd_host(eng._h, C.byref(cl), C.byref(sc), th, V, C.byref(op), imgs.ctypes.data,
+                                     C.byref(st)) == 0, L.sct_last_error()
+        dev = eng.render(ec, escan(P, R), thetas)
+        np.testing.assert_array_equal(imgs, dev.images.cpu().numpy())
+        up = (np.random.default_rng(rep).uniform(-1, 1, (V, R, R))).astype(np.float32)
+        gh = {k: np.zeros_like(host[k]) for k in host}
+        g = _capi.sct_grads()
+        for k in gh:
+            setattr(g, k, gh[k].ctypes.data)
+        assert L.sct_render_bwd_host(eng._h, st, C.byref(cl), up.ctypes.data, C.byref(g), None) == 0, \
+            L.sct_last_error()
+        L.sct_fwd_free(st)
+        gd = P.CloudGrads(ec.size())
+        eng.render_backward(ec, dev, torch.from_numpy(up).cuda(), gd)
+        for k, t in zip(("rho_raw", "pos", "scale_raw", "rot"), gd.tensors()):
+            np.testing.assert_array_equal(gh[k], t.cpu().numpy())

@@ -14,6 +14,8 @@ from paper_2405_20693_b200 import _capi, scenes  # noqa: E402
 ca = scenes.make_cloud(3)
 eng = P.Engine(0)
 L = _capi.load()
+if os.environ.get("ATOMIC"):
+    L.sct_ctx_set_deterministic(eng._h, 0)
 thetas = [2 * np.pi * i / 75 for i in range(75)]
 pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
 host = {k: pin(getattr(ca, k)) for k in ("rho_raw", "pos", "scale_raw", "rot")}
@@ -42,4 +44,4 @@ for it in range(15):
     t2 = time.perf_counter()
     L.sct_fwd_free(st)
     res.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2)))
-print(os.environ.get("SCT_HOST_CHUNKS", "auto"), res[3:])
+print(os.environ.get("SCT_HOST_UNITS", "1"), os.environ.get("SCT_HOST_CHUNKS", "auto"), res[3:])
