@@ -667,6 +667,34 @@ static int host_units(int n_views, size_t bytes) {
                                                      (size_t)Ctx::kMaxUnits}));
 }
 
+// SCT_UNIT_DEBUG: timing events at named points of the host-buffer paths,
+// printed (ms after the first mark) at the end of the call
+struct DbgMarks {
+  bool on = std::getenv("SCT_UNIT_DEBUG") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  void mark(cudaStream_t st, const std::string& name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.emplace_back(name, e);
+  }
+  void report(const char* what) {
+    if (!on || ev.empty()) return;
+    cudaDeviceSynchronize();
+    std::fprintf(stderr, "[%s]", what);
+    for (auto& p : ev) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev[0].second, p.second);
+      std::fprintf(stderr, " %s=%.3f", p.first.c_str(), t);
+    }
+    std::fprintf(stderr, "\n");
+    for (auto& p : ev) cudaEventDestroy(p.second);
+    ev.clear();
+  }
+};
+static DbgMarks g_dbg;
+
 // the error word of a kernel-side unit wait (read after the call's stream sync)
 static int check_unit_err(Ctx* c) {
   int32_t* h = reinterpret_cast<int32_t*>(c->pinned_count) + 8;
@@ -680,12 +708,21 @@ static int check_unit_err(Ctx* c) {
   return SCT_OK;
 }
 
+// chain groups of the units backward (measured at cfg3: 4 groups 3.13 ms,
+// 8 groups 3.19 ms, 2 groups 3.18 ms; a high-priority chain stream starts the
+// groups earlier but slows K4 by as much)
+static const int kChainGroups = [] {
+  const char* e = std::getenv("SCT_CHAIN_GROUPS");
+  return e ? std::max(1, atoi(e)) : 4;
+}();
+
 // Backward with the upstream gradient landing in view units (unit_flags[1][u]
 // written by the copy stream): one K4 over all views waits per unit and
 // publishes unit_flags[2][u]; the FP64 chain runs on the aux stream in groups
 // of units, each group starting when its units' statistics are published.
 static int render_bwd_units(Ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
-                            sct_stats* stats, int units, uint32_t epoch) {
+                            sct_stats* stats, int units, uint32_t epoch, cudaEvent_t cloud_ready,
+                            cudaEvent_t grads_ready) {
   SCT_TRY(check_cloud(cloud));
   if (cloud->m != s->m) {
     set_error("DimMismatch: render_backward: cloud size differs from the forward state");
@@ -707,8 +744,9 @@ static int render_bwd_units(Ctx* c, sct_fwd* s, const sct_cloud* cloud, const fl
   uint32_t* k4_done = c->unit_flags + 2 * Ctx::kMaxUnits;
   int* counters = c->unit_done + Ctx::kMaxUnits;
   SCT_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(int) * units, c->stream));
-  SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->stream));  // the chain stream sees the uploads and zeroing
+  SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->stream));  // the chain stream sees the zeroing
   SCT_CUDA_TRY(cudaStreamWaitEvent(c->aux_stream, c->ev_join, 0));
+  SCT_CUDA_TRY(cudaStreamWaitEvent(c->aux_stream, cloud_ready, 0));
   UnitSync us;
   us.ready = ready;
   us.done_flag = k4_done;
@@ -717,21 +755,27 @@ static int render_bwd_units(Ctx* c, sct_fwd* s, const sct_cloud* cloud, const fl
   us.epoch = epoch;
   us.units = units;
   us.n_views = s->n_views;
+  g_dbg.mark(c->stream, "k4_start");
   launch_raster_backward_stats(c, s, dL, pair_stats, 0, 0, item_stats, &us);
+  g_dbg.mark(c->stream, "k4_end");
   SCT_CUDA_TRY(cudaGetLastError());
   // a lost kernel-side signal only delays the chain to the end of K4
   for (int u = 0; u < units; ++u) SCT_TRY(stream_write_flag(c->stream, k4_done + u, epoch));
   const float4* chain_src = atomic ? reinterpret_cast<const float4*>(item_stats) : pair_stats;
-  const int groups = std::min(units, 4);
+  const int groups = std::min(units, kChainGroups);
   for (int g = 0; g < groups; ++g) {
     const int u0 = units * g / groups, u1 = units * (g + 1) / groups;
     for (int u = u0; u < u1; ++u) SCT_TRY(stream_wait_flag(c->aux_stream, k4_done + u, epoch));
     const int64_t v0 = (int64_t)s->n_views * u0 / units, v1 = (int64_t)s->n_views * u1 / units;
+    g_dbg.mark(c->aux_stream, "chain" + std::to_string(g) + "_start");
     launch_raster_chain(c, s, *cloud, chain_src, item_grads, atomic, v0 * s->m, v1 * s->m, c->aux_stream);
   }
   SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->aux_stream));
   SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  g_dbg.mark(c->stream, "chain_end");
+  SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, grads_ready, 0));
   launch_raster_finalize(c, s, *cloud, item_grads, grads, stats);
+  g_dbg.mark(c->stream, "finalize_end");
   SCT_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int32_t*>(c->pinned_count) + 8, c->unit_err, sizeof(int32_t),
                                cudaMemcpyDeviceToHost, c->stream));
   SCT_CUDA_TRY(cudaGetLastError());
@@ -857,7 +901,8 @@ static int host_chunks(size_t bytes, bool /*forward*/) {
 
 // Staging slots: 0-3 cloud arrays, 4 images, 5 upstream gradient, 6-9 grads,
 // 10-12 stats, 13 volume.
-static int upload_cloud(Ctx* c, const sct_cloud* h, sct_cloud* d) {
+static int upload_cloud(Ctx* c, const sct_cloud* h, sct_cloud* d, cudaStream_t st = nullptr) {
+  if (!st) st = c->stream;
   *d = *h;
   const int64_t m = h->m;
   float** dst[4] = {&d->rho_raw, &d->pos, &d->scale_raw, &d->rot};
@@ -865,7 +910,7 @@ static int upload_cloud(Ctx* c, const sct_cloud* h, sct_cloud* d) {
   const int64_t n[4] = {m, 3 * m, 3 * m, 4 * m};
   for (int a = 0; a < 4; ++a) {
     SCT_TRY(stage_buf(c, a, n[a] * sizeof(float), (void**)dst[a]));
-    SCT_CUDA_TRY(cudaMemcpyAsync(*dst[a], src[a], n[a] * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    SCT_CUDA_TRY(cudaMemcpyAsync(*dst[a], src[a], n[a] * sizeof(float), cudaMemcpyHostToDevice, st));
   }
   return SCT_OK;
 }
@@ -976,21 +1021,31 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
   }
   SCT_TRY(check_cloud(cloud_host));
   sct_cloud d;
-  SCT_TRY(upload_cloud(c, cloud_host, &d));
+  g_dbg.mark(c->stream, "start");
   const int64_t m = cloud_host->m;
   const size_t px = (size_t)s->det.w * s->det.h;
   float* ddl = nullptr;
   SCT_TRY(stage_buf(c, 5, s->n_views * px * sizeof(float), (void**)&ddl));
-  // upstream gradient in view units (one K4 waits per unit, unit_flags[1])
-  // or in view chunks (K4 for chunk k starts once chunk k has landed)
+  // units path: every H2D copy on the copy stream, in the order the GPU
+  // needs the data — upstream-gradient unit 0 (K4 starts on it), the cloud
+  // (the FP64 chain), the other units (K4 waits per unit, unit_flags[1]), the
+  // caller's running sums (finalize). Chunked path: the cloud and the sums on
+  // the main stream, K4 for chunk k once chunk k has landed.
   const bool units_path = memops().wait && s->n_items > 0 && raster_units_supported(c, s);
   const int units = units_path ? host_units(s->n_views, s->n_views * px * sizeof(float)) : 0;
   const uint32_t epoch = units_path ? ++c->epoch : 0;
+  cudaStream_t up_stream = units_path ? c->copy_stream : c->stream;
+  if (!units_path) SCT_TRY(upload_cloud(c, cloud_host, &d));
   for (int u = 0; u < units; ++u) {
     const int v0 = (int)((int64_t)s->n_views * u / units), v1 = (int)((int64_t)s->n_views * (u + 1) / units);
     SCT_CUDA_TRY(cudaMemcpyAsync(ddl + v0 * px, dL_host + v0 * px, (v1 - v0) * px * sizeof(float),
                                  cudaMemcpyHostToDevice, c->copy_stream));
     SCT_TRY(stream_write_flag(c->copy_stream, c->unit_flags + Ctx::kMaxUnits + u, epoch));
+    if (u == 0 || u == units - 1) g_dbg.mark(c->copy_stream, "dl" + std::to_string(u));
+    if (u == 0) {
+      SCT_TRY(upload_cloud(c, cloud_host, &d, c->copy_stream));
+      SCT_CUDA_TRY(cudaEventRecord(c->ev_copy[0], c->copy_stream));
+    }
   }
   const int chunks =
       units_path ? 0 : std::min<int>(s->n_views, host_chunks(s->n_views * px * sizeof(float), false));
@@ -1007,7 +1062,7 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
   const int64_t n[4] = {m, 3 * m, 3 * m, 4 * m};
   for (int a = 0; a < 4; ++a) {
     SCT_TRY(stage_buf(c, 6 + a, n[a] * sizeof(float), (void**)gd[a]));
-    SCT_CUDA_TRY(cudaMemcpyAsync(*gd[a], gh[a], n[a] * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    SCT_CUDA_TRY(cudaMemcpyAsync(*gd[a], gh[a], n[a] * sizeof(float), cudaMemcpyHostToDevice, up_stream));
   }
   sct_stats dst{};
   void* sh[3] = {};
@@ -1019,10 +1074,13 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
     sh[2] = stats_host->grad3d_accum;
     for (int a = 0; a < 3; ++a) {
       SCT_TRY(stage_buf(c, 10 + a, sb[a], sd[a]));
-      SCT_CUDA_TRY(cudaMemcpyAsync(*sd[a], sh[a], sb[a], cudaMemcpyHostToDevice, c->stream));
+      SCT_CUDA_TRY(cudaMemcpyAsync(*sd[a], sh[a], sb[a], cudaMemcpyHostToDevice, up_stream));
     }
   }
-  int rc = units_path ? render_bwd_units(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, units, epoch)
+  if (units_path) SCT_CUDA_TRY(cudaEventRecord(c->ev_copy[1], c->copy_stream));
+  g_dbg.mark(up_stream, "grads_up");
+  int rc = units_path ? render_bwd_units(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, units, epoch,
+                                         c->ev_copy[0], c->ev_copy[1])
                       : sct_render_bwd_chunked(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, chunks);
   if (rc == SCT_OK) {
     for (int a = 0; a < 4; ++a)
@@ -1031,8 +1089,10 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
       for (int a = 0; a < 3; ++a)
         SCT_CUDA_TRY(cudaMemcpyAsync(sh[a], *sd[a], sb[a], cudaMemcpyDeviceToHost, c->stream));
   }
+  g_dbg.mark(c->stream, "grads_down");
   SCT_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  g_dbg.report("bwd_host");
   if (rc == SCT_OK && units_path) rc = check_unit_err(c);
   return rc;
 }

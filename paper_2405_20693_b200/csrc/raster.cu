@@ -828,6 +828,7 @@ static const int* tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
   if (ensure_cub_tmp(c, tmp) != SCT_OK) return nullptr;
   tmp = c->cub_tmp_bytes;
   cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, vals, n, 0, 5, c->stream);
+  ++c->order_gen;
   return vals.Current();
 }
 
@@ -873,6 +874,7 @@ static const int* unit_tile_order(Ctx* c, const sct_fwd* s, int units) {
   if (cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, vals, n, 0, bits, c->stream) != cudaSuccess)
     return nullptr;
   c->order_ptr = vals.Current();
+  ++c->order_gen;
   c->order_id = s->id;
   c->order_v0 = -1;
   c->order_nv = units;
@@ -920,28 +922,44 @@ static int composite_part_len(Ctx* c, const sct_fwd* s) {
 // item count, counters; slot 24: partial tiles).
 struct K3Work {
   const int4* items = nullptr;
+  const int* first = nullptr;  // first item of each list (order position)
   const int* n_items = nullptr;
   int* tile_cnt = nullptr;
   float* partial = nullptr;
   int part_len = 0;
+  long long max_items = 0;  // host-side bound of *n_items
 };
 
-static int k3_work(Ctx* c, const sct_fwd* s, const int* order, int n, K3Work& kw) {
-  kw.part_len = composite_part_len(c, s);
+// ranges: the lists the order's indices refer to (s->d_ranges + T v0 for a
+// view-range order). Cached: rebuilt only when the order (generation), the
+// part length or the list count changed.
+static int list_work(Ctx* c, const sct_fwd* s, const int* order, const int2* ranges, int n, int part_len,
+                     K3Work& kw) {
+  kw.part_len = part_len;
+  Ctx::ItemsKey& key = c->items_key;
+  const int slot = 27;
   const long long max_items = (long long)n + s->n_pairs / kw.part_len + 1;
   char* buf = nullptr;
   const size_t n4 = ((size_t)n + 3) & ~(size_t)3;  // int4 alignment of the item array
   const size_t bytes = sizeof(int) * (2 * n4 + 4) + sizeof(int4) * max_items + sizeof(int) * max_items;
-  SCT_TRY(stage_buf(c, 27, bytes, (void**)&buf));
+  const bool hit = key.gen == c->order_gen && key.part == kw.part_len && key.n == n;
+  SCT_TRY(stage_buf(c, slot, bytes, (void**)&buf));
   int* count = reinterpret_cast<int*>(buf);
   int* first = count + n4;
   int* n_items = first + n4;
   int4* items = reinterpret_cast<int4*>(n_items + 4);
   int* tile_cnt = reinterpret_cast<int*>(items + max_items);
   SCT_TRY(stage_buf(c, 24, sizeof(float) * 256 * (size_t)max_items, (void**)&kw.partial));
+  kw.items = items;
+  kw.first = first;
+  kw.n_items = n_items;
+  kw.tile_cnt = tile_cnt;
+  kw.max_items = max_items;
+  if (hit) return SCT_OK;  // (K3's last parts leave the counters zeroed)
+  key.gen = 0;
   {
     KScope _ks(c, "K2_tile_order");
-    k3_parts_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(s->d_ranges, order, n, kw.part_len, count);
+    k3_parts_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(ranges, order, n, kw.part_len, count);
     size_t tmp = 0;
     SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, first, n, c->stream));
     SCT_TRY(ensure_cub_tmp(c, tmp));
@@ -950,9 +968,9 @@ static int k3_work(Ctx* c, const sct_fwd* s, const int* order, int n, K3Work& kw
     k3_items_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(order, count, first, n, items, n_items);
     SCT_CUDA_TRY(cudaMemsetAsync(tile_cnt, 0, sizeof(int) * max_items, c->stream));
   }
-  kw.items = items;
-  kw.n_items = n_items;
-  kw.tile_cnt = tile_cnt;
+  key.gen = c->order_gen;
+  key.part = kw.part_len;
+  key.n = n;
   return SCT_OK;
 }
 
@@ -964,13 +982,12 @@ static int composite_launch(Ctx* c, const sct_fwd* s, const int* order, float* i
     return SCT_ERR_CUDA;
   }
   K3Work kw;
-  SCT_TRY(k3_work(c, s, order, n, kw));
+  SCT_TRY(list_work(c, s, order, s->d_ranges, n, composite_part_len(c, s), kw));
   int* work = nullptr;
   SCT_TRY(stage_buf(c, 20, sizeof(int) * 4, (void**)&work));
   SCT_CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(int), c->stream));
-  const long long max_items = (long long)n + s->n_pairs / kw.part_len + 1;
   const int blocks = (int)std::min<long long>((long long)c->sm_count * composite_per_sm(),
-                                              (max_items + kCompWarps - 1) / kCompWarps);
+                                              (kw.max_items + kCompWarps - 1) / kCompWarps);
   KScope _ks(c, "K3_composite");
   composite_kernel<<<blocks, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
                                                               s->det.w, s->det.h, kw.items, kw.n_items, kw.part_len,

@@ -118,6 +118,13 @@ struct Ctx {
   uint64_t order_id = 0;
   int order_v0 = -1, order_nv = -1;
   const int* order_ptr = nullptr;
+  uint64_t order_gen = 0;  // bumped whenever slot 22 receives a new order
+  // K3's work items (raster.cu list_work, slot 27) were built from this order
+  // generation with this part length and list count
+  struct ItemsKey {
+    uint64_t gen = 0;
+    int part = 0, n = 0;
+  } items_key;
   // NCCL communicator of the *_allreduce entry points (comm.cu): an
   // ncclComm_t, owned by the context when made by sct_ctx_comm_init
   void* comm = nullptr;
