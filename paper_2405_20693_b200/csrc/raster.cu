@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, con
     if (it < n_items) r = rect[it];
     const int rxy = ((int)(unsigned short)r.x) | ((int)r.y << 16);
     const int rzw = ((int)(unsigned short)r.z) | ((int)r.w << 16);
+    const float inv_nx_l = 1.f / (float)max(r.y - r.x + 1, 1);  // rank -> (row, col) by reciprocal
     const int32_t o_0 = __shfl_sync(0xffffffffu, o_l, 0);
     for (int32_t p0 = o_0; p0 < o_end; p0 += 32) {
       const int32_t p = p0 + lane;
@@ -87,11 +88,15 @@ __global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, con
       const int32_t oj = __shfl_sync(0xffffffffu, o_l, j);
       const int jxy = __shfl_sync(0xffffffffu, rxy, j);
       const int jzw = __shfl_sync(0xffffffffu, rzw, j);
+      const float inv_nx = __shfl_sync(0xffffffffu, inv_nx_l, j);
       if (p < o_end) {
         const int x0 = (short)(jxy & 0xffff), x1 = (short)(jxy >> 16), y0 = (short)(jzw & 0xffff);
         const int nx = x1 - x0 + 1;
         const int rank = p - oj;
-        const int ty = y0 + rank / nx, tx = x0 + rank % nx;
+        int q = (int)((float)rank * inv_nx);  // rank < 2^24: off by at most one, corrected exactly
+        if (q * nx > rank) --q;
+        if ((q + 1) * nx <= rank) ++q;
+        const int ty = y0 + q, tx = x0 + (rank - q * nx);
         const long long item = w0 + j;
         keys[p] = (KeyT)(ty * tiles_x + tx);
         vals[p] = (int32_t)item;
@@ -103,7 +108,7 @@ __global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, con
 
 // (view, tile) ranges of the sorted raster pairs: tile from the key, view
 // from the item (item = view * m + kernel; quotient by a float reciprocal
-// with an exact integer correction). Thread p closes the range at p and opens
+// with an exact integer correction). Pair p closes the range at p and opens
 // the one at p + 1 when the slot changes.
 __device__ __forceinline__ int div_m(int x, int m, float inv_m) {
   int q = (int)((float)x * inv_m);
@@ -111,21 +116,62 @@ __device__ __forceinline__ int div_m(int x, int m, float inv_m) {
   if ((long long)(q + 1) * m <= x) ++q;
   return q;
 }
+// Eight consecutive pairs per thread (16/32-byte vector loads of the keys
+// and items, the next group's first pair for the closing test), so each
+// thread has several loads in flight: the scalar form was latency-bound at a
+// quarter of the HBM rate.
 template <typename KeyT>
 __global__ void __launch_bounds__(256) raster_ranges_kernel(long long n_pairs, const KeyT* __restrict__ keys,
                                                             const int32_t* __restrict__ vals, int m, float inv_m,
                                                             long long tiles_per_view, int2* __restrict__ ranges) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_pairs;
-       p += (long long)gridDim.x * blockDim.x) {
-    const long long slot = (long long)div_m(vals[p], m, inv_m) * tiles_per_view + keys[p];
-    if (p == 0) ranges[slot].x = 0;
-    if (p == n_pairs - 1) {
-      ranges[slot].y = (int)n_pairs;
+  const long long groups = (n_pairs + 7) / 8;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < groups;
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long p0 = 8 * g;
+    KeyT k[9];
+    int32_t v[9];
+    if (p0 + 8 <= n_pairs) {
+      if (sizeof(KeyT) == 2) {
+        const uint4 kv = *reinterpret_cast<const uint4*>(keys + p0);
+        const uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          k[2 * i] = (KeyT)(w[i] & 0xffffu);
+          k[2 * i + 1] = (KeyT)(w[i] >> 16);
+        }
+      } else {
+        const uint4 k0 = *reinterpret_cast<const uint4*>(keys + p0);
+        const uint4 k1 = *reinterpret_cast<const uint4*>(keys + p0 + 4);
+        k[0] = (KeyT)k0.x, k[1] = (KeyT)k0.y, k[2] = (KeyT)k0.z, k[3] = (KeyT)k0.w;
+        k[4] = (KeyT)k1.x, k[5] = (KeyT)k1.y, k[6] = (KeyT)k1.z, k[7] = (KeyT)k1.w;
+      }
+      const int4 v0 = *reinterpret_cast<const int4*>(vals + p0);
+      const int4 v1 = *reinterpret_cast<const int4*>(vals + p0 + 4);
+      v[0] = v0.x, v[1] = v0.y, v[2] = v0.z, v[3] = v0.w;
+      v[4] = v1.x, v[5] = v1.y, v[6] = v1.z, v[7] = v1.w;
     } else {
-      const long long next = (long long)div_m(vals[p + 1], m, inv_m) * tiles_per_view + keys[p + 1];
-      if (next != slot) {
-        ranges[slot].y = (int)(p + 1);
-        ranges[next].x = (int)(p + 1);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        k[i] = p0 + i < n_pairs ? keys[p0 + i] : (KeyT)0;
+        v[i] = p0 + i < n_pairs ? vals[p0 + i] : 0;
+      }
+    }
+    const bool has_next = p0 + 8 < n_pairs;
+    k[8] = has_next ? keys[p0 + 8] : (KeyT)0;
+    v[8] = has_next ? vals[p0 + 8] : 0;
+    long long slot[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) slot[i] = (long long)div_m(v[i], m, inv_m) * tiles_per_view + k[i];
+    if (p0 == 0) ranges[slot[0]].x = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const long long p = p0 + i;
+      if (p >= n_pairs) break;
+      if (p == n_pairs - 1) {
+        ranges[slot[i]].y = (int)n_pairs;
+      } else if (slot[i + 1] != slot[i]) {
+        ranges[slot[i]].y = (int)(p + 1);
+        ranges[slot[i + 1]].x = (int)(p + 1);
       }
     }
   }
@@ -772,10 +818,10 @@ void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16
   if (n_pairs == 0) return;
   KScope _ks(c, "K2_ranges");
   if (keys16)
-    raster_ranges_kernel<uint16_t><<<grid_cap(c, n_pairs, 256), 256, 0, c->stream>>>(
+    raster_ranges_kernel<uint16_t><<<grid_cap(c, (n_pairs + 7) / 8, 256), 256, 0, c->stream>>>(
         n_pairs, static_cast<const uint16_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
   else
-    raster_ranges_kernel<uint32_t><<<grid_cap(c, n_pairs, 256), 256, 0, c->stream>>>(
+    raster_ranges_kernel<uint32_t><<<grid_cap(c, (n_pairs + 7) / 8, 256), 256, 0, c->stream>>>(
         n_pairs, static_cast<const uint32_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
 }
 
