@@ -286,7 +286,7 @@ void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int3
 void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
                                  int32_t bricks_y, const int2* ranges, const int32_t* vals,
                                  const float4* rec, const short4* lo, const short4* hi,
-                                 const int32_t* offset, const sct_cloud& cl, const float* dL,
+                                 const int32_t* offset, const sct_cloud& cl, int64_t n_pairs, const float* dL,
                                  float4* pair_stats);
 // FP64 chain rules
 // per_item: pair_stats holds one pre-summed 8-float record per item (atomic mode)

@@ -404,16 +404,21 @@ __device__ __forceinline__ uint32_t pack_h2(float lo_k, float hi_k) {
 __global__ void __launch_bounds__(32 * kVMmaWarps, 7) voxel_backward_mma_kernel(
     BrickGeo G, const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ lo, const short4* __restrict__ hi, const int32_t* __restrict__ offset,
-    const float* __restrict__ dL, float* __restrict__ pair_stats) {
+    const float* __restrict__ dL, float* __restrict__ pair_stats, int parts) {
   // B fragments [slice][lane] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}: n tile 0
   // (moments 0-7) for all lanes; n tile 1 holds moments 8, 9 only (lanes 0-7)
   __shared__ uint4 s_g[32][32];
   __shared__ uint4 s_g1[32][8];
   __shared__ float s_gmax[kVMmaWarps];
   int tx, ty, tz;
-  brick_of(G, blockIdx.x, tx, ty, tz);
+  brick_of(G, blockIdx.x / parts, tx, ty, tz);
   const int brick = (tz * G.by + ty) * G.bx + tx;
-  const int2 rg = ranges[brick];
+  int2 rg = ranges[brick];
+  if (parts > 1) {  // part of the list (small grids)
+    const int len = rg.y - rg.x, s0 = rg.x, part = blockIdx.x % parts;
+    rg.x = s0 + (int)((long long)len * part / parts);
+    rg.y = s0 + (int)((long long)len * (part + 1) / parts);
+  }
   if (rg.y <= rg.x) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = lane & 3, gq = lane >> 2;
@@ -662,9 +667,15 @@ void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int3
 void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
                                  int32_t bricks_y, const int2* ranges, const int32_t* vals, const float4* rec,
                                  const short4* lo, const short4* hi, const int32_t* offset, const sct_cloud&,
-                                 const float* dL, float4* pair_stats) {
+                                 int64_t n_pairs, const float* dL, float4* pair_stats) {
   const long long nb = (long long)bricks_x * bricks_y * (zb1 - zb0);
   if (nb <= 0) return;
+  // small grids (the train step's TV sub-volume: 64 bricks): several CTAs per
+  // list (>= 64 kernels each; pair statistics are independent) until the grid
+  // fills the CTA slots (7 per SM)
+  const double avg_len = (double)n_pairs / (double)nb;
+  int parts = 1;
+  while (parts < 32 && nb * parts * 2 <= (long long)c->sm_count * 7 && avg_len / (2 * parts) >= 64.0) parts *= 2;
   // SCT_K8=simt selects the FP32 SIMT statistics kernel; default: tensor-core moments
   static const bool simt = [] {
     const char* e = std::getenv("SCT_K8");
@@ -676,9 +687,9 @@ void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t
         make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL,
         reinterpret_cast<float*>(pair_stats));
   else
-    voxel_backward_mma_kernel<<<(unsigned)nb, 32 * kVMmaWarps, 0, c->stream>>>(
+    voxel_backward_mma_kernel<<<(unsigned)(nb * parts), 32 * kVMmaWarps, 0, c->stream>>>(
         make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL,
-        reinterpret_cast<float*>(pair_stats));
+        reinterpret_cast<float*>(pair_stats), parts);
 }
 
 }  // namespace sct
