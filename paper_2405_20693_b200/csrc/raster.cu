@@ -13,6 +13,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -841,6 +842,36 @@ __global__ void __launch_bounds__(256) tile_order_keys_kernel(const int2* __rest
   }
 }
 
+// tile_order_keys_kernel + the stable 5-bit sort in one CTA, for small
+// workloads (n <= kSmallOrder)
+constexpr int kSmallOrderThreads = 256, kSmallOrderItems = 16;
+constexpr int kSmallOrder = kSmallOrderThreads * kSmallOrderItems;
+__global__ void __launch_bounds__(kSmallOrderThreads) tile_order_small_kernel(const int2* __restrict__ ranges,
+                                                                              long long base, int n,
+                                                                              int32_t* __restrict__ order) {
+  using Sort = cub::BlockRadixSort<uint32_t, kSmallOrderThreads, kSmallOrderItems, int32_t>;
+  __shared__ typename Sort::TempStorage tmp;
+  uint32_t key[kSmallOrderItems];
+  int32_t idx[kSmallOrderItems];
+#pragma unroll
+  for (int i = 0; i < kSmallOrderItems; ++i) {
+    const int w = threadIdx.x * kSmallOrderItems + i;  // blocked arrangement: input order = w
+    if (w < n) {
+      const int2 r = ranges[base + w];
+      key[i] = 31u - (uint32_t)(32 - __clz(max(r.y - r.x, 0)));
+    } else {
+      key[i] = 31u;  // padding sorts after every real list (stable, larger index)
+    }
+    idx[i] = w;
+  }
+  Sort(tmp).Sort(key, idx, 0, 5);
+#pragma unroll
+  for (int i = 0; i < kSmallOrderItems; ++i) {
+    const int w = threadIdx.x * kSmallOrderItems + i;
+    if (w < n) order[w] = idx[i];
+  }
+}
+
 // keys for the chunked order: (chunk of the view, descending length octave)
 __global__ void __launch_bounds__(256) tile_order_chunk_keys_kernel(const int2* __restrict__ ranges, int n,
                                                                     int tiles_per_view, int n_views, int chunks,
@@ -866,6 +897,11 @@ static const int* tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
   int32_t* i0 = reinterpret_cast<int32_t*>(k1 + n);
   int32_t* i1 = i0 + n;
   KScope _ks(c, "K2_tile_order");
+  if (n <= kSmallOrder) {  // one CTA instead of the device-wide sort's launches (train step: 256 lists)
+    tile_order_small_kernel<<<1, kSmallOrderThreads, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
+    ++c->order_gen;
+    return i0;
+  }
   tile_order_keys_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, k0, i0);
   cub::DoubleBuffer<uint32_t> keys(k0, k1);
   cub::DoubleBuffer<int32_t> vals(i0, i1);
@@ -1004,7 +1040,7 @@ static int list_work(Ctx* c, const sct_fwd* s, const int* order, const int2* ran
   if (hit) return SCT_OK;  // (K3's last parts leave the counters zeroed)
   key.gen = 0;
   {
-    KScope _ks(c, "K2_tile_order");
+    KScope _ks(c, "K2_k3_items");
     k3_parts_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(ranges, order, n, kw.part_len, count);
     size_t tmp = 0;
     SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, first, n, c->stream));
