@@ -771,10 +771,10 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
         st[4] = fmaf(oy, fmaf(oy, m[0], 2.f * m[2]), m[4]);
         st[5] = fmaf(ox, fmaf(oy, m[0], m[2]), fmaf(oy, m[1], m[5]));
         const long long it = vals[rg.x + e];
-        if (item_stats) {
-          float* dst = item_stats + 8 * it;
-#pragma unroll
-          for (int k = 0; k < 6; ++k) atomicAdd(dst + k, st[k]);
+        if (item_stats) {  // vector reductions (sm_90+): 2 instead of 6 L1 wavefronts per pair
+          float4* dst = reinterpret_cast<float4*>(item_stats + 8 * it);
+          atomicAdd(dst, make_float4(st[0], st[1], st[2], st[3]));
+          atomicAdd(reinterpret_cast<float2*>(dst + 1), make_float2(st[4], st[5]));
         } else {
           const short4 r = rect[it];
           const long long slot = offset[it] + (ty - r.z) * (r.y - r.x + 1) + (tx - r.x);
