@@ -112,7 +112,7 @@ class ClockSampler:
     measured to stall this process's driver calls (host syncs) for tens of ms,
     so it is not used."""
 
-    def __init__(self, index, period_s=0.05):
+    def __init__(self, index, period_s=0.01):
         self.index = index
         self.period = period_s
         self.samples = []
@@ -162,7 +162,8 @@ class ClockSampler:
         reasons = sorted({n for _, r in self.samples for n, b in bits.items() if r & b})
         sm = [s for s, _ in self.samples]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz, "samples": len(sm),
-                "min_mhz": min(sm) if sm else None, "reasons": reasons, "source": "NVML, 50 ms period"}
+                "min_mhz": min(sm) if sm else None, "reasons": reasons,
+                "source": f"NVML, {self.period * 1e3:.0f} ms period"}
 
 
 # ------------------------------------------------------------------ CPU oracle leg
