@@ -844,7 +844,7 @@ __global__ void __launch_bounds__(256) tile_order_keys_kernel(const int2* __rest
 
 // tile_order_keys_kernel + the stable 5-bit sort in one CTA, for small
 // workloads (n <= kSmallOrder)
-constexpr int kSmallOrderThreads = 256, kSmallOrderItems = 16;
+constexpr int kSmallOrderThreads = 512, kSmallOrderItems = 24;
 constexpr int kSmallOrder = kSmallOrderThreads * kSmallOrderItems;
 __global__ void __launch_bounds__(kSmallOrderThreads) tile_order_small_kernel(const int2* __restrict__ ranges,
                                                                               long long base, int n,
