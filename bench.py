@@ -190,11 +190,33 @@ def cpu_oracle_rate(ca, thetas, res, n_views, steps=1):
     return done / dt, threads, dt, views
 
 
+def cpu_voxel_rate(ca, grid, slab=32):
+    """FP64 CPU restatement of voxelize + voxelize_backward (oracle/, OpenMP on
+    all host threads) on a bounded sample of the cfg4 workload: the same cloud
+    on the central z-slab of `slab` voxel layers of the same grid. Returns
+    (voxels/s, threads, seconds, sample description)."""
+    from oracle import oracle as O
+    O.build()
+    O.set_threads(0)
+    threads = O.max_threads()
+    oc = O.Cloud.from_arrays(ca.s_min, *ca.as_float64())
+    nx, ny, nz = grid.dims
+    z0 = (nz - slab) // 2
+    sub = O.GridSpec((nx, ny, slab), (grid.origin_mm[0], grid.origin_mm[1],
+                                      grid.origin_mm[2] + z0 * grid.spacing_mm[2]), tuple(grid.spacing_mm))
+    up = np.random.default_rng(3).uniform(-1, 1, sub.shape_zyx)
+    t0 = time.perf_counter()
+    O.voxelize(oc, sub)
+    O.voxelize_backward(oc, sub, up, O.Grads.zeros(oc.m))
+    dt = time.perf_counter() - t0
+    return nx * ny * slab / dt, threads, dt, f"{nx}x{ny}x{slab} central z-slab of the {nx}x{ny}x{nz} grid"
+
+
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    w, ca, thetas, _ = make_workload()
+    w, ca, thetas, vol = make_workload()
     per_step = 1  # one view of render + render_backward per step (bounded sample)
     for _ in range(args.warmup):
         cpu_oracle_rate(ca, thetas, w.res, per_step)
@@ -210,7 +232,21 @@ def run_reference(args):
         "note": "CPU restatement of the reference (oracle/); the reference itself cannot be built here "
                 "(Eigen3/libpng/vendor absent) — see DESIGN.md",
     }
+    if not args.no_voxel:  # the second metric of BASELINE.json on the same CPU path (cfg4, bounded sample)
+        from paper_2405_20693_b200 import scenes
+        w4 = scenes.CONFIGS[4]
+        grid = _grid_for_extent((-1, -1, -1), (1, 1, 1), (w4.n_vox,) * 3)
+        vrate, vthreads, vdt, sample = cpu_voxel_rate(scenes.make_cloud(4, vol=vol), grid)
+        line["voxelizer"] = {"metric": "voxelized voxels/sec (fwd+bwd)", "value": vrate, "unit": "voxels/s",
+                             "cores": vthreads, "kind": "port", "seconds": vdt,
+                             "sample": sample + " (voxelize + voxelize_backward, fp64, OpenMP)"}
     print(json.dumps(line), flush=True)
+
+
+def _grid_for_extent(lo, hi, dims):
+    """voxelizer.cpp:8-14 without importing the CUDA package (the reference arm runs the CPU path only)."""
+    from oracle import oracle as O
+    return O.grid_for_extent(lo, hi, dims)
 
 
 # ------------------------------------------------------------------ engine arm
@@ -555,10 +591,27 @@ def run_voxel(args, eng, vol, world, rank, dev):
             ach = fl * vge / (ms / args.steps / 1000.0) / 1e12
             kern[name]["achieved_tflops"] = ach
             kern[name]["frac_fp32_peak"] = ach / fp32_peak
-    return {"metric": "voxelized voxels/sec (fwd+bwd)", "value": grid.voxel_count() * args.steps / (total_ms / 1e3),
-            "unit": "voxels/s", "ms_per_step": total_ms / args.steps,
-            "workload": "cfg4 (BASELINE configs[3]): " + w.description, "vge_per_pass": vge, "pairs": pairs,
-            "kernels": kern}
+    res = {"metric": "voxelized voxels/sec (fwd+bwd)", "value": grid.voxel_count() * args.steps / (total_ms / 1e3),
+           "unit": "voxels/s", "ms_per_step": total_ms / args.steps,
+           "workload": "cfg4 (BASELINE configs[3]): " + w.description, "vge_per_pass": vge, "pairs": pairs,
+           "kernels": kern}
+    if world == 1:
+        # voxelize alone (SURVEY.md §8d reports both rates)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(eng.stream)
+        for _ in range(args.steps):
+            eng.voxelize(cloud, grid, out=out)
+        e1.record(eng.stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        res["fwd_only"] = {"value": grid.voxel_count() / (ms / 1e3), "unit": "voxels/s", "ms_per_step": ms}
+        if rank == 0 and not args.no_cpu:
+            rate, threads, dt, sample = cpu_voxel_rate(ca, grid)
+            res["cpu_baseline"] = {"value": rate, "unit": "voxels/s", "cores": threads, "kind": "port",
+                                   "sample": f"{sample} (voxelize + voxelize_backward, fp64, OpenMP), "
+                                             f"{dt:.1f} s"}
+    return res
 
 
 def main():
