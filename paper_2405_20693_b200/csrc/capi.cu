@@ -949,9 +949,8 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
     cudaEvent_t e0 = nullptr, e1 = nullptr, ec[Ctx::kMaxUnits] = {};
     unsigned long long* stamp = nullptr;
     if (dbg) {
-      cudaMalloc((void**)&stamp, (4 * Ctx::kMaxUnits + 1) * sizeof(unsigned long long));
-      cudaMemset(stamp, 0xff, (2 * Ctx::kMaxUnits + 1) * sizeof(unsigned long long));
-      cudaMemset(stamp + 2 * Ctx::kMaxUnits + 1, 0, 2 * Ctx::kMaxUnits * sizeof(unsigned long long));
+      cudaMalloc((void**)&stamp, (Ctx::kMaxUnits + 1) * sizeof(unsigned long long));
+      cudaMemset(stamp, 0xff, (Ctx::kMaxUnits + 1) * sizeof(unsigned long long));
       us.stamp = stamp;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
@@ -981,19 +980,12 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
         cudaEventDestroy(ec[u]);
       }
       std::fprintf(stderr, "\n");
-      unsigned long long hs[4 * Ctx::kMaxUnits + 1];
+      unsigned long long hs[Ctx::kMaxUnits + 1];
       cudaMemcpy(hs, stamp, sizeof(hs), cudaMemcpyDeviceToHost);
-      std::fprintf(stderr, "[units] longest item (ms)");
-      for (int u = 0; u < units; ++u) std::fprintf(stderr, " %.3f", 1e-6 * (double)hs[3 * Ctx::kMaxUnits + 1 + u]);
+      std::fprintf(stderr, "[units] published at (ms after the first claim)");
+      for (int u = 0; u < units; ++u)
+        std::fprintf(stderr, " %.3f", 1e-6 * (double)(hs[u] - hs[Ctx::kMaxUnits]));
       std::fprintf(stderr, "\n");
-      const char* what[3] = {"published", "first claim", "last claim"};
-      const int off[3] = {0, Ctx::kMaxUnits + 1, 2 * Ctx::kMaxUnits + 1};
-      for (int k = 0; k < 3; ++k) {
-        std::fprintf(stderr, "[units] %s at (ms after first claim)", what[k]);
-        for (int u = 0; u < units; ++u)
-          std::fprintf(stderr, " %.3f", 1e-6 * (double)(hs[off[k] + u] - hs[Ctx::kMaxUnits]));
-        std::fprintf(stderr, "\n");
-      }
       cudaFree(stamp);
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);

@@ -275,15 +275,7 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= total) break;
     const int4 it = items[c];  // (view * T + tile, part, parts, first item of the list)
-    unsigned long long t_claim = 0;
-    if (us.stamp && lane == 0) {
-      const unsigned long long now = global_ns();
-      t_claim = now;
-      const int uu = unit_of_view(it.x / tiles_per_view, us.n_views, us.units);
-      atomicMin(us.stamp + Ctx::kMaxUnits, now);
-      atomicMin(us.stamp + Ctx::kMaxUnits + 1 + uu, now);
-      atomicMax(us.stamp + 2 * Ctx::kMaxUnits + 1 + uu, now);
-    }
+    if (us.stamp && lane == 0) atomicMin(us.stamp + Ctx::kMaxUnits, (unsigned long long)global_ns());
     const int w = it.x, part = it.y, parts = it.z;
     const int view = w / tiles_per_view;
     const int tile = w % tiles_per_view;
@@ -343,9 +335,6 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
         if (done) tile_cnt[it.w] = 0;  // ready for the next launch
       }
       done = __shfl_sync(0xffffffffu, done, 0);
-      if (us.stamp && lane == 0)
-        atomicMax(us.stamp + 3 * Ctx::kMaxUnits + 1 + unit_of_view(view, us.n_views, us.units),
-                  global_ns() - t_claim);
       if (!done) continue;
       __threadfence();
 #pragma unroll
@@ -378,9 +367,6 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
       __threadfence();
       __syncwarp();
       if (lane == 0) unit_signal(us, unit_of_view(view, us.n_views, us.units));
-      if (us.stamp && lane == 0)
-        atomicMax(us.stamp + 3 * Ctx::kMaxUnits + 1 + unit_of_view(view, us.n_views, us.units),
-                  global_ns() - t_claim);
     }
   }
 }

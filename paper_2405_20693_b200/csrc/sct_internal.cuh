@@ -150,7 +150,7 @@ struct UnitSync {
   uint32_t epoch = 0;
   int units = 0, n_views = 0;
   int per_view = 0;  // lists (x parts) per view
-  unsigned long long* stamp = nullptr;  // diagnostics (SCT_UNIT_DEBUG): [u] publish time, [kMaxUnits] first claim
+  unsigned long long* stamp = nullptr;  // SCT_UNIT_DEBUG: [u] publish time, [kMaxUnits] first claim (K3)
 };
 
 #ifdef __CUDACC__
