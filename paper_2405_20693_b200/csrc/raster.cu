@@ -607,6 +607,10 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
     float* __restrict__ item_stats, UnitSync us) {
   __shared__ uint4 s_g[16][32];  // [slice][lane] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}
   __shared__ float s_gmax[kMmaWarps];
+  // per-warp double buffer of the 16 records (and items) of a chunk, filled
+  // by cp.async one chunk ahead (no registers held across the chunk's work)
+  __shared__ __align__(16) float4 s_rec[kMmaWarps][2][16][2];
+  __shared__ int s_it[kMmaWarps][2][16];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = lane & 3, gq = lane >> 2;
   const float px_off = (float)(8 * (t & 1)) + 0.5f;
@@ -678,28 +682,38 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
     const float px0 = (float)u0 + px_off;
     const float py_base = (float)v0 + py_off;
     const int n_list = rg.y - rg.x;
-    // records of kernels gq and gq + 8 of a chunk (quads share the loads); the
-    // next chunk's are fetched while the current one is evaluated
-    float4 na[2], nb[2];
-    auto fetch = [&](int cb) {
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int e = cb + gq + 8 * k;
-        if (e < n_list) {
-          const long long it = vals[rg.x + e];
-          na[k] = __ldg(rec + 2 * it);
-          nb[k] = __ldg(rec + 2 * it + 1);
-        } else {
-          na[k] = make_float4(0.f, 0.f, 0.f, 1.f);
-          nb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+    // records of a chunk: lane l copies half (l & 1) of kernel (l >> 1)'s
+    // record into the warp's buffer with cp.async, one chunk ahead; the item
+    // index of the chunk after that is loaded meanwhile (two-deep pipeline);
+    // lanes then read kernels gq and gq + 8 from shared memory
+    constexpr int kStride = 16 * kMmaWarps;
+    const int ck = lane >> 1, ch = lane & 1;
+    auto load_idx = [&](int cb) { return cb + ck < n_list ? vals[rg.x + cb + ck] : -1; };
+    auto issue = [&](int buf, int it) {
+      if (it >= 0) {
+        cp_async16(&s_rec[warp][buf][ck][ch], rec + 2 * (long long)it + ch);
+      } else {  // past the list: a record that evaluates to zero
+        s_rec[warp][buf][ck][ch] = ch ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, 1.f);
       }
+      if (ch == 0) s_it[warp][buf][ck] = it;
+      cp_async_commit();
     };
-    fetch(16 * warp);
-    for (int cb = 16 * warp; cb < n_list; cb += 16 * kMmaWarps) {
-      float4 ra[2] = {na[0], na[1]}, rb[2] = {nb[0], nb[1]};
+    int next_it = load_idx(16 * warp);
+    issue(0, next_it);
+    next_it = load_idx(16 * warp + kStride);
+    int buf = 0;
+    for (int cb = 16 * warp; cb < n_list; cb += kStride, buf ^= 1) {
+      if (cb + kStride < n_list) {
+        issue(buf ^ 1, next_it);
+        next_it = load_idx(cb + 2 * kStride);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        cp_async_wait_all();
+      }
+      __syncwarp();
+      const float4 ra[2] = {s_rec[warp][buf][gq][0], s_rec[warp][buf][gq + 8][0]};
+      const float4 rb[2] = {s_rec[warp][buf][gq][1], s_rec[warp][buf][gq + 8][1]};
       const bool ok[2] = {cb + gq < n_list, cb + gq + 8 < n_list};
-      if (cb + 16 * kMmaWarps < n_list) fetch(cb + 16 * kMmaWarps);
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 2
       for (int q = 0; q < 8; ++q) {
@@ -756,7 +770,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
         st[3] = fmaf(ox, fmaf(ox, m[0], 2.f * m[1]), m[3]);
         st[4] = fmaf(oy, fmaf(oy, m[0], 2.f * m[2]), m[4]);
         st[5] = fmaf(ox, fmaf(oy, m[0], m[2]), fmaf(oy, m[1], m[5]));
-        const long long it = vals[rg.x + e];
+        const long long it = s_it[warp][buf][gq + 8 * kk];
         if (item_stats) {  // vector reductions (sm_90+): 2 instead of 6 L1 wavefronts per pair
           float4* dst = reinterpret_cast<float4*>(item_stats + 8 * it);
           atomicAdd(dst, make_float4(st[0], st[1], st[2], st[3]));
@@ -769,6 +783,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
           *reinterpret_cast<float2*>(dst + 1) = make_float2(st[4], st[5]);
         }
       }
+      __syncwarp();  // the next chunk's copy overwrites this buffer
     }
     if (us.done) {  // host path: publish the unit to the chain stream once all its lists are done
       __threadfence();
