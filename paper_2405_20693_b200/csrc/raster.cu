@@ -246,6 +246,43 @@ __device__ __forceinline__ void row8px(float e[8], float dx, float A, float A2, 
   }
 }
 
+// Two kernels at once in packed FP32x2 arithmetic (FFMA2 / FMUL2 / FADD2 on
+// sm_100): element i of every float2 belongs to kernel i of the pair and is
+// computed with exactly the scalar path's operations and rounding, so each
+// kernel's pixel values equal run4 / run8's; one instruction issues both.
+__device__ __forceinline__ void run4x2(float2 e[4], float2 dx, float2 A, float2 A2, float2 bdy, float2 apb,
+                                       float2 cdy2o, float2 K) {
+  const float2 t = __ffma2_rn(A, dx, bdy);
+  const float2 L = __ffma2_rn(dx, t, cdy2o);
+  const float2 D = __ffma2_rn(A2, dx, apb);
+  float2 E = make_float2(ex2(L.x), ex2(L.y));
+  float2 R = make_float2(ex2(fminf(D.x, 126.f)), ex2(fminf(D.y, 126.f)));
+  e[0] = E;
+  E = __fmul2_rn(E, R);
+  R = __fmul2_rn(R, K);
+  e[1] = E;
+  E = __fmul2_rn(E, R);
+  R = __fmul2_rn(R, K);
+  e[2] = E;
+  e[3] = __fmul2_rn(E, R);
+}
+
+__device__ __forceinline__ void run8x2(float2 e[8], float2 dx, float2 A, float2 A2, float2 bdy, float2 apb,
+                                       float2 cdy2o, float2 K) {
+  const float2 t = __ffma2_rn(A, dx, bdy);
+  const float2 L = __ffma2_rn(dx, t, cdy2o);
+  const float2 D = __ffma2_rn(A2, dx, apb);
+  float2 E = make_float2(ex2(L.x), ex2(L.y));
+  float2 R = make_float2(ex2(fminf(D.x, 126.f)), ex2(fminf(D.y, 126.f)));
+  e[0] = E;
+#pragma unroll
+  for (int k = 1; k < 8; ++k) {
+    E = __fmul2_rn(E, R);
+    if (k < 7) R = __fmul2_rn(R, K);
+    e[k] = E;
+  }
+}
+
 // K3: one warp per work item = one part of one (view, tile) list; lane = 1
 // row x 8 columns (two 4-pixel runs sharing the per-row setup). Lists longer
 // than kPart kernels are cut into parts of kPart (K3Work): every work item is
@@ -264,8 +301,10 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     int tiles_x, int tiles_per_view, int W, int H, const int4* __restrict__ items, const int* __restrict__ n_items,
     int part_len, int* __restrict__ work, int* __restrict__ tile_cnt, float* __restrict__ partial,
     float* __restrict__ images, UnitSync us) {
-  __shared__ float4 sa[kCompWarps][32];
-  __shared__ float4 sb[kCompWarps][32];
+  // a chunk's 32 records as 16 kernel pairs, fields interleaved so that one
+  // LDS.128 yields two float2 operands: [pair][0] = (cx0, cx1, cy0, cy1),
+  // [1] = (amp0, amp1, K0, K1), [2] = (A0, A1, B0, B1), [3] = (C0, C1, 2A0, 2A1)
+  __shared__ float4 sp[kCompWarps][16][4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = lane >> 1;
   const int total = *n_items;
@@ -287,41 +326,60 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     int2 rg = ranges[w];
     rg.x += part * part_len;
     rg.y = min(rg.y, rg.x + part_len);
-    float acc[8];
+    // even and odd kernels of the list accumulate in the two halves of acc2
+    float2 acc2[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-    float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na;
+    for (int k = 0; k < 8; ++k) acc2[k] = make_float2(0.f, 0.f);
+    float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na;  // past the list: amplitude 0
     if (rg.x + lane < rg.y) {
       const long long item = vals[rg.x + lane];
       na = __ldg(rec + 2 * item);
       nb = __ldg(rec + 2 * item + 1);
     }
+    const float2 py2 = make_float2(py, py), px2 = make_float2(px0, px0);
+    const float2 c64 = make_float2(64.f, 64.f), neg = make_float2(-1.f, -1.f);
     for (int base = rg.x; base < rg.y; base += 32) {
       const int n = min(32, rg.y - base);
       __syncwarp();
-      sa[warp][lane] = na;
-      sb[warp][lane] = nb;
+      {
+        float* d = reinterpret_cast<float*>(&sp[warp][lane >> 1][0]) + (lane & 1);
+        d[0] = na.x;  d[2] = na.y;  d[4] = na.z;  d[6] = na.w;
+        d[8] = nb.x;  d[10] = nb.y; d[12] = nb.z; d[14] = nb.w;
+      }
       __syncwarp();
+      na = make_float4(0.f, 0.f, 0.f, 0.f);
+      nb = na;
       if (base + 32 + lane < rg.y) {  // prefetch the next chunk
         const long long item = vals[base + 32 + lane];
         na = __ldg(rec + 2 * item);
         nb = __ldg(rec + 2 * item + 1);
       }
 #pragma unroll 2
-      for (int j = 0; j < n; ++j) {
-        const float4 a = sa[warp][j];  // cx cy amp*2^-64 K
-        const float4 b = sb[warp][j];  // A B C 2A
-        const float dy = py - a.y;
-        const float bdy = b.y * dy;
-        const float apb = b.x + bdy;
-        const float cdy2o = fmaf(b.z * dy, dy, 64.f);
-        const float dx = px0 - a.x;
-        float e[8];
-        row8px(e, dx, b.x, b.w, bdy, apb, cdy2o, a.w, kRun8MaxA_K3);  // warp-uniform branch
+      for (int j = 0; j < (n + 1) >> 1; ++j) {  // an odd list's last pair has a zero-amplitude twin
+        const float4 p0 = sp[warp][j][0], p1 = sp[warp][j][1], p2 = sp[warp][j][2], p3 = sp[warp][j][3];
+        const float2 cx = make_float2(p0.x, p0.y), cy = make_float2(p0.z, p0.w);
+        const float2 amp = make_float2(p1.x, p1.y), K = make_float2(p1.z, p1.w);
+        const float2 A = make_float2(p2.x, p2.y), B = make_float2(p2.z, p2.w);
+        const float2 Cc = make_float2(p3.x, p3.y), A2 = make_float2(p3.z, p3.w);
+        const float2 dy = __ffma2_rn(neg, cy, py2);  // py - cy
+        const float2 bdy = __fmul2_rn(B, dy);
+        const float2 apb = __fadd2_rn(A, bdy);
+        const float2 cdy2o = __ffma2_rn(__fmul2_rn(Cc, dy), dy, c64);
+        const float2 dx = __ffma2_rn(neg, cx, px2);  // px0 - cx
+        float2 e[8];
+        if (fabsf(A.x) <= kRun8MaxA_K3 && fabsf(A.y) <= kRun8MaxA_K3) {  // warp-uniform
+          run8x2(e, dx, A, A2, bdy, apb, cdy2o, K);
+        } else {
+          run4x2(e, dx, A, A2, bdy, apb, cdy2o, K);
+          run4x2(e + 4, __fadd2_rn(dx, make_float2(4.f, 4.f)), A, A2, bdy, apb, cdy2o, K);
+        }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] = fmaf(a.z, e[k], acc[k]);
+        for (int k = 0; k < 8; ++k) acc2[k] = __ffma2_rn(amp, e[k], acc2[k]);
       }
     }
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = acc2[k].x + acc2[k].y;
     if (parts > 1) {
       // partial tile of this part (lane: row, 8 columns), then the last part sums all parts in order
       float4* mine = reinterpret_cast<float4*>(partial + (long long)(it.w + part) * 256) + 2 * lane;
