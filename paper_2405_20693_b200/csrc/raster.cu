@@ -666,8 +666,11 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
   __shared__ uint4 s_g[16][32];  // [slice][lane] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}
   __shared__ float s_gmax[kMmaWarps];
   // per-warp double buffer of the 16 records (and items) of a chunk, filled
-  // by cp.async one chunk ahead (no registers held across the chunk's work)
-  __shared__ __align__(16) float4 s_rec[kMmaWarps][2][16][2];
+  // by cp.async one chunk ahead (no registers held across the chunk's work);
+  // kernels gq and gq + 8 form pair gq with their fields interleaved, so one
+  // LDS.128 yields two float2 operands: [pair][0] = (cx, cx', cy, cy'),
+  // [1] = (amp, amp', K, K'), [2] = (A, A', B, B'), [3] = (C, C', 2A, 2A')
+  __shared__ __align__(16) float4 s_rec[kMmaWarps][2][8][4];
   __shared__ int s_it[kMmaWarps][2][16];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = lane & 3, gq = lane >> 2;
@@ -740,18 +743,22 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
     const float px0 = (float)u0 + px_off;
     const float py_base = (float)v0 + py_off;
     const int n_list = rg.y - rg.x;
-    // records of a chunk: lane l copies half (l & 1) of kernel (l >> 1)'s
-    // record into the warp's buffer with cp.async, one chunk ahead; the item
-    // index of the chunk after that is loaded meanwhile (two-deep pipeline);
-    // lanes then read kernels gq and gq + 8 from shared memory
+    // records of a chunk: lane l copies floats 4 (l & 1) .. +3 of kernel
+    // (l >> 1)'s record into its pair slot with 4-byte cp.async, one chunk
+    // ahead; the item index of the chunk after that is loaded meanwhile
+    // (two-deep pipeline); lane quads then read their pair gq
     constexpr int kStride = 16 * kMmaWarps;
     const int ck = lane >> 1, ch = lane & 1;
     auto load_idx = [&](int cb) { return cb + ck < n_list ? vals[rg.x + cb + ck] : -1; };
     auto issue = [&](int buf, int it) {
+      float* d = reinterpret_cast<float*>(&s_rec[warp][buf][ck & 7][0]) + (ck >> 3);
       if (it >= 0) {
-        cp_async16(&s_rec[warp][buf][ck][ch], rec + 2 * (long long)it + ch);
-      } else {  // past the list: a record that evaluates to zero
-        s_rec[warp][buf][ck][ch] = ch ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, 1.f);
+        const float* src = reinterpret_cast<const float*>(rec + 2 * (long long)it) + 4 * ch;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cp_async4(d + 2 * (4 * ch + i), src + i);
+      } else {  // past the list (masked by `ok`): any finite record
+#pragma unroll
+        for (int i = 0; i < 4; ++i) d[2 * (4 * ch + i)] = 0.f;
       }
       if (ch == 0) s_it[warp][buf][ck] = it;
       cp_async_commit();
@@ -769,28 +776,35 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
         cp_async_wait_all();
       }
       __syncwarp();
-      const float4 ra[2] = {s_rec[warp][buf][gq][0], s_rec[warp][buf][gq + 8][0]};
-      const float4 rb[2] = {s_rec[warp][buf][gq][1], s_rec[warp][buf][gq + 8][1]};
+      const float4 f0 = s_rec[warp][buf][gq][0], f1 = s_rec[warp][buf][gq][1];
+      const float4 f2 = s_rec[warp][buf][gq][2], f3 = s_rec[warp][buf][gq][3];
+      // kernels gq (.x) and gq + 8 (.y), evaluated together in FP32x2
+      const float2 cy = make_float2(f0.z, f0.w), K = make_float2(f1.z, f1.w);
+      const float2 A = make_float2(f2.x, f2.y), B = make_float2(f2.z, f2.w);
+      const float2 Cc = make_float2(f3.x, f3.y), A2 = make_float2(f3.z, f3.w);
+      const float2 dx = __ffma2_rn(make_float2(-1.f, -1.f), make_float2(f0.x, f0.y), make_float2(px0, px0));
+      const float2 dx4 = __fadd2_rn(dx, make_float2(4.f, 4.f));
       const bool ok[2] = {cb + gq < n_list, cb + gq + 8 < n_list};
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 2
       for (int q = 0; q < 8; ++q) {
         const float py = py_base + 2.f * q;
+        const float2 dy = __ffma2_rn(make_float2(-1.f, -1.f), cy, make_float2(py, py));
+        const float2 bdy = __fmul2_rn(B, dy);
+        const float2 apb = __fadd2_rn(A, bdy);
+        float2 cdy2o = __ffma2_rn(__fmul2_rn(Cc, dy), dy, make_float2(15.f, 15.f));
+        if (!ok[0]) cdy2o.x = -1e30f;
+        if (!ok[1]) cdy2o.y = -1e30f;
+        // (always two 4-runs here: the 8-run's per-thread branch diverges
+        // across the 16 kernels of a chunk and measured 19 % slower)
+        float2 e[8];
+        run4x2(e, dx, A, A2, bdy, apb, cdy2o, K);
+        run4x2(e + 4, dx4, A, A2, bdy, apb, cdy2o, K);
         float E[2][8];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const float4 a = ra[k], b = rb[k];
-          const float dy = py - a.y;
-          const float bdy = b.y * dy;
-          const float apb = b.x + bdy;
-          const float cdy2o = ok[k] ? fmaf(b.z * dy, dy, 15.f) : -1e30f;
-          const float dx = px0 - a.x;
-          // (always two 4-runs here: the 8-run's per-thread branch diverges
-          // across the 16 kernels of a chunk and measured 19 % slower)
-          const Run4 e0 = run4(dx, b.x, b.w, bdy, apb, cdy2o, a.w);
-          const Run4 e1 = run4(dx + 4.f, b.x, b.w, bdy, apb, cdy2o, a.w);
-          E[k][0] = e0.e0; E[k][1] = e0.e1; E[k][2] = e0.e2; E[k][3] = e0.e3;
-          E[k][4] = e1.e0; E[k][5] = e1.e1; E[k][6] = e1.e2; E[k][7] = e1.e3;
+        for (int i = 0; i < 8; ++i) {
+          E[0][i] = e[i].x;
+          E[1][i] = e[i].y;
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // two m16n8k16 slices per row pair, four pixels each
@@ -819,8 +833,8 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
       const int kk = t == 1 ? 1 : 0;
       const int e = cb + gq + 8 * kk;
       if (t < 2 && e < n_list) {
-        const float ox = (float)(u0 + 8) - (kk ? ra[1].x : ra[0].x);
-        const float oy = (float)(v0 + 8) - (kk ? ra[1].y : ra[0].y);
+        const float ox = (float)(u0 + 8) - (kk ? f0.y : f0.x);
+        const float oy = (float)(v0 + 8) - (kk ? f0.w : f0.z);
         float st[6];
         st[0] = m[0];
         st[1] = fmaf(ox, m[0], m[1]);
