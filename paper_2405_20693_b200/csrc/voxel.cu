@@ -172,6 +172,60 @@ __device__ __forceinline__ void row8(float e[8], bool rec_ok, float dx0, float s
   }
 }
 
+// row8 for two rows of one kernel at once (rows z and z + 4 of a lane: same
+// x geometry, their own c1 / c0o) in packed FP32x2 arithmetic (FFMA2 / FMUL2
+// on sm_100); element r of every float2 is exactly row8's value for row r.
+__device__ __forceinline__ void row8x2(float2 e[8], bool rec_ok, float dx0, float sx, float qxx, float2 c1,
+                                       float2 c0o, float K) {
+  const float2 K2 = make_float2(K, K), q2 = make_float2(qxx, qxx);
+  if (qxx * sx * sx >= -1.5f) {
+    const float qs = qxx * sx;
+    const float2 d0 = make_float2(dx0, dx0);
+    const float2 t = __ffma2_rn(q2, d0, c1);
+    const float2 L = __ffma2_rn(d0, t, c0o);
+    const float2 D = __ffma2_rn(make_float2(2.f * qs, 2.f * qs), d0,
+                                __ffma2_rn(c1, make_float2(sx, sx), make_float2(qs * sx, qs * sx)));
+    float2 E = make_float2(ex2v(L.x), ex2v(L.y));
+    float2 R = make_float2(ex2v(fminf(D.x, 126.f)), ex2v(fminf(D.y, 126.f)));
+    e[0] = E;
+#pragma unroll
+    for (int c = 1; c < 8; ++c) {
+      E = __fmul2_rn(E, R);
+      if (c < 7) R = __fmul2_rn(R, K2);
+      e[c] = E;
+    }
+  } else if (rec_ok) {
+    const float qs = qxx * sx;
+    const float2 dbase = __ffma2_rn(c1, make_float2(sx, sx), make_float2(qs * sx, qs * sx));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float dxs = fmaf(4.f * h, sx, dx0);
+      const float2 dx = make_float2(dxs, dxs);
+      const float2 t = __ffma2_rn(q2, dx, c1);
+      const float2 L = __ffma2_rn(dx, t, c0o);
+      const float2 D = __ffma2_rn(make_float2(2.f * qs, 2.f * qs), dx, dbase);
+      float2 E = make_float2(ex2v(L.x), ex2v(L.y));
+      float2 R = make_float2(ex2v(fminf(D.x, 126.f)), ex2v(fminf(D.y, 126.f)));
+      e[4 * h] = E;
+      E = __fmul2_rn(E, R);
+      R = __fmul2_rn(R, K2);
+      e[4 * h + 1] = E;
+      E = __fmul2_rn(E, R);
+      R = __fmul2_rn(R, K2);
+      e[4 * h + 2] = E;
+      e[4 * h + 3] = __fmul2_rn(E, R);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float dxs = fmaf((float)c, sx, dx0);
+      const float2 dx = make_float2(dxs, dxs);
+      const float2 L = __ffma2_rn(dx, __ffma2_rn(q2, dx, c1), c0o);
+      e[c] = make_float2(ex2v(L.x), ex2v(L.y));
+    }
+  }
+}
+
 // K7: one warp per brick, four bricks per CTA; lane = rows (y, z) and (y, z+4),
 // 8 voxels each. Each warp stages its brick list 32 records at a time through
 // its own shared memory, prefetching the next chunk into registers.
@@ -205,11 +259,10 @@ __global__ void __launch_bounds__(32 * kEvalWarps) voxel_eval_kernel(BrickGeo G,
   const int ly = lane & 7, lz = lane >> 3;  // rows (ly, lz) and (ly, lz + 4)
   const float fy = (float)ly * G.spf.y;
   const float fz0 = (float)lz * G.spf.z, fz1 = (float)(lz + 4) * G.spf.z;
-  float acc[2][8];
+  float2 acc2[8];  // (row z, row z + 4) per column
 #pragma unroll
-  for (int r = 0; r < 2; ++r)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[r][c] = 0.f;
+  for (int c = 0; c < 8; ++c) acc2[c] = make_float2(0.f, 0.f);
+  const float2 fz = make_float2(fz0, fz1);
   float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na, nc = na;
   auto fetch = [&](int p) {
     const long long i = vals[p];
@@ -234,17 +287,25 @@ __global__ void __launch_bounds__(32 * kEvalWarps) voxel_eval_kernel(BrickGeo G,
       const float4 o = sC[warp][j];
       const bool rec_ok = q.x * G.spf.x * G.spf.x >= -8.f;
       const float dy = a.y + fy;
+      // both rows together: per element the scalar path's operations
+      const float2 dz = __fadd2_rn(make_float2(a.z, a.z), fz);
+      const float ody = o.z * dy, qdy = q.y * dy;
+      const float2 c0o = __ffma2_rn(make_float2(qdy, qdy), make_float2(dy, dy),
+                                    __ffma2_rn(__fmul2_rn(make_float2(q.z, q.z), dz), dz,
+                                               __ffma2_rn(make_float2(ody, ody), dz, make_float2(64.f, 64.f))));
+      const float2 c1 = __ffma2_rn(make_float2(o.x, o.x), make_float2(dy, dy),
+                                   __fmul2_rn(make_float2(o.y, o.y), dz));
+      float2 e[8];
+      row8x2(e, rec_ok, a.x, G.spf.x, q.x, c1, c0o, q.w);
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const float dz = a.z + (r ? fz1 : fz0);
-        const float c0o = fmaf(q.y * dy, dy, fmaf(q.z * dz, dz, fmaf(o.z * dy, dz, 64.f)));
-        const float c1 = fmaf(o.x, dy, o.y * dz);
-        float e[8];
-        row8<true>(e, rec_ok, a.x, G.spf.x, q.x, c1, c0o, q.w);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(a.w, e[c], acc[r][c]);
-      }
+      for (int c = 0; c < 8; ++c) acc2[c] = __ffma2_rn(make_float2(a.w, a.w), e[c], acc2[c]);
     }
+  }
+  float acc[2][8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    acc[0][c] = acc2[c].x;
+    acc[1][c] = acc2[c].y;
   }
   const int y = ty * kTileVox + ly, x0 = tx * kTileVox;
 #pragma unroll
