@@ -172,6 +172,33 @@ __device__ __forceinline__ void row8(float e[8], bool rec_ok, float dx0, float s
   }
 }
 
+// row8's two 4-voxel runs for two kernels at once (K8: kernels gq and gq + 8
+// of a chunk, each with its own x geometry) in packed FP32x2
+__device__ __forceinline__ void run4x2v(float2 e[8], float2 dx0, float sx, float2 qxx, float2 c1, float2 c0o,
+                                        float2 K) {
+  const float2 s2 = make_float2(sx, sx);
+  const float2 qs = __fmul2_rn(qxx, s2);
+  const float2 dbase = __ffma2_rn(c1, s2, __fmul2_rn(qs, s2));  // D(dx) = 2 qxx sx dx + c1 sx + qxx sx^2
+  const float2 qs2 = __fmul2_rn(make_float2(2.f, 2.f), qs);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float2 dx = __ffma2_rn(make_float2(4.f * h, 4.f * h), s2, dx0);
+    const float2 t = __ffma2_rn(qxx, dx, c1);
+    const float2 L = __ffma2_rn(dx, t, c0o);
+    const float2 D = __ffma2_rn(qs2, dx, dbase);
+    float2 E = make_float2(ex2v(L.x), ex2v(L.y));
+    float2 R = make_float2(ex2v(fminf(D.x, 126.f)), ex2v(fminf(D.y, 126.f)));
+    e[4 * h] = E;
+    E = __fmul2_rn(E, R);
+    R = __fmul2_rn(R, K);
+    e[4 * h + 1] = E;
+    E = __fmul2_rn(E, R);
+    R = __fmul2_rn(R, K);
+    e[4 * h + 2] = E;
+    e[4 * h + 3] = __fmul2_rn(E, R);
+  }
+}
+
 // row8 for two rows of one kernel at once (rows z and z + 4 of a lane: same
 // x geometry, their own c1 / c0o) in packed FP32x2 arithmetic (FFMA2 / FMUL2
 // on sm_100); element r of every float2 is exactly row8's value for row r.
@@ -561,19 +588,37 @@ __global__ void __launch_bounds__(32 * kVMmaWarps, 7) voxel_backward_mma_kernel(
       bzk[k] = (float)(c0z - (double)a.z);
       rec_ok[k] = qk[k].x * sx * sx >= -8.f;
     }
+    const float2 bx2 = make_float2(bxk[0], bxk[1]), by2 = make_float2(byk[0], byk[1]);
+    const float2 bz2 = make_float2(bzk[0], bzk[1]);
+    const float2 qx2 = make_float2(qk[0].x, qk[1].x), qy2 = make_float2(qk[0].y, qk[1].y);
+    const float2 qz2 = make_float2(qk[0].z, qk[1].z), K2 = make_float2(qk[0].w, qk[1].w);
+    const float2 ox2 = make_float2(okk[0].x, okk[1].x), oy2 = make_float2(okk[0].y, okk[1].y);
+    const float2 oz2 = make_float2(okk[0].z, okk[1].z), c15 = make_float2(15.f, 15.f);
     float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 2
     for (int q = 0; q < 16; ++q) {
       const int r = 4 * q + t;
       const float fy = (float)(r & 7) * sy, fz = (float)(r >> 3) * sz;
       float E[2][8];
+      {  // kernels gq (.x) and gq + 8 (.y) in packed FP32x2; elementwise the scalar row8
+        const float2 dy = __fadd2_rn(by2, make_float2(fy, fy)), dz = __fadd2_rn(bz2, make_float2(fz, fz));
+        float2 c0o = __ffma2_rn(__fmul2_rn(qy2, dy), dy,
+                                __ffma2_rn(__fmul2_rn(qz2, dz), dz, __ffma2_rn(__fmul2_rn(oz2, dy), dz, c15)));
+        if (!valid[0]) c0o.x = -1e30f;
+        if (!valid[1]) c0o.y = -1e30f;
+        const float2 c1 = __ffma2_rn(ox2, dy, __fmul2_rn(oy2, dz));
+        if (rec_ok[0] && rec_ok[1]) {
+          float2 e[8];
+          run4x2v(e, bx2, sx, qx2, c1, c0o, K2);
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const float dy = byk[k] + fy, dz = bzk[k] + fz;
-        const float4 qq = qk[k], oo = okk[k];
-        const float c0o = valid[k] ? fmaf(qq.y * dy, dy, fmaf(qq.z * dz, dz, fmaf(oo.z * dy, dz, 15.f))) : -1e30f;
-        const float c1 = fmaf(oo.x, dy, oo.y * dz);
-        row8(E[k], rec_ok[k], bxk[k], sx, qq.x, c1, c0o, qq.w);
+          for (int i = 0; i < 8; ++i) {
+            E[0][i] = e[i].x;
+            E[1][i] = e[i].y;
+          }
+        } else {
+          row8(E[0], rec_ok[0], bxk[0], sx, qk[0].x, c1.x, c0o.x, qk[0].w);
+          row8(E[1], rec_ok[1], bxk[1], sx, qk[1].x, c1.y, c0o.y, qk[1].w);
+        }
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
