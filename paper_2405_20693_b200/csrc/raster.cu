@@ -209,47 +209,18 @@ __device__ __forceinline__ Run4 run4(float dx, float A, float A2, float bdy, flo
   return r;
 }
 
-// Eight pixels from one pair of MUFU ops (19 instead of 22 + 1 instructions
-// for two runs). Along a row L(x) = -a (x - x*)^2 + L*, a = |A|; a pixel that
-// matters (L >= -24: 2^-24 of the kernel's amplitude) sits within sqrt(24 / a)
-// of x*, so the run's first pixel is at most 49 a + 14 sqrt(24 a) below it.
-// It must stay above the ftz floor: -190 with K3's +64 offset (a <= 1.6);
-// narrower kernels take two 4-runs (a warp-uniform branch in K3).
+// Eight pixels from one pair of MUFU ops (run8x2 below; 19 instead of 22 + 1
+// instructions for two 4-runs). Along a row L(x) = -a (x - x*)^2 + L*, a = |A|;
+// a pixel that matters (L >= -24: 2^-24 of the kernel's amplitude) sits within
+// sqrt(24 / a) of x*, so the run's first pixel is at most 49 a + 14 sqrt(24 a)
+// below it. It must stay above the ftz floor: -190 with K3's +64 offset
+// (a <= 1.6); narrower kernels take two 4-runs (a warp-uniform branch in K3).
 constexpr float kRun8MaxA_K3 = 1.5f;
-__device__ __forceinline__ void run8(float e[8], float dx, float A, float A2, float bdy, float apb, float cdy2o,
-                                     float K) {
-  const float t = fmaf(A, dx, bdy);
-  const float L = fmaf(dx, t, cdy2o);
-  const float D = fmaf(A2, dx, apb);
-  float E = ex2(L);
-  float R = ex2(fminf(D, 126.f));
-  e[0] = E;
-#pragma unroll
-  for (int k = 1; k < 8; ++k) {
-    E *= R;
-    if (k < 7) R *= K;
-    e[k] = E;
-  }
-}
-
-// the 8 pixels of a row at dx, dx+1, ..., dx+7: one 8-run when the kernel is
-// wide enough, else two 4-runs
-__device__ __forceinline__ void row8px(float e[8], float dx, float A, float A2, float bdy, float apb, float cdy2o,
-                                       float K, float amax) {
-  if (fabsf(A) <= amax) {
-    run8(e, dx, A, A2, bdy, apb, cdy2o, K);
-  } else {
-    const Run4 a = run4(dx, A, A2, bdy, apb, cdy2o, K);
-    const Run4 b = run4(dx + 4.f, A, A2, bdy, apb, cdy2o, K);
-    e[0] = a.e0; e[1] = a.e1; e[2] = a.e2; e[3] = a.e3;
-    e[4] = b.e0; e[5] = b.e1; e[6] = b.e2; e[7] = b.e3;
-  }
-}
 
 // Two kernels at once in packed FP32x2 arithmetic (FFMA2 / FMUL2 / FADD2 on
 // sm_100): element i of every float2 belongs to kernel i of the pair and is
-// computed with exactly the scalar path's operations and rounding, so each
-// kernel's pixel values equal run4 / run8's; one instruction issues both.
+// computed with exactly the scalar path's operations and rounding (run4's; an
+// 8-run continues the same recurrence); one instruction issues both.
 __device__ __forceinline__ void run4x2(float2 e[4], float2 dx, float2 A, float2 A2, float2 bdy, float2 apb,
                                        float2 cdy2o, float2 K) {
   const float2 t = __ffma2_rn(A, dx, bdy);
