@@ -756,6 +756,9 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
       const float2 dx = __ffma2_rn(make_float2(-1.f, -1.f), make_float2(f0.x, f0.y), make_float2(px0, px0));
       const float2 dx4 = __fadd2_rn(dx, make_float2(4.f, 4.f));
       const bool ok[2] = {cb + gq < n_list, cb + gq + 8 < n_list};
+      // one 8-run per row when every kernel of the chunk is wide enough
+      // (warp-uniform; the +15 offset bounds it at |A| <= 1.25, see run8x2)
+      const bool r8 = __all_sync(0xffffffffu, fabsf(A.x) <= 1.25f && fabsf(A.y) <= 1.25f);
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 2
       for (int q = 0; q < 8; ++q) {
@@ -766,11 +769,13 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
         float2 cdy2o = __ffma2_rn(__fmul2_rn(Cc, dy), dy, make_float2(15.f, 15.f));
         if (!ok[0]) cdy2o.x = -1e30f;
         if (!ok[1]) cdy2o.y = -1e30f;
-        // (always two 4-runs here: the 8-run's per-thread branch diverges
-        // across the 16 kernels of a chunk and measured 19 % slower)
         float2 e[8];
-        run4x2(e, dx, A, A2, bdy, apb, cdy2o, K);
-        run4x2(e + 4, dx4, A, A2, bdy, apb, cdy2o, K);
+        if (r8) {
+          run8x2(e, dx, A, A2, bdy, apb, cdy2o, K);
+        } else {
+          run4x2(e, dx, A, A2, bdy, apb, cdy2o, K);
+          run4x2(e + 4, dx4, A, A2, bdy, apb, cdy2o, K);
+        }
         float E[2][8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
