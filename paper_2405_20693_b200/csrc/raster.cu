@@ -1035,9 +1035,11 @@ static int composite_per_sm() {
 // and host-buffer paths cut, and therefore sum, every list identically):
 // 256 kernels, halved (down to 32) while the state has fewer items than twice
 // the GPU's warp slots (small workloads: the train step renders one view).
-// Measured at cfg3 (B200): K3 1.37 ms at 256 and 512, 1.40 at 128, 1.47 at
-// 64, 1.54 uncut; the longest item of the unit-ordered host path takes
-// 0.2 ms at 256 vs 0.4 at 512, which sets when the first D2H copy can start.
+// Measured at cfg3 (B200, scalar K3): 1.37 ms at 256 and 512, 1.40 at 128,
+// 1.47 at 64, 1.54 uncut; the longest item of the unit-ordered host path
+// takes 0.2 ms at 256 vs 0.4 at 512, which sets when the first D2H copy can
+// start. With the FP32x2 K3: 1.20 ms at 256, 1.185 at 512, but e2e 13.0k vs
+// 12.4-12.6k projections/s, so 256 stays.
 static int composite_part_len(Ctx* c, const sct_fwd* s) {
   if (const char* e = std::getenv("SCT_K3_PART")) return std::max(32, atoi(e));
   const long long lists = (long long)s->det.tiles_x * s->det.tiles_y * s->n_views;
