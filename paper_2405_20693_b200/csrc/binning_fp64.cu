@@ -50,7 +50,9 @@ __global__ void __launch_bounds__(256) gauss_prep_kernel(long long m, double s_m
 // One thread per (view, kernel) item; item = view * m + kernel (view-major, so
 // a stable sort on the (view, tile) key leaves each tile list ascending in
 // kernel index exactly like the reference's serial push_back, rasterizer.cpp:124-133).
-__global__ void __launch_bounds__(256) raster_preprocess_kernel(
+// (3 CTAs per SM: 80 registers with a small spill beat 95 registers at two
+// CTAs — FP64 latency-bound; 0.293 -> 0.285 ms at cfg3)
+__global__ void __launch_bounds__(256, 3) raster_preprocess_kernel(
     long long m, long long n_items, const float* __restrict__ pos, const double* __restrict__ prep,
     const ViewParams* __restrict__ views, DetParams det, RasterParams rp, float4* __restrict__ rec,
     short4* __restrict__ rect, int32_t* __restrict__ count, uint8_t* __restrict__ vis) {
