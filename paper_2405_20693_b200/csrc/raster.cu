@@ -757,7 +757,11 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
       const float2 dx4 = __fadd2_rn(dx, make_float2(4.f, 4.f));
       const bool ok[2] = {cb + gq < n_list, cb + gq + 8 < n_list};
       // one 8-run per row when every kernel of the chunk is wide enough
-      // (warp-uniform; the +15 offset bounds it at |A| <= 1.25, see run8x2)
+      // (warp-uniform). With the +15 offset E' flushes below L = -141. A
+      // pixel p of the run with L(p) >= -11 (2^-11 of the peak: binary16 E's
+      // own rounding) has L(first) >= L(p) - 49a - 14a|p - x*| >= -11 - 49a -
+      // 14 sqrt(11 a) >= -125 for a = |A| <= 1.25: no value above binary16
+      // resolution is lost. (K3's +64 offset allows 1.5 at the 2^-24 level.)
       const bool r8 = __all_sync(0xffffffffu, fabsf(A.x) <= 1.25f && fabsf(A.y) <= 1.25f);
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 2

@@ -200,7 +200,9 @@ __device__ __forceinline__ void run4x2v(float2 e[8], float2 dx0, float sx, float
 }
 
 // one 8-voxel run for two kernels at once (K8, warp-uniform when every
-// kernel of the chunk has Qxx sx^2 >= -1.25: the +15 offset's ftz bound)
+// kernel of the chunk has Qxx sx^2 >= -1.25: with the +15 offset no value
+// above 2^-11 of the kernel's peak — binary16 E's resolution — can sit in a
+// run whose first voxel flushes; the derivation is at raster.cu's K4 8-run)
 __device__ __forceinline__ void run8x2v(float2 e[8], float2 dx0, float sx, float2 qxx, float2 c1, float2 c0o,
                                         float2 K) {
   const float2 s2 = make_float2(sx, sx);
