@@ -316,25 +316,66 @@ __global__ void __launch_bounds__(128) raster_finalize_kernel(
   }
 }
 
+// The 10 pair-statistic sums of every kernel (FP64): eight lanes per kernel,
+// lane j summing pairs j, j + 8, ... in order, then a fixed xor-shuffle tree
+// — deterministic, and eight times the threads of the one-thread-per-kernel
+// chain for the latency-bound 48-byte pair gathers.
+__global__ void __launch_bounds__(256) voxel_pair_sum_kernel(long long m, const int32_t* __restrict__ offset,
+                                                             const int32_t* __restrict__ count,
+                                                             const float4* __restrict__ ps,
+                                                             double* __restrict__ sums) {
+  const int j = threadIdx.x & 7;
+  for (long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3; g < ((m + 3) & ~3LL);
+       g += ((long long)gridDim.x * blockDim.x) >> 3) {  // all lanes of a warp iterate together
+    const bool live = g < m;
+    const int32_t n = live ? count[g] : 0;
+    const long long p0 = live ? offset[g] : 0;
+    double s[10];
+#pragma unroll
+    for (int a = 0; a < 10; ++a) s[a] = 0.0;
+    for (int q = j; q < n; q += 8) {
+      const float4 a = __ldg(ps + 3 * (p0 + q)), b = __ldg(ps + 3 * (p0 + q) + 1), c = __ldg(ps + 3 * (p0 + q) + 2);
+      s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
+      s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+      s[8] += c.x; s[9] += c.y;
+    }
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1)
+#pragma unroll
+      for (int a = 0; a < 10; ++a) s[a] += __shfl_xor_sync(0xffffffffu, s[a], off);
+    if (live) {  // lane j writes sums j and j + 8 (all lanes hold all ten)
+#pragma unroll
+      for (int a = 0; a < 10; ++a)
+        if ((a & 7) == j) sums[a * m + g] = s[a];
+    }
+  }
+}
+
 // voxelizer.cpp:192-223
 __global__ void __launch_bounds__(128) voxel_chain_kernel(
     long long m, double s_min, const float* __restrict__ rho_raw, const float* __restrict__ pos,
     const float* __restrict__ scale_raw, const float* __restrict__ rot, const int32_t* __restrict__ offset,
-    const int32_t* __restrict__ count, const float4* __restrict__ ps, float* __restrict__ g_rho,
-    float* __restrict__ g_pos, float* __restrict__ g_scale, float* __restrict__ g_rotp) {
+    const int32_t* __restrict__ count, const float4* __restrict__ ps, const double* __restrict__ sums,
+    float* __restrict__ g_rho, float* __restrict__ g_pos, float* __restrict__ g_scale,
+    float* __restrict__ g_rotp) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     const int32_t n = count[i];
     if (n == 0) continue;  // not touched
     double s[10];
+    if (sums) {  // pre-summed by voxel_pair_sum_kernel
 #pragma unroll
-    for (int a = 0; a < 10; ++a) s[a] = 0.0;
-    const long long p0 = offset[i];
-    for (long long p = p0; p < p0 + n; ++p) {
-      const float4 a = ps[3 * p], b = ps[3 * p + 1], c = ps[3 * p + 2];
-      s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
-      s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
-      s[8] += c.x; s[9] += c.y;
+      for (int a = 0; a < 10; ++a) s[a] = sums[a * m + i];
+    } else {
+#pragma unroll
+      for (int a = 0; a < 10; ++a) s[a] = 0.0;
+      const long long p0 = offset[i];
+      for (long long p = p0; p < p0 + n; ++p) {
+        const float4 a = ps[3 * p], b = ps[3 * p + 1], c = ps[3 * p + 2];
+        s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
+        s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+        s[8] += c.x; s[9] += c.y;
+      }
     }
     const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
     const dM3 q = d_inv3(d_covariance(k));
@@ -414,12 +455,20 @@ void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,
                         const float4* pair_stats, sct_grads* g) {
   if (cl.m == 0) return;
+  double* sums = nullptr;
+  if (dev_alloc(c, (void**)&sums, 10 * cl.m * sizeof(double)) != SCT_OK) return;
+  {
+    KScope _ks(c, "K8_voxel_pair_sum");
+    voxel_pair_sum_kernel<<<grid_cap(c, 8 * cl.m, 256), 256, 0, c->stream>>>(cl.m, offset, count, pair_stats,
+                                                                              sums);
+  }
   {
     KScope _ks(c, "K8_voxel_chain");
     voxel_chain_kernel<<<grid_cap(c, cl.m, 128), 128, 0, c->stream>>>(cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
                                                                      cl.scale_raw, cl.rot, offset, count, pair_stats,
-                                                                     g->rho_raw, g->pos, g->scale_raw, g->rot);
+                                                                     sums, g->rho_raw, g->pos, g->scale_raw, g->rot);
   }
+  dev_free(c, sums);
 }
 
 }  // namespace sct
