@@ -16,7 +16,7 @@ namespace {
 // K0: view-independent per-Gaussian quantities, once per kernel: the 3D
 // covariance Sigma (all 9 entries, d_covariance order — its rounding is not
 // symmetric, so both halves are kept) and rho = act_density(rho_raw).
-// prep[i] = {S00 S01 S02 S10 S11 S12 S20 S21 S22, rho}.
+// prep[a][i] (SoA, a = 0..17) = {S00 S01 S02 S10 S11 S12 S20 S21 S22, rho, Sigma^-1 (6), det Sigma, 0}.
 __global__ void __launch_bounds__(256) gauss_prep_kernel(long long m, double s_min, const float* __restrict__ rho_raw,
                                                          const float* __restrict__ pos,
                                                          const float* __restrict__ scale_raw,
@@ -26,10 +26,10 @@ __global__ void __launch_bounds__(256) gauss_prep_kernel(long long m, double s_m
     const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
     dM3 r;
     const dM3 s = d_covariance(k, &r);
-    double* o = prep + kPrepStride * i;
+    auto o = [&](int a) -> double& { return prep[(long long)a * m + i]; };  // SoA: coalesced across kernels
 #pragma unroll
-    for (int a = 0; a < 9; ++a) o[a] = s.m[a / 3][a % 3];
-    o[9] = d_act_density(k.rho_raw);
+    for (int a = 0; a < 9; ++a) o(a) = s.m[a / 3][a % 3];
+    o(9) = d_act_density(k.rho_raw);
     // Sigma^-1 = R diag(1/s^2) R^T (well conditioned: no inversion of Sigma)
     // and det Sigma = prod s_k^2, for the chain kernel's identities
     double is2[3];
@@ -39,11 +39,11 @@ __global__ void __launch_bounds__(256) gauss_prep_kernel(long long m, double s_m
 #pragma unroll
     for (int e = 0; e < 6; ++e) {
       const int a = ij[e][0], b = ij[e][1];
-      o[10 + e] = __fma_rn(r.m[a][0] * is2[0], r.m[b][0],
+      o(10 + e) = __fma_rn(r.m[a][0] * is2[0], r.m[b][0],
                            __fma_rn(r.m[a][1] * is2[1], r.m[b][1], r.m[a][2] * is2[2] * r.m[b][2]));
     }
-    o[16] = (k.s[0] * k.s[0]) * (k.s[1] * k.s[1]) * (k.s[2] * k.s[2]);
-    o[17] = 0.0;
+    o(16) = (k.s[0] * k.s[0]) * (k.s[1] * k.s[1]) * (k.s[2] * k.s[2]);
+    o(17) = 0.0;
   }
 }
 
@@ -63,12 +63,12 @@ __global__ void __launch_bounds__(256, 3) raster_preprocess_kernel(
     const long long i = item - v * m;
     const double p[3] = {(double)pos[3 * i], (double)pos[3 * i + 1], (double)pos[3 * i + 2]};
     dM3 sigma;
-    const double* pr = prep + kPrepStride * i;
+    auto pr = [&](int a) { return prep[(long long)a * m + i]; };
 #pragma unroll
-    for (int a = 0; a < 9; ++a) sigma.m[a / 3][a % 3] = pr[a];
+    for (int a = 0; a < 9; ++a) sigma.m[a / 3][a % 3] = pr(a);
     const ViewParams view = views[v];
     dProj g;
-    if (!d_project(p, sigma, pr[9], view, det, rp, g)) {
+    if (!d_project(p, sigma, pr(9), view, det, rp, g)) {
       count[item] = 0;
       vis[item] = 0;
       rect[item] = make_short4(1, 0, 1, 0);

@@ -67,11 +67,11 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
     const ViewParams& V = views[v];
     const double* W = V.rot;
     const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
-    const double* pr = prep + kPrepStride * i;
-    const Sym3 Sg{pr[0], pr[1], pr[2], pr[4], pr[5], pr[8]};
-    const double rho = pr[9];
-    const Sym3 Si{pr[10], pr[11], pr[12], pr[13], pr[14], pr[15]};  // Sigma^-1
-    const double detS = pr[16];
+    auto pr = [&](int a) { return prep[(long long)a * m + i]; };  // SoA [kPrepStride][m]
+    const Sym3 Sg{pr(0), pr(1), pr(2), pr(4), pr(5), pr(8)};
+    const double rho = pr(9);
+    const Sym3 Si{pr(10), pr(11), pr(12), pr(13), pr(14), pr(15)};  // Sigma^-1
+    const double detS = pr(16);
     const double x = fma(W[0], px, fma(W[1], py, W[2] * pz)) + V.t[0];
     const double y = fma(W[3], px, fma(W[4], py, W[5] * pz)) + V.t[1];
     const double z = fma(W[6], px, fma(W[7], py, W[8] * pz)) + V.t[2];

@@ -243,7 +243,7 @@ struct sct_fwd {
   void* d_keys = nullptr;              // [pairs] sorted tile keys (uint16 if tile_bits <= 16, else uint32)
   int32_t* d_vals = nullptr;           // [pairs] sorted item index
   int2* d_ranges = nullptr;            // [V*T] [start,end) into sorted pairs
-  double* d_prep = nullptr;            // [m][kPrepStride] Sigma (9) + rho, FP64
+  double* d_prep = nullptr;            // [kPrepStride][m] (SoA) Sigma (9), rho, Sigma^-1 (6), det, FP64
 };
 
 struct sct_ctx : public sct::Ctx {};
