@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
         na = __ldg(rec + 2 * item);
         nb = __ldg(rec + 2 * item + 1);
       }
-#pragma unroll 2
+#pragma unroll 8
       for (int j = 0; j < (n + 1) >> 1; ++j) {  // an odd list's last pair has a zero-amplitude twin
         const float4 p0 = sp[warp][j][0], p1 = sp[warp][j][1], p2 = sp[warp][j][2], p3 = sp[warp][j][3];
         const float2 cx = make_float2(p0.x, p0.y), cy = make_float2(p0.z, p0.w);
