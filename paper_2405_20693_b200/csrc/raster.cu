@@ -764,7 +764,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
       // resolution is lost. (K3's +64 offset allows 1.5 at the 2^-24 level.)
       const bool r8 = __all_sync(0xffffffffu, fabsf(A.x) <= 1.25f && fabsf(A.y) <= 1.25f);
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
+#pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float py = py_base + 2.f * q;
         const float2 dy = __ffma2_rn(make_float2(-1.f, -1.f), cy, make_float2(py, py));
