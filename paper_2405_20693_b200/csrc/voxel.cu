@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(32 * kEvalWarps) voxel_eval_kernel(BrickGeo G,
     sC[warp][lane] = nc;
     __syncwarp();
     if (base + 32 + lane < rg.y) fetch(base + 32 + lane);
+#pragma unroll 4
     for (int j = 0; j < n; ++j) {
       const float4 a = sA[warp][j];
       const float4 q = sB[warp][j];
@@ -618,7 +619,7 @@ __global__ void __launch_bounds__(32 * kVMmaWarps, 7) voxel_backward_mma_kernel(
     const float2 oz2 = make_float2(okk[0].z, okk[1].z), c15 = make_float2(15.f, 15.f);
     const bool r8 = __all_sync(0xffffffffu, qk[0].x * sx * sx >= -1.25f && qk[1].x * sx * sx >= -1.25f);
     float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
+#pragma unroll 4
     for (int q = 0; q < 16; ++q) {
       const int r = 4 * q + t;
       const float fy = (float)(r & 7) * sy, fz = (float)(r >> 3) * sz;
