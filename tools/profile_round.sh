@@ -2,7 +2,7 @@
 # ncu evidence for profiles/: launch list of a short bench run (per-launch
 # durations, clocks uncontrolled) and --set full captures of the hot raster and
 # voxel kernels (all only after the same command exited 0 without ncu).
-TAG=${1:-r01_v8}
+TAG=${1:-r01_v9}
 CMD="python bench.py --no-cpu --no-e2e --no-train --steps 2 --warmup 3"
 $CMD > gpurun_out/plain_$TAG.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1
