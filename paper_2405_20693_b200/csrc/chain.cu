@@ -268,7 +268,8 @@ __global__ void __launch_bounds__(256) view_sum_kernel(long long m, int n_views,
     double acc = 0.0;
     if (a < kItemOut) {
       const float* src = item + a * n_items + i;
-      for (int v = 0; v < n_views; ++v) acc += (double)src[(long long)v * m];
+#pragma unroll 8
+      for (int v = 0; v < n_views; ++v) acc += (double)__ldg(src + (long long)v * m);  // loads ahead, sums in order
     } else {
       for (int v = 0; v < n_views; ++v) acc += (double)vis[(long long)v * m + i];
     }
