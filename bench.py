@@ -152,9 +152,14 @@ class ClockSampler:
     def stop(self):
         if self.thread is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: " + getattr(self, "err", "")]}
+        nv = self.nv
+        try:  # one more sample at the end of the timed region (the thread may have been descheduled)
+            self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                 nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+        except Exception:  # noqa: BLE001
+            pass
         self.stop_flag = True
         self.thread.join()
-        nv = self.nv
         bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                 "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
                 "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
