@@ -29,30 +29,8 @@ SHEPP_LOGAN = np.array([
     [0.1, 0.023, 0.046, 0.020, 0.06, -0.605, 0.0, 0.0],
 ], dtype=np.float64)
 
-_ready = False
-
-
 def _lib():
-    global _ready
-    L = O.lib()
-    if not _ready:
-        sig = {
-            "orc_phantom": (None, [C.c_int, D, I32, D, D, F]),
-            "orc_sample_trilinear": (C.c_double, [F, I32, D, D, D]),
-            "orc_project_volume": (C.c_int, [F, I32, D, D, D, I32, C.c_double, C.c_double, D]),
-            "orc_view_seed": (C.c_uint64, [C.c_uint64, C.c_int]),
-            "orc_add_noise": (C.c_int, [F, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, D]),
-            "orc_fdk": (C.c_int, [F, C.c_int, D, I32, D, I32, D, D, C.c_int, D]),
-            "orc_nn_distances": (None, [C.c_int, D, D]),
-            "orc_sample_init_cloud": (C.c_int, [VP, F, I32, D, D, C.c_int, C.c_double, C.c_double, C.c_double,
-                                                D, D, D, D]),
-        }
-        for name, (res, args) in sig.items():
-            f = getattr(L, name)
-            f.restype = res
-            f.argtypes = args
-        _ready = True
-    return L
+    return O.lib()
 
 
 def _d(a):

@@ -10,6 +10,7 @@ voxelizer.hpp:60-72, objectives.hpp:24-31, trainer.cpp:34-36,144-163).
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import subprocess
@@ -19,9 +20,15 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liborc.so")
-_lib = None
+# the reference itself, compiled from /root/reference by `make -C oracle ref`
+# (ref_capi.cpp + ref_shim/); it exports the same orc_* ABI
+_REF_LIB_PATH = os.path.join(_HERE, "_ref", "libsplatct_ref.so")
+_REF_SRC = "/root/reference/proj/core/src"
+_libs: dict = {}
+_active = os.environ.get("SCT_ORACLE", "port")
 
 D = C.POINTER(C.c_double)
+F = C.POINTER(C.c_float)
 I32 = C.POINTER(C.c_int32)
 I64 = C.POINTER(C.c_int64)
 VP = C.c_void_p
@@ -30,76 +37,145 @@ VP = C.c_void_p
 def build(force: bool = False) -> str:
     newest = max(os.path.getmtime(os.path.join(_HERE, s)) for s in ("splatct_oracle.cpp", "fixtures_oracle.cpp"))
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < newest:
-        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+        subprocess.run(["make", "-s", "-C", _HERE, "liborc.so"], check=True)
     return _LIB_PATH
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            build()
-        L = C.CDLL(_LIB_PATH)
-        sig = {
-            "orc_last_error": (C.c_char_p, []),
-            "orc_set_threads": (None, [C.c_int]),
-            "orc_max_threads": (C.c_int, []),
-            "orc_rng_new": (VP, [C.c_uint64]),
-            "orc_rng_free": (None, [VP]),
-            "orc_rng_uniform": (C.c_double, [VP, C.c_double, C.c_double]),
-            "orc_rng_normal": (C.c_double, [VP]),
-            "orc_random_cloud": (None, [VP, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double, D, D, D, D]),
-            "orc_kernel_to_raw": (None, [C.c_int, C.c_double, D, D, D, D, D, D]),
-            "orc_activate": (None, [C.c_int, C.c_double, D, D, D, D]),
-            "orc_random_image": (None, [VP, C.c_int, C.c_double, C.c_double, D]),
-            "orc_view_transform": (None, [D, I32, C.c_double, D, D]),
-            "orc_detector": (None, [D, I32, D]),
-            "orc_local_jacobian": (C.c_int, [D, I32, D, D]),
-            "orc_ray_space_point": (None, [D, I32, D, D]),
-            "orc_pixel_ray": (None, [D, I32, C.c_double, C.c_int, C.c_int, D, D]),
-            "orc_covariance": (None, [C.c_int, C.c_double, D, D, D, D, C.c_int, D]),
-            "orc_density_at": (C.c_double, [C.c_int, C.c_double, D, D, D, D, D]),
-            "orc_ray_march_density": (C.c_double, [C.c_int, C.c_double, D, D, D, D, D, D, C.c_double]),
-            "orc_normalize_rotations": (None, [C.c_int, D]),
-            "orc_cov_param_grads": (None, [C.c_int, C.c_double, D, D, D, D, C.c_int, D, D, D]),
-            "orc_project_kernel": (C.c_int, [C.c_int, C.c_double, D, D, D, D, C.c_int, D, I32, C.c_double, D, D]),
-            "orc_render": (VP, [C.c_int, C.c_double, D, D, D, D, D, I32, C.c_double, D]),
-            "orc_render_free": (None, [VP]),
-            "orc_render_image": (None, [VP, D]),
-            "orc_render_n_visible": (C.c_int, [VP]),
-            "orc_render_n_pairs": (C.c_int64, [VP]),
-            "orc_render_tile_lists": (None, [VP, I64, I32]),
-            "orc_render_visible": (None, [VP, I32, D]),
-            "orc_render_backward": (C.c_int, [VP, C.c_int, C.c_double, D, D, D, D, D, I32, C.c_double, D, D,
-                                              D, D, D, D, D, I32, D]),
-            "orc_raster_chain_from_stats": (None, [C.c_int, C.c_double, D, D, D, D, D, I32, C.c_double, D,
-                                                   C.c_int, I32, D, D, D, D, D]),
-            "orc_grid_for_extent": (None, [D, D, I32, D, D]),
-            "orc_voxelize": (None, [C.c_int, C.c_double, D, D, D, D, I32, D, D, C.c_double, D]),
-            "orc_voxelize_backward": (C.c_int, [C.c_int, C.c_double, D, D, D, D, I32, D, D, C.c_double, D,
-                                                D, D, D, D]),
-            "orc_voxel_bins": (C.c_int64, [C.c_int, C.c_double, D, D, D, D, I32, D, D, C.c_double, I64, I32]),
-            "orc_random_subvolume_spec": (None, [VP, D, D, D, C.c_int, D]),
-            "orc_tv3d": (C.c_int, [I32, D, D, D]),
-            "orc_l1": (C.c_int, [C.c_int, D, D, D, D]),
-            "orc_dssim": (C.c_int, [C.c_int, C.c_int, D, D, D, D]),
-            "orc_adaptive_control": (VP, [VP, C.c_int, C.c_double, C.POINTER(D), D, I32, D, C.c_double,
-                                          C.c_double, C.c_double, C.c_double, D]),
-            "orc_ac_size": (C.c_int, [VP]),
-            "orc_ac_counts": (None, [VP, C.POINTER(C.c_int)]),
-            "orc_ac_get": (None, [VP, C.c_int, D]),
-            "orc_ac_free": (None, [VP]),
-            "orc_normal_draws": (None, [VP, C.c_int, D]),
-            "orc_lr_at": (C.c_double, [C.c_double, C.c_double, C.c_int, C.c_int]),
-            "orc_adam_step": (None, [C.c_int64, D, D, D, D, C.c_double, C.c_int, C.c_double, C.c_double,
-                                     C.c_double]),
-        }
-        for name, (res, args) in sig.items():
-            f = getattr(L, name)
+def build_ref() -> str | None:
+    """Compile the reference's own sources into oracle/_ref (only where
+    /root/reference exists; elsewhere the prebuilt .so, if shipped, is used)."""
+    if os.path.isdir(_REF_SRC):
+        subprocess.run(["make", "-s", "-C", _HERE, "ref"], check=True)
+    return _REF_LIB_PATH if os.path.exists(_REF_LIB_PATH) else None
+
+
+def ref_available() -> bool:
+    return os.path.exists(_REF_LIB_PATH)
+
+
+_SIG = {
+    "orc_last_error": (C.c_char_p, []),
+    "orc_set_threads": (None, [C.c_int]),
+    "orc_max_threads": (C.c_int, []),
+    "orc_rng_new": (VP, [C.c_uint64]),
+    "orc_rng_free": (None, [VP]),
+    "orc_rng_uniform": (C.c_double, [VP, C.c_double, C.c_double]),
+    "orc_rng_normal": (C.c_double, [VP]),
+    "orc_random_cloud": (None, [VP, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double, D, D, D, D]),
+    "orc_kernel_to_raw": (None, [C.c_int, C.c_double, D, D, D, D, D, D]),
+    "orc_activate": (None, [C.c_int, C.c_double, D, D, D, D]),
+    "orc_random_image": (None, [VP, C.c_int, C.c_double, C.c_double, D]),
+    "orc_view_transform": (None, [D, I32, C.c_double, D, D]),
+    "orc_detector": (None, [D, I32, D]),
+    "orc_local_jacobian": (C.c_int, [D, I32, D, D]),
+    "orc_ray_space_point": (None, [D, I32, D, D]),
+    "orc_pixel_ray": (None, [D, I32, C.c_double, C.c_int, C.c_int, D, D]),
+    "orc_covariance": (None, [C.c_int, C.c_double, D, D, D, D, C.c_int, D]),
+    "orc_density_at": (C.c_double, [C.c_int, C.c_double, D, D, D, D, D]),
+    "orc_ray_march_density": (C.c_double, [C.c_int, C.c_double, D, D, D, D, D, D, C.c_double]),
+    "orc_normalize_rotations": (None, [C.c_int, D]),
+    "orc_cov_param_grads": (None, [C.c_int, C.c_double, D, D, D, D, C.c_int, D, D, D]),
+    "orc_project_kernel": (C.c_int, [C.c_int, C.c_double, D, D, D, D, C.c_int, D, I32, C.c_double, D, D]),
+    "orc_render": (VP, [C.c_int, C.c_double, D, D, D, D, D, I32, C.c_double, D]),
+    "orc_render_free": (None, [VP]),
+    "orc_render_image": (None, [VP, D]),
+    "orc_render_n_visible": (C.c_int, [VP]),
+    "orc_render_n_pairs": (C.c_int64, [VP]),
+    "orc_render_tile_lists": (None, [VP, I64, I32]),
+    "orc_render_visible": (None, [VP, I32, D]),
+    "orc_render_backward": (C.c_int, [VP, C.c_int, C.c_double, D, D, D, D, D, I32, C.c_double, D, D,
+                                      D, D, D, D, D, I32, D]),
+    "orc_raster_chain_from_stats": (None, [C.c_int, C.c_double, D, D, D, D, D, I32, C.c_double, D,
+                                           C.c_int, I32, D, D, D, D, D]),
+    "orc_grid_for_extent": (None, [D, D, I32, D, D]),
+    "orc_voxelize": (None, [C.c_int, C.c_double, D, D, D, D, I32, D, D, C.c_double, D]),
+    "orc_voxelize_backward": (C.c_int, [C.c_int, C.c_double, D, D, D, D, I32, D, D, C.c_double, D,
+                                        D, D, D, D]),
+    "orc_voxel_bins": (C.c_int64, [C.c_int, C.c_double, D, D, D, D, I32, D, D, C.c_double, I64, I32]),
+    "orc_random_subvolume_spec": (None, [VP, D, D, D, C.c_int, D]),
+    "orc_tv3d": (C.c_int, [I32, D, D, D]),
+    "orc_l1": (C.c_int, [C.c_int, D, D, D, D]),
+    "orc_dssim": (C.c_int, [C.c_int, C.c_int, D, D, D, D]),
+    "orc_adaptive_control": (VP, [VP, C.c_int, C.c_double, C.POINTER(D), D, I32, D, C.c_double,
+                                  C.c_double, C.c_double, C.c_double, D]),
+    "orc_ac_size": (C.c_int, [VP]),
+    "orc_ac_counts": (None, [VP, C.POINTER(C.c_int)]),
+    "orc_ac_get": (None, [VP, C.c_int, D]),
+    "orc_ac_stats": (None, [VP, D, I32, D]),
+    "orc_ac_free": (None, [VP]),
+    "orc_normal_draws": (None, [VP, C.c_int, D]),
+    "orc_lr_at": (C.c_double, [C.c_double, C.c_double, C.c_int, C.c_int]),
+    "orc_adam_step": (None, [C.c_int64, D, D, D, D, C.c_double, C.c_int, C.c_double, C.c_double,
+                             C.c_double]),
+    # fixtures (fixtures_oracle.cpp / simulator.cpp, fdk.cpp)
+    "orc_phantom": (None, [C.c_int, D, I32, D, D, F]),
+    "orc_shepp_logan": (C.c_int, [D, C.c_int]),
+    "orc_sample_trilinear": (C.c_double, [F, I32, D, D, D]),
+    "orc_project_volume": (C.c_int, [F, I32, D, D, D, I32, C.c_double, C.c_double, D]),
+    "orc_view_seed": (C.c_uint64, [C.c_uint64, C.c_int]),
+    "orc_add_noise": (C.c_int, [F, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, D]),
+    "orc_fdk": (C.c_int, [F, C.c_int, D, I32, D, I32, D, D, C.c_int, D]),
+    "orc_nn_distances": (None, [C.c_int, D, D]),
+    "orc_sample_init_cloud": (C.c_int, [VP, F, I32, D, D, C.c_int, C.c_double, C.c_double, C.c_double,
+                                        D, D, D, D]),
+    # reference-only: the training loop and the I/O containers
+    "orc_train": (VP, [C.c_int, C.c_double, D, D, D, D, D, I32, C.c_int, D, D, D, I32, C.c_uint64, D,
+                       C.c_int, C.POINTER(C.c_int)]),
+    "orc_save_cloud": (C.c_int, [C.c_char_p, C.c_int, C.c_double, D, D, D, D]),
+    "orc_load_cloud": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_int), D, D, D, D, D]),
+    "orc_write_volume": (C.c_int, [C.c_char_p, I32, D, D, D]),
+    "orc_read_volume": (C.c_int, [C.c_char_p, C.c_int64, I32, D, D, D]),
+    "orc_write_image": (C.c_int, [C.c_char_p, C.c_int, C.c_int, D]),
+    "orc_read_image": (C.c_int, [C.c_char_p, C.c_int64, I32, D]),
+}
+
+
+def _load(kind: str):
+    if kind not in _libs:
+        if kind == "reference":
+            path = _REF_LIB_PATH
+            if not os.path.exists(path):
+                build_ref()
+            if not os.path.exists(path):
+                raise OracleError("reference library oracle/_ref/libsplatct_ref.so is not built")
+        elif kind == "port":
+            path = _LIB_PATH
+            if not os.path.exists(path):
+                build()
+        else:
+            raise ValueError(kind)
+        L = C.CDLL(path)
+        for name, (res, args) in _SIG.items():
+            f = getattr(L, name, None)
+            if f is None:
+                continue
             f.restype = res
             f.argtypes = args
-        _lib = L
-    return _lib
+        _libs[kind] = L
+    return _libs[kind]
+
+
+def lib():
+    """The active oracle library: "port" (the FP64 restatement, default) or
+    "reference" (the reference's own sources, oracle/_ref)."""
+    return _load(_active)
+
+
+def active() -> str:
+    return _active
+
+
+@contextlib.contextmanager
+def using(kind: str):
+    """Run oracle calls inside the block against `kind` ("port" | "reference")."""
+    global _active
+    prev = _active
+    _load(kind)
+    _active = kind
+    try:
+        yield
+    finally:
+        _active = prev
 
 
 def _d(a):
@@ -274,11 +350,12 @@ class Rng:
     """std::mt19937_64 with libstdc++ distributions (the reference tests' RNG)."""
 
     def __init__(self, seed: int):
-        self._h = lib().orc_rng_new(seed)
+        self._L = lib()
+        self._h = self._L.orc_rng_new(seed)
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib is not None:
-            _lib.orc_rng_free(self._h)
+        if getattr(self, "_h", None):
+            self._L.orc_rng_free(self._h)
             self._h = None
 
     def uniform(self, lo=0.0, hi=1.0):
@@ -386,42 +463,43 @@ class Rendered:
 
     def __init__(self, handle, w, h):
         self._h = handle
+        self._L = lib()
         self.width, self.height = w, h
         self.tiles_x = (w + 15) // 16
         self.tiles_y = (h + 15) // 16
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib is not None:
-            _lib.orc_render_free(self._h)
+        if getattr(self, "_h", None):
+            self._L.orc_render_free(self._h)
             self._h = None
 
     @property
     def image(self):
         out = np.zeros(self.width * self.height)
-        lib().orc_render_image(self._h, _d(out))
+        self._L.orc_render_image(self._h, _d(out))
         return out.reshape(self.height, self.width)
 
     @property
     def n_visible(self):
-        return lib().orc_render_n_visible(self._h)
+        return self._L.orc_render_n_visible(self._h)
 
     @property
     def n_pairs(self):
-        return lib().orc_render_n_pairs(self._h)
+        return self._L.orc_render_n_pairs(self._h)
 
     def tile_lists(self):
         """(offsets[T+1] int64, kernel_idx[pairs] int32), lists in kernel indices."""
         T = self.tiles_x * self.tiles_y
         off = np.zeros(T + 1, dtype=np.int64)
         idx = np.zeros(max(self.n_pairs, 1), dtype=np.int32)
-        lib().orc_render_tile_lists(self._h, _i64(off), _i32(idx))
+        self._L.orc_render_tile_lists(self._h, _i64(off), _i32(idx))
         return off, idx[: self.n_pairs]
 
     def visible(self):
         n = self.n_visible
         k = np.zeros(max(n, 1), dtype=np.int32)
         rec = np.zeros(max(n, 1) * 11)
-        lib().orc_render_visible(self._h, _i32(k), _d(rec))
+        self._L.orc_render_visible(self._h, _i32(k), _d(rec))
         return k[:n], rec.reshape(-1, 11)[:n]
 
 
@@ -443,7 +521,7 @@ def render_backward(cloud: Cloud, cfg: ScannerConfig, theta: float, fwd: Rendere
         raise DimMismatch("render_backward: upstream gradient dims mismatch")
     st = (None, None, None) if stats is None else (_d(stats.grad2d_norm_accum), _i32(stats.grad_count),
                                                      _d(stats.grad3d_accum))
-    _check(lib().orc_render_backward(fwd._h, *cloud._args(), _d(g), _i32(r), theta, _d(opts._arr()), _d(dL),
+    _check(fwd._L.orc_render_backward(fwd._h, *cloud._args(), _d(g), _i32(r), theta, _d(opts._arr()), _d(dL),
                                      *grads._args(), *st))
 
 
@@ -604,3 +682,122 @@ def set_threads(n: int):
 
 def max_threads() -> int:
     return lib().orc_max_threads()
+
+
+# ----------------------------------------------------------------- reference-only entry points
+class _RefIO:
+    """The reference's container readers/writers (io.cpp:18-213), from oracle/_ref."""
+
+    def __init__(self):
+        self.L = _load("reference")
+
+    def _ok(self, rc):
+        if rc != 0:
+            raise OracleError(self.L.orc_last_error().decode())
+
+    def save_cloud(self, c: "Cloud", path: str):
+        self._ok(self.L.orc_save_cloud(path.encode(), *c._args()))
+
+    def load_cloud(self, path: str) -> "Cloud":
+        m, s = C.c_int(0), C.c_double(0.0)
+        z = np.zeros(1)
+        self._ok(self.L.orc_load_cloud(path.encode(), 0, C.byref(m), C.byref(s), _d(z), _d(z), _d(z), _d(z)))
+        n = m.value
+        c = Cloud(s.value, np.zeros(n), np.zeros(3 * n), np.zeros(3 * n), np.zeros(4 * n))
+        self._ok(self.L.orc_load_cloud(path.encode(), n, C.byref(m), C.byref(s), *[_d(a) for a in
+                                        (c.rho_raw, c.pos, c.scale_raw, c.rot)]))
+        return c
+
+    def write_image(self, img, path: str):
+        img = np.ascontiguousarray(img, dtype=np.float64)
+        self._ok(self.L.orc_write_image(path.encode(), img.shape[1], img.shape[0], _d(img)))
+
+    def read_image(self, path: str) -> np.ndarray:
+        wh = np.zeros(2, np.int32)
+        z = np.zeros(1)
+        self._ok(self.L.orc_read_image(path.encode(), 0, _i32(wh), _d(z)))
+        out = np.zeros(int(wh[0]) * int(wh[1]))
+        self._ok(self.L.orc_read_image(path.encode(), out.size, _i32(wh), _d(out)))
+        return out.reshape(int(wh[1]), int(wh[0]))
+
+    def write_volume(self, vol, grid: "GridSpec", path: str):
+        vol = np.ascontiguousarray(vol, dtype=np.float64)
+        self._ok(self.L.orc_write_volume(path.encode(), *grid._args(), _d(vol)))
+
+    def read_volume(self, path: str):
+        dims = np.zeros(3, np.int32)
+        o, s, z = np.zeros(3), np.zeros(3), np.zeros(1)
+        self._ok(self.L.orc_read_volume(path.encode(), 0, _i32(dims), _d(o), _d(s), _d(z)))
+        out = np.zeros(int(np.prod(dims)))
+        self._ok(self.L.orc_read_volume(path.encode(), out.size, _i32(dims), _d(o), _d(s), _d(out)))
+        g = GridSpec(tuple(int(d) for d in dims), tuple(o), tuple(s))
+        return out.reshape(g.shape_zyx), g
+
+
+def reference_io() -> _RefIO:
+    return _RefIO()
+
+
+def ac_stats(h, m):
+    out = Stats.zeros(m)
+    lib().orc_ac_stats(h, _d(out.grad2d_norm_accum), _i32(out.grad_count), _d(out.grad3d_accum))
+    return out
+
+
+@dataclass
+class TrainConfig:  # trainer.hpp:11-45 (fields the hot-path train loop uses)
+    iters: int = 30
+    lr_position: float = 0.0002
+    lr_density: float = 0.01
+    lr_scale: float = 0.005
+    lr_rotation: float = 0.001
+    lr_final_ratio: float = 0.1
+    lambda_ssim: float = 0.25
+    lambda_tv: float = 0.05
+    tv_grid_dim: int = 32
+    adaptive_start: int = 500
+    adaptive_end: int = 15000
+    densify_interval: int = 100
+    densify_grad_threshold: float = 0.00005
+    prune_density_threshold: float = 0.005
+    split_scale_threshold_frac: float = 0.01
+    split_factor: float = 1.6
+    mode: int = 0
+    output_dims: tuple = (64, 64, 64)
+    history_interval: int = 10
+    seed: int = 0
+
+
+def train_reference(cloud: Cloud, cfg: ScannerConfig, angles, images, tc: TrainConfig):
+    """The reference's own `train` (trainer.cpp:232-345), unmodified, from
+    oracle/_ref. images [V][H][W] (un-normalised projections). Returns
+    (Cloud, adam dict, Stats, history [n][6] = iter, l1, dssim, tv, total, kernels)."""
+    L = _load("reference")
+    g, r = cfg._geo()
+    imgs = np.ascontiguousarray(images, dtype=np.float64)
+    ang = np.ascontiguousarray(angles, dtype=np.float64)
+    cd = np.array([tc.lr_position, tc.lr_density, tc.lr_scale, tc.lr_rotation, tc.lr_final_ratio, tc.lambda_ssim,
+                   tc.lambda_tv, tc.densify_grad_threshold, tc.prune_density_threshold,
+                   tc.split_scale_threshold_frac, tc.split_factor], dtype=np.float64)
+    ci = np.array([tc.iters, tc.tv_grid_dim, tc.adaptive_start, tc.adaptive_end, tc.densify_interval, tc.mode,
+                   *tc.output_dims, tc.history_interval], dtype=np.int32)
+    max_h = tc.iters + 1
+    hist = np.zeros(6 * max_h)
+    nh = C.c_int(0)
+    h = L.orc_train(*cloud._args(), _d(g), _i32(r), len(ang), _d(ang), _d(imgs), _d(cd), _i32(ci), tc.seed,
+                    _d(hist), max_h, C.byref(nh))
+    if not h:
+        raise OracleError(L.orc_last_error().decode())
+    try:
+        n = L.orc_ac_size(h)
+        strides = (1, 3, 3, 4, 1, 1, 3, 3, 3, 3, 4, 4)
+        out = []
+        for a in range(12):
+            buf = np.zeros(max(1, strides[a] * n))
+            L.orc_ac_get(h, a, _d(buf))
+            out.append(buf[: strides[a] * n])
+        st = Stats.zeros(n)
+        L.orc_ac_stats(h, _d(st.grad2d_norm_accum), _i32(st.grad_count), _d(st.grad3d_accum))
+    finally:
+        L.orc_ac_free(h)
+    return Cloud(cloud.s_min, *out[:4]), dict(zip(ADAM_KEYS, out[4:])), st, hist[: 6 * nh.value].reshape(-1, 6)

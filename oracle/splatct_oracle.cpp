@@ -1573,6 +1573,16 @@ void orc_ac_get(void* h, int a, double* out) {
   auto* r = static_cast<ACResult*>(h);
   std::memcpy(out, r->a[a].data(), r->a[a].size() * sizeof(double));
 }
+// Statistics the cloud carries after adaptive control: remove_kernels compacts
+// them and add_kernel appends zeros (gaussian_cloud.cpp:48-110), then
+// reset_grad_stats (gaussian_cloud.cpp:119-123, called at trainer.cpp:228)
+// zeroes all three arrays.
+void orc_ac_stats(void* h, double* norm_acc, int32_t* count, double* g3d) {
+  const size_t n = static_cast<ACResult*>(h)->a[0].size();
+  std::fill(norm_acc, norm_acc + n, 0.0);
+  std::fill(count, count + n, 0);
+  std::fill(g3d, g3d + 3 * n, 0.0);
+}
 void orc_ac_free(void* h) { delete static_cast<ACResult*>(h); }
 // n consecutive draws of one std::normal_distribution(0,1) object
 void orc_normal_draws(void* rp, int n, double* out) {

@@ -12,10 +12,15 @@ def manifest():
         return json.load(f)
 
 
-def cloud_arrays():
-    """(s_min, rho_raw, pos, scale_raw, rot) fp32 from cloud.ckpt."""
+RASTER_SETS = ["rectified", "biased_frozen_nolp", "narrow_eps0", "narrow_eps01"]
+
+
+def cloud_arrays(case: str = "rectified"):
+    """(s_min, rho_raw, pos, scale_raw, rot) fp32 from the case's cloud
+    (cloud_narrow.ckpt for the narrow-kernel sets, else cloud.ckpt)."""
     from paper_2405_20693_b200 import io as sio
-    c = sio.load_cloud(os.path.join(GOLDEN, "cloud.ckpt"), device="cpu")
+    narrow = case in manifest().get("narrow_sets", [])
+    c = sio.load_cloud(os.path.join(GOLDEN, "cloud_narrow.ckpt" if narrow else "cloud.ckpt"), device="cpu")
     return (c.s_min,) + tuple(getattr(c, k).numpy() for k in ("rho_raw", "pos", "scale_raw", "rot"))
 
 

@@ -1,17 +1,22 @@
 """Generate the committed golden fixtures (SURVEY.md §8c "Golden vectors").
 
-The reference ships no golden vectors and cannot be built here, so these are
-produced by the FP64 oracle restatement (oracle/) AFTER it passes the
-reference's own known-answer and property tests (tests/test_oracle_kats.py).
-They pin the engine and guard the oracle against drift: tests/test_golden_cpu.py
-re-runs the oracle against them, tests/test_gpu_golden.py runs the engine.
+The reference ships no golden vectors, so these are OUTPUTS OF THE REFERENCE
+ITSELF: its unmodified sources (/root/reference/proj/core/src) compiled into
+oracle/_ref/libsplatct_ref.so by `make -C oracle ref` (oracle/ref_capi.cpp over
+the Eigen / nlohmann::json / libpng build shims in oracle/ref_shim/), called
+through the same orc_* ABI as the FP64 restatement (oracle.using("reference")).
+The containers are written by the reference's own io.cpp writers
+(save_cloud / write_image / write_volume). tests/test_golden_cpu.py checks the
+FP64 restatement (oracle/splatct_oracle.cpp) against them, and
+tests/test_gpu_golden.py runs the engine against them.
 
 Containers follow the reference formats (io.cpp): the cloud is a `.ckpt`
 (io.cpp:171-182), images `.img` (:106-117), volumes `.vol` (:72-83), all fp32
 little-endian behind a one-line JSON header; the integer binning (tile lists
 per view, voxel brick lists) and the fp64 gradients are `.npz`.
 
-Run from the repo root:  python tests/golden/make_golden.py
+Run from the repo root (needs /root/reference or a prebuilt oracle/_ref):
+    python tests/golden/make_golden.py
 """
 import json
 import os
@@ -34,6 +39,14 @@ OPTION_SETS = {
     "rectified": dict(mode=0),
     "biased_frozen_nolp": dict(mode=1, lowpass_eps_px=0.0, freeze_jacobian=True),
 }
+# Narrow-kernel case (rasterizer.cpp:44-50,151 with lowpass_eps_px = 0 / 0.1,
+# test_rasterizer.cpp:49,186): sub-pixel kernels, projected sigma 0.03-0.3 px,
+# where exp(-1/2 d^T Q d) falls by orders of magnitude between neighbouring pixels.
+NARROW = dict(seed=43, m=400, pos_radius=0.6, scale_min=0.0008, scale_max=0.012)
+NARROW_SETS = {
+    "narrow_eps0": dict(mode=0, lowpass_eps_px=0.0),
+    "narrow_eps01": dict(mode=0, lowpass_eps_px=0.1),
+}
 # Voxel case: non-cubic grid with dims not multiples of 8 and an off-centre origin.
 VOXEL = dict(lo=(-1.0, -0.9, -0.8), hi=(1.0, 0.9, 0.7), dims=(21, 18, 13), upstream_seed=3)
 
@@ -45,7 +58,7 @@ def f32_cloud(c):
 
 def raster_case(cloud, opt_name):
     cfg = O.ScannerConfig(detector_res_px=RASTER["res"])
-    opts = O.RasterOptions(**OPTION_SETS[opt_name])
+    opts = O.RasterOptions(**{**OPTION_SETS, **NARROW_SETS}[opt_name])
     w, h = RASTER["res"]
     rng = O.Rng(RASTER["upstream_seed"])
     images, ups, offs, idxs = [], [], [], []
@@ -76,22 +89,27 @@ def voxel_case(cloud):
 
 
 def main():
-    import torch  # noqa: F401  (io.py builds GaussianCloud on the CPU device)
-    from paper_2405_20693_b200 import io as sio
-    from paper_2405_20693_b200.engine import GaussianCloud, GridSpec
+    with O.using("reference"):
+        _main()
+
+
+def _main():
+    rio = O.reference_io()
 
     c = f32_cloud(O.random_cloud(O.Rng(RASTER["seed"]), RASTER["m"], RASTER["pos_radius"], RASTER["scale_min"],
                                  RASTER["scale_max"]))
-    sio.save_cloud(GaussianCloud(c.s_min, c.rho_raw, c.pos, c.scale_raw, c.rot, device="cpu"),
-                   os.path.join(HERE, "cloud.ckpt"))
-    manifest = {"generator": "tests/golden/make_golden.py (oracle/ FP64 restatement)", "raster": RASTER,
-                "option_sets": OPTION_SETS, "voxel": VOXEL, "cases": {}}
-    for name in OPTION_SETS:
-        r = raster_case(c, name)
+    rio.save_cloud(c, os.path.join(HERE, "cloud.ckpt"))
+    cn = f32_cloud(O.random_cloud(O.Rng(NARROW["seed"]), NARROW["m"], NARROW["pos_radius"], NARROW["scale_min"],
+                                  NARROW["scale_max"]))
+    rio.save_cloud(cn, os.path.join(HERE, "cloud_narrow.ckpt"))
+    manifest = {"generator": "tests/golden/make_golden.py (the reference's own sources, oracle/_ref)",
+                "raster": RASTER, "option_sets": {**OPTION_SETS, **NARROW_SETS}, "narrow": NARROW,
+                "narrow_sets": list(NARROW_SETS), "voxel": VOXEL, "cases": {}}
+    for name in list(OPTION_SETS) + list(NARROW_SETS):
+        r = raster_case(cn if name in NARROW_SETS else c, name)
         for v in range(len(RASTER["thetas"])):
-            sio.write_image(r["images"][v], os.path.join(HERE, f"raster_{name}_view{v}.img"),
-                            {"theta_rad": RASTER["thetas"][v]})
-        sio.write_image(r["upstream"].reshape(-1, RASTER["res"][0]), os.path.join(HERE, f"raster_{name}_dL.img"))
+            rio.write_image(r["images"][v], os.path.join(HERE, f"raster_{name}_view{v}.img"))
+        rio.write_image(r["upstream"].reshape(-1, RASTER["res"][0]), os.path.join(HERE, f"raster_{name}_dL.img"))
         g, st = r["grads"], r["stats"]
         np.savez_compressed(
             os.path.join(HERE, f"raster_{name}.npz"),
@@ -102,10 +120,8 @@ def main():
         manifest["cases"][name] = {"pairs_per_view": [int(len(i)) for i in r["idx"]]}
     vx = voxel_case(c)
     gr = vx["grid"]
-    sio.write_volume(vx["volume"].astype(np.float32),
-                     GridSpec(gr.dims, gr.origin_mm, gr.spacing_mm), os.path.join(HERE, "voxel_volume.vol"))
-    sio.write_volume(vx["upstream"].astype(np.float32),
-                     GridSpec(gr.dims, gr.origin_mm, gr.spacing_mm), os.path.join(HERE, "voxel_dL.vol"))
+    rio.write_volume(vx["volume"], gr, os.path.join(HERE, "voxel_volume.vol"))
+    rio.write_volume(vx["upstream"], gr, os.path.join(HERE, "voxel_dL.vol"))
     g = vx["grads"]
     np.savez_compressed(os.path.join(HERE, "voxel.npz"), offsets=vx["offsets"], idx=vx["idx"],
                         g_rho_raw=g.rho_raw, g_pos=g.pos, g_scale_raw=g.scale_raw, g_rot=g.rot)

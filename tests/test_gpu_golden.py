@@ -1,5 +1,6 @@
 """The engine (through the C-ABI) against the committed golden fixtures
-(tests/golden/, FP64 oracle outputs in the reference container formats):
+(tests/golden/, outputs of the reference's own sources — oracle/_ref — in the
+reference container formats, written by its io.cpp):
 tile lists and voxel brick lists bit-exact, images / volumes <= 1e-4 rel L2,
 gradients and adaptive statistics <= 1e-3 (BASELINE.json parity bars), in both
 reduction modes."""
@@ -15,18 +16,18 @@ from tests._helpers import rel_l2  # noqa: E402
 IMG_TOL, GRAD_TOL = 1e-4, 1e-3
 
 
-def _setup():
+def _setup(case="rectified"):
     if not torch.cuda.is_available():
         pytest.skip("needs CUDA")
     import paper_2405_20693_b200 as P
-    s_min, *arrs = G.cloud_arrays()
+    s_min, *arrs = G.cloud_arrays(case)
     return P, P.GaussianCloud(s_min, *arrs)
 
 
 @pytest.mark.parametrize("deterministic", [True, False])
-@pytest.mark.parametrize("name", ["rectified", "biased_frozen_nolp"])
+@pytest.mark.parametrize("name", G.RASTER_SETS)
 def test_engine_matches_raster_golden(name, deterministic):
-    P, c = _setup()
+    P, c = _setup(name)
     eng = P.Engine(0, deterministic=deterministic)
     man, imgs, dL, z = G.raster(name)
     w, h = man["raster"]["res"]

@@ -2,7 +2,10 @@
 and property test the reference ships for the hot path. The reference has no
 golden vectors; these are its own tests re-expressed in pytest,
 on the same std::mt19937_64 scenes (file:line cited per test).
-CPU only — no GPU needed."""
+Every test runs twice: against the FP64 restatement ("port") and against the
+reference's own sources compiled into oracle/_ref ("reference") — the latter
+shows the build shims (oracle/ref_shim/) reproduce the reference's own test
+verdicts. CPU only — no GPU needed."""
 import math
 
 import numpy as np
@@ -10,6 +13,14 @@ import pytest
 
 from oracle import oracle as O
 from tests._helpers import finite_difference_check
+
+
+@pytest.fixture(autouse=True, params=["port", "reference"])
+def oracle_kind(request):
+    if request.param == "reference" and not O.ref_available():
+        pytest.skip("oracle/_ref (the compiled reference) not built")
+    with O.using(request.param):
+        yield request.param
 
 
 def single_kernel_cloud(rho, p, s, q=(1.0, 0.0, 0.0, 0.0), s_min=2e-4):
