@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -100,6 +101,16 @@ int stage_buf(Ctx* c, int slot, size_t bytes, void** p) {
   return SCT_OK;
 }
 
+// Staging slots are (re)allocated in `stream` order from the stream-ordered
+// pool; before another stream (the copy stream) touches them, it must be
+// ordered after those allocations (and after any cudaFreeAsync of the slot's
+// previous block).
+int stage_publish(Ctx* c, cudaStream_t other) {
+  SCT_CUDA_TRY(cudaEventRecord(c->ev_stage, c->stream));
+  SCT_CUDA_TRY(cudaStreamWaitEvent(other, c->ev_stage, 0));
+  return SCT_OK;
+}
+
 int ensure_cub_tmp(Ctx* c, size_t bytes) {
   if (bytes <= c->cub_tmp_bytes) return SCT_OK;
   if (c->cub_tmp) cudaFreeAsync(c->cub_tmp, c->stream);
@@ -116,9 +127,21 @@ static int bits_for(uint64_t n) {  // smallest b with 2^b >= n (n >= 1)
   return b;
 }
 
-// exclusive scan of count[0..n] (count[n] == 0) into offset[0..n]; returns offset[n]
+// exclusive scan of count[0..n] (count[n] == 0) into offset[0..n]; returns offset[n].
+// The total is first summed in int64 (cub Reduce into a 64-bit output): an
+// int32 total between 2^31 and 2^32 + 2^31 would wrap to a plausible value.
 static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t* total) {
   SCT_CUDA_TRY(cudaMemsetAsync(count + n, 0, sizeof(int32_t), c->stream));
+  {
+    long long* d_sum = c->sum64;
+    size_t tmp = 0;
+    SCT_CUDA_TRY(cub::DeviceReduce::Sum(nullptr, tmp, count, d_sum, n + 1, c->stream));
+    SCT_TRY(ensure_cub_tmp(c, tmp));
+    tmp = c->cub_tmp_bytes;
+    SCT_CUDA_TRY(cub::DeviceReduce::Sum(c->cub_tmp, tmp, count, d_sum, n + 1, c->stream));
+    SCT_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(c->pinned_count) + 64, d_sum, sizeof(long long),
+                                 cudaMemcpyDeviceToHost, c->stream));
+  }
   size_t tmp = 0;
   SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, offset, n + 1, c->stream));
   SCT_TRY(ensure_cub_tmp(c, tmp));
@@ -128,10 +151,12 @@ static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64
     SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, offset, n + 1, c->stream));
   }
   int32_t t = 0;
+  long long t64 = 0;
   SCT_CUDA_TRY(cudaMemcpyAsync(c->pinned_count, offset + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
   std::memcpy(&t, c->pinned_count, sizeof(int32_t));
-  if (t < 0) {
+  std::memcpy(&t64, reinterpret_cast<char*>(c->pinned_count) + 64, sizeof(long long));
+  if (t64 > INT32_MAX || t < 0) {
     set_error("DataError: more than 2^31-1 (tile, kernel) pairs in one call; split the views into batches");
     return SCT_ERR_DATA;
   }
@@ -334,7 +359,7 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
       cudaGetLastError();
     }
   }
-  if (cudaMallocHost((void**)&c->pinned_count, 64) != cudaSuccess ||
+  if (cudaMallocHost((void**)&c->pinned_count, 128) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
@@ -346,12 +371,13 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
     cudaEventCreateWithFlags(&c->ev_copy[a], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_stage, cudaEventDisableTiming);
   // unit signal words: 3 flag arrays, 2 counter arrays, the error word
   // (device memory: kernel-side polls of mapped host words cost a PCIe read
   // each, measured 50x slower for K4)
   char* u = nullptr;
-  if (cudaMalloc((void**)&u, 6 * Ctx::kMaxUnits * sizeof(uint32_t)) != cudaSuccess ||
-      cudaMemset(u, 0, 6 * Ctx::kMaxUnits * sizeof(uint32_t)) != cudaSuccess) {
+  const size_t words = (6 * Ctx::kMaxUnits * sizeof(uint32_t) + 15) & ~size_t(15);
+  if (cudaMalloc((void**)&u, words + 16) != cudaSuccess || cudaMemset(u, 0, words + 16) != cudaSuccess) {
     sct_ctx_destroy(c);
     set_error("CUDA error: context signal allocation failed");
     return SCT_ERR_CUDA;
@@ -359,6 +385,7 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
   c->unit_flags = reinterpret_cast<uint32_t*>(u);
   c->unit_done = reinterpret_cast<int*>(c->unit_flags + 3 * Ctx::kMaxUnits);
   c->unit_err = c->unit_done + 2 * Ctx::kMaxUnits;
+  c->sum64 = reinterpret_cast<long long*>(u + words);
   *out = c;
   return SCT_OK;
 }
@@ -378,6 +405,7 @@ int sct_ctx_destroy(sct_ctx* c) {
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_stage) cudaEventDestroy(c->ev_stage);
   if (c->unit_flags) cudaFree(c->unit_flags);
   delete c;
   return SCT_OK;
@@ -928,6 +956,7 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
   const size_t px = (size_t)scanner->det_res_px[0] * scanner->det_res_px[1];
   float* dimg = nullptr;
   SCT_TRY(stage_buf(c, 4, n_views * px * sizeof(float), (void**)&dimg));
+  SCT_TRY(stage_publish(c, c->copy_stream));
   // binning for all views, then one composite whose view units are copied
   // to the host (copy stream) as they complete
   int rc = sct_render_fwd(c, &d, scanner, thetas, n_views, opts, nullptr, state);
@@ -1018,6 +1047,19 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
   const size_t px = (size_t)s->det.w * s->det.h;
   float* ddl = nullptr;
   SCT_TRY(stage_buf(c, 5, s->n_views * px * sizeof(float), (void**)&ddl));
+  // every staging slot this call touches is sized here, on the main stream,
+  // and the copy stream is ordered after those allocations (stage_publish)
+  {
+    void* tmp = nullptr;
+    const int64_t na[4] = {m, 3 * m, 3 * m, 4 * m};
+    for (int a = 0; a < 4; ++a) SCT_TRY(stage_buf(c, a, na[a] * sizeof(float), &tmp));
+    for (int a = 0; a < 4; ++a) SCT_TRY(stage_buf(c, 6 + a, na[a] * sizeof(float), &tmp));
+    if (stats_host) {
+      const size_t sz[3] = {m * sizeof(float), m * sizeof(int32_t), 3 * m * sizeof(float)};
+      for (int a = 0; a < 3; ++a) SCT_TRY(stage_buf(c, 10 + a, sz[a], &tmp));
+    }
+    SCT_TRY(stage_publish(c, c->copy_stream));
+  }
   // units path: every H2D copy on the copy stream, in the order the GPU
   // needs the data — upstream-gradient unit 0 (K4 starts on it), the cloud
   // (the FP64 chain), the other units (K4 waits per unit, unit_flags[1]), the
@@ -1074,6 +1116,12 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
   int rc = units_path ? render_bwd_units(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, units, epoch,
                                          c->ev_copy[0], c->ev_copy[1])
                       : sct_render_bwd_chunked(c, s, &d, ddl, &dg, stats_host ? &dst : nullptr, chunks);
+  if (rc == SCT_OK && units_path) {
+    // a timed-out unit wait leaves the device sums incomplete: check the error
+    // word before anything is copied into the caller's accumulate buffers
+    SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    rc = check_unit_err(c);
+  }
   if (rc == SCT_OK) {
     for (int a = 0; a < 4; ++a)
       SCT_CUDA_TRY(cudaMemcpyAsync(gh[a], *gd[a], n[a] * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
@@ -1085,7 +1133,6 @@ int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, con
   SCT_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
   g_dbg.report("bwd_host");
-  if (rc == SCT_OK && units_path) rc = check_unit_err(c);
   return rc;
 }
 

@@ -217,6 +217,29 @@ __device__ __forceinline__ Run4 run4(float dx, float A, float A2, float bdy, flo
 // (a <= 1.6); narrower kernels take two 4-runs (a warp-uniform branch in K3).
 constexpr float kRun8MaxA_K3 = 1.5f;
 
+// Narrow kernels (rasterizer.cpp:44-50,151 with a small or zero low-pass:
+// projected sigma below ~0.25 px) fall by orders of magnitude between
+// neighbouring pixels, and a 4-run's recurrence can lose its peak: a pixel p
+// that matters (L(p) >= -T, 2^-T of the amplitude) has a run head with
+// L(first) >= -T - 9a - 6 sqrt(T a), which must stay above the ftz floor
+// (-190 with K3's +64 offset, T = 24; -141 with K4's +15, T = 10). That holds
+// for a = |A| <= 8.5 (K3) and <= 8.25 (K4); the default 0.3 px low-pass keeps
+// a <= 0.5 log2(e) / 0.09 = 8.01. Beyond those bounds the kernels take a
+// direct evaluation, one MUFU.EX2 per pixel (warp-uniform branch).
+constexpr float kRun4MaxA_K3 = 8.5f;
+constexpr float kRun4MaxA_K4 = 8.25f;
+
+// Direct evaluation of 8 consecutive pixels of a row for two kernels:
+// E(dx + k) = 2^(L(dx + k)), L = (A x + B dy) x + (C dy^2 + offset).
+__device__ __forceinline__ void direct8x2(float2 e[8], float2 dx, float2 A, float2 bdy, float2 cdy2o) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float2 x = __fadd2_rn(dx, make_float2((float)k, (float)k));
+    const float2 L = __ffma2_rn(x, __ffma2_rn(A, x, bdy), cdy2o);
+    e[k] = make_float2(ex2(L.x), ex2(L.y));
+  }
+}
+
 // Two kernels at once in packed FP32x2 arithmetic (FFMA2 / FMUL2 / FADD2 on
 // sm_100): element i of every float2 belongs to kernel i of the pair and is
 // computed with exactly the scalar path's operations and rounding (run4's; an
@@ -338,11 +361,14 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
         const float2 cdy2o = __ffma2_rn(__fmul2_rn(Cc, dy), dy, c64);
         const float2 dx = __ffma2_rn(neg, cx, px2);  // px0 - cx
         float2 e[8];
-        if (fabsf(A.x) <= kRun8MaxA_K3 && fabsf(A.y) <= kRun8MaxA_K3) {  // warp-uniform
+        const float amax = fmaxf(fabsf(A.x), fabsf(A.y));  // warp-uniform: one kernel pair per step
+        if (amax <= kRun8MaxA_K3) {
           run8x2(e, dx, A, A2, bdy, apb, cdy2o, K);
-        } else {
+        } else if (amax <= kRun4MaxA_K3) {
           run4x2(e, dx, A, A2, bdy, apb, cdy2o, K);
           run4x2(e + 4, __fadd2_rn(dx, make_float2(4.f, 4.f)), A, A2, bdy, apb, cdy2o, K);
+        } else {
+          direct8x2(e, dx, A, bdy, cdy2o);
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc2[k] = __ffma2_rn(amp, e[k], acc2[k]);
@@ -511,10 +537,24 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
         // and d = F_c - F_15-c (F = g E): R0 += s, R1 += c' d, R2 += c'^2 s —
         // 7 instead of 8 ops per column pair. Runs 0/3 and 1/2 are paired.
         float R0 = 0.f, R1 = 0.f, R2 = 0.f;
+        const bool narrow = fabsf(b.x) > kRun4MaxA_K4;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const Run4 lo = run4(dx0 + 4.f * q, b.x, b.w, bdy, apb, cdy2o, a.w);
-          const Run4 hi = run4(dx0 + 4.f * (3 - q), b.x, b.w, bdy, apb, cdy2o, a.w);
+          Run4 lo, hi;
+          if (!narrow) {
+            lo = run4(dx0 + 4.f * q, b.x, b.w, bdy, apb, cdy2o, a.w);
+            hi = run4(dx0 + 4.f * (3 - q), b.x, b.w, bdy, apb, cdy2o, a.w);
+          } else {  // direct evaluation (see kRun4MaxA_K4)
+            float ev[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float xl = dx0 + (float)(4 * q + k), xh = dx0 + (float)(4 * (3 - q) + k);
+              ev[k] = ex2(fmaf(xl, fmaf(b.x, xl, bdy), cdy2o));
+              ev[4 + k] = ex2(fmaf(xh, fmaf(b.x, xh, bdy), cdy2o));
+            }
+            lo = Run4{ev[0], ev[1], ev[2], ev[3]};
+            hi = Run4{ev[4], ev[5], ev[6], ev[7]};
+          }
           const float el[4] = {lo.e0, lo.e1, lo.e2, lo.e3};
           const float eh[4] = {hi.e0, hi.e1, hi.e2, hi.e3};
 #pragma unroll
@@ -671,13 +711,18 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int u0 = tx * kTilePx, v0 = ty * kTilePx;
     const float* dtile = dL + ((long long)view * H + v0) * W + u0;
+    // host path: the copy engine is still writing later units of dL while this
+    // kernel runs, so the non-coherent (read-only for the whole kernel) path
+    // must not be used for it; L2-coherent loads instead (ld.global.cg)
+    const bool streamed = us.ready != nullptr;
+    auto ld_dl = [streamed](const float* p) { return streamed ? __ldcg(p) : __ldg(p); };
     // --- G fragments of this tile: per-tile power-of-two scale first
     float gm = 0.f;
 #pragma unroll
     for (int i = 0; i < 256 / (32 * kMmaWarps); ++i) {
       const int p = threadIdx.x + 32 * kMmaWarps * i;
       const int c = p & 15, r = p >> 4;
-      if (v0 + r < H && u0 + c < W) gm = fmaxf(gm, fabsf(__ldg(dtile + (long long)r * W + c)));
+      if (v0 + r < H && u0 + c < W) gm = fmaxf(gm, fabsf(ld_dl(dtile + (long long)r * W + c)));
     }
     gm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gm)));
     if (lane == 0) s_gmax[warp] = gm;
@@ -697,7 +742,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int c = 8 * (t & 1) + 4 * h + i;
-          const float g = (v0 + r < H && u0 + c < W) ? __ldg(dtile + (long long)r * W + c) * gscale : 0.f;
+          const float g = (v0 + r < H && u0 + c < W) ? ld_dl(dtile + (long long)r * W + c) * gscale : 0.f;
           const float cp = (float)c - 7.5f, rp = (float)r - 7.5f;
           const float phi = n == 0 ? 1.f : n == 1 ? cp : n == 2 ? rp : n == 3 ? cp * cp : n == 4 ? rp * rp
                           : n == 5 ? cp * rp : 0.f;
@@ -763,6 +808,8 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
       // 14 sqrt(11 a) >= -125 for a = |A| <= 1.25: no value above binary16
       // resolution is lost. (K3's +64 offset allows 1.5 at the 2^-24 level.)
       const bool r8 = __all_sync(0xffffffffu, fabsf(A.x) <= 1.25f && fabsf(A.y) <= 1.25f);
+      const bool direct =
+          __any_sync(0xffffffffu, fabsf(A.x) > kRun4MaxA_K4 || fabsf(A.y) > kRun4MaxA_K4);
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -776,9 +823,11 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
         float2 e[8];
         if (r8) {
           run8x2(e, dx, A, A2, bdy, apb, cdy2o, K);
-        } else {
+        } else if (!direct) {
           run4x2(e, dx, A, A2, bdy, apb, cdy2o, K);
           run4x2(e + 4, dx4, A, A2, bdy, apb, cdy2o, K);
+        } else {
+          direct8x2(e, dx, A, bdy, cdy2o);
         }
         float E[2][8];
 #pragma unroll

@@ -92,7 +92,8 @@ struct Ctx {
   // grow-only scratch reused across calls
   void* cub_tmp = nullptr;
   size_t cub_tmp_bytes = 0;
-  int64_t* pinned_count = nullptr;  // small pinned host word for D2H of counts
+  int64_t* pinned_count = nullptr;  // small pinned host words (128 B) for D2H of counts
+  long long* sum64 = nullptr;       // device word: int64 total of a count scan
   int sm_count = 148;
   // copy stream + events for the host-buffer entry points (H2D/D2H of view
   // chunks overlap the compute of neighbouring chunks)
@@ -101,6 +102,7 @@ struct Ctx {
   // the statistics kernel of chunk k+1 runs on the main stream
   cudaStream_t aux_stream = nullptr;
   cudaEvent_t ev_join = nullptr;
+  cudaEvent_t ev_stage = nullptr;  // staging slots (re)allocated on `stream`, before another stream uses them
   static constexpr int kChunkEvents = 16;
   cudaEvent_t ev_compute[kChunkEvents] = {};
   cudaEvent_t ev_copy[kChunkEvents] = {};
