@@ -229,17 +229,34 @@ double sct_lr_at(double lr_init, double final_ratio, int32_t t, int32_t iters);
  * (synchronises the context stream). sct_adaptive_apply writes the compacted
  * survivors (Adam state carried) followed by the new kernels in parent order
  * (zero Adam state) into out / out_adam (device buffers of new_m kernels).
- * gauss: device float [6 * n_split] standard-normal draws, per split kernel and
- * child in the order (z, y, x) — the reference's consumption order — may be
- * NULL when n_split == 0. The caller resets the gradient statistics. */
+ * gauss: device double [6 * n_split] standard-normal draws, per split kernel and
+ * child in the order (z, y, x) — the reference's consumption order, e.g. from
+ * sct_rng_normal — may be NULL when n_split == 0. The caller resets the
+ * gradient statistics (gaussian_cloud.cpp:119-123 zeroes all three). */
 typedef struct sct_ac_plan sct_ac_plan;
 int sct_adaptive_plan(sct_ctx* ctx, const sct_cloud* cloud, const sct_stats* stats, double prune_density_threshold,
                       double densify_grad_threshold, double split_scale_threshold_frac, double split_factor,
                       const double extent_size_mm[3], sct_ac_plan** plan, int64_t* new_m, int64_t* n_split,
                       int32_t counts[3]);
 int sct_adaptive_apply(sct_ctx* ctx, sct_ac_plan* plan, const sct_cloud* cloud, const sct_adam_state* adam,
-                       const float* grad3d_accum, const float* gauss, sct_cloud* out, sct_adam_state* out_adam);
+                       const float* grad3d_accum, const double* gauss, sct_cloud* out, sct_adam_state* out_adam);
 int sct_adaptive_free(sct_ac_plan* plan);
+
+/* ---- the trainer's host random stream (trainer.cpp:254-258) -------------- */
+/* One std::mt19937_64(seed) with libstdc++'s distributions, drawn in the
+ * reference trainer's order: sct_rng_shuffle = std::shuffle of the view order
+ * at each epoch start (trainer.cpp:269-273, reshuffled in place);
+ * sct_rng_subvolume_origin = random_subvolume_spec's origin (voxelizer.cpp:226-239,
+ * three uniform(0,1) draws); sct_rng_normal = n draws of ONE
+ * std::normal_distribution(0,1) object (one adaptive_control call, trainer.cpp:184). */
+typedef struct sct_rng sct_rng;
+int sct_rng_create(uint64_t seed, sct_rng** out);
+int sct_rng_destroy(sct_rng* rng);
+int sct_rng_shuffle(sct_rng* rng, int32_t* values, int32_t n);
+int sct_rng_subvolume_origin(sct_rng* rng, const double lo[3], const double hi[3], const double spacing[3], int32_t d,
+                             double origin[3]);
+int sct_rng_normal(sct_rng* rng, int64_t n, double* out);
+int sct_rng_uniform(sct_rng* rng, int64_t n, double lo, double hi, double* out);
 
 /* ---- fixture generation (simulator.cpp, fdk.cpp) ------- */
 /* Analytic ellipsoid phantom (simulator.cpp:31-65): ellipsoids [n][8] host

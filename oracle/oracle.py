@@ -104,6 +104,7 @@ _SIG = {
     "orc_ac_stats": (None, [VP, D, I32, D]),
     "orc_ac_free": (None, [VP]),
     "orc_normal_draws": (None, [VP, C.c_int, D]),
+    "orc_shuffle": (None, [VP, C.c_int, I32]),
     "orc_lr_at": (C.c_double, [C.c_double, C.c_double, C.c_int, C.c_int]),
     "orc_adam_step": (None, [C.c_int64, D, D, D, D, C.c_double, C.c_int, C.c_double, C.c_double,
                              C.c_double]),
@@ -658,6 +659,13 @@ def adaptive_control(rng: Rng, cloud: Cloud, adam: dict, stats: Stats, prune_thr
     finally:
         lib().orc_ac_free(h)
     return Cloud(cloud.s_min, *out[:4]), dict(zip(ADAM_KEYS, out[4:])), tuple(cnt)
+
+
+def shuffle(rng: Rng, values: np.ndarray) -> np.ndarray:
+    """std::shuffle on a std::vector<int> (trainer.cpp:270); reference library only."""
+    v = np.ascontiguousarray(values, dtype=np.int32).copy()
+    _load("reference").orc_shuffle(rng._h, v.size, _i32(v))
+    return v
 
 
 def normal_draws(rng: Rng, n: int) -> np.ndarray:

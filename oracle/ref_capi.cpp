@@ -506,6 +506,12 @@ void orc_ac_stats(void* h, double* norm_acc, int32_t* count, double* g3d) {
   std::memcpy(g3d, r->st_3d.data(), r->st_3d.size() * sizeof(double));
 }
 void orc_ac_free(void* h) { delete static_cast<ACResult*>(h); }
+// trainer.cpp:270: std::shuffle(order.begin(), order.end(), rng) on a std::vector<int>
+void orc_shuffle(void* rp, int n, int32_t* values) {
+  std::vector<int> order(values, values + n);
+  std::shuffle(order.begin(), order.end(), *static_cast<std::mt19937_64*>(rp));
+  for (int i = 0; i < n; ++i) values[i] = order[i];
+}
 void orc_normal_draws(void* rp, int n, double* out) {
   auto& rng = *static_cast<std::mt19937_64*>(rp);
   std::normal_distribution<double> gauss(0.0, 1.0);

@@ -113,6 +113,12 @@ SIGNATURES = {
     "sct_render_bwd_allreduce": (C.c_int, [VP, VP, P(sct_cloud), VP, P(sct_grads), P(sct_stats)]),
     "sct_voxelize_bwd_allreduce": (C.c_int, [VP, P(sct_cloud), P(sct_grid), C.c_double, C.c_int32, C.c_int32, VP,
                                              P(sct_grads)]),
+    "sct_rng_create": (C.c_int, [C.c_uint64, P(VP)]),
+    "sct_rng_destroy": (C.c_int, [VP]),
+    "sct_rng_shuffle": (C.c_int, [VP, I32, C.c_int32]),
+    "sct_rng_subvolume_origin": (C.c_int, [VP, D, D, D, C.c_int32, D]),
+    "sct_rng_normal": (C.c_int, [VP, C.c_int64, D]),
+    "sct_rng_uniform": (C.c_int, [VP, C.c_int64, C.c_double, C.c_double, D]),
     "sct_host_alloc": (C.c_int, [P(VP), C.c_size_t]),
     "sct_host_free": (C.c_int, [VP]),
     "sct_debug_pointer_type": (C.c_int, [VP]),

@@ -63,7 +63,7 @@ __global__ void ac_apply_kernel(long long m, long long m_kept, sct_cloud in, sct
                                 const float* __restrict__ g3d, const uint8_t* __restrict__ action,
                                 const int32_t* __restrict__ keep_out, const int32_t* __restrict__ keep_pos,
                                 const int32_t* __restrict__ new_pos, const int32_t* __restrict__ split_ord,
-                                const float* __restrict__ gauss, ACParams P, sct_cloud out, sct_adam_state aout) {
+                                const double* __restrict__ gauss, ACParams P, sct_cloud out, sct_adam_state aout) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     const int a = action[i];
@@ -118,8 +118,8 @@ __global__ void ac_apply_kernel(long long m, long long m_kept, sct_cloud in, sct
         }
       } else {  // split (trainer.cpp:209-223)
         const dM3 R = d_rotation_matrix(qr);  // rotation_matrix() of the raw quaternion
-        const float* g = gauss + 6 * (long long)split_ord[i] + 3 * c;
-        const double local[3] = {(double)g[2] * s[0], (double)g[1] * s[1], (double)g[0] * s[2]};
+        const double* g = gauss + 6 * (long long)split_ord[i] + 3 * c;
+        const double local[3] = {g[2] * s[0], g[1] * s[1], g[0] * s[2]};
         for (int k = 0; k < 3; ++k) {
           cp[k] = p[k] + (R.m[k][0] * local[0] + R.m[k][1] * local[1] + R.m[k][2] * local[2]);
           cs[k] = fmax(s[k] / P.split_factor, P.s_min * (1.0 + 1e-6));
@@ -252,7 +252,7 @@ int sct_adaptive_plan(sct_ctx* c, const sct_cloud* cloud, const sct_stats* stats
 }
 
 int sct_adaptive_apply(sct_ctx* c, sct_ac_plan* p, const sct_cloud* cloud, const sct_adam_state* adam,
-                       const float* grad3d_accum, const float* gauss, sct_cloud* out, sct_adam_state* out_adam) {
+                       const float* grad3d_accum, const double* gauss, sct_cloud* out, sct_adam_state* out_adam) {
   if (!c || !p || !cloud || !adam || !out || !out_adam || !grad3d_accum) {
     set_error("ConfigError: null argument");
     return SCT_ERR_CONFIG;

@@ -504,11 +504,13 @@ class Engine:
     def adaptive_control(self, cloud: GaussianCloud, extent_size_mm: Sequence[float],
                          prune_density_threshold: float = 0.005, densify_grad_threshold: float = 0.00005,
                          split_scale_threshold_frac: float = 0.01, split_factor: float = 1.6,
-                         gauss: Optional[torch.Tensor] = None, generator: Optional[torch.Generator] = None):
+                         gauss: Optional[torch.Tensor] = None, generator: Optional[torch.Generator] = None,
+                         rng: Optional["HostRng"] = None):
         """trainer.cpp:167-230 on the device: prune, clone, split; returns (new cloud with carried /
         zeroed Adam state and reset statistics, (pruned, cloned, split)). The split positions use
-        6 standard-normal draws per split kernel (z, y, x per child); pass ``gauss`` to supply them
-        (e.g. a reference std::mt19937_64 stream), otherwise they come from torch.randn."""
+        6 standard-normal draws per split kernel (z, y, x per child): from ``rng`` (the trainer's
+        std::mt19937_64 stream, one normal_distribution per call like the reference), or
+        ``gauss`` supplied directly, else torch.randn."""
         if not split_factor > 1.0:
             raise ConfigError("train: split_factor must be > 1")
         cl, st = cloud._c(), cloud._stats_c()
@@ -525,8 +527,11 @@ class Engine:
             out = GaussianCloud(cloud.s_min, e(1), e(3), e(3), e(4), device=self.device)
             if ns > 0:
                 if gauss is None:
-                    gauss = torch.randn(6 * ns, dtype=torch.float32, device=self.device, generator=generator)
-                gauss = gauss.to(device=self.device, dtype=torch.float32).contiguous()
+                    if rng is not None:  # the reference's stream (trainer.cpp:184,213-216)
+                        gauss = torch.from_numpy(rng.normal(6 * ns))
+                    else:
+                        gauss = torch.randn(6 * ns, dtype=torch.float64, device=self.device, generator=generator)
+                gauss = gauss.to(device=self.device, dtype=torch.float64).contiguous()
                 if gauss.numel() < 6 * ns:
                     raise ConfigError(f"adaptive control: need {6 * ns} normal draws, got {gauss.numel()}")
             ocl, ost, ast = out._c(), out._adam_c(), cloud._adam_c()
@@ -536,6 +541,50 @@ class Engine:
         finally:
             self.lib.sct_adaptive_free(plan)
         return out, tuple(int(x) for x in counts)
+
+
+class HostRng:
+    """The reference trainer's single std::mt19937_64 stream (trainer.cpp:254-258),
+    product host code in the engine library (csrc/rng.cu): libstdc++'s engine,
+    std::shuffle and distributions, drawn in the reference's order."""
+
+    def __init__(self, seed: int):
+        self.lib = _capi.load()
+        h = C.c_void_p()
+        _check(self.lib.sct_rng_create(int(seed) & ((1 << 64) - 1), C.byref(h)))
+        self._h = h
+
+    def shuffle(self, values: np.ndarray) -> np.ndarray:
+        """std::shuffle in place (int32 array)."""
+        assert values.dtype == np.int32 and values.flags.c_contiguous
+        _check(self.lib.sct_rng_shuffle(self._h, values.ctypes.data_as(C.POINTER(C.c_int32)), int(values.size)))
+        return values
+
+    def subvolume_origin(self, lo, hi, spacing, d: int):
+        a = [(C.c_double * 3)(*[float(x) for x in v]) for v in (lo, hi, spacing)]
+        out = (C.c_double * 3)()
+        _check(self.lib.sct_rng_subvolume_origin(self._h, a[0], a[1], a[2], int(d), out))
+        return tuple(out)
+
+    def normal(self, n: int) -> np.ndarray:
+        out = np.zeros(max(1, n), dtype=np.float64)
+        _check(self.lib.sct_rng_normal(self._h, int(n), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out[:n]
+
+    def uniform(self, n: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+        out = np.zeros(max(1, n), dtype=np.float64)
+        _check(self.lib.sct_rng_uniform(self._h, int(n), float(lo), float(hi),
+                                        out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out[:n]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                self.lib.sct_rng_destroy(h)
+            except Exception:  # noqa: BLE001 (interpreter shutdown)
+                pass
+            self._h = None
 
 
 class VoxelState:

@@ -1,5 +1,5 @@
 """Device-resident training iteration of the reference trainer (BASELINE
-configs[1], "full train step"): trainer.cpp:268-319 without adaptive control.
+configs[1], "full train step"): trainer.cpp:266-330, adaptive control included.
 
 One iteration = render the selected view(s) (rasterizer.cpp:112-157), form
 L1 + lambda_ssim * D-SSIM on projections normalised by the dataset maximum and
@@ -9,7 +9,13 @@ sub-grid at the output spacing (voxelize -> tv3d_loss -> lambda_tv-scaled
 voxelize_backward, trainer.cpp:290-300), the non-finite check
 (trainer.cpp:302-308) and the four Adam groups with the exponential learning
 rate followed by quaternion renormalisation (trainer.cpp:310-319) — all on the
-GPU through the C ABI; the host only picks the view and the sub-grid origin.
+GPU through the C ABI; the host only picks the view and the sub-grid origin,
+from the reference's own random stream: one std::mt19937_64(cfg.seed)
+(trainer.cpp:254-258) with libstdc++'s std::shuffle and distributions
+(engine.HostRng, csrc/rng.cu), consumed in the reference's order — view
+shuffle at each epoch start, the sub-volume origin every iteration, the split
+draws of adaptive control — so a seed selects the same views, sub-grids and
+split positions as the reference trainer.
 """
 from __future__ import annotations
 
@@ -20,8 +26,8 @@ from typing import Optional, Sequence
 import numpy as np
 import torch
 
-from .engine import (CloudGrads, DivergenceDetected, Engine, GaussianCloud, GridSpec, RasterOptions, ScannerConfig,
-                     lr_at)
+from .engine import (CloudGrads, DivergenceDetected, Engine, GaussianCloud, GridSpec, HostRng, RasterOptions,
+                     ScannerConfig, lr_at)
 
 
 @dataclass
@@ -73,14 +79,18 @@ class Trainer:
         self.output_spacing = tuple(ext[k] / cfg.output_dims[k] for k in range(3))
         self.opts = RasterOptions(mode=cfg.mode)
         self.t = 0
-        self.rng = np.random.default_rng(cfg.seed)
-        self.order: list = []
+        self.rng = HostRng(cfg.seed)
+        self.order = np.arange(len(self.angles), dtype=np.int32)  # trainer.cpp:255-256
+        self.epoch_pos = len(self.angles)  # forces a shuffle on first use
 
     def next_view(self) -> int:
-        """Shuffled epochs (trainer.cpp:269-273)."""
-        if not self.order:
-            self.order = list(self.rng.permutation(len(self.angles)))
-        return int(self.order.pop(0))
+        """Shuffled epochs (trainer.cpp:269-273): the order is reshuffled in place."""
+        if self.epoch_pos >= len(self.angles):
+            self.rng.shuffle(self.order)
+            self.epoch_pos = 0
+        v = int(self.order[self.epoch_pos])
+        self.epoch_pos += 1
+        return v
 
     def step(self, view: Optional[int] = None, sub_origin: Optional[tuple] = None) -> dict:
         cfg, eng, cloud = self.cfg, self.eng, self.cloud
@@ -96,9 +106,9 @@ class Trainer:
         fwd.free()
         tv = torch.zeros((), dtype=torch.float64, device=eng.device)
         if cfg.lambda_tv > 0.0:
-            if sub_origin is None:
-                sub_origin = random_subvolume_origin(self.scanner.extent_min_mm, self.scanner.extent_max_mm,
-                                                     self.output_spacing, cfg.tv_grid_dim, self.rng.random(3))
+            if sub_origin is None:  # voxelizer.cpp:226-239 on the trainer's stream
+                sub_origin = self.rng.subvolume_origin(self.scanner.extent_min_mm, self.scanner.extent_max_mm,
+                                                       self.output_spacing, cfg.tv_grid_dim)
             d = cfg.tv_grid_dim
             sub = GridSpec((d, d, d), sub_origin, self.output_spacing)
             vol, vstate = eng.voxelize(cloud, sub, keep_state=True)  # bins once for fwd + bwd
@@ -128,6 +138,7 @@ class Trainer:
         self.cloud, counts = self.eng.adaptive_control(
             self.cloud, ext, prune_density_threshold=cfg.prune_density_threshold,
             densify_grad_threshold=cfg.densify_grad_threshold,
-            split_scale_threshold_frac=cfg.split_scale_threshold_frac, split_factor=cfg.split_factor, gauss=gauss)
+            split_scale_threshold_frac=cfg.split_scale_threshold_frac, split_factor=cfg.split_factor, gauss=gauss,
+            rng=self.rng if gauss is None else None)
         self.grads.resize(self.cloud.size(), device=self.eng.device)
         return counts

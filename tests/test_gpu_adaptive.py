@@ -56,7 +56,7 @@ def test_adaptive_control_matches_oracle(m, seed):
     onc, oad, ocnt = O.adaptive_control(O.Rng(seed), oc, oadam, st, extent_size=ext)
     draws = O.normal_draws(O.Rng(seed), 6 * ocnt[2])
 
-    nc, cnt = eng.adaptive_control(cl, ext, gauss=torch.from_numpy(draws.astype(np.float32)))
+    nc, cnt = eng.adaptive_control(cl, ext, gauss=torch.from_numpy(draws))
     torch.cuda.synchronize()
     assert cnt == tuple(ocnt)
     assert nc.size() == onc.m

@@ -146,8 +146,7 @@ def cfg5():
     w = scenes.CONFIGS[5]
     # the device fixture path (phantom + FDK-free init; parity-tested in
     # test_gpu_fixtures.py) — the host numpy path takes minutes at 512^3
-    grid = P.grid_for_extent((-1, -1, -1), (1, 1, 1), (w.n_vox,) * 3)
-    vol = simulate.phantom_shepp_logan_3d((w.n_vox,) * 3)
+    vol, grid = simulate.phantom_shepp_logan_3d((w.n_vox,) * 3)
     cl = simulate.sample_init_cloud(vol, grid, w.m, s_min_mm=2e-4, seed=0)
     raw = {k: getattr(cl, k).cpu().numpy().astype(np.float64) for k in ("rho_raw", "pos", "scale_raw", "rot")}
     rho = np.where(raw["rho_raw"] > 30.0, raw["rho_raw"], np.log1p(np.exp(np.minimum(raw["rho_raw"], 30.0))))

@@ -103,7 +103,7 @@ def test_train_with_adaptive_control():
     onc, oad, ocnt = O.adaptive_control(O.Rng(17), ocl, {k: h(v) for k, v in c.adam.items()}, st,
                                         cfg.prune_density_threshold, cfg.densify_grad_threshold,
                                         cfg.split_scale_threshold_frac, cfg.split_factor, (2.0, 2.0, 2.0))
-    draws = torch.from_numpy(O.normal_draws(O.Rng(17), 6 * ocnt[2]).astype(np.float32))
+    draws = torch.from_numpy(O.normal_draws(O.Rng(17), 6 * ocnt[2]))
     counts = tr.adaptive_control(gauss=draws)
     assert counts == tuple(ocnt) and sum(counts) > 0
     assert tr.cloud.size() == onc.m
