@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsplatct_b200.so")
+# SCT_LIB_VARIANT selects an alternative in-tree build for A/B measurements
+# (tools/variants.sh); the default is the product library.
+LIB_PATH = os.path.join(_HERE, os.environ.get("SCT_LIB_VARIANT", "libsplatct_b200.so"))
 
 F = C.POINTER(C.c_float)
 D = C.POINTER(C.c_double)

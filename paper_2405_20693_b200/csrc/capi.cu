@@ -544,6 +544,26 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   launch_raster_preprocess(c, *cloud, s->d_prep, s->d_views, n_views, s->det, s->rp, s->d_rec, s->d_rect,
                            s->d_count, s->d_vis);
   if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs))) return fail(rc);
+  // Binning: one stable counting scatter straight into (tile, view, kernel)
+  // order when the tile table fits in shared memory (raster.cu bin_*), else
+  // emit + radix sort. SCT_BIN=sort forces the latter.
+  static const bool force_sort = [] {
+    const char* e = std::getenv("SCT_BIN");
+    return e && std::string(e) == "sort";
+  }();
+  if (!force_sort && raster_bin_scatter_fits(s->det.tiles_x, s->det.tiles_y)) {
+    if ((rc = dev_alloc(c, (void**)&s->d_vals, std::max<int64_t>(s->n_pairs, 1) * sizeof(int32_t)))) return fail(rc);
+    if ((rc = launch_raster_bin_scatter(c, n_views, s->m, s->det.tiles_x, s->det.tiles_y, s->d_rect, s->d_vals,
+                                        s->d_ranges, s->n_pairs)))
+      return fail(rc);
+    if (images) launch_raster_composite(c, s, images);
+    if (cudaGetLastError() != cudaSuccess) {
+      set_error("CUDA error: kernel launch in sct_render_fwd");
+      return fail(SCT_ERR_CUDA);
+    }
+    *state = s;
+    return SCT_OK;
+  }
   // Pairs are emitted view-major (and kernel-ascending within a view), so a
   // STABLE sort on the tile bits alone already groups them by (tile, view)
   // with each list ascending in kernel index: fewer radix passes than the

@@ -107,6 +107,210 @@ __global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, con
 }
 
 
+// ---------------------------------------------------------------------------
+// K2 binning as one stable counting scatter (replaces emit + radix sort +
+// ranges when the tile table fits in shared memory). The reference's lists
+// (rasterizer.cpp:119-132) are, per (view, tile), the visible kernels in
+// ascending index; items are view-major (item = view * m + kernel), so the
+// target order is (tile, view, kernel) — a stable counting sort on the tile.
+//   bin_count:   block (chunk c, view v) of consecutive items counts the
+//                pairs per tile -> H[tile][view][chunk];
+//   exclusive scan of H (cub) -> S: S[t][v][c] is where block (v, c)'s pairs
+//                of tile t start; S[t][v][0] .. S[t][v+1][0] is list (v, t);
+//   bin_scatter: the block recounts per warp (4 contiguous warp ranges),
+//                prefixes the warps per tile, then each warp walks its items
+//                32 at a time in item order: the rank of a lane's pair in tile
+//                (tx, ty) among the round's earlier lanes is
+//                popc(colmask[tx] & rowmask[ty] & lanes_below) — rectangles are
+//                products of a column and a row range, so two 32-bit masks per
+//                tile column / row give the exact stable rank;
+//   bin_ranges:  (view, tile) ranges straight from S.
+constexpr int kBinWarps = 4;
+// shared memory of the scatter: 4 warps x (tile counters + column and row
+// masks) words + a chunk of rectangles (>= 256)
+constexpr int64_t kScatterSmem = 225 * 1024;
+
+__global__ void __launch_bounds__(256) bin_count_kernel(const short4* __restrict__ rect, long long m, int chunk,
+                                                        int T, int tiles_x, int32_t* __restrict__ H) {
+  extern __shared__ uint32_t hist[];
+  const int c = blockIdx.x, v = blockIdx.y;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) hist[t] = 0;
+  __syncthreads();
+  const long long i0 = (long long)v * m + (long long)c * chunk;
+  const long long i1 = (long long)v * m + min((long long)(c + 1) * chunk, m);
+  // four rectangles in flight per thread (the loop is latency-bound otherwise)
+  for (long long i = i0 + threadIdx.x; i < i1; i += 4 * blockDim.x) {
+    short4 r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      r[k] = i + k * blockDim.x < i1 ? __ldg(rect + i + k * blockDim.x) : make_short4(0, -1, 0, -1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      for (int ty = r[k].z; ty <= r[k].w; ++ty)
+        for (int tx = r[k].x; tx <= r[k].y; ++tx) atomicAdd(&hist[ty * tiles_x + tx], 1u);
+  }
+  __syncthreads();
+  int32_t* h = H + ((long long)v * gridDim.x + c) * T;  // block-major [view][chunk][tile], coalesced
+  for (int t = threadIdx.x; t < T; t += blockDim.x) h[t] = (int32_t)hist[t];
+}
+
+// Exclusive prefix of the counts in (tile, view, chunk) order from the
+// block-major table H[b][t] (b = view * chunks + chunk): S = TB[t] + P[b][t]
+// with P the exclusive prefix down each tile column and TB the exclusive
+// prefix of the column totals. Columns are scanned in row segments of
+// kSegRows rows (pass 1 segment sums, pass 2 segment prefixes + column
+// totals + tile bases, pass 3 apply); every access is coalesced across tiles.
+constexpr int kSegRows = 64;
+__global__ void __launch_bounds__(256) bin_colsum_kernel(const int32_t* __restrict__ H, int n_rows, int T,
+                                                         int32_t* __restrict__ seg) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, g = blockIdx.y;
+  if (t >= T) return;
+  const int r0 = g * kSegRows, r1 = min(n_rows, r0 + kSegRows);
+  int32_t acc = 0;
+#pragma unroll 8
+  for (int r = r0; r < r1; ++r) acc += H[(long long)r * T + t];
+  seg[(long long)g * T + t] = acc;
+}
+__global__ void __launch_bounds__(256) bin_segscan_kernel(int32_t* __restrict__ seg, int n_seg, int T,
+                                                          int32_t* __restrict__ coltot) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  int32_t run = 0;
+#pragma unroll 8
+  for (int g = 0; g < n_seg; ++g) {
+    const int32_t x = seg[(long long)g * T + t];
+    seg[(long long)g * T + t] = run;
+    run += x;
+  }
+  coltot[t] = run;
+}
+// one block: exclusive prefix of the column totals -> tile_base[0..T], tile_base[T] = pairs
+__global__ void __launch_bounds__(1024) bin_tilebase_kernel(const int32_t* __restrict__ coltot, int T,
+                                                            int32_t* __restrict__ tile_base) {
+  __shared__ int32_t part[1024];
+  const int per = (T + blockDim.x - 1) / blockDim.x;
+  const int t0 = min(T, (int)threadIdx.x * per), t1 = min(T, t0 + per);
+  int32_t mine = 0;
+  for (int t = t0; t < t1; ++t) mine += coltot[t];
+  part[threadIdx.x] = mine;
+  __syncthreads();
+  for (int d = 1; d < (int)blockDim.x; d <<= 1) {  // Hillis-Steele inclusive scan
+    const int32_t y = threadIdx.x >= (unsigned)d ? part[threadIdx.x - d] : 0;
+    __syncthreads();
+    part[threadIdx.x] += y;
+    __syncthreads();
+  }
+  int32_t run = part[threadIdx.x] - mine;
+  for (int t = t0; t < t1; ++t) {
+    tile_base[t] = run;
+    run += coltot[t];
+  }
+  if (threadIdx.x == blockDim.x - 1) tile_base[T] = part[threadIdx.x];
+}
+__global__ void __launch_bounds__(256) bin_apply_kernel(int32_t* __restrict__ H, const int32_t* __restrict__ seg,
+                                                        const int32_t* __restrict__ tile_base, int n_rows, int T) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, g = blockIdx.y;
+  if (t >= T) return;
+  const int r0 = g * kSegRows, r1 = min(n_rows, r0 + kSegRows);
+  int32_t run = tile_base[t] + seg[(long long)g * T + t];
+  for (int r = r0; r < r1; ++r) {
+    const long long k = (long long)r * T + t;
+    const int32_t x = H[k];
+    H[k] = run;  // in place: H becomes S
+    run += x;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short4* __restrict__ rect, long long m,
+                                                                     int chunk, int T, int tiles_x, int tiles_y,
+                                                                     const int32_t* __restrict__ S,
+                                                                     int32_t* __restrict__ vals) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* cnt = sm;                              // [kBinWarps][T]
+  uint32_t* colm = sm + kBinWarps * T;             // [kBinWarps][tiles_x]
+  uint32_t* rowm = colm + kBinWarps * tiles_x;     // [kBinWarps][tiles_y]
+  short4* srect = reinterpret_cast<short4*>(rowm + kBinWarps * tiles_y);  // [chunk] the block's rectangles
+  const int c = blockIdx.x, v = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long i0 = (long long)v * m + (long long)c * chunk;
+  const long long i1 = (long long)v * m + min((long long)(c + 1) * chunk, m);
+  const long long per = (((i1 - i0) + kBinWarps * 32 - 1) / (kBinWarps * 32)) * 32;  // items per warp
+  const long long w0 = i0 + warp * per, w1 = min(w0 + per, i1);
+  uint32_t* mycnt = cnt + warp * T;
+  uint32_t* mycol = colm + warp * tiles_x;
+  uint32_t* myrow = rowm + warp * tiles_y;
+  for (int t = threadIdx.x; t < kBinWarps * T; t += blockDim.x) cnt[t] = 0;
+  __syncthreads();
+  // phase A: per-warp tile counts; the rectangles are kept in shared memory
+  // for phase C (four loads in flight per lane)
+  for (long long i = w0 + lane; i < w1; i += 4 * 32) {
+    short4 r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r[k] = i + 32 * k < w1 ? __ldg(rect + i + 32 * k) : make_short4(0, -1, 0, -1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (i + 32 * k < w1) srect[i + 32 * k - i0] = r[k];
+      for (int ty = r[k].z; ty <= r[k].w; ++ty)
+        for (int tx = r[k].x; tx <= r[k].y; ++tx) atomicAdd(&mycnt[ty * tiles_x + tx], 1u);
+    }
+  }
+  __syncthreads();
+  // phase B: per tile, the block's global start plus the earlier warps' counts
+  const int32_t* sb = S + ((long long)v * gridDim.x + c) * T;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    uint32_t run = (uint32_t)sb[t];
+#pragma unroll
+    for (int w = 0; w < kBinWarps; ++w) {
+      const uint32_t x = cnt[w * T + t];
+      cnt[w * T + t] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+  // phase C: rounds of 32 items in item order; stable rank by row / column masks
+  const uint32_t below = (1u << lane) - 1u;
+  for (long long base = w0; base < w1; base += 32) {
+    const long long i = base + lane;
+    short4 r = make_short4(0, -1, 0, -1);
+    if (i < w1) r = srect[i - i0];
+    for (int k = lane; k < tiles_x; k += 32) mycol[k] = 0;
+    for (int k = lane; k < tiles_y; k += 32) myrow[k] = 0;
+    __syncwarp();
+    const uint32_t bit = 1u << lane;
+    if (r.y >= r.x && r.w >= r.z) {
+      for (int tx = r.x; tx <= r.y; ++tx) atomicOr(&mycol[tx], bit);
+      for (int ty = r.z; ty <= r.w; ++ty) atomicOr(&myrow[ty], bit);
+    }
+    __syncwarp();
+    for (int ty = r.z; ty <= r.w; ++ty) {
+      const uint32_t rm = myrow[ty];
+      for (int tx = r.x; tx <= r.y; ++tx) {
+        const int t = ty * tiles_x + tx;
+        const uint32_t rank = __popc(mycol[tx] & rm & below);
+        vals[mycnt[t] + rank] = (int32_t)i;
+      }
+    }
+    __syncwarp();
+    for (int ty = r.z; ty <= r.w; ++ty)
+      for (int tx = r.x; tx <= r.y; ++tx) atomicAdd(&mycnt[ty * tiles_x + tx], 1u);
+    __syncwarp();
+  }
+}
+
+// (view, tile) list = [S[v][0][t], S[v+1][0][t]) with S[V][0][t] = the next tile's
+// base (tile_base[t + 1]).
+__global__ void __launch_bounds__(256) bin_ranges_kernel(const int32_t* __restrict__ S,
+                                                         const int32_t* __restrict__ tile_base, int n_chunks,
+                                                         int n_views, int T, int2* __restrict__ ranges) {
+  const long long n = (long long)n_views * T;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(k / T), t = (int)(k % T);
+    const int32_t a = S[(long long)v * n_chunks * T + t];
+    const int32_t b = v + 1 < n_views ? S[(long long)(v + 1) * n_chunks * T + t] : tile_base[t + 1];
+    ranges[k] = make_int2(a, b);
+  }
+}
+
 // (view, tile) ranges of the sorted raster pairs: tile from the key, view
 // from the item (item = view * m + kernel; quotient by a float reciprocal
 // with an exact integer correction). Pair p closes the range at p and opens
@@ -654,6 +858,12 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
 #ifndef SCT_K4_WARPS
 #define SCT_K4_WARPS 4
 #endif
+#ifndef SCT_K4_ACC2
+#define SCT_K4_ACC2 0
+#endif
+#ifndef SCT_K4_REC16
+#define SCT_K4_REC16 0
+#endif
 constexpr int kMmaWarps = SCT_K4_WARPS;
 
 __device__ __forceinline__ void mma_f16(float (&d)[4], __half2 a0, __half2 a1, __half2 a2, __half2 a3, uint32_t b0,
@@ -767,6 +977,18 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
     const int ck = lane >> 1, ch = lane & 1;
     auto load_idx = [&](int cb) { return cb + ck < n_list ? vals[rg.x + cb + ck] : -1; };
     auto issue = [&](int buf, int it) {
+#if SCT_K4_REC16
+      // plain layout [kernel][2] float4: one 16-byte cp.async per lane
+      float4* d16 = reinterpret_cast<float4*>(&s_rec[warp][buf][0][0]) + 2 * ck + ch;
+      if (it >= 0) {
+        cp_async16(d16, rec + 2 * (long long)it + ch);
+      } else {
+        *d16 = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (ch == 0) s_it[warp][buf][ck] = it;
+      cp_async_commit();
+      return;
+#endif
       float* d = reinterpret_cast<float*>(&s_rec[warp][buf][ck & 7][0]) + (ck >> 3);
       if (it >= 0) {
         const float* src = reinterpret_cast<const float*>(rec + 2 * (long long)it) + 4 * ch;
@@ -792,8 +1014,15 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
         cp_async_wait_all();
       }
       __syncwarp();
+#if SCT_K4_REC16
+      const float4* rk = reinterpret_cast<const float4*>(&s_rec[warp][buf][0][0]);
+      const float4 ra0 = rk[2 * gq], ra1 = rk[2 * gq + 1], rb0 = rk[2 * gq + 16], rb1 = rk[2 * gq + 17];
+      const float4 f0 = make_float4(ra0.x, rb0.x, ra0.y, rb0.y), f1 = make_float4(ra0.z, rb0.z, ra0.w, rb0.w);
+      const float4 f2 = make_float4(ra1.x, rb1.x, ra1.y, rb1.y), f3 = make_float4(ra1.z, rb1.z, ra1.w, rb1.w);
+#else
       const float4 f0 = s_rec[warp][buf][gq][0], f1 = s_rec[warp][buf][gq][1];
       const float4 f2 = s_rec[warp][buf][gq][2], f3 = s_rec[warp][buf][gq][3];
+#endif
       // kernels gq (.x) and gq + 8 (.y), evaluated together in FP32x2
       const float2 cy = make_float2(f0.z, f0.w), K = make_float2(f1.z, f1.w);
       const float2 A = make_float2(f2.x, f2.y), B = make_float2(f2.z, f2.w);
@@ -811,6 +1040,11 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
       const bool direct =
           __any_sync(0xffffffffu, fabsf(A.x) > kRun4MaxA_K4 || fabsf(A.y) > kRun4MaxA_K4);
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#if SCT_K4_ACC2
+      float acc2[4] = {0.f, 0.f, 0.f, 0.f};  // the lo parts: two independent MMA chains
+#else
+      float (&acc2)[4] = acc;
+#endif
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float py = py_base + 2.f * q;
@@ -843,9 +1077,13 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
           const __half2 a2 = __floats2half2_rn(E[0][4 * h + 2], E[0][4 * h + 3]);
           const __half2 a3 = __floats2half2_rn(E[1][4 * h + 2], E[1][4 * h + 3]);
           mma_f16(acc, a0, a1, a2, a3, gb.x, gb.y);
-          mma_f16(acc, a0, a1, a2, a3, gb.z, gb.w);
+          mma_f16(acc2, a0, a1, a2, a3, gb.z, gb.w);
         }
       }
+#if SCT_K4_ACC2
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] += acc2[k];
+#endif
       // acc: c0,c1 = moments 2t, 2t+1 of kernel gq; c2,c3 = of kernel gq + 8.
       // Lane t = 0 finishes kernel gq, lane t = 1 kernel gq + 8.
       const int base = lane & ~3;
@@ -914,6 +1152,74 @@ void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32
   else
     raster_emit_kernel<uint32_t><<<grid_cap(c, n_items, 256), 256, 0, c->stream>>>(
         n_items, rect, offset, tiles_x, static_cast<uint32_t*>(keys), vals);
+}
+
+// Counting-scatter binning (bin_* kernels above). Needs the per-warp tile
+// table in shared memory: T <= kMaxScatterTiles, else the caller keeps the
+// radix-sort path. Returns false when not applicable.
+bool raster_bin_scatter_fits(int tiles_x, int tiles_y) {
+  const int64_t T = (int64_t)tiles_x * tiles_y;
+  return kBinWarps * (T + tiles_x + tiles_y) * 4 + 256 * (int64_t)sizeof(short4) <= kScatterSmem &&
+         T * 4 <= 48 * 1024;  // bin_count's histogram (default shared limit)
+}
+
+int launch_raster_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, const short4* rect,
+                              int32_t* vals, int2* ranges, int64_t n_pairs) {
+  const int64_t T = (int64_t)tiles_x * tiles_y;
+  if (n_pairs == 0 || m == 0) return SCT_OK;
+  // chunk size: the count table H holds (V * chunks) x T entries (<= ~64M), and
+  // the scatter keeps a chunk's rectangles in shared memory next to its tables
+  const int64_t target = 64ll << 20;
+  static const int64_t min_chunk = [] {
+    const char* e = std::getenv("SCT_BIN_CHUNK");
+    return e ? std::max<int64_t>(256, atoll(e)) : 1024;
+  }();
+  const int64_t tables = (kBinWarps * (T + tiles_x + tiles_y)) * sizeof(uint32_t);
+  const int64_t max_chunk = ((kScatterSmem - tables) / (int64_t)sizeof(short4)) / 256 * 256;
+  int64_t chunk = std::max<int64_t>(min_chunk, (m * n_views * T + target - 1) / target);
+  chunk = std::min<int64_t>(((chunk + 255) / 256) * 256, max_chunk);
+  const int64_t n_chunks = (m + chunk - 1) / chunk;
+  const int64_t rows = n_views * n_chunks;
+  const int64_t n_seg = (rows + kSegRows - 1) / kSegRows;
+  int32_t *H = nullptr, *seg = nullptr, *tb = nullptr;
+  SCT_TRY(dev_alloc(c, (void**)&H, rows * T * sizeof(int32_t)));
+  SCT_TRY(dev_alloc(c, (void**)&seg, n_seg * T * sizeof(int32_t)));
+  SCT_TRY(dev_alloc(c, (void**)&tb, (2 * T + 1) * sizeof(int32_t)));
+  int32_t* tb2 = tb + T;  // tile bases [T + 1]; tb[0..T) holds the column totals
+  const dim3 grid((unsigned)n_chunks, (unsigned)n_views);
+  {
+    KScope _ks(c, "K2_bin_count");
+    bin_count_kernel<<<grid, 256, T * sizeof(uint32_t), c->stream>>>(rect, m, (int)chunk, (int)T, tiles_x, H);
+  }
+  {
+    KScope _ks(c, "K2_bin_scan");
+    const dim3 g2((unsigned)((T + 255) / 256), (unsigned)n_seg);
+    bin_colsum_kernel<<<g2, 256, 0, c->stream>>>(H, (int)rows, (int)T, seg);
+    bin_segscan_kernel<<<(unsigned)((T + 255) / 256), 256, 0, c->stream>>>(seg, (int)n_seg, (int)T, tb);
+    bin_tilebase_kernel<<<1, 1024, 0, c->stream>>>(tb, (int)T, tb2);
+    bin_apply_kernel<<<g2, 256, 0, c->stream>>>(H, seg, tb2, (int)rows, (int)T);
+  }
+  {
+    KScope _ks(c, "K2_bin_scatter");
+    const size_t smem = (kBinWarps * (T + tiles_x + tiles_y)) * sizeof(uint32_t) + chunk * sizeof(short4);
+    static bool attr = false;
+    if (!attr) {
+      SCT_CUDA_TRY(cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kScatterSmem));
+      attr = true;
+    }
+    bin_scatter_kernel<<<grid, 32 * kBinWarps, smem, c->stream>>>(rect, m, (int)chunk, (int)T, tiles_x, tiles_y, H,
+                                                                  vals);
+  }
+  {
+    KScope _ks(c, "K2_bin_ranges");
+    bin_ranges_kernel<<<grid_cap(c, n_views * T, 256), 256, 0, c->stream>>>(H, tb2, (int)n_chunks, (int)n_views,
+                                                                            (int)T, ranges);
+  }
+  dev_free(c, H);
+  dev_free(c, seg);
+  dev_free(c, tb);
+  return SCT_OK;
 }
 
 void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,

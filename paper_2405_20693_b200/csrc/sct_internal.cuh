@@ -268,6 +268,9 @@ void launch_voxel_preprocess(Ctx* c, const sct_cloud& cl, const sct_grid& g, dou
 // FP32 hot kernels
 void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32_t* offset, int tiles_x,
                         void* keys, bool keys16, int32_t* vals);
+bool raster_bin_scatter_fits(int tiles_x, int tiles_y);
+int launch_raster_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, const short4* rect,
+                              int32_t* vals, int2* ranges, int64_t n_pairs);
 void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,
                           int64_t tiles_per_view, int2* ranges);
 void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images);
