@@ -172,12 +172,28 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle leg
-def cpu_oracle_rate(ca, thetas, res, n_views, steps=1):
-    """FP64 CPU restatement (oracle/, OpenMP on all host threads) timed on a
-    bounded sample of the same workload: n_views views of render +
-    render_backward. Returns (projections/s, threads, seconds)."""
+def cpu_kind():
+    """The CPU path timed beside the engine: the reference itself (its unmodified
+    sources compiled into oracle/_ref by `make -C oracle ref`; kind "reference")
+    when that library is present, else the FP64 restatement (oracle/liborc.so;
+    kind "port"). Both run the reference's OpenMP placement on all host threads."""
     from oracle import oracle as O
+    if O.ref_available():
+        return "reference"
     O.build()
+    return "port"
+
+
+def cpu_oracle_rate(ca, thetas, res, n_views, steps=1):
+    """The CPU path (cpu_kind) timed on a bounded sample of the same workload:
+    n_views views of render + render_backward. Returns (projections/s, threads,
+    seconds, views)."""
+    from oracle import oracle as O
+    with O.using(cpu_kind()):
+        return _cpu_oracle_rate(O, ca, thetas, res, n_views, steps)
+
+
+def _cpu_oracle_rate(O, ca, thetas, res, n_views, steps):
     O.set_threads(0)
     threads = O.max_threads()
     oc = O.Cloud.from_arrays(ca.s_min, *ca.as_float64())
@@ -196,12 +212,16 @@ def cpu_oracle_rate(ca, thetas, res, n_views, steps=1):
 
 
 def cpu_voxel_rate(ca, grid, slab=32):
-    """FP64 CPU restatement of voxelize + voxelize_backward (oracle/, OpenMP on
-    all host threads) on a bounded sample of the cfg4 workload: the same cloud
-    on the central z-slab of `slab` voxel layers of the same grid. Returns
+    """voxelize + voxelize_backward on the CPU path (cpu_kind; OpenMP on all
+    host threads) on a bounded sample of the cfg4 workload: the same cloud on
+    the central z-slab of `slab` voxel layers of the same grid. Returns
     (voxels/s, threads, seconds, sample description)."""
     from oracle import oracle as O
-    O.build()
+    with O.using(cpu_kind()):
+        return _cpu_voxel_rate(O, ca, grid, slab)
+
+
+def _cpu_voxel_rate(O, ca, grid, slab):
     O.set_threads(0)
     threads = O.max_threads()
     oc = O.Cloud.from_arrays(ca.s_min, *ca.as_float64())
@@ -222,6 +242,7 @@ def run_reference(args):
     if rank != 0:
         return
     w, ca, thetas, vol = make_workload()
+    kind = cpu_kind()
     per_step = 1  # one view of render + render_backward per step (bounded sample)
     for _ in range(args.warmup):
         cpu_oracle_rate(ca, thetas, w.res, per_step)
@@ -231,11 +252,14 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": 1000.0 * dt / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cfg3 (BASELINE configs[2]) " + w.description, "sample": "1 view/step"},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{args.steps} steps x 1 view (render+render_backward, fp64, OpenMP)"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "CPU restatement of the reference (oracle/); the reference itself cannot be built here "
-                "(Eigen3/libpng/vendor absent) — see DESIGN.md",
+        "note": ("the reference's own render / render_backward (its unmodified core sources compiled into "
+                 "oracle/_ref with the Eigen / nlohmann::json / libpng build shims, -O3 as its Release build)"
+                 if kind == "reference" else
+                 "FP64 CPU restatement of the reference (oracle/); oracle/_ref (the compiled reference) is "
+                 "not present on this box — see DESIGN.md"),
     }
     if not args.no_voxel:  # the second metric of BASELINE.json on the same CPU path (cfg4, bounded sample)
         from paper_2405_20693_b200 import scenes
@@ -243,7 +267,7 @@ def run_reference(args):
         grid = _grid_for_extent((-1, -1, -1), (1, 1, 1), (w4.n_vox,) * 3)
         vrate, vthreads, vdt, sample = cpu_voxel_rate(scenes.make_cloud(4, vol=vol), grid)
         line["voxelizer"] = {"metric": "voxelized voxels/sec (fwd+bwd)", "value": vrate, "unit": "voxels/s",
-                             "cores": vthreads, "kind": "port", "seconds": vdt,
+                             "cores": vthreads, "kind": kind, "seconds": vdt,
                              "sample": sample + " (voxelize + voxelize_backward, fp64, OpenMP)"}
     print(json.dumps(line), flush=True)
 
@@ -387,8 +411,10 @@ def run_engine(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, threads, dt, views = cpu_oracle_rate(ca, thetas, w.res, args.cpu_views)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{len(views)} of the 75 cfg3 views (render+render_backward, fp64 CPU restatement, "
+        ck = cpu_kind()
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": ck,
+               "sample": f"{len(views)} of the 75 cfg3 views (render+render_backward, fp64, "
+                         f"{'the reference compiled from its sources' if ck == 'reference' else 'CPU restatement'}, "
                          f"OpenMP {threads} threads), {dt:.1f} s"}
 
     if rank == 0:
@@ -613,7 +639,7 @@ def run_voxel(args, eng, vol, world, rank, dev):
         res["fwd_only"] = {"value": grid.voxel_count() / (ms / 1e3), "unit": "voxels/s", "ms_per_step": ms}
         if rank == 0 and not args.no_cpu:
             rate, threads, dt, sample = cpu_voxel_rate(ca, grid)
-            res["cpu_baseline"] = {"value": rate, "unit": "voxels/s", "cores": threads, "kind": "port",
+            res["cpu_baseline"] = {"value": rate, "unit": "voxels/s", "cores": threads, "kind": cpu_kind(),
                                    "sample": f"{sample} (voxelize + voxelize_backward, fp64, OpenMP), "
                                              f"{dt:.1f} s"}
     return res

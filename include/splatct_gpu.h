@@ -124,6 +124,16 @@ int sct_ctx_destroy(sct_ctx* ctx);
 int sct_ctx_set_stream(sct_ctx* ctx, void* stream);
 int sct_ctx_sync(sct_ctx* ctx);
 /* deterministic != 0: fixed-order reductions everywhere (default 1). */
+/* Sync-free binning (capacity mode). With a capacity > 0 the render forward
+ * (when its tile table fits the counting scatter) and the voxel binning do not
+ * read the pair count back to the host: their pair buffers hold `capacity`
+ * pairs and a device word records any call whose pairs exceeded it (those
+ * pairs are dropped). sct_ctx_take_overflow synchronises, returns and clears
+ * that word; a caller checks it before trusting results. 0 = exact mode
+ * (default: one host readback per binning). Lets a training loop run without
+ * host synchronisation. */
+int sct_ctx_set_capacity(sct_ctx* ctx, int64_t raster_pairs, int64_t voxel_pairs);
+int sct_ctx_take_overflow(sct_ctx* ctx, int32_t* overflowed);
 int sct_ctx_set_deterministic(sct_ctx* ctx, int deterministic);
 const char* sct_last_error(void);
 const char* sct_version(void);

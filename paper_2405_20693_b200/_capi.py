@@ -62,6 +62,8 @@ SIGNATURES = {
     "sct_ctx_set_stream": (C.c_int, [VP, VP]),
     "sct_ctx_sync": (C.c_int, [VP]),
     "sct_ctx_set_deterministic": (C.c_int, [VP, C.c_int]),
+    "sct_ctx_set_capacity": (C.c_int, [VP, C.c_int64, C.c_int64]),
+    "sct_ctx_take_overflow": (C.c_int, [VP, I32]),
     "sct_last_error": (C.c_char_p, []),
     "sct_version": (C.c_char_p, []),
     "sct_ctx_kernel_launches": (C.c_int64, [VP]),

@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(256) voxel_preprocess_kernel(
     }
     count[i] = empty ? 0 : (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1);
     lo_out[i] = make_short4((short)lo[0], (short)lo[1], (short)lo[2], 0);
-    hi_out[i] = make_short4((short)hi[0], (short)hi[1], (short)hi[2], 0);
+    // an empty kernel gets an empty box (hi < lo on every axis): the counting
+    // scatter binning reads boxes, not counts
+    hi_out[i] = empty ? make_short4((short)(lo[0] - 1), (short)(lo[1] - 1), (short)(lo[2] - 1), 0)
+                      : make_short4((short)hi[0], (short)hi[1], (short)hi[2], 0);
     // precompute(): Q = Sigma^-1, rho (log2-scaled for exp2; cross terms doubled)
     const dM3 q = d_inv3(sigma);
     const double rho = d_act_density(k.rho_raw);

@@ -130,7 +130,9 @@ static int bits_for(uint64_t n) {  // smallest b with 2^b >= n (n >= 1)
 // exclusive scan of count[0..n] (count[n] == 0) into offset[0..n]; returns offset[n].
 // The total is first summed in int64 (cub Reduce into a 64-bit output): an
 // int32 total between 2^31 and 2^32 + 2^31 would wrap to a plausible value.
-static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t* total) {
+// cap > 0 (capacity mode): no host readback — *total = cap and a device check
+// flags c->overflow when the pairs exceed it.
+static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t* total, int64_t cap = 0) {
   SCT_CUDA_TRY(cudaMemsetAsync(count + n, 0, sizeof(int32_t), c->stream));
   {
     long long* d_sum = c->sum64;
@@ -149,6 +151,11 @@ static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64
   {
     KScope _ks(c, "K2_scan(cub)", false);
     SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, offset, n + 1, c->stream));
+  }
+  if (cap > 0) {
+    launch_count_check(c, offset + n, cap);
+    *total = cap;
+    return SCT_OK;
   }
   int32_t t = 0;
   long long t64 = 0;
@@ -278,12 +285,30 @@ static int voxel_bin(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull
   SCT_TRY(dev_alloc(c, (void**)&b.ranges, nbr * sizeof(int2)));
   SCT_CUDA_TRY(cudaMemsetAsync(b.ranges, 0, nbr * sizeof(int2), c->stream));
   launch_voxel_preprocess(c, cl, g, cull, b.zb0, b.zb1, b.bx, b.by, b.rec, b.lo, b.hi, b.count);
-  SCT_TRY(scan_counts(c, b.count, b.offset, m, &b.n_pairs));
-  const int bits = bits_for((uint64_t)nbr);
+  // Brick lists: the stable counting scatter (raster.cu launch_bin_scatter)
+  // when the brick table fits in shared memory, else emit + radix sort.
+  // Capacity mode (sct_ctx_set_capacity): no host readback of the pair count;
+  // the buffers hold cap pairs (sort path: the unused tail carries a padding
+  // key beyond every brick id, so it sorts last and the range scan skips it).
+  const bool scatter = bin_scatter_fits(b.bx, b.by, b.bz);
+  const int64_t cap = c->cap_voxel;
+  SCT_TRY(scan_counts(c, b.count, b.offset, m, &b.n_pairs, cap));
+  if (scatter) {
+    SCT_TRY(dev_alloc(c, (void**)&b.vals, std::max<int64_t>(b.n_pairs, 1) * sizeof(int32_t)));
+    SCT_TRY(launch_bin_scatter(c, 1, m, b.bx, b.by, b.bz, b.lo, b.hi, b.vals, b.ranges, b.n_pairs, nullptr));
+    SCT_CUDA_TRY(cudaGetLastError());
+    return SCT_OK;
+  }
+  const int bits = bits_for((uint64_t)(cap > 0 ? nbr + 1 : nbr));
   const bool k16 = bits <= 16;
-  SCT_TRY(dev_alloc(c, &b.keys, b.n_pairs * (k16 ? sizeof(uint16_t) : sizeof(uint32_t))));
-  SCT_TRY(dev_alloc(c, (void**)&b.vals, b.n_pairs * sizeof(int32_t)));
-  launch_voxel_emit(c, m, b.lo, b.hi, b.offset, b.bx, b.by, b.keys, k16, b.vals);
+  const size_t ksz = k16 ? sizeof(uint16_t) : sizeof(uint32_t);
+  SCT_TRY(dev_alloc(c, &b.keys, std::max<int64_t>(b.n_pairs, 1) * ksz));
+  SCT_TRY(dev_alloc(c, (void**)&b.vals, std::max<int64_t>(b.n_pairs, 1) * sizeof(int32_t)));
+  if (cap > 0) {
+    SCT_CUDA_TRY(cudaMemsetAsync(b.keys, 0xff, b.n_pairs * ksz, c->stream));
+    SCT_CUDA_TRY(cudaMemsetAsync(b.vals, 0, b.n_pairs * sizeof(int32_t), c->stream));
+  }
+  launch_voxel_emit(c, m, b.lo, b.hi, b.offset, b.bx, b.by, b.keys, k16, b.vals, cap > 0 ? cap : INT64_MAX);
   if (bits > 0) {
     if (k16) {
       uint16_t* kp = static_cast<uint16_t*>(b.keys);
@@ -295,7 +320,7 @@ static int voxel_bin(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull
       b.keys = kp;
     }
   }
-  launch_key_ranges(c, b.n_pairs, b.keys, k16, b.ranges);
+  launch_key_ranges(c, b.n_pairs, b.keys, k16, b.ranges, nbr);
   SCT_CUDA_TRY(cudaGetLastError());
   return SCT_OK;
 }
@@ -314,6 +339,7 @@ static void free_state_buffers(sct_fwd* s) {
   dev_free(c, s->d_vis);
   dev_free(c, s->d_keys);
   dev_free(c, s->d_vals);
+  dev_free(c, s->d_total);
   dev_free(c, s->d_ranges);
   dev_free(c, s->d_prep);
 }
@@ -386,6 +412,7 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
   c->unit_done = reinterpret_cast<int*>(c->unit_flags + 3 * Ctx::kMaxUnits);
   c->unit_err = c->unit_done + 2 * Ctx::kMaxUnits;
   c->sum64 = reinterpret_cast<long long*>(u + words);
+  c->overflow = reinterpret_cast<int*>(u + words + 8);
   *out = c;
   return SCT_OK;
 }
@@ -420,6 +447,29 @@ int sct_ctx_set_stream(sct_ctx* c, void* stream) {
 int sct_ctx_sync(sct_ctx* c) {
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
   SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
+
+int sct_ctx_set_capacity(sct_ctx* c, int64_t raster_pairs, int64_t voxel_pairs) {
+  if (!c || raster_pairs < 0 || voxel_pairs < 0 || raster_pairs > INT32_MAX || voxel_pairs > INT32_MAX) {
+    set_error("ConfigError: capacities must be in [0, 2^31)");
+    return SCT_ERR_CONFIG;
+  }
+  c->cap_raster = raster_pairs;
+  c->cap_voxel = voxel_pairs;
+  return SCT_OK;
+}
+
+int sct_ctx_take_overflow(sct_ctx* c, int32_t* overflowed) {
+  if (!c || !overflowed) {
+    set_error("ConfigError: null argument");
+    return SCT_ERR_CONFIG;
+  }
+  int h = 0;
+  SCT_CUDA_TRY(cudaMemcpyAsync(&h, c->overflow, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (h) SCT_CUDA_TRY(cudaMemsetAsync(c->overflow, 0, sizeof(int), c->stream));
+  *overflowed = h;
   return SCT_OK;
 }
 
@@ -543,7 +593,19 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   launch_gauss_prep(c, *cloud, s->d_prep);
   launch_raster_preprocess(c, *cloud, s->d_prep, s->d_views, n_views, s->det, s->rp, s->d_rec, s->d_rect,
                            s->d_count, s->d_vis);
-  if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs))) return fail(rc);
+  // capacity mode: sync-free when the counting scatter applies (the radix
+  // sort needs the exact count on the host)
+  const bool scatter = raster_bin_scatter_fits(s->det.tiles_x, s->det.tiles_y);
+  const int64_t cap = (c->cap_raster > 0 && scatter) ? c->cap_raster : 0;
+  if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs, cap))) return fail(rc);
+  if (cap > 0) {
+    s->exact = false;
+    if ((rc = dev_alloc(c, (void**)&s->d_total, sizeof(int32_t)))) return fail(rc);
+    if (cudaMemsetAsync(s->d_total, 0, sizeof(int32_t), c->stream) != cudaSuccess) {
+      set_error("CUDA error: memset");
+      return fail(SCT_ERR_CUDA);
+    }
+  }
   // Binning: one stable counting scatter straight into (tile, view, kernel)
   // order when the tile table fits in shared memory (raster.cu bin_*), else
   // emit + radix sort. SCT_BIN=sort forces the latter.
@@ -551,10 +613,10 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
     const char* e = std::getenv("SCT_BIN");
     return e && std::string(e) == "sort";
   }();
-  if (!force_sort && raster_bin_scatter_fits(s->det.tiles_x, s->det.tiles_y)) {
+  if ((!force_sort || cap > 0) && scatter) {
     if ((rc = dev_alloc(c, (void**)&s->d_vals, std::max<int64_t>(s->n_pairs, 1) * sizeof(int32_t)))) return fail(rc);
     if ((rc = launch_raster_bin_scatter(c, n_views, s->m, s->det.tiles_x, s->det.tiles_y, s->d_rect, s->d_vals,
-                                        s->d_ranges, s->n_pairs)))
+                                        s->d_ranges, s->n_pairs, s->n_pairs, s->d_total)))
       return fail(rc);
     if (images) launch_raster_composite(c, s, images);
     if (cudaGetLastError() != cudaSuccess) {
@@ -842,6 +904,16 @@ int sct_fwd_free(sct_fwd* s) {
   return SCT_OK;
 }
 
+// the pair count of a state (a device read in capacity mode)
+static int64_t state_pairs(sct_fwd* s) {
+  if (s->exact || !s->d_total) return s->n_pairs;
+  int32_t t = 0;
+  if (cudaMemcpyAsync(&t, s->d_total, sizeof(int32_t), cudaMemcpyDeviceToHost, s->ctx->stream) != cudaSuccess ||
+      cudaStreamSynchronize(s->ctx->stream) != cudaSuccess)
+    return s->n_pairs;
+  return t;
+}
+
 // Algorithmic work of a forward state: GPE = sum over (view, tile) of
 // |tile list| x pixels inside the detector for that tile (the trip count of
 // rasterizer.cpp:144-153, identical for rasterizer.cpp:225-241).
@@ -860,13 +932,13 @@ int sct_fwd_work(sct_fwd* s, int64_t* gpe, int64_t* n_pairs) {
     g += (int64_t)(r[k].y - r[k].x) * pw * ph;
   }
   if (gpe) *gpe = g;
-  if (n_pairs) *n_pairs = s->n_pairs;
+  if (n_pairs) *n_pairs = state_pairs(s);
   return SCT_OK;
 }
 
 int sct_fwd_info(sct_fwd* s, int64_t* n_pairs, int32_t* tiles_x, int32_t* tiles_y, int64_t* n_visible) {
   if (!s) return SCT_ERR_CONFIG;
-  if (n_pairs) *n_pairs = s->n_pairs;
+  if (n_pairs) *n_pairs = state_pairs(s);
   if (tiles_x) *tiles_x = s->det.tiles_x;
   if (tiles_y) *tiles_y = s->det.tiles_y;
   if (n_visible) {

@@ -130,24 +130,44 @@ constexpr int kBinWarps = 4;
 // masks) words + a chunk of rectangles (>= 256)
 constexpr int64_t kScatterSmem = 225 * 1024;
 
-__global__ void __launch_bounds__(256) bin_count_kernel(const short4* __restrict__ rect, long long m, int chunk,
-                                                        int T, int tiles_x, int32_t* __restrict__ H) {
+// Item boxes in tile units, inclusive: the raster's rect (tx0, tx1, ty0, ty1)
+// (hi == nullptr, one tile layer) or the voxelizer's brick box lo = (x0, y0,
+// z0), hi = (x1, y1, z1). Tile id = (z * tiles_y + y) * tiles_x + x.
+struct Box {
+  int x0, x1, y0, y1, z0, z1;
+};
+__device__ __forceinline__ Box load_box(const short4* __restrict__ a, const short4* __restrict__ b, long long i,
+                                        bool valid) {
+  Box r{0, -1, 0, -1, 0, -1};
+  if (!valid) return r;
+  const short4 p = __ldg(a + i);
+  if (!b) return Box{p.x, p.y, p.z, p.w, 0, 0};
+  const short4 q = __ldg(b + i);
+  return Box{p.x, q.x, p.y, q.y, p.z, q.z};
+}
+__device__ __forceinline__ bool box_empty(const Box& r) { return r.x1 < r.x0 || r.y1 < r.y0 || r.z1 < r.z0; }
+
+__global__ void __launch_bounds__(256) bin_count_kernel(const short4* __restrict__ rect, const short4* __restrict__ hi,
+                                                        long long m, int chunk, int T, int tiles_x, int tiles_y,
+                                                        int32_t* __restrict__ H) {
   extern __shared__ uint32_t hist[];
   const int c = blockIdx.x, v = blockIdx.y;
   for (int t = threadIdx.x; t < T; t += blockDim.x) hist[t] = 0;
   __syncthreads();
   const long long i0 = (long long)v * m + (long long)c * chunk;
   const long long i1 = (long long)v * m + min((long long)(c + 1) * chunk, m);
-  // four rectangles in flight per thread (the loop is latency-bound otherwise)
+  // four boxes in flight per thread (the loop is latency-bound otherwise)
   for (long long i = i0 + threadIdx.x; i < i1; i += 4 * blockDim.x) {
-    short4 r[4];
+    Box r[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      r[k] = i + k * blockDim.x < i1 ? __ldg(rect + i + k * blockDim.x) : make_short4(0, -1, 0, -1);
+    for (int k = 0; k < 4; ++k) r[k] = load_box(rect, hi, i + k * blockDim.x, i + k * blockDim.x < i1);
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      for (int ty = r[k].z; ty <= r[k].w; ++ty)
-        for (int tx = r[k].x; tx <= r[k].y; ++tx) atomicAdd(&hist[ty * tiles_x + tx], 1u);
+    for (int k = 0; k < 4; ++k) {
+      if (box_empty(r[k])) continue;
+      for (int tz = r[k].z0; tz <= r[k].z1; ++tz)
+        for (int ty = r[k].y0; ty <= r[k].y1; ++ty)
+          for (int tx = r[k].x0; tx <= r[k].x1; ++tx) atomicAdd(&hist[(tz * tiles_y + ty) * tiles_x + tx], 1u);
+    }
   }
   __syncthreads();
   int32_t* h = H + ((long long)v * gridDim.x + c) * T;  // block-major [view][chunk][tile], coalesced
@@ -186,7 +206,8 @@ __global__ void __launch_bounds__(256) bin_segscan_kernel(int32_t* __restrict__ 
 }
 // one block: exclusive prefix of the column totals -> tile_base[0..T], tile_base[T] = pairs
 __global__ void __launch_bounds__(1024) bin_tilebase_kernel(const int32_t* __restrict__ coltot, int T,
-                                                            int32_t* __restrict__ tile_base) {
+                                                            int32_t* __restrict__ tile_base, long long cap,
+                                                            int* __restrict__ overflow, int32_t* __restrict__ total) {
   __shared__ int32_t part[1024];
   const int per = (T + blockDim.x - 1) / blockDim.x;
   const int t0 = min(T, (int)threadIdx.x * per), t1 = min(T, t0 + per);
@@ -205,7 +226,17 @@ __global__ void __launch_bounds__(1024) bin_tilebase_kernel(const int32_t* __res
     tile_base[t] = run;
     run += coltot[t];
   }
-  if (threadIdx.x == blockDim.x - 1) tile_base[T] = part[threadIdx.x];
+  if (threadIdx.x == blockDim.x - 1) {
+    tile_base[T] = part[threadIdx.x];
+    if (total) *total = part[threadIdx.x];
+    if ((long long)part[threadIdx.x] > cap) atomicOr(overflow, 1);
+  }
+}
+
+// capacity mode: flag a count scan whose total exceeds the pair buffers
+__global__ void count_check_kernel(const int32_t* __restrict__ offset_end, const long long* __restrict__ sum64,
+                                   long long cap, int* __restrict__ overflow) {
+  if ((long long)*offset_end > cap || *sum64 > cap || *offset_end < 0) atomicOr(overflow, 1);
 }
 __global__ void __launch_bounds__(256) bin_apply_kernel(int32_t* __restrict__ H, const int32_t* __restrict__ seg,
                                                         const int32_t* __restrict__ tile_base, int n_rows, int T) {
@@ -213,23 +244,30 @@ __global__ void __launch_bounds__(256) bin_apply_kernel(int32_t* __restrict__ H,
   if (t >= T) return;
   const int r0 = g * kSegRows, r1 = min(n_rows, r0 + kSegRows);
   int32_t run = tile_base[t] + seg[(long long)g * T + t];
-  for (int r = r0; r < r1; ++r) {
-    const long long k = (long long)r * T + t;
-    const int32_t x = H[k];
-    H[k] = run;  // in place: H becomes S
-    run += x;
+  // 16 loads in flight before the in-place stores (H becomes S)
+  for (int rb = r0; rb < r1; rb += 16) {
+    int32_t x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = rb + k < r1 ? H[(long long)(rb + k) * T + t] : 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (rb + k < r1) H[(long long)(rb + k) * T + t] = run;
+      run += x[k];
+    }
   }
 }
 
-__global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short4* __restrict__ rect, long long m,
+__global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short4* __restrict__ rect,
+                                                                     const short4* __restrict__ hi, long long m,
                                                                      int chunk, int T, int tiles_x, int tiles_y,
-                                                                     const int32_t* __restrict__ S,
-                                                                     int32_t* __restrict__ vals) {
+                                                                     int tiles_z, const int32_t* __restrict__ S,
+                                                                     int32_t* __restrict__ vals, uint32_t cap) {
   extern __shared__ uint32_t sm[];
   uint32_t* cnt = sm;                              // [kBinWarps][T]
   uint32_t* colm = sm + kBinWarps * T;             // [kBinWarps][tiles_x]
   uint32_t* rowm = colm + kBinWarps * tiles_x;     // [kBinWarps][tiles_y]
-  short4* srect = reinterpret_cast<short4*>(rowm + kBinWarps * tiles_y);  // [chunk] the block's rectangles
+  uint32_t* laym = rowm + kBinWarps * tiles_y;     // [kBinWarps][tiles_z]
+  short4* sbox = reinterpret_cast<short4*>(laym + kBinWarps * tiles_z);  // [chunk][2] the block's boxes
   const int c = blockIdx.x, v = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long i0 = (long long)v * m + (long long)c * chunk;
@@ -239,19 +277,25 @@ __global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short
   uint32_t* mycnt = cnt + warp * T;
   uint32_t* mycol = colm + warp * tiles_x;
   uint32_t* myrow = rowm + warp * tiles_y;
+  uint32_t* mylay = laym + warp * tiles_z;
   for (int t = threadIdx.x; t < kBinWarps * T; t += blockDim.x) cnt[t] = 0;
   __syncthreads();
-  // phase A: per-warp tile counts; the rectangles are kept in shared memory
-  // for phase C (four loads in flight per lane)
+  // phase A: per-warp tile counts; the boxes are kept in shared memory for
+  // phase C (four loads in flight per lane)
   for (long long i = w0 + lane; i < w1; i += 4 * 32) {
-    short4 r[4];
+    Box r[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) r[k] = i + 32 * k < w1 ? __ldg(rect + i + 32 * k) : make_short4(0, -1, 0, -1);
+    for (int k = 0; k < 4; ++k) r[k] = load_box(rect, hi, i + 32 * k, i + 32 * k < w1);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (i + 32 * k < w1) srect[i + 32 * k - i0] = r[k];
-      for (int ty = r[k].z; ty <= r[k].w; ++ty)
-        for (int tx = r[k].x; tx <= r[k].y; ++tx) atomicAdd(&mycnt[ty * tiles_x + tx], 1u);
+      if (i + 32 * k >= w1) continue;
+      sbox[2 * (i + 32 * k - i0)] = make_short4(r[k].x0, r[k].x1, r[k].y0, r[k].y1);
+      sbox[2 * (i + 32 * k - i0) + 1] = make_short4(r[k].z0, r[k].z1, 0, 0);
+      if (box_empty(r[k])) continue;
+      for (int tz = r[k].z0; tz <= r[k].z1; ++tz)
+        for (int ty = r[k].y0; ty <= r[k].y1; ++ty)
+          for (int tx = r[k].x0; tx <= r[k].x1; ++tx)
+            atomicAdd(&mycnt[(tz * tiles_y + ty) * tiles_x + tx], 1u);
     }
   }
   __syncthreads();
@@ -267,32 +311,47 @@ __global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short
     }
   }
   __syncthreads();
-  // phase C: rounds of 32 items in item order; stable rank by row / column masks
+  // phase C: rounds of 32 items in item order; a box is the product of a
+  // column, a row and a layer range, so the stable rank of a pair among the
+  // round's earlier items is popc(colmask & rowmask & layermask & lanes_below)
   const uint32_t below = (1u << lane) - 1u;
   for (long long base = w0; base < w1; base += 32) {
     const long long i = base + lane;
-    short4 r = make_short4(0, -1, 0, -1);
-    if (i < w1) r = srect[i - i0];
+    Box r{0, -1, 0, -1, 0, -1};
+    if (i < w1) {
+      const short4 p = sbox[2 * (i - i0)], q = sbox[2 * (i - i0) + 1];
+      r = Box{p.x, p.y, p.z, p.w, q.x, q.y};
+    }
     for (int k = lane; k < tiles_x; k += 32) mycol[k] = 0;
     for (int k = lane; k < tiles_y; k += 32) myrow[k] = 0;
+    for (int k = lane; k < tiles_z; k += 32) mylay[k] = 0;
     __syncwarp();
     const uint32_t bit = 1u << lane;
-    if (r.y >= r.x && r.w >= r.z) {
-      for (int tx = r.x; tx <= r.y; ++tx) atomicOr(&mycol[tx], bit);
-      for (int ty = r.z; ty <= r.w; ++ty) atomicOr(&myrow[ty], bit);
+    const bool any = !box_empty(r);
+    if (any) {
+      for (int tx = r.x0; tx <= r.x1; ++tx) atomicOr(&mycol[tx], bit);
+      for (int ty = r.y0; ty <= r.y1; ++ty) atomicOr(&myrow[ty], bit);
+      for (int tz = r.z0; tz <= r.z1; ++tz) atomicOr(&mylay[tz], bit);
     }
     __syncwarp();
-    for (int ty = r.z; ty <= r.w; ++ty) {
-      const uint32_t rm = myrow[ty];
-      for (int tx = r.x; tx <= r.y; ++tx) {
-        const int t = ty * tiles_x + tx;
-        const uint32_t rank = __popc(mycol[tx] & rm & below);
-        vals[mycnt[t] + rank] = (int32_t)i;
+    if (any) {
+      for (int tz = r.z0; tz <= r.z1; ++tz) {
+        const uint32_t lm = mylay[tz] & below;
+        for (int ty = r.y0; ty <= r.y1; ++ty) {
+          const uint32_t rm = myrow[ty] & lm;
+          for (int tx = r.x0; tx <= r.x1; ++tx) {
+            const int t = (tz * tiles_y + ty) * tiles_x + tx;
+            const uint32_t pos = mycnt[t] + __popc(mycol[tx] & rm);
+            if (pos < cap) vals[pos] = (int32_t)i;  // beyond: capacity overflow (flagged by bin_tilebase)
+          }
+        }
       }
     }
     __syncwarp();
-    for (int ty = r.z; ty <= r.w; ++ty)
-      for (int tx = r.x; tx <= r.y; ++tx) atomicAdd(&mycnt[ty * tiles_x + tx], 1u);
+    if (any)
+      for (int tz = r.z0; tz <= r.z1; ++tz)
+        for (int ty = r.y0; ty <= r.y1; ++ty)
+          for (int tx = r.x0; tx <= r.x1; ++tx) atomicAdd(&mycnt[(tz * tiles_y + ty) * tiles_x + tx], 1u);
     __syncwarp();
   }
 }
@@ -1157,25 +1216,38 @@ void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32
 // Counting-scatter binning (bin_* kernels above). Needs the per-warp tile
 // table in shared memory: T <= kMaxScatterTiles, else the caller keeps the
 // radix-sort path. Returns false when not applicable.
-bool raster_bin_scatter_fits(int tiles_x, int tiles_y) {
-  const int64_t T = (int64_t)tiles_x * tiles_y;
-  return kBinWarps * (T + tiles_x + tiles_y) * 4 + 256 * (int64_t)sizeof(short4) <= kScatterSmem &&
+static int64_t scatter_tables(int64_t tx, int64_t ty, int64_t tz) {
+  return kBinWarps * (tx * ty * tz + tx + ty + tz) * (int64_t)sizeof(uint32_t);
+}
+bool bin_scatter_fits(int tiles_x, int tiles_y, int tiles_z) {
+  const int64_t T = (int64_t)tiles_x * tiles_y * tiles_z;
+  return scatter_tables(tiles_x, tiles_y, tiles_z) + 256 * 2 * (int64_t)sizeof(short4) <= kScatterSmem &&
          T * 4 <= 48 * 1024;  // bin_count's histogram (default shared limit)
 }
+bool raster_bin_scatter_fits(int tiles_x, int tiles_y) { return bin_scatter_fits(tiles_x, tiles_y, 1); }
 
-int launch_raster_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, const short4* rect,
-                              int32_t* vals, int2* ranges, int64_t n_pairs) {
-  const int64_t T = (int64_t)tiles_x * tiles_y;
-  if (n_pairs == 0 || m == 0) return SCT_OK;
+void launch_count_check(Ctx* c, const int32_t* offset_end, int64_t cap) {
+  count_check_kernel<<<1, 1, 0, c->stream>>>(offset_end, c->sum64, (long long)cap, c->overflow);
+}
+
+// Stable counting-scatter binning of n_views x m items with boxes (lo, hi)
+// over a tiles_x x tiles_y x tiles_z tile grid (raster: hi == nullptr, one
+// layer). cap: size of vals (pairs beyond it are dropped and flag
+// c->overflow); total (nullable): device word receiving the pair count;
+// ranges [n_views][T] (nullable when only the totals are needed).
+int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, int tiles_z, const short4* lo,
+                       const short4* hi, int32_t* vals, int2* ranges, int64_t cap, int32_t* total) {
+  const int64_t T = (int64_t)tiles_x * tiles_y * tiles_z;
+  if (m == 0 || n_views == 0) return SCT_OK;
   // chunk size: the count table H holds (V * chunks) x T entries (<= ~64M), and
-  // the scatter keeps a chunk's rectangles in shared memory next to its tables
+  // the scatter keeps a chunk's boxes in shared memory next to its tables
   const int64_t target = 64ll << 20;
   static const int64_t min_chunk = [] {
     const char* e = std::getenv("SCT_BIN_CHUNK");
     return e ? std::max<int64_t>(256, atoll(e)) : 1024;
   }();
-  const int64_t tables = (kBinWarps * (T + tiles_x + tiles_y)) * sizeof(uint32_t);
-  const int64_t max_chunk = ((kScatterSmem - tables) / (int64_t)sizeof(short4)) / 256 * 256;
+  const int64_t tables = scatter_tables(tiles_x, tiles_y, tiles_z);
+  const int64_t max_chunk = ((kScatterSmem - tables) / (2 * (int64_t)sizeof(short4))) / 256 * 256;
   int64_t chunk = std::max<int64_t>(min_chunk, (m * n_views * T + target - 1) / target);
   chunk = std::min<int64_t>(((chunk + 255) / 256) * 256, max_chunk);
   const int64_t n_chunks = (m + chunk - 1) / chunk;
@@ -1189,29 +1261,31 @@ int launch_raster_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, i
   const dim3 grid((unsigned)n_chunks, (unsigned)n_views);
   {
     KScope _ks(c, "K2_bin_count");
-    bin_count_kernel<<<grid, 256, T * sizeof(uint32_t), c->stream>>>(rect, m, (int)chunk, (int)T, tiles_x, H);
+    bin_count_kernel<<<grid, 256, T * sizeof(uint32_t), c->stream>>>(lo, hi, m, (int)chunk, (int)T, tiles_x, tiles_y,
+                                                                     H);
   }
   {
     KScope _ks(c, "K2_bin_scan");
     const dim3 g2((unsigned)((T + 255) / 256), (unsigned)n_seg);
     bin_colsum_kernel<<<g2, 256, 0, c->stream>>>(H, (int)rows, (int)T, seg);
     bin_segscan_kernel<<<(unsigned)((T + 255) / 256), 256, 0, c->stream>>>(seg, (int)n_seg, (int)T, tb);
-    bin_tilebase_kernel<<<1, 1024, 0, c->stream>>>(tb, (int)T, tb2);
+    bin_tilebase_kernel<<<1, 1024, 0, c->stream>>>(tb, (int)T, tb2, (long long)cap, c->overflow, total);
     bin_apply_kernel<<<g2, 256, 0, c->stream>>>(H, seg, tb2, (int)rows, (int)T);
   }
   {
     KScope _ks(c, "K2_bin_scatter");
-    const size_t smem = (kBinWarps * (T + tiles_x + tiles_y)) * sizeof(uint32_t) + chunk * sizeof(short4);
+    const size_t smem = tables + chunk * 2 * sizeof(short4);
     static bool attr = false;
     if (!attr) {
       SCT_CUDA_TRY(cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kScatterSmem));
       attr = true;
     }
-    bin_scatter_kernel<<<grid, 32 * kBinWarps, smem, c->stream>>>(rect, m, (int)chunk, (int)T, tiles_x, tiles_y, H,
-                                                                  vals);
+    bin_scatter_kernel<<<grid, 32 * kBinWarps, smem, c->stream>>>(
+        lo, hi, m, (int)chunk, (int)T, tiles_x, tiles_y, tiles_z, H, vals,
+        (uint32_t)std::min<int64_t>(cap, UINT32_MAX));
   }
-  {
+  if (ranges) {
     KScope _ks(c, "K2_bin_ranges");
     bin_ranges_kernel<<<grid_cap(c, n_views * T, 256), 256, 0, c->stream>>>(H, tb2, (int)n_chunks, (int)n_views,
                                                                             (int)T, ranges);
@@ -1220,6 +1294,12 @@ int launch_raster_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, i
   dev_free(c, seg);
   dev_free(c, tb);
   return SCT_OK;
+}
+
+int launch_raster_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, const short4* rect,
+                              int32_t* vals, int2* ranges, int64_t n_pairs, int64_t cap, int32_t* total) {
+  if (n_pairs == 0) return SCT_OK;
+  return launch_bin_scatter(c, n_views, m, tiles_x, tiles_y, 1, rect, nullptr, vals, ranges, cap, total);
 }
 
 void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,

@@ -94,6 +94,11 @@ struct Ctx {
   size_t cub_tmp_bytes = 0;
   int64_t* pinned_count = nullptr;  // small pinned host words (128 B) for D2H of counts
   long long* sum64 = nullptr;       // device word: int64 total of a count scan
+  // sync-free binning (sct_ctx_set_capacity): pair buffers of a fixed capacity
+  // instead of a host readback of the pair count; a device overflow word is
+  // set when a call's pairs exceed it (sct_ctx_take_overflow)
+  int64_t cap_raster = 0, cap_voxel = 0;
+  int* overflow = nullptr;
   int sm_count = 148;
   // copy stream + events for the host-buffer entry points (H2D/D2H of view
   // chunks overlap the compute of neighbouring chunks)
@@ -244,6 +249,8 @@ struct sct_fwd {
   uint8_t* d_vis = nullptr;            // [items] visible flag
   void* d_keys = nullptr;              // [pairs] sorted tile keys (uint16 if tile_bits <= 16, else uint32)
   int32_t* d_vals = nullptr;           // [pairs] sorted item index
+  bool exact = true;                   // n_pairs is the pair count (else the capacity; count in d_total)
+  int32_t* d_total = nullptr;          // [1] pair count on the device (capacity mode)
   int2* d_ranges = nullptr;            // [V*T] [start,end) into sorted pairs
   double* d_prep = nullptr;            // [kPrepStride][m] (SoA) Sigma (9), rho, Sigma^-1 (6), det, FP64
 };
@@ -270,7 +277,11 @@ void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32
                         void* keys, bool keys16, int32_t* vals);
 bool raster_bin_scatter_fits(int tiles_x, int tiles_y);
 int launch_raster_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, const short4* rect,
-                              int32_t* vals, int2* ranges, int64_t n_pairs);
+                              int32_t* vals, int2* ranges, int64_t n_pairs, int64_t cap, int32_t* total);
+void launch_count_check(Ctx* c, const int32_t* offset_end, int64_t cap);
+bool bin_scatter_fits(int tiles_x, int tiles_y, int tiles_z);
+int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, int tiles_z, const short4* lo,
+                       const short4* hi, int32_t* vals, int2* ranges, int64_t cap, int32_t* total);
 void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,
                           int64_t tiles_per_view, int2* ranges);
 void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images);
@@ -283,8 +294,11 @@ int launch_raster_composite_units(Ctx* c, const sct_fwd* s, float* images, UnitS
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0 = 0,
                                   int nv = 0, float* item_stats = nullptr, const UnitSync* us = nullptr);
 void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, const int32_t* offset,
-                       int32_t bricks_x, int32_t bricks_y, void* keys, bool keys16, int32_t* vals);
-void launch_key_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, int2* ranges);
+                       int32_t bricks_x, int32_t bricks_y, void* keys, bool keys16, int32_t* vals,
+                       int64_t cap = INT64_MAX);
+// keys >= n_keys are capacity-mode padding (sorted after every real key) and are skipped
+void launch_key_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, int2* ranges,
+                       int64_t n_keys = INT64_MAX);
 void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x,
                        int32_t bricks_y, const int2* ranges, const int32_t* vals, const float4* rec,
                        const sct_cloud& cl, int64_t n_pairs, float* vol);

@@ -46,7 +46,8 @@ template <typename KeyT>
 __global__ void __launch_bounds__(256) voxel_emit_kernel(long long m, const short4* __restrict__ lo,
                                                          const short4* __restrict__ hi,
                                                          const int32_t* __restrict__ offset, int bx, int by,
-                                                         KeyT* __restrict__ keys, int32_t* __restrict__ vals) {
+                                                         KeyT* __restrict__ keys, int32_t* __restrict__ vals,
+                                                         long long cap) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long w0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < m;
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256) voxel_emit_kernel(long long m, const shor
       const int jxy = __shfl_sync(0xffffffffu, axy, j);
       const int jn = __shfl_sync(0xffffffffu, nxy, j);
       const int jz = __shfl_sync(0xffffffffu, az, j);
-      if (p < o_end) {
+      if (p < o_end && p < cap) {  // cap: capacity-mode buffers (the overflow is flagged by the count check)
         const int x0 = (short)(jxy & 0xffff), y0 = (short)(jxy >> 16);
         const int nx = jn & 0xffff, ny = jn >> 16;
         const int rank = p - oj;
@@ -93,10 +94,11 @@ __global__ void __launch_bounds__(256) voxel_emit_kernel(long long m, const shor
 // [start, end) of each key's run in the sorted pairs (key = slot)
 template <typename KeyT>
 __global__ void __launch_bounds__(256) key_ranges_kernel(long long n_pairs, const KeyT* __restrict__ keys,
-                                                         int2* __restrict__ ranges) {
+                                                         int2* __restrict__ ranges, long long n_keys) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_pairs;
        p += (long long)gridDim.x * blockDim.x) {
     const KeyT k = keys[p];
+    if ((long long)k >= n_keys) continue;  // capacity-mode padding (sorted last)
     if (p == 0) ranges[k].x = 0;
     if (p == n_pairs - 1) {
       ranges[k].y = (int)n_pairs;
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(256) key_ranges_kernel(long long n_pairs, cons
       const KeyT k2 = keys[p + 1];
       if (k2 != k) {
         ranges[k].y = (int)(p + 1);
-        ranges[k2].x = (int)(p + 1);
+        if ((long long)k2 < n_keys) ranges[k2].x = (int)(p + 1);
       }
     }
   }
@@ -742,28 +744,30 @@ BrickGeo make_geo(const sct_grid& g, int zb0, int zb1, int bx, int by) {
 }  // namespace
 
 void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, const int32_t* offset,
-                       int32_t bricks_x, int32_t bricks_y, void* keys, bool keys16, int32_t* vals) {
+                       int32_t bricks_x, int32_t bricks_y, void* keys, bool keys16, int32_t* vals, int64_t cap) {
   if (m == 0) return;
   long long b = (m + 255) / 256;
   if (b > (long long)c->sm_count * 16) b = (long long)c->sm_count * 16;
   KScope _ks(c, "K6_voxel_emit");
   if (keys16)
     voxel_emit_kernel<uint16_t><<<(int)b, 256, 0, c->stream>>>(m, lo, hi, offset, bricks_x, bricks_y,
-                                                               static_cast<uint16_t*>(keys), vals);
+                                                               static_cast<uint16_t*>(keys), vals, (long long)cap);
   else
     voxel_emit_kernel<uint32_t><<<(int)b, 256, 0, c->stream>>>(m, lo, hi, offset, bricks_x, bricks_y,
-                                                               static_cast<uint32_t*>(keys), vals);
+                                                               static_cast<uint32_t*>(keys), vals, (long long)cap);
 }
 
-void launch_key_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, int2* ranges) {
+void launch_key_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, int2* ranges, int64_t n_keys) {
   if (n_pairs == 0) return;
   long long b = (n_pairs + 255) / 256;
   if (b > (long long)c->sm_count * 16) b = (long long)c->sm_count * 16;
   KScope _ks(c, "K2_ranges");
   if (keys16)
-    key_ranges_kernel<uint16_t><<<(int)b, 256, 0, c->stream>>>(n_pairs, static_cast<const uint16_t*>(keys), ranges);
+    key_ranges_kernel<uint16_t><<<(int)b, 256, 0, c->stream>>>(n_pairs, static_cast<const uint16_t*>(keys), ranges,
+                                                                (long long)n_keys);
   else
-    key_ranges_kernel<uint32_t><<<(int)b, 256, 0, c->stream>>>(n_pairs, static_cast<const uint32_t*>(keys), ranges);
+    key_ranges_kernel<uint32_t><<<(int)b, 256, 0, c->stream>>>(n_pairs, static_cast<const uint32_t*>(keys), ranges,
+                                                                (long long)n_keys);
 }
 
 void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int32_t bricks_x, int32_t bricks_y,

@@ -295,6 +295,18 @@ class Engine:
     def kernel_launches(self) -> int:
         return int(self.lib.sct_ctx_kernel_launches(self._h))
 
+    def set_capacity(self, raster_pairs: int = 0, voxel_pairs: int = 0):
+        """Sync-free binning: fixed-capacity pair buffers instead of a host readback of
+        each binning's pair count (0 = exact mode, the default). Pairs beyond a capacity
+        are dropped and recorded; check take_overflow() before trusting results."""
+        _check(self.lib.sct_ctx_set_capacity(self._h, int(raster_pairs), int(voxel_pairs)))
+
+    def take_overflow(self) -> bool:
+        """Synchronises; True when a capacity-mode binning overflowed since the last call."""
+        f = C.c_int32(0)
+        _check(self.lib.sct_ctx_take_overflow(self._h, C.byref(f)))
+        return bool(f.value)
+
     def set_timing(self, enable: bool):
         """Bracket every engine launch with CUDA events on the context stream."""
         _check(self.lib.sct_ctx_set_timing(self._h, int(enable)))

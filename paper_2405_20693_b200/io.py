@@ -2,7 +2,10 @@
 header line, then little-endian float32 payload arrays. Clouds (.ckpt),
 volumes (.vol) and images (.img) written here are readable by the reference
 and vice versa; the float32 payload is exactly the engine's device layout, so
-loading is one read into pinned memory and one H2D copy per array.
+the device fast path is one read of the whole payload into one pinned staging
+buffer and ONE host-to-device copy (the arrays are views of that device
+buffer); saving is one device-to-host copy of all arrays into one pinned
+buffer and one write.
 
 Extension (the reference does not save optimizer state, io.cpp:201-211): with
 ``include_adam=True`` the Adam moments are appended after the four parameter
@@ -37,6 +40,41 @@ def _write(path: str, header: dict, arrays) -> None:
                 f.write(np.ascontiguousarray(a, dtype="<f4").tobytes())
     except OSError as e:
         raise DataError(f"cannot write {path}: {e}") from e
+
+
+def _device_payload(path: str, payload: bytes, count: int, device) -> torch.Tensor:
+    """The first `count` floats of the payload on `device`: one pinned staging
+    buffer, one (non-blocking) H2D copy."""
+    if 4 * count > len(payload):
+        raise FileFormatError(f"{path}: truncated payload")
+    host = torch.frombuffer(bytearray(payload[:4 * count]), dtype=torch.float32) if count else \
+        torch.empty(0, dtype=torch.float32)
+    if str(device) == "cpu" or not torch.cuda.is_available():
+        return host.clone()
+    pinned = torch.empty(count, dtype=torch.float32, pin_memory=True)
+    pinned.copy_(host)
+    out = torch.empty(count, dtype=torch.float32, device=device)
+    out.copy_(pinned, non_blocking=True)
+    torch.cuda.current_stream(out.device).synchronize()  # the pinned buffer is released on return
+    return out
+
+
+def _host_arrays(tensors) -> list:
+    """Device tensors -> host numpy arrays through ONE device-to-host copy into
+    one pinned buffer (one pass over PCIe instead of one per array)."""
+    ts = [t.detach().reshape(-1) for t in tensors]
+    if not ts or not all(t.is_cuda for t in ts):
+        return [t.cpu().numpy() for t in ts]
+    flat = torch.cat([t.to(torch.float32) for t in ts])
+    pinned = torch.empty(flat.numel(), dtype=torch.float32, pin_memory=True)
+    pinned.copy_(flat, non_blocking=True)
+    torch.cuda.current_stream(flat.device).synchronize()
+    out, off = [], 0
+    host = pinned.numpy()
+    for t in ts:
+        out.append(host[off:off + t.numel()])
+        off += t.numel()
+    return out
 
 
 def _read(path: str):
@@ -75,12 +113,12 @@ def save_cloud(cloud: GaussianCloud, path: str, include_adam: bool = False) -> N
          "activations": {"density": "softplus", "scale": "exp_floor"}, "s_min_mm": cloud.s_min,
          "fields": ["rho_raw", "positions_mm", "scales_raw", "rotations_wxyz"], "dtype": "float32",
          "endianness": "little", "version": 1}
-    arrays = [t.detach().cpu().numpy() for t in (cloud.rho_raw, cloud.pos, cloud.scale_raw, cloud.rot)]
+    tensors = [cloud.rho_raw, cloud.pos, cloud.scale_raw, cloud.rot]
     if include_adam:
         keys = ["m_rho", "v_rho", "m_pos", "v_pos", "m_scale", "v_scale", "m_rot", "v_rot"]
         h["fields_extra"] = ["adam_" + k for k in keys]
-        arrays += [cloud.adam[k].detach().cpu().numpy() for k in keys]
-    _write(path, h, arrays)
+        tensors += [cloud.adam[k] for k in keys]
+    _write(path, h, _host_arrays(tensors))
 
 
 def load_cloud(path: str, device="cuda") -> GaussianCloud:
@@ -93,22 +131,22 @@ def load_cloud(path: str, device="cuda") -> GaussianCloud:
     act = h.get("activations")
     if act is not None and (act.get("density") != "softplus" or act.get("scale") != "exp_floor"):
         raise FileFormatError(f"{path}: unsupported activation names")
-    off = 0
-    rho, off = _take(path, payload, off, m)
-    pos, off = _take(path, payload, off, 3 * m)
-    sc, off = _take(path, payload, off, 3 * m)
-    rot, off = _take(path, payload, off, 4 * m)
-    pin = (lambda a: torch.from_numpy(a).pin_memory()) if torch.cuda.is_available() and str(device) != "cpu" \
-        else torch.from_numpy
-    cloud = GaussianCloud(float(h.get("s_min_mm", 1e-4)), pin(rho), pin(pos), pin(sc), pin(rot), device=device)
-    extra = h.get("fields_extra") or []
+    extra = [n for n in (h.get("fields_extra") or []) if n.startswith("adam_")]
     sizes = {"rho": m, "pos": 3 * m, "scale": 3 * m, "rot": 4 * m}
+    n_extra = sum(sizes[n[len("adam_"):].split("_", 1)[1]] for n in extra)
+    # the parameters (and the optional moments) in one transfer
+    dev = _device_payload(path, payload, 11 * m + n_extra, device)
+    off = 0
+    parts = []
+    for n in (m, 3 * m, 3 * m, 4 * m):
+        parts.append(dev[off:off + n])
+        off += n
+    cloud = GaussianCloud(float(h.get("s_min_mm", 1e-4)), *parts, device=device)
     for name in extra:
-        if not name.startswith("adam_"):
-            continue
         k = name[len("adam_"):]
-        a, off = _take(path, payload, off, sizes[k.split("_", 1)[1]])
-        cloud.adam[k].copy_(torch.from_numpy(a))
+        n = sizes[k.split("_", 1)[1]]
+        cloud.adam[k].copy_(dev[off:off + n])
+        off += n
     return cloud
 
 

@@ -26,8 +26,8 @@ from typing import Optional, Sequence
 import numpy as np
 import torch
 
-from .engine import (CloudGrads, DivergenceDetected, Engine, GaussianCloud, GridSpec, HostRng, RasterOptions,
-                     ScannerConfig, lr_at)
+from .engine import (CloudGrads, DataError, DivergenceDetected, Engine, GaussianCloud, GridSpec, HostRng,
+                     RasterOptions, ScannerConfig, lr_at)
 
 
 @dataclass
@@ -52,6 +52,13 @@ class TrainConfig:  # trainer.hpp:13-44 (the fields the iteration uses)
     seed: int = 0
     mode: int = 0
     check_every: int = 1  # iterations between host-side non-finite checks
+    # Sync-free binning (Engine.set_capacity): after a calibration iteration in
+    # exact mode (the first one, and the first after each adaptive control) the
+    # pair buffers get `capacity_margin` x the measured pair counts and no
+    # binning reads its count back to the host. Overflow is checked with the
+    # non-finite check (every check_every iterations) and raises DataError.
+    sync_free: bool = False
+    capacity_margin: float = 3.0
 
 
 def random_subvolume_origin(lo, hi, spacing, d, u):
@@ -82,6 +89,7 @@ class Trainer:
         self.rng = HostRng(cfg.seed)
         self.order = np.arange(len(self.angles), dtype=np.int32)  # trainer.cpp:255-256
         self.epoch_pos = len(self.angles)  # forces a shuffle on first use
+        self._calibrate = cfg.sync_free  # next iteration measures the pair counts (exact mode)
 
     def next_view(self) -> int:
         """Shuffled epochs (trainer.cpp:269-273): the order is reshuffled in place."""
@@ -98,7 +106,11 @@ class Trainer:
         t = self.t
         if view is None:
             view = self.next_view()
+        calibrate = self._calibrate
+        if calibrate:
+            eng.set_capacity(0, 0)
         fwd = eng.render(cloud, self.scanner, self.angles[view], self.opts)
+        raster_pairs = fwd.n_pairs() if calibrate else 0
         vals, dL = eng.photometric_loss(fwd.images, self.measured_norm[view:view + 1], render_scale=self.inv_norm,
                                         lambda_ssim=cfg.lambda_ssim, grad_scale=self.inv_norm)
         self.grads.zero_()  # grads.resize(M), trainer.cpp:283
@@ -111,13 +123,29 @@ class Trainer:
                                                        self.output_spacing, cfg.tv_grid_dim)
             d = cfg.tv_grid_dim
             sub = GridSpec((d, d, d), sub_origin, self.output_spacing)
+            if calibrate:  # the densest sub-grid placement bounds the TV binning
+                full = GridSpec(tuple(int(round((self.scanner.extent_max_mm[k] - self.scanner.extent_min_mm[k])
+                                                / self.output_spacing[k])) for k in range(3)),
+                                tuple(self.scanner.extent_min_mm), self.output_spacing)
+                self._voxel_pairs = max(1, eng.voxel_work(cloud, full)[1])
             vol, vstate = eng.voxelize(cloud, sub, keep_state=True)  # bins once for fwd + bwd
             tv, g_tv = eng.tv3d_loss(vol, cfg.lambda_tv)
             eng.voxelize_backward(cloud, sub, g_tv, self.grads, state=vstate)
             vstate.free()
         total = vals[0, 0] + cfg.lambda_ssim * vals[0, 1] + cfg.lambda_tv * tv  # trainer.cpp:302-303
-        if cfg.check_every and t % cfg.check_every == 0 and not math.isfinite(float(total.item())):
-            raise DivergenceDetected(f"non-finite loss at iteration {t}")
+        if cfg.check_every and t % cfg.check_every == 0:
+            if not math.isfinite(float(total.item())):
+                raise DivergenceDetected(f"non-finite loss at iteration {t}")
+            if cfg.sync_free and not calibrate and eng.take_overflow():
+                raise DataError(f"sync-free binning exceeded its pair capacity by iteration {t}; "
+                                "raise TrainConfig.capacity_margin")
+        if calibrate:
+            # a sub-grid's pairs are bounded by the full-extent grid's (same brick size; at
+            # most 8x from the brick alignment), capped by the margin
+            vp = getattr(self, "_voxel_pairs", 0)
+            eng.set_capacity(int(cfg.capacity_margin * raster_pairs) + 65536,
+                             int(min(8 * vp, cfg.capacity_margin * vp)) + 65536 if cfg.lambda_tv > 0.0 else 0)
+            self._calibrate = False
         lrs = [lr_at(cfg.lr_position, cfg.lr_final_ratio, t, cfg.iters),
                lr_at(cfg.lr_density, cfg.lr_final_ratio, t, cfg.iters),
                lr_at(cfg.lr_scale, cfg.lr_final_ratio, t, cfg.iters),
@@ -141,4 +169,5 @@ class Trainer:
             split_scale_threshold_frac=cfg.split_scale_threshold_frac, split_factor=cfg.split_factor, gauss=gauss,
             rng=self.rng if gauss is None else None)
         self.grads.resize(self.cloud.size(), device=self.eng.device)
+        self._calibrate = cfg.sync_free  # new kernel count: re-measure the pair counts
         return counts
