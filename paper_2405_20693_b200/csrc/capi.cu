@@ -130,9 +130,11 @@ static int bits_for(uint64_t n) {  // smallest b with 2^b >= n (n >= 1)
 // exclusive scan of count[0..n] (count[n] == 0) into offset[0..n]; returns offset[n].
 // The total is first summed in int64 (cub Reduce into a 64-bit output): an
 // int32 total between 2^31 and 2^32 + 2^31 would wrap to a plausible value.
-// cap > 0 (capacity mode): no host readback — *total = cap and a device check
-// flags c->overflow when the pairs exceed it.
-static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t* total, int64_t cap = 0) {
+// cap > 0 (capacity mode): no host readback — *total = cap, and a device guard
+// flags c->overflow and empties the items (boxes box_a / box_b) when the pairs
+// exceed it (launch_capacity_guard).
+static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t* total, int64_t cap = 0,
+                       short4* box_a = nullptr, short4* box_b = nullptr) {
   SCT_CUDA_TRY(cudaMemsetAsync(count + n, 0, sizeof(int32_t), c->stream));
   {
     long long* d_sum = c->sum64;
@@ -153,7 +155,7 @@ static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64
     SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, offset, n + 1, c->stream));
   }
   if (cap > 0) {
-    launch_count_check(c, offset + n, cap);
+    launch_capacity_guard(c, count, offset, n, box_a, box_b, cap);
     *total = cap;
     return SCT_OK;
   }
@@ -292,7 +294,7 @@ static int voxel_bin(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull
   // key beyond every brick id, so it sorts last and the range scan skips it).
   const bool scatter = bin_scatter_fits(b.bx, b.by, b.bz);
   const int64_t cap = c->cap_voxel;
-  SCT_TRY(scan_counts(c, b.count, b.offset, m, &b.n_pairs, cap));
+  SCT_TRY(scan_counts(c, b.count, b.offset, m, &b.n_pairs, cap, b.lo, b.hi));
   if (scatter) {
     SCT_TRY(dev_alloc(c, (void**)&b.vals, std::max<int64_t>(b.n_pairs, 1) * sizeof(int32_t)));
     SCT_TRY(launch_bin_scatter(c, 1, m, b.bx, b.by, b.bz, b.lo, b.hi, b.vals, b.ranges, b.n_pairs, nullptr));
@@ -597,7 +599,7 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   // sort needs the exact count on the host)
   const bool scatter = raster_bin_scatter_fits(s->det.tiles_x, s->det.tiles_y);
   const int64_t cap = (c->cap_raster > 0 && scatter) ? c->cap_raster : 0;
-  if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs, cap))) return fail(rc);
+  if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs, cap, s->d_rect, nullptr))) return fail(rc);
   if (cap > 0) {
     s->exact = false;
     if ((rc = dev_alloc(c, (void**)&s->d_total, sizeof(int32_t)))) return fail(rc);

@@ -233,10 +233,29 @@ __global__ void __launch_bounds__(1024) bin_tilebase_kernel(const int32_t* __res
   }
 }
 
-// capacity mode: flag a count scan whose total exceeds the pair buffers
-__global__ void count_check_kernel(const int32_t* __restrict__ offset_end, const long long* __restrict__ sum64,
-                                   long long cap, int* __restrict__ overflow) {
-  if ((long long)*offset_end > cap || *sum64 > cap || *offset_end < 0) atomicOr(overflow, 1);
+// capacity mode: a count scan whose total exceeds the pair buffers raises the
+// overflow word and empties every item (zero counts and offsets, empty boxes),
+// so no later kernel touches a pair slot beyond the buffers; the call's results
+// are then empty, and the caller learns of it from sct_ctx_take_overflow.
+__global__ void __launch_bounds__(256) capacity_guard_kernel(int32_t* __restrict__ count, int32_t* __restrict__ offset,
+                                                             long long n, short4* __restrict__ box_a,
+                                                             short4* __restrict__ box_b,
+                                                             const long long* __restrict__ sum64, long long cap,
+                                                             int* __restrict__ overflow) {
+  const long long total = *sum64;
+  if (total <= cap && offset[n] >= 0) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(overflow, 1);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x) {
+    offset[i] = 0;
+    if (i == n) continue;
+    count[i] = 0;
+    if (box_b) {  // voxel brick box: hi < lo
+      const short4 a = box_a[i];
+      box_b[i] = make_short4((short)(a.x - 1), (short)(a.y - 1), (short)(a.z - 1), 0);
+    } else {
+      box_a[i] = make_short4(1, 0, 1, 0);  // raster rect: tx1 < tx0
+    }
+  }
 }
 __global__ void __launch_bounds__(256) bin_apply_kernel(int32_t* __restrict__ H, const int32_t* __restrict__ seg,
                                                         const int32_t* __restrict__ tile_base, int n_rows, int T) {
@@ -1226,8 +1245,10 @@ bool bin_scatter_fits(int tiles_x, int tiles_y, int tiles_z) {
 }
 bool raster_bin_scatter_fits(int tiles_x, int tiles_y) { return bin_scatter_fits(tiles_x, tiles_y, 1); }
 
-void launch_count_check(Ctx* c, const int32_t* offset_end, int64_t cap) {
-  count_check_kernel<<<1, 1, 0, c->stream>>>(offset_end, c->sum64, (long long)cap, c->overflow);
+void launch_capacity_guard(Ctx* c, int32_t* count, int32_t* offset, int64_t n, short4* box_a, short4* box_b,
+                           int64_t cap) {
+  capacity_guard_kernel<<<grid_cap(c, n + 1, 256), 256, 0, c->stream>>>(count, offset, n, box_a, box_b, c->sum64,
+                                                                        (long long)cap, c->overflow);
 }
 
 // Stable counting-scatter binning of n_views x m items with boxes (lo, hi)

@@ -1,11 +1,14 @@
 """Sync-free binning (Engine.set_capacity / sct_ctx_set_capacity): fixed-capacity
 pair buffers instead of a host readback of each binning's pair count.
 
-* results are identical to exact mode (tile lists, brick lists, images,
-  volumes, gradients) for the raster and the voxel path;
-* a capacity below the pair count raises the overflow word (and only then);
-* the train loop in sync-free mode reproduces exact mode bit for bit,
-  densification included.
+* tile and brick lists are identical to exact mode; images, volumes and
+  gradients agree to FP32 rounding (the host-side work split of K3 / K4 / K8
+  follows the pair count in exact mode and the capacity in capacity mode, which
+  can regroup a list's 16-kernel chunks);
+* a capacity below the pair count raises the overflow word (and only then),
+  and the overflowing call is emptied rather than writing past its buffers;
+* the train loop in sync-free mode reproduces exact mode (same densification
+  events and kernel counts, parameters to FP32 rounding).
 """
 import numpy as np
 import pytest
@@ -55,8 +58,9 @@ def test_capacity_mode_matches_exact_mode():
     for (oa, ia), (ob, ib) in zip(a[0], b[0]):
         np.testing.assert_array_equal(oa, ob)
         np.testing.assert_array_equal(ia, ib)
-    for x, y in zip(a[1:5], b[1:5]):
-        assert torch.equal(x, y)
+    for name, x, y in zip(("images", "raster grads", "volume", "voxel grads"), a[1:5], b[1:5]):
+        err = float(torch.linalg.norm((x - y).double()) / torch.linalg.norm(x.double()))
+        assert err < 1e-5, (name, err)
     assert a[5] == b[5] and not b[6]
 
 
@@ -67,7 +71,8 @@ def test_capacity_overflow_is_flagged():
     eng = P.Engine(0)
     eng.set_capacity(1000, 1000)
     f = eng.render(c, P.ScannerConfig(detector_res_px=(128, 128)), [0.3])
-    assert f.n_pairs() > 1000
+    # an overflowing call is emptied (no pair is written beyond the buffers) and flagged
+    assert f.n_pairs() == 0 and float(f.images.abs().sum()) == 0.0
     assert eng.take_overflow()
     assert not eng.take_overflow()  # cleared
     eng.voxelize(c, P.grid_for_extent((-1, -1, -1), (1, 1, 1), (32, 32, 32)))
@@ -98,4 +103,5 @@ def test_sync_free_training_matches_exact_training():
         runs[sync_free] = (sizes, tr.cloud)
     assert runs[False][0] == runs[True][0] and len(set(runs[True][0])) > 1
     for k in ("rho_raw", "pos", "scale_raw", "rot"):
-        assert torch.equal(getattr(runs[False][1], k), getattr(runs[True][1], k)), k
+        x, y = getattr(runs[False][1], k).double(), getattr(runs[True][1], k).double()
+        assert float(torch.linalg.norm(x - y) / torch.linalg.norm(x)) < 1e-4, k
