@@ -244,6 +244,10 @@ struct RenderedProjection {
   Image image;
   int tiles_x = 0, tiles_y = 0;
   std::shared_ptr<sct_fwd> state;
+  // what the device state was built with: render_backward rebuilds nothing, so
+  // a backward call with another angle or other options is rejected
+  double theta_rad = 0.0;
+  RasterOptions opts;
   // tile_visible expressed in kernel indices (visible[vi].kernel_index)
   std::vector<std::vector<int>> tile_kernels() const {
     const int T = tiles_x * tiles_y;
@@ -273,12 +277,23 @@ inline RenderedProjection render(const GaussianCloud& cloud, const ScannerConfig
   r.image.data.assign(img.begin(), img.end());
   r.tiles_x = (w + 15) / 16;
   r.tiles_y = (h + 15) / 16;
+  r.theta_rad = theta_rad;
+  r.opts = opts;
   return r;
 }
 
-inline void render_backward(GaussianCloud& cloud, const ScannerConfig& config, double /*theta_rad*/,
+// rasterizer.cpp:195-198. The reference re-projects each visible kernel with the
+// caller's theta_rad / opts (rasterizer.cpp:199,266); the engine keeps the forward
+// pass's projection on the device, so both must equal the forward call's.
+inline void render_backward(GaussianCloud& cloud, const ScannerConfig& config, double theta_rad,
                             const RenderedProjection& fwd, const Image& dL_dimage, CloudGrads& grads,
-                            const RasterOptions& /*opts*/ = {}, bool accumulate_stats = false) {
+                            const RasterOptions& opts = {}, bool accumulate_stats = false) {
+  if (!fwd.state) throw ConfigError("render_backward: no forward state");
+  const RasterOptions& f = fwd.opts;
+  if (theta_rad != fwd.theta_rad || opts.mode != f.mode || opts.lowpass_eps_px != f.lowpass_eps_px ||
+      opts.dilation_compensation != f.dilation_compensation || opts.freeze_jacobian != f.freeze_jacobian ||
+      opts.cull_mahalanobis != f.cull_mahalanobis)
+    throw ConfigError("render_backward: theta_rad / opts differ from the forward call's");
   if (dL_dimage.width != config.detector_res_px[0] || dL_dimage.height != config.detector_res_px[1])
     throw DimMismatch("render_backward: upstream gradient dims mismatch");
   const int m = cloud.size();

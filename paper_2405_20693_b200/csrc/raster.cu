@@ -22,6 +22,7 @@
 #include <string>
 
 #include "sct_internal.cuh"
+#include "tcgen05.cuh"
 
 namespace sct {
 
@@ -1210,6 +1211,358 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
   }
 }
 
+// K4 on the 5th-generation tensor cores (tcgen05 + TMEM): SCT_K4=tc. Measured at
+// parity with the mma.sync form at cfg3 (1.91 vs 1.88 ms, DESIGN.md §3 "K4"): K4 is
+// bound by issuing the E evaluation, which both forms share, not by the MMA; the
+// mma.sync form stays the default and serves the host-buffer (unit-pipelined) path.
+// Same product M = E G as above, transposed onto the Blackwell datapath:
+//   * thread = kernel: a CTA holds 128 kernels of a (view, tile) list per chunk,
+//     kernel i of the chunk owning TMEM lane i. Each thread evaluates its
+//     kernel's E over the tile (exp2 recurrence, rows 2q and 2q+1 packed in
+//     FP32x2) and stores it as binary16 pairs straight into tensor memory
+//     (tcgen05.st): A[kernel][pixel], one row pair (16 columns) per buffer,
+//     kTcABuf buffers in flight;
+//   * G (hi/lo binary16, moments n = 0..5 hi, 8..13 lo) sits in shared memory
+//     in the canonical K-major no-swizzle layout, built once per tile;
+//   * a fifth warp issues tcgen05.mma kind::f16 M=128 N=16 K=16 (two per row
+//     pair, FP32 accumulate in TMEM, D double-buffered per chunk) and
+//     tcgen05.commit releases the A buffer / publishes D through mbarriers;
+//   * each thread reads its kernel's 16 accumulator columns (tcgen05.ld) and
+//     applies the binomial shift: no fragment shuffles, no B-fragment LDS.
+//     The epilogue of chunk c runs in the middle of chunk c + 1, when its
+//     MMAs have long completed.
+// Records and list indices are staged per thread with cp.async (one and two
+// chunks ahead; each thread reads back only what it copied itself).
+// Numerics are those of the mma.sync form (same E, same G split, FP32 accumulate).
+// Persistent CTAs take (list, part) work items from a global counter in the
+// given order; empty lists are skipped by the claiming thread.
+constexpr int kTcWarps = 4;  // compute warps (128 TMEM lanes)
+constexpr int kTcThreads = 32 * (kTcWarps + 1);
+constexpr int kTcABuf = 4;  // row-pair A buffers (16 TMEM columns each)
+constexpr uint32_t kTcDCol = 16 * kTcABuf;
+constexpr uint32_t kTcCols = 128;  // A 4 x 16, D 2 x 16 (+ 32 spare)
+#ifndef SCT_K4TC_CTAS
+#define SCT_K4TC_CTAS 4
+#endif
+constexpr int kTcCtas = SCT_K4TC_CTAS;  // CTAs per SM (kTcCols TMEM columns each, <= 512 per SM)
+static_assert(kTcCtas * kTcCols <= 512, "TMEM columns per SM");
+constexpr uint32_t kSleepNs = 0x100000;  // mbarrier waits: stay suspended until the phase completes
+
+// byte offset of G[n][k] (moment n, pixel k) in the K-major no-swizzle layout:
+// core matrix (k / 8, n / 8) of 8 rows x 16 bytes; LBO (next 8 pixels) = 256 B,
+// SBO (next 8 moments) = 128 B; the K = 16 slice j starts at 512 j
+__device__ __forceinline__ int g_off(int n, int k) { return ((k >> 3) * 2 + (n >> 3)) * 128 + (n & 7) * 16 + (k & 7) * 2; }
+
+struct TcRow {  // per-kernel constants of the E evaluation (scalars: FFMA2 / FMUL2 take them as broadcast operands)
+  float A, A2, B, C, K, dx, cy;
+  bool ok;
+};
+__device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
+
+// E of rows 2q (.x) and 2q+1 (.y), 16 columns, into A buffer q % kTcABuf.
+// MODE 0: one 8-run per half row, 1: two 4-runs, 2: direct evaluation.
+template <int MODE>
+__device__ __forceinline__ void tc_row_pair(const TcRow& k, int q, float py0, uint32_t tl, uint64_t* aempty,
+                                            uint64_t* afull, uint32_t parity, int lane) {
+  const float py = py0 + (float)(2 * q);
+  const float2 dy = make_float2(py - k.cy, py + 1.f - k.cy);
+  const float2 bdy = __fmul2_rn(bc(k.B), dy);
+  const float2 apb = __fadd2_rn(bc(k.A), bdy);
+  float2 cdy2o = __ffma2_rn(__fmul2_rn(bc(k.C), dy), dy, make_float2(15.f, 15.f));
+  if (!k.ok) cdy2o = make_float2(-1e30f, -1e30f);
+  const int b = q % kTcABuf;
+  tc::mbar_wait_sleep(&aempty[b], parity ^ 1, kSleepNs);
+  tc::fence_after_sync();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // columns 8h .. 8h+7
+    float2 e[8];
+    const float2 dxh = bc(k.dx + 8.f * h);
+    if (MODE == 0) {
+      run8x2(e, dxh, bc(k.A), bc(k.A2), bdy, apb, cdy2o, bc(k.K));
+    } else if (MODE == 1) {
+      run4x2(e, dxh, bc(k.A), bc(k.A2), bdy, apb, cdy2o, bc(k.K));
+      run4x2(e + 4, bc(k.dx + 8.f * h + 4.f), bc(k.A), bc(k.A2), bdy, apb, cdy2o, bc(k.K));
+    } else {
+      direct8x2(e, dxh, bc(k.A), bdy, cdy2o);
+    }
+    uint32_t p0[4], p1[4];  // pixel pairs of row 2q (A columns 16b + 4h ..) / 2q+1 (16b + 8 + 4h ..)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      p0[j] = h2_bits(__floats2half2_rn(e[2 * j].x, e[2 * j + 1].x));
+      p1[j] = h2_bits(__floats2half2_rn(e[2 * j].y, e[2 * j + 1].y));
+    }
+    tc::tmem_st4(tl + 16 * b + 4 * h, p0);
+    tc::tmem_st4(tl + 16 * b + 8 + 4 * h, p1);
+  }
+  tc::tmem_wait_st();
+  tc::fence_before_sync();
+  __syncwarp();
+  if (lane == 0) tc::mbar_arrive(&afull[b]);
+}
+
+template <int MODE>
+__device__ __forceinline__ void tc_rows4(const TcRow& k, int q0, float py0, uint32_t tl, uint64_t* aempty,
+                                         uint64_t* afull, uint32_t parity, int lane) {
+#pragma unroll 1
+  for (int q = q0; q < q0 + 4; ++q) tc_row_pair<MODE>(k, q, py0, tl, aempty, afull, parity, lane);
+}
+
+__global__ void __launch_bounds__(kTcThreads, kTcCtas) backward_stats_tc_kernel(
+    const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
+    const short4* __restrict__ rect, const int32_t* __restrict__ offset, int tiles_x, int tiles_per_view, int W,
+    int H, int view0, const int* __restrict__ order, int parts, int n_work, int* __restrict__ work,
+    const float* __restrict__ dL, float* __restrict__ pair_stats, float* __restrict__ item_stats, UnitSync us) {
+  __shared__ __align__(1024) unsigned char s_g[16 * 256 * 2];
+  __shared__ __align__(8) uint64_t bar_afull[kTcABuf], bar_aempty[kTcABuf], bar_dfull[2], bar_dempty[2];
+  __shared__ __align__(16) float4 s_rec[2][32 * kTcWarps][2];  // per-thread staging (own slots)
+  __shared__ int s_idx[2][32 * kTcWarps];
+  __shared__ uint32_t s_taddr;
+  __shared__ int4 s_item[2];  // current / next work item
+  __shared__ float s_gmax[kTcWarps];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool issuer = warp == kTcWarps;
+  // zero moments 6, 7, 14, 15 once (never rewritten)
+  for (int e = tid; e < 4 * 256; e += kTcThreads) {
+    const int n = (e >> 8) < 2 ? 6 + (e >> 8) : 12 + (e >> 8), k = e & 255;
+    *reinterpret_cast<__half*>(s_g + g_off(n, k)) = __float2half(0.f);
+  }
+  tc::fence_proxy_async_smem();
+  if (warp == 0) {
+    tc::tmem_alloc(&s_taddr, kTcCols);
+    tc::tmem_relinquish();
+  }
+  if (tid == 0) {
+    for (int b = 0; b < kTcABuf; ++b) {
+      tc::mbar_init(&bar_afull[b], kTcWarps);
+      tc::mbar_init(&bar_aempty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&bar_dfull[b], 1);
+      tc::mbar_init(&bar_dempty[b], kTcWarps);
+    }
+    tc::mbar_init_fence();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = s_taddr;
+  const uint32_t tlane = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+  const uint32_t idesc = tc::idesc_f16_f32(128, 16);
+  uint32_t ck = 0;  // chunks so far: A buffer uses (2 per chunk) and D buffer phases
+  // claim the next non-empty (list, part) in the order: {work index, list, start, end};
+  // empty lists are published right away (host path)
+  auto claim = [&]() -> int4 {
+    for (;;) {
+      const int c = atomicAdd(work, 1);
+      if (c >= n_work) return make_int4(-1, 0, 0, 0);
+      const int w = order[c / parts], p = c % parts;
+      const int2 rg = ranges[(long long)view0 * tiles_per_view + w];
+      const int len = rg.y - rg.x;
+      const int a0 = rg.x + (int)((long long)len * p / parts), a1 = rg.x + (int)((long long)len * (p + 1) / parts);
+      if (a1 > a0) return make_int4(c, w, a0, a1);
+      if (us.done) unit_signal(us, unit_of_view(view0 + w / tiles_per_view, us.n_views, us.units));
+    }
+  };
+  const bool host_path = us.done != nullptr || us.ready != nullptr;
+  if (tid == 0) {
+    const int4 f = claim();
+    if (f.x >= 0 && us.ready) unit_wait(us, unit_of_view(view0 + f.y / tiles_per_view, us.n_views, us.units));
+    s_item[0] = f;
+  }
+  __syncthreads();
+  for (int cur = 0;; cur ^= 1) {
+    const int4 itm = s_item[cur];
+    if (itm.x < 0) break;
+    const int w = itm.y;
+    const int tile = w % tiles_per_view, view = view0 + w / tiles_per_view;
+    const int2 rg = make_int2(itm.z, itm.w);
+    const int n_list = rg.y - rg.x;
+    const int n_chunks = (n_list + 127) >> 7;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int u0 = tx * kTilePx, v0 = ty * kTilePx;
+    if (issuer) {
+      __syncthreads();  // G of this tile is ready
+      // ---------------- MMA issue: per chunk, 8 row pairs x 2 K-slices into D[ck & 1]
+      for (int ch = 0; ch < n_chunks; ++ch, ++ck) {
+        const uint32_t d = ck & 1;
+        tc::mbar_wait_sleep(&bar_dempty[d], ((ck >> 1) & 1) ^ 1, kSleepNs);
+        tc::fence_after_sync();
+        const uint32_t dt = tbase + kTcDCol + 16 * d;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int b = q % kTcABuf;
+          const uint32_t use = 2 * ck + q / kTcABuf;  // uses of buffer b so far
+          tc::mbar_wait_sleep(&bar_afull[b], use & 1, kSleepNs);
+          tc::fence_after_sync();
+          if (lane == 0) {
+            const uint32_t at = tbase + 16 * b;
+            tc::mma_f16_ts(dt, at, tc::smem_desc_kmajor(s_g + 512 * (2 * q), 256, 128), idesc, q > 0);
+            tc::mma_f16_ts(dt, at + 8, tc::smem_desc_kmajor(s_g + 512 * (2 * q + 1), 256, 128), idesc, 1);
+            tc::commit(&bar_aempty[b]);  // A buffer b free once these MMAs completed
+            if (q == 7) tc::commit(&bar_dfull[d]);
+          }
+          __syncwarp();
+        }
+        if (ch == 0 && lane == 0) s_item[cur ^ 1] = claim();  // the next item, while this one runs
+      }
+    } else {
+      // ---------------- G of this tile (per-tile power-of-two scale, hi/lo split)
+      float inv_s;
+      {
+        const float* dtile = dL + ((long long)view * H + v0) * W + u0;
+        const bool streamed = us.ready != nullptr;  // host path: L2-coherent loads (copies still landing)
+        float g[2];
+        float gm = 0.f;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int p = tid + 128 * i, r = p >> 4, cc = p & 15;
+          const float* src = dtile + (long long)r * W + cc;
+          g[i] = (v0 + r < H && u0 + cc < W) ? (streamed ? __ldcg(src) : __ldg(src)) : 0.f;
+          gm = fmaxf(gm, fabsf(g[i]));
+        }
+        gm = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gm)));
+        if (lane == 0) s_gmax[warp] = gm;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcWarps) : "memory");
+#pragma unroll
+        for (int k = 0; k < kTcWarps; ++k) gm = fmaxf(gm, s_gmax[k]);
+        const float S = gm > 0.f ? exp2f(floorf(log2f(16384.f / (gm * 56.25f * 0x1p-15f)))) : 1.f;
+        const float gscale = 0x1p-15f * S;
+        inv_s = 1.f / S;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int p = tid + 128 * i, r = p >> 4, cc = p & 15;
+          const float gs = g[i] * gscale, cp = (float)cc - 7.5f, rpf = (float)r - 7.5f;
+          const float phi[6] = {1.f, cp, rpf, cp * cp, rpf * rpf, cp * rpf};
+#pragma unroll
+          for (int n = 0; n < 6; ++n) {
+            const float v = gs * phi[n];
+            const __half hi = __float2half_rn(v);
+            *reinterpret_cast<__half*>(s_g + g_off(n, p)) = hi;
+            *reinterpret_cast<__half*>(s_g + g_off(8 + n, p)) = __float2half_rn(v - __half2float(hi));
+          }
+        }
+        tc::fence_proxy_async_smem();  // G -> visible to the tensor core
+      }
+      // prologue of the staging pipeline: index 0 (direct), record 0 and index 1 (cp.async)
+      {
+        const int it0 = tid < n_list ? vals[rg.x + tid] : -1;
+        s_idx[0][tid] = it0;
+        float4* dst = &s_rec[0][tid][0];
+        if (it0 >= 0) {
+          cp_async16(dst, rec + 2 * (long long)it0);
+          cp_async16(dst + 1, rec + 2 * (long long)it0 + 1);
+        } else {
+          dst[0] = make_float4(0.f, 0.f, 0.f, 1.f);
+          dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (128 + tid < n_list) cp_async4(&s_idx[1][tid], vals + rg.x + 128 + tid);
+        else s_idx[1][tid] = -1;
+        cp_async_commit();
+      }
+      __syncthreads();  // G ready for the issuer
+      const float px0 = (float)u0 + 0.5f, py0 = (float)v0 + 0.5f;
+      // pending epilogue (the previous chunk of this list)
+      int pend_it = -1;
+      float pend_cx = 0.f, pend_cy = 0.f;
+      uint32_t pend_ck = 0;
+      auto epilogue = [&]() {
+        const uint32_t d = pend_ck & 1;
+        tc::mbar_wait_sleep(&bar_dfull[d], (pend_ck >> 1) & 1, kSleepNs);
+        tc::fence_after_sync();
+        uint32_t acc[16];
+        tc::tmem_ld16(tlane + kTcDCol + 16 * d, acc);
+        tc::tmem_wait_ld();
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&bar_dempty[d]);
+        if (pend_it < 0) return;
+        float m[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) m[k] = (__uint_as_float(acc[k]) + __uint_as_float(acc[8 + k])) * inv_s;
+        const float ox = (float)(u0 + 8) - pend_cx;
+        const float oy = (float)(v0 + 8) - pend_cy;
+        float st[6];
+        st[0] = m[0];
+        st[1] = fmaf(ox, m[0], m[1]);
+        st[2] = fmaf(oy, m[0], m[2]);
+        st[3] = fmaf(ox, fmaf(ox, m[0], 2.f * m[1]), m[3]);
+        st[4] = fmaf(oy, fmaf(oy, m[0], 2.f * m[2]), m[4]);
+        st[5] = fmaf(ox, fmaf(oy, m[0], m[2]), fmaf(oy, m[1], m[5]));
+        if (item_stats) {
+          float4* dst = reinterpret_cast<float4*>(item_stats + 8 * (long long)pend_it);
+          atomicAdd(dst, make_float4(st[0], st[1], st[2], st[3]));
+          atomicAdd(reinterpret_cast<float2*>(dst + 1), make_float2(st[4], st[5]));
+        } else {
+          const short4 r = rect[pend_it];
+          const long long slot = offset[pend_it] + (ty - r.z) * (r.y - r.x + 1) + (tx - r.x);
+          float4* dst = reinterpret_cast<float4*>(pair_stats + 8 * slot);
+          dst[0] = make_float4(st[0], st[1], st[2], st[3]);
+          *reinterpret_cast<float2*>(dst + 1) = make_float2(st[4], st[5]);
+        }
+      };
+      for (int ch = 0; ch < n_chunks; ++ch, ++ck) {
+        cp_async_wait_all();  // record ch, index ch + 1 (own slots)
+        const int sb = ch & 1;
+        const int it = s_idx[sb][tid];
+        const float4 ra = s_rec[sb][tid][0], rb = s_rec[sb][tid][1];  // {cx, cy, amp, K}, {A, B, C, 2A}
+        if (ch + 1 < n_chunks) {  // stage record ch + 1 and index ch + 2
+          const int itn = s_idx[sb ^ 1][tid];
+          float4* dst = &s_rec[sb ^ 1][tid][0];
+          if (itn >= 0) {
+            cp_async16(dst, rec + 2 * (long long)itn);
+            cp_async16(dst + 1, rec + 2 * (long long)itn + 1);
+          } else {
+            dst[0] = make_float4(0.f, 0.f, 0.f, 1.f);
+            dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          const int e2 = (ch + 2) * 128 + tid;
+          if (e2 < n_list) cp_async4(&s_idx[sb][tid], vals + rg.x + e2);
+          else s_idx[sb][tid] = -1;
+          cp_async_commit();
+        }
+        TcRow k;
+        k.A = rb.x;
+        k.B = rb.y;
+        k.C = rb.z;
+        k.A2 = rb.w;
+        k.K = ra.w;
+        k.dx = px0 - ra.x;
+        k.cy = ra.y;
+        k.ok = it >= 0;
+        const float aa = fabsf(rb.x);
+        const int mode = __all_sync(0xffffffffu, aa <= 1.25f) ? 0 : __any_sync(0xffffffffu, aa > kRun4MaxA_K4) ? 2 : 1;
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {  // A-buffer use 2 ck + half: parity = half
+          if (mode == 0) tc_rows4<0>(k, 4 * half, py0, tlane, bar_aempty, bar_afull, half, lane);
+          else if (mode == 1) tc_rows4<1>(k, 4 * half, py0, tlane, bar_aempty, bar_afull, half, lane);
+          else tc_rows4<2>(k, 4 * half, py0, tlane, bar_aempty, bar_afull, half, lane);
+          if (half == 0 && ch > 0) epilogue();
+        }
+        pend_it = it;
+        pend_cx = ra.x;
+        pend_cy = ra.y;
+        pend_ck = ck;
+      }
+      if (n_chunks > 0) epilogue();
+      if (us.done) __threadfence();
+    }
+    // every chunk's accumulator was read (so every MMA reading G completed)
+    // before the next tile's G overwrites it; the next item is in s_item[cur ^ 1]
+    __syncthreads();
+    if (host_path) {  // publish this list's unit, wait for the next one's upstream gradient
+      if (tid == 0) {
+        if (us.done) unit_signal(us, unit_of_view(view, us.n_views, us.units));
+        const int4 nx = s_item[cur ^ 1];
+        if (nx.x >= 0 && us.ready) unit_wait(us, unit_of_view(view0 + nx.y / tiles_per_view, us.n_views, us.units));
+      }
+      __syncthreads();
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, kTcCols);
+}
+
 int grid_cap(Ctx* c, long long n, int block) {
   long long b = (n + block - 1) / block;
   const long long cap = (long long)c->sm_count * 16;
@@ -1472,15 +1825,19 @@ static const int* unit_tile_order(Ctx* c, const sct_fwd* s, int units) {
   return c->order_ptr;
 }
 
-// SCT_K4=simt selects the FP32 SIMT statistics kernel (the reference-order
-// arithmetic without tensor cores); default: the tensor-core kernel
-static bool k4_simt() {
-  static const bool simt = [] {
+enum class K4Impl { kTc, kMma, kSimt };
+// SCT_K4 selects the statistics kernel: "mma" (default: mma.sync f16, FP32
+// accumulate), "tc" (tcgen05 + TMEM; device-resident calls only), "simt" (FP32
+// SIMT, no tensor cores: the reference-order arithmetic)
+static K4Impl k4_impl() {
+  static const K4Impl impl = [] {
     const char* e = std::getenv("SCT_K4");
-    return e && std::string(e) == "simt";
+    const std::string v = e ? e : "";
+    return v == "simt" ? K4Impl::kSimt : v == "tc" ? K4Impl::kTc : K4Impl::kMma;
   }();
-  return simt;
+  return impl;
 }
+static bool k4_simt() { return k4_impl() == K4Impl::kSimt; }
 
 static int composite_per_sm() {
   static int per_sm = 0;
@@ -1635,6 +1992,17 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
   while (parts < 16 && total * parts * 2 <= (long long)c->sm_count * 8 && avg_len / (2 * parts) >= 64.0) parts *= 2;
   UnitSync ks = us ? *us : UnitSync{};
   ks.per_view = T * parts;
+  if (k4_impl() == K4Impl::kTc && !ks.ready && !ks.done) {
+    int* work = nullptr;
+    if (stage_buf(c, 20, sizeof(int) * 4, (void**)&work) != SCT_OK) return;
+    cudaMemsetAsync(work + 1, 0, sizeof(int), c->stream);
+    const long long n_work = total * parts;
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((long long)c->sm_count * kTcCtas, n_work));
+    backward_stats_tc_kernel<<<blocks, kTcThreads, 0, c->stream>>>(
+        s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
+        parts, (int)n_work, work + 1, dL, ps, item_stats, ks);
+    return;
+  }
   backward_stats_mma_kernel<<<(unsigned)(total * parts), 32 * kMmaWarps, 0, c->stream>>>(
       s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
       parts, dL, ps, item_stats, ks);

@@ -132,6 +132,21 @@ int main() {
   } catch (const S::DimMismatch&) {
     fails += report("DimMismatch thrown", 0, 0);
   }
+  // backward with another angle / other options than the forward call: rejected
+  try {
+    S::render_backward(cloud, cfg, theta + 0.1, fwd, up, g);
+    fails += report("ConfigError on theta mismatch", 1, 0);
+  } catch (const S::ConfigError&) {
+    fails += report("ConfigError on theta mismatch", 0, 0);
+  }
+  try {
+    S::RasterOptions frozen;
+    frozen.freeze_jacobian = true;
+    S::render_backward(cloud, cfg, theta, fwd, up, g, frozen);
+    fails += report("ConfigError on opts mismatch", 1, 0);
+  } catch (const S::ConfigError&) {
+    fails += report("ConfigError on opts mismatch", 0, 0);
+  }
   orc_rng_free(rng);
   std::printf("%s (%d failures)\n", fails ? "FAIL" : "ALL PASS", fails);
   return fails;
