@@ -29,7 +29,49 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "projections/sec (fwd+bwd)"
+DTYPE = ("fp32 pixel sums (K4/K8: E rounded to binary16 with a hi/lo binary16 split of g, FP32 accumulate, "
+         "on the tensor pipe; fp32_simt_arm = the all-FP32 SIMT form); FP64 binning preprocess + chain rules")
 UNIT = "projections/s"
+
+# Hardware-unit evidence per kernel (ncu, tools/profile_round2.sh -> tools/hw_units.py):
+# the busiest unit (issue slots, FP32/FP64/XU/tensor pipes, L1 wavefronts, L2, DRAM)
+# and its fraction of peak. Static: read from the committed profile, not measured here.
+HW_PROFILE = "profiles/r02b_hw_units.json"
+NCU_NAMES = {
+    "K0_gauss_prep": ["gauss_prep_kernel"], "K1_raster_preprocess": ["raster_preprocess_kernel"],
+    "K2_bin_count": ["bin_count_kernel"],
+    "K2_bin_scan": ["bin_colsum_kernel", "bin_segscan_kernel", "bin_tilebase_kernel", "bin_apply_kernel"],
+    "K2_bin_scatter": ["bin_scatter_kernel"], "K2_bin_ranges": ["bin_ranges_kernel"],
+    "K2_tile_order": ["tile_order_keys_kernel"], "K2_k3_items": ["k3_parts_kernel", "k3_items_kernel"],
+    "K3_composite": ["composite_kernel"], "K4_backward_stats": ["backward_stats_mma_kernel"],
+    "K5_raster_chain": ["raster_chain_kernel<0>"], "K5_view_sum": ["view_sum_kernel"],
+    "K5_raster_finalize": ["raster_finalize_kernel"],
+    "K6_voxel_preprocess": ["voxel_preprocess_kernel"], "K6_voxel_emit": ["voxel_emit_kernel<unsigned short>"],
+    "K2_ranges": ["key_ranges_kernel<unsigned short>"], "K7_voxel_eval": ["voxel_eval_kernel"],
+    "K8_voxel_backward_stats": ["voxel_backward_mma_kernel"], "K8_voxel_pair_sum": ["voxel_pair_sum_kernel"],
+    "K8_voxel_chain": ["voxel_chain_kernel"],
+    "K9_tv3d": ["tv3d_kernel", "tv3d_finish_kernel"], "K10_adam": ["adam_kernel"],
+    "K11_ssim": ["ssim_h_kernel", "ssim_v_kernel", "ssim_adj_v_kernel", "ssim_adj_h_kernel",
+                 "photometric_finish_kernel"],
+    "AC_adaptive": ["ac_classify_kernel", "ac_apply_kernel"],
+}
+
+
+def hw_units():
+    try:
+        return json.load(open(os.path.join(ROOT, HW_PROFILE)))
+    except Exception:
+        return {}
+
+
+def hw_of(units, key):
+    """{unit, frac, dram_gbs_under_ncu, thread_inst_per_launch} of the busiest ncu launch family of a kernel."""
+    rows = [units[n] for n in NCU_NAMES.get(key, []) if n in units]
+    if not rows:
+        return None
+    r = max(rows, key=lambda x: x["ncu_us_per_launch"] * x["launches"])
+    return {"unit": r["bound_unit"], "frac": r["bound_frac"], "dram_gbs_under_ncu": r["dram_gbs_under_ncu"],
+            "units": r["units"], "source": HW_PROFILE + " (ncu, cold cache, not this run)"}
 
 
 def parse():
@@ -44,6 +86,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-voxel", action="store_true")
     p.add_argument("--no-train", action="store_true")
+    p.add_argument("--no-simt-arm", action="store_true",
+                   help="skip the FP32 SIMT arm (SCT_K4=simt SCT_K8=simt, a child process at N=1)")
     p.add_argument("--reduction", default="atomic", choices=["deterministic", "atomic"],
                    help="backward reduction: the parallel-atomic mode the north star prescribes (warp/tensor "
                         "pre-reduction, then global atomics per kernel; SPEC.md:224-226), or the reference's "
@@ -317,6 +361,13 @@ def run_engine(args):
     fwd = step()
     gpe, n_pairs = fwd.work()  # this rank's algorithmic work per step
     fwd.free()
+    # sync-free binning (capacity mode): the pair buffers are sized from the measured
+    # count, so no step reads a count back to the host; overflow is checked after timing
+    capacity = int(n_pairs * 1.02) + 65536
+    eng.set_capacity(capacity, 0)
+    for _ in range(2):
+        step().free()
+    torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
@@ -341,6 +392,8 @@ def run_engine(args):
         f.free()
     barrier()
     clocks = sampler.stop()
+    if eng.take_overflow():
+        raise RuntimeError(f"capacity-mode binning overflowed ({capacity} pair slots)")
     kt = eng.timing_report()
     eng.set_timing(False)
     launches = eng.kernel_launches() - launches0
@@ -371,6 +424,11 @@ def run_engine(args):
         ach = flops_per_gpe[name] * gpe / (ms / args.steps / 1000.0) / 1e12  # all launches of a step
         kernels[name]["achieved_tflops"] = ach
         kernels[name]["frac_fp32_peak"] = ach / fp32_peak
+    hw = hw_units()
+    for name in kernels:
+        h = hw_of(hw, name)
+        if h:
+            kernels[name]["hw"] = {k: v for k, v in h.items() if k != "units"}
     dname = dom if dom in flops_per_gpe else max(flops_per_gpe, key=lambda k: kt[k][0])
     ms, n = kt[dname]
     ach = flops_per_gpe[dname] * gpe / (ms / args.steps / 1000.0) / 1e12
@@ -393,19 +451,34 @@ def run_engine(args):
         # the FP32 pipes execute, reported against the same peak.
         simt = 13 * gpe / (ms / args.steps / 1000.0) / 1e12
         rf.update({"simt_achieved": simt, "simt_frac": simt / fp32_peak,
-                   "note": "frac > 1: 15 of the 28 algorithmic FLOP/GPE run on tensor cores (mma.sync f16, "
-                           "FP32 accumulate); simt_frac is the FP32-pipe share (13 FLOP/GPE) vs the FP32 peak"})
+                   "note": "frac is algorithmic (SURVEY.md 8d: 28 FLOP/GPE as if every pixel evaluated the "
+                           "quadratic form, an exp and 6 moment FMAs) and exceeds 1 because the kernel executes "
+                           "less: E by an exp2 ratio recurrence (2 FMUL per pixel pair per 8-pixel run, one "
+                           "MUFU pair per run), the moments as an f16 x f16 -> FP32 GEMM on the tensor pipe "
+                           "(mma.sync). The hardware fraction is `hw`: the busiest unit from ncu."})
+    h = hw_of(hw, dname)
+    if h:
+        rf["hw"] = h
 
     # --- e2e through the host-buffer C ABI
     e2e = e2e_first
     if not args.no_e2e and e2e is None:
         e2e = run_e2e(args, eng, ca, scanner, my_thetas, up_host, len(thetas), world, dev)
 
+    if eng.take_overflow():
+        raise RuntimeError(f"capacity-mode binning overflowed in the e2e leg ({capacity} pair slots)")
+    eng.set_capacity(0, 0)
+
     # --- voxelizer (configs[3])
     vox = None if args.no_voxel else run_voxel(args, eng, vol, world, rank, dev)
 
     # --- full train iteration (configs[1]), one GPU per replica
     train = None if args.no_train or rank != 0 else run_train(args, eng, dev)
+
+    # --- the all-FP32 SIMT arm of K4 / K8 (child process: the variant is fixed per process)
+    simt_arm = None
+    if rank == 0 and world == 1 and not args.no_simt_arm:
+        simt_arm = run_simt_arm(args)
 
     # --- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -421,20 +494,43 @@ def run_engine(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": warmup_run, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "fp32 (FP64 binning preprocess + chain rules)",
+            "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
             "data": "synthetic: Shepp-Logan phantom, sample_init_cloud + anisotropic jitter (seeded), U(-1,1) dL/dI",
             "config": {"workload": "cfg3 (BASELINE configs[2]): " + w.description, "gaussians": ca.m,
                        "views": len(thetas), "detector_px": [w.res, w.res], "pairs_per_step_rank0": n_pairs,
                        "gpe_per_step_rank0": gpe, "l2": "flushed between timed steps (256 MiB write)",
                        "parallelism": f"views sharded over {world} rank(s); NCCL all-reduce of 11*M grads",
-                       "reduction": args.reduction},
+                       "reduction": args.reduction,
+                       "binning": f"sync-free capacity mode ({capacity} pair slots = 1.02 x measured + 65536; "
+                                  "overflow checked after the timed region)"},
             "clocks": clocks, "gpu_launches": launches, "roofline": rf, "kernels": kernels, "e2e": e2e,
             "cpu_baseline": cpu, "voxelizer": vox, "train_step": train,
+            "fp32_simt_arm": simt_arm,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_simt_arm(args):
+    """The same device-resident cfg3 step (and cfg4 voxel pass) with K4 / K8 in FP32 on the
+    SIMT pipes (no binary16 rounding of E): SCT_K4=simt SCT_K8=simt in a child bench."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--no-cpu", "--no-e2e", "--no-train", "--no-simt-arm",
+           "--steps", str(min(args.steps, 5)), "--warmup", "3", "--reduction", args.reduction]
+    env = dict(os.environ, SCT_K4="simt", SCT_K8="simt")
+    try:
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 (reported, not fatal: the main line stands)
+        return {"error": str(e)[:200]}
+    v = d.get("voxelizer") or {}
+    return {"value": d["value"], "unit": UNIT, "ms_per_step": d["ms_per_step"],
+            "K4_backward_stats_ms": d["kernels"]["K4_backward_stats"]["ms_per_step"],
+            "voxel_value": v.get("value"), "K8_ms": (v.get("kernels") or {}).get("K8_voxel_backward_stats",
+                                                                                {}).get("ms_per_step"),
+            "parity": "tests/test_gpu_k4_variants.py (simt smoke vs the oracle); FP32 rounding only",
+            "env": "SCT_K4=simt SCT_K8=simt", "steps": d["steps"]}
 
 
 def run_e2e(args, eng, ca, scanner, thetas, up_host, n_total_views, world, dev):
@@ -538,7 +634,7 @@ def run_train(args, eng, dev):
     meas = f.images.clone()
     f.free()
     cloud = P.GaussianCloud(ca.s_min, ca.rho_raw, ca.pos, ca.scale_raw, ca.rot, device=dev)
-    cfg = TrainConfig(iters=1000, output_dims=(w.n_vox,) * 3, tv_grid_dim=32, check_every=0)
+    cfg = TrainConfig(iters=1000, output_dims=(w.n_vox,) * 3, tv_grid_dim=32, check_every=0, sync_free=True)
     tr = Trainer(eng, cloud, sc, angles, meas, cfg)
     warm_up(tr.step, max(3, args.warmup))
     n = max(10, args.steps)
@@ -551,11 +647,17 @@ def run_train(args, eng, dev):
     b.record(eng.stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / n
+    if eng.take_overflow():
+        raise RuntimeError("train step: sync-free binning overflowed its capacity")
+    eng.set_capacity(0, 0)
     return {"metric": "train iterations/sec", "value": 1000.0 / ms, "unit": "iters/s", "ms_per_iter": ms,
             "workload": "cfg2 (BASELINE configs[1]): " + w.description, "iters": n,
             "last_total_loss": float(out["total"]), "engine_launches_per_iter": (eng.kernel_launches() - launches0) / n,
+            "binning": "sync-free (TrainConfig.sync_free: capacity from a calibration iteration, overflow "
+                       "checked after the timed region)",
             "note": "1 view per iteration as trainer.cpp:268-276; context: the paper's RTX 3090 CUDA code "
-                    "runs ~15.5 ms/iter (PAPER.md:211, derived)"}
+                    "runs ~15.5 ms/iter (PAPER.md:211, derived)",
+            "hw": {k: hw_of(hw_units(), k) for k in ("K9_tv3d", "K10_adam", "K11_ssim", "AC_adaptive")}}
 
 
 def run_voxel(args, eng, vol, world, rank, dev):
@@ -622,6 +724,11 @@ def run_voxel(args, eng, vol, world, rank, dev):
             ach = fl * vge / (ms / args.steps / 1000.0) / 1e12
             kern[name]["achieved_tflops"] = ach
             kern[name]["frac_fp32_peak"] = ach / fp32_peak
+    hw = hw_units()
+    for name in kern:
+        h = hw_of(hw, name)
+        if h:
+            kern[name]["hw"] = {k: v for k, v in h.items() if k != "units"}
     res = {"metric": "voxelized voxels/sec (fwd+bwd)", "value": grid.voxel_count() * args.steps / (total_ms / 1e3),
            "unit": "voxels/s", "ms_per_step": total_ms / args.steps,
            "workload": "cfg4 (BASELINE configs[3]): " + w.description, "vge_per_pass": vge, "pairs": pairs,

@@ -674,7 +674,7 @@ int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
   }
   if (s->n_items == 0) return SCT_OK;
   float4* pair_stats = nullptr;
-  float* item_grads = nullptr;
+  double* vsum = nullptr;
   // deterministic (default): per-(tile, kernel) slots reduced in the
   // reference's fixed tile order; otherwise the parallel-atomic mode of
   // SPEC.md:224-226 accumulates straight into 8-float per-item records.
@@ -687,7 +687,8 @@ int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
   } else {
     SCT_TRY(stage_buf(c, 14, 2 * s->n_pairs * sizeof(float4), (void**)&pair_stats));
   }
-  SCT_TRY(stage_buf(c, 15, 11 * s->n_items * sizeof(float), (void**)&item_grads));
+  const int nch = chunks > 0 ? chunks : 1;
+  SCT_TRY(stage_buf(c, 15, chain_sums_bytes(s, nch), (void**)&vsum));
   // View chunks pipeline the two backward stages: the statistics kernel of
   // chunk k+1 (FP32, issue-bound) runs on the main stream while the FP64
   // chain of chunk k (latency-bound) runs on the aux stream; items of view v
@@ -697,7 +698,6 @@ int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
   // gradient is already resident — the issue-bound K4 yields the slots K5
   // takes — and pays off on the host-buffer path, where it also hides the
   // chunked H2D copies; so it is used there only)
-  const int nch = chunks > 0 ? chunks : 1;
   const float4* chain_src = atomic ? reinterpret_cast<const float4*>(item_stats) : pair_stats;
   for (int k = 0; k < nch; ++k) {
     const int v0 = (int)((int64_t)s->n_views * k / nch), v1 = (int)((int64_t)s->n_views * (k + 1) / nch);
@@ -706,17 +706,17 @@ int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
     if (nch > 1) {
       SCT_CUDA_TRY(cudaEventRecord(c->ev_compute[k], c->stream));
       SCT_CUDA_TRY(cudaStreamWaitEvent(c->aux_stream, c->ev_compute[k], 0));
-      launch_raster_chain(c, s, *cloud, chain_src, item_grads, atomic, (int64_t)v0 * s->m, (int64_t)v1 * s->m,
+      launch_raster_chain(c, s, *cloud, chain_src, vsum + k * chain_sums_bytes(s, 1) / 8, atomic, v0, v1,
                           c->aux_stream);
     } else {
-      launch_raster_chain(c, s, *cloud, chain_src, item_grads, atomic);
+      launch_raster_chain(c, s, *cloud, chain_src, vsum, atomic);
     }
   }
   if (nch > 1) {
     SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->aux_stream));
     SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   }
-  launch_raster_finalize(c, s, *cloud, item_grads, grads, stats);
+  launch_raster_finalize(c, s, *cloud, vsum, nch, grads, stats);
   SCT_CUDA_TRY(cudaGetLastError());
   return SCT_OK;
 }
@@ -844,14 +844,15 @@ static int render_bwd_units(Ctx* c, sct_fwd* s, const sct_cloud* cloud, const fl
   const bool atomic = !c->deterministic;
   float4* pair_stats = nullptr;
   float* item_stats = nullptr;
-  float* item_grads = nullptr;
+  double* vsum = nullptr;
   if (atomic) {
     SCT_TRY(stage_buf(c, 14, 8 * s->n_items * sizeof(float), (void**)&item_stats));
     SCT_CUDA_TRY(cudaMemsetAsync(item_stats, 0, 8 * s->n_items * sizeof(float), c->stream));
   } else {
     SCT_TRY(stage_buf(c, 14, 2 * s->n_pairs * sizeof(float4), (void**)&pair_stats));
   }
-  SCT_TRY(stage_buf(c, 15, 11 * s->n_items * sizeof(float), (void**)&item_grads));
+  const int groups = std::min(units, kChainGroups);
+  SCT_TRY(stage_buf(c, 15, chain_sums_bytes(s, groups), (void**)&vsum));
   uint32_t* ready = c->unit_flags + Ctx::kMaxUnits;
   uint32_t* k4_done = c->unit_flags + 2 * Ctx::kMaxUnits;
   int* counters = c->unit_done + Ctx::kMaxUnits;
@@ -874,19 +875,19 @@ static int render_bwd_units(Ctx* c, sct_fwd* s, const sct_cloud* cloud, const fl
   // a lost kernel-side signal only delays the chain to the end of K4
   for (int u = 0; u < units; ++u) SCT_TRY(stream_write_flag(c->stream, k4_done + u, epoch));
   const float4* chain_src = atomic ? reinterpret_cast<const float4*>(item_stats) : pair_stats;
-  const int groups = std::min(units, kChainGroups);
   for (int g = 0; g < groups; ++g) {
     const int u0 = units * g / groups, u1 = units * (g + 1) / groups;
     for (int u = u0; u < u1; ++u) SCT_TRY(stream_wait_flag(c->aux_stream, k4_done + u, epoch));
     const int64_t v0 = (int64_t)s->n_views * u0 / units, v1 = (int64_t)s->n_views * u1 / units;
     g_dbg.mark(c->aux_stream, "chain" + std::to_string(g) + "_start");
-    launch_raster_chain(c, s, *cloud, chain_src, item_grads, atomic, v0 * s->m, v1 * s->m, c->aux_stream);
+    launch_raster_chain(c, s, *cloud, chain_src, vsum + g * chain_sums_bytes(s, 1) / 8, atomic, (int)v0, (int)v1,
+                        c->aux_stream);
   }
   SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->aux_stream));
   SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   g_dbg.mark(c->stream, "chain_end");
   SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, grads_ready, 0));
-  launch_raster_finalize(c, s, *cloud, item_grads, grads, stats);
+  launch_raster_finalize(c, s, *cloud, vsum, groups, grads, stats);
   g_dbg.mark(c->stream, "finalize_end");
   SCT_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int32_t*>(c->pinned_count) + 8, c->unit_err, sizeof(int32_t),
                                cudaMemcpyDeviceToHost, c->stream));

@@ -1,18 +1,24 @@
 // FP64 per-Gaussian chain rules (K5, K8-chain).
 //
-// raster_chain_kernel: one thread per visible (view, kernel) item. Sums the
-//   item's per-tile statistics in the reference's fixed tile order
-//   (rasterizer.cpp:245-257), rebuilds the projection chain in FP64
-//   (rasterizer.cpp:266-268) and runs rasterizer.cpp:270-327 down to
-//   dL/drho, dL/dpos and dL/dSigma. Writes 11 floats per item.
-// raster_finalize_kernel: one thread per kernel. Sums its items over the
-//   views in view order, then applies the parts of the chain that are linear
-//   and view-independent once per kernel: rho through the softplus
+// raster_chain_kernel: L lanes per kernel (L a power of two <= 32 chosen from
+//   the view count), lane l taking the kernel's views l, l + L, ... of a view
+//   range. Per visible (view, kernel) item: sums the item's per-tile
+//   statistics in the reference's fixed tile order (rasterizer.cpp:245-257),
+//   rebuilds the projection chain in FP64 (rasterizer.cpp:266-268) and runs
+//   rasterizer.cpp:270-327 down to dL/drho, dL/dpos and dL/dSigma. The lanes
+//   sum their items in view order, then a fixed xor tree sums the L lanes:
+//   the view sums leave the kernel as 11 doubles + a visible count per kernel
+//   and view range (no per-item outputs through HBM; deterministic).
+// raster_finalize_kernel: one thread per kernel. Sums the view-range partials
+//   in range order, then applies the parts of the chain that are linear and
+//   view-independent once per kernel: rho through the softplus
 //   (rasterizer.cpp:329) and Sigma -> (scale_raw, q_raw)
 //   (gaussian_cloud.cpp:151-202). Also the adaptive statistics
 //   (rasterizer.cpp:333-340). Accumulates (+=) like the reference.
 // voxel_chain_kernel: voxelizer.cpp:192-223 per touched kernel.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "fp64_math.cuh"
 #include "project.cuh"
@@ -35,21 +41,15 @@ struct Sym3 {
 // Sigma and rho read from the per-Gaussian prep record, FMAs allowed. The
 // math is the same chain as rasterizer.cpp:270-327; it does not feed binning,
 // so it need not be bit-identical to the preprocess.
+// the chain of one visible item (view v, kernel i) into out[kItemOut]
 template <bool kParallel>
-__global__ void __launch_bounds__(128) raster_chain_kernel(
-    long long m, long long n_items, long long item0, long long item1, const float* __restrict__ pos,
-    const double* __restrict__ prep, const ViewParams* __restrict__ views, DetParams det, RasterParams rp,
-    const uint8_t* __restrict__ vis, const int32_t* __restrict__ offset, const float4* __restrict__ pair_stats,
-    float* __restrict__ out) {
-  for (long long item = item0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; item < item1;
-       item += (long long)gridDim.x * blockDim.x) {
-    if (!vis[item]) {  // culled in this view: contributes nothing to the view sums
-#pragma unroll
-      for (int a = 0; a < kItemOut; ++a) out[a * n_items + item] = 0.f;
-      continue;
-    }
-    const long long v = item / m;
-    const long long i = item - v * m;
+__device__ __forceinline__ void item_chain(long long m, long long v, long long i, const float* __restrict__ pos,
+                                           const double* __restrict__ prep, const ViewParams* __restrict__ views,
+                                           const DetParams& det, const RasterParams& rp,
+                                           const int32_t* __restrict__ offset, const float4* __restrict__ pair_stats,
+                                           double out[kItemOut]) {
+  {
+    const long long item = v * m + i;
     // fixed-order reduction over the item's tiles (rasterizer.cpp:245-257)
     double S0 = 0, S1x = 0, S1y = 0, Sxx = 0, Syy = 0, Sxy = 0;
     // offset == nullptr: parallel-atomic mode, one pre-summed record per item
@@ -209,17 +209,64 @@ __global__ void __launch_bounds__(128) raster_chain_kernel(
     const double gy = fma(W[1], gp0, fma(W[4], gp1, W[7] * gp2));
     const double gz = fma(W[2], gp0, fma(W[5], gp1, W[8] * gp2));
     const double nx = gcx * 0.5 * det.w, ny = gcy * 0.5 * det.h;
-    out[0 * n_items + item] = (float)g_rho;
-    out[1 * n_items + item] = (float)gx;
-    out[2 * n_items + item] = (float)gy;
-    out[3 * n_items + item] = (float)gz;
-    out[4 * n_items + item] = (float)gS.xx;
-    out[5 * n_items + item] = (float)gS.yy;
-    out[6 * n_items + item] = (float)gS.zz;
-    out[7 * n_items + item] = (float)gS.xy;
-    out[8 * n_items + item] = (float)gS.xz;
-    out[9 * n_items + item] = (float)gS.yz;
-    out[10 * n_items + item] = (float)sqrt(fma(nx, nx, ny * ny));
+    out[0] = g_rho;
+    out[1] = gx;
+    out[2] = gy;
+    out[3] = gz;
+    out[4] = gS.xx;
+    out[5] = gS.yy;
+    out[6] = gS.zz;
+    out[7] = gS.xy;
+    out[8] = gS.xz;
+    out[9] = gS.yz;
+    out[10] = sqrt(fma(nx, nx, ny * ny));
+  }
+}
+
+// K5: L lanes per kernel over views [v0, v1); writes vsum[a * m + i] (a < kItemOut:
+// the view sums, a = kItemOut: the visible count). All lanes of a warp take the
+// same number of kernel iterations (m rounded up to 32 / L) for the shuffles.
+#ifndef SCT_CHAIN_MINB
+#define SCT_CHAIN_MINB 4
+#endif
+template <bool kParallel, int L>
+__global__ void __launch_bounds__(128, SCT_CHAIN_MINB) raster_chain_kernel(
+    long long m, int v0, int v1, const float* __restrict__ pos, const double* __restrict__ prep,
+    const ViewParams* __restrict__ views, DetParams det, RasterParams rp, const uint8_t* __restrict__ vis,
+    const int32_t* __restrict__ offset, const float4* __restrict__ pair_stats, double* __restrict__ vsum) {
+  // lane-private running sums in shared memory ([a][thread], FP64): keeps the
+  // chain's register budget at 128 without spills
+  __shared__ double s_acc[kItemOut + 1][128];
+  const int tid = threadIdx.x, lane = tid & (L - 1);
+  const long long seg_stride = (long long)gridDim.x * blockDim.x / L;
+  const long long m_pad = (m + (32 / L) - 1) / (32 / L) * (32 / L);
+  for (long long i = (blockIdx.x * (long long)blockDim.x + tid) / L; i < m_pad; i += seg_stride) {
+#pragma unroll
+    for (int a = 0; a <= kItemOut; ++a) s_acc[a][tid] = 0.0;
+    if (i < m) {
+      for (int v = v0 + lane; v < v1; v += L) {
+        if (!vis[(long long)v * m + i]) continue;  // culled in this view: contributes nothing
+        double o[kItemOut];
+        item_chain<kParallel>(m, v, i, pos, prep, views, det, rp, offset, pair_stats, o);
+#pragma unroll
+        for (int a = 0; a < kItemOut; ++a) s_acc[a][tid] += o[a];
+        s_acc[kItemOut][tid] += 1.0;
+      }
+    }
+#pragma unroll
+    for (int off = L / 2; off > 0; off >>= 1) {  // fixed tree over the L lanes
+      __syncwarp();
+      if (lane < off) {
+#pragma unroll
+        for (int a = 0; a <= kItemOut; ++a) s_acc[a][tid] += s_acc[a][tid + off];
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && i < m) {
+#pragma unroll
+      for (int a = 0; a <= kItemOut; ++a) vsum[a * m + i] = s_acc[a][tid];
+    }
+    __syncwarp();
   }
 }
 
@@ -256,40 +303,26 @@ __device__ __forceinline__ void d_cov_param_grads(const dKernel& k, const dM3& G
   for (int kk = 0; kk < 4; ++kk) g_rot[kk] = (c[kk] - qn[kk] * qc) / nrm;
 }
 
-// Sum of the item outputs over the views, in view order, one thread per
-// (output, kernel) so the reads are coalesced; row kItemOut counts the views in
-// which the kernel is visible (grad_count, rasterizer.cpp:337-338).
-__global__ void __launch_bounds__(256) view_sum_kernel(long long m, int n_views, const uint8_t* __restrict__ vis,
-                                                       const float* __restrict__ item, double* __restrict__ vsum) {
-  const long long n_items = m * n_views;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (kItemOut + 1) * m;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long a = t / m, i = t - a * m;
-    double acc = 0.0;
-    if (a < kItemOut) {
-      const float* src = item + a * n_items + i;
-#pragma unroll 8
-      for (int v = 0; v < n_views; ++v) acc += (double)__ldg(src + (long long)v * m);  // loads ahead, sums in order
-    } else {
-      for (int v = 0; v < n_views; ++v) acc += (double)vis[(long long)v * m + i];
-    }
-    vsum[t] = acc;
-  }
-}
-
 __global__ void __launch_bounds__(128) raster_finalize_kernel(
     long long m, double s_min, const float* __restrict__ rho_raw, const float* __restrict__ pos,
     const float* __restrict__ scale_raw, const float* __restrict__ rot, const double* __restrict__ vsum,
     float* __restrict__ g_rho, float* __restrict__ g_pos,
     float* __restrict__ g_scale, float* __restrict__ g_rotp, float* __restrict__ st_norm,
-    int32_t* __restrict__ st_count, float* __restrict__ st_3d) {
+    int32_t* __restrict__ st_count, float* __restrict__ st_3d, int groups) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
-    // view sums from view_sum_kernel: [kItemOut][m] + visible count at [kItemOut][m]
+    // view-range partials from raster_chain_kernel: [groups][kItemOut + 1][m], summed in range order
     double acc[kItemOut];
 #pragma unroll
     for (int a = 0; a < kItemOut; ++a) acc[a] = vsum[a * m + i];
-    const int nvis = (int)vsum[kItemOut * m + i];
+    double nv = vsum[kItemOut * m + i];
+    for (int g = 1; g < groups; ++g) {
+      const double* p = vsum + (long long)g * (kItemOut + 1) * m;
+#pragma unroll
+      for (int a = 0; a < kItemOut; ++a) acc[a] += p[a * m + i];
+      nv += p[kItemOut * m + i];
+    }
+    const int nvis = (int)nv;
     if (nvis == 0) continue;
     const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
     g_rho[i] += (float)(acc[0] * d_act_density_grad(k.rho_raw));
@@ -422,35 +455,64 @@ int grid_cap(Ctx* c, long long n, int block) {
 
 }  // namespace
 
-void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float4* pair_stats,
-                         float* item_grads, bool per_item, int64_t item0, int64_t item1, cudaStream_t stream) {
-  if (item1 < 0) item1 = s->n_items;
-  if (item1 <= item0) return;
-  cudaStream_t st = stream ? stream : c->stream;
-  KScope _ks(c, "K5_raster_chain", true, st);
-  auto kern = s->det.parallel ? raster_chain_kernel<true> : raster_chain_kernel<false>;
-  kern<<<grid_cap(c, item1 - item0, 128), 128, 0, st>>>(s->m, s->n_items, item0, item1, cl.pos, s->d_prep,
-                                                        s->d_views, s->det, s->rp, s->d_vis,
-                                                        per_item ? nullptr : s->d_offset, pair_stats, item_grads);
+int64_t chain_sums_bytes(const sct_fwd* s, int groups) {
+  return (int64_t)groups * (kItemOut + 1) * s->m * (int64_t)sizeof(double);
 }
 
-void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float* item_grads, sct_grads* g,
-                            sct_stats* st) {
+template <bool P>
+static void chain_launch(int lanes, int grid, cudaStream_t st, long long m, int v0, int v1, const float* pos,
+                         const double* prep, const ViewParams* views, const DetParams& det, const RasterParams& rp,
+                         const uint8_t* vis, const int32_t* offset, const float4* ps, double* vsum) {
+#define SCT_CHAIN_L(L) \
+  case L:              \
+    raster_chain_kernel<P, L><<<grid, 128, 0, st>>>(m, v0, v1, pos, prep, views, det, rp, vis, offset, ps, vsum); \
+    break;
+  switch (lanes) {
+    SCT_CHAIN_L(1)
+    SCT_CHAIN_L(2)
+    SCT_CHAIN_L(4)
+    SCT_CHAIN_L(8)
+    SCT_CHAIN_L(16)
+    SCT_CHAIN_L(32)
+  }
+#undef SCT_CHAIN_L
+}
+
+void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float4* pair_stats, double* vsum,
+                         bool per_item, int v0, int v1, cudaStream_t stream) {
+  if (v1 < 0) v1 = s->n_views;
   if (s->m == 0) return;
-  double* vsum = nullptr;
-  if (dev_alloc(c, (void**)&vsum, (kItemOut + 1) * s->m * sizeof(double)) != SCT_OK) return;
-  {
-    KScope _ks(c, "K5_view_sum");
-    view_sum_kernel<<<grid_cap(c, (kItemOut + 1) * s->m, 256), 256, 0, c->stream>>>(s->m, s->n_views, s->d_vis,
-                                                                                     item_grads, vsum);
-  }
-  {
-    KScope _ks(c, "K5_raster_finalize");
-    raster_finalize_kernel<<<grid_cap(c, s->m, 128), 128, 0, c->stream>>>(
-        s->m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, vsum, g->rho_raw, g->pos, g->scale_raw, g->rot,
-        st ? st->grad2d_norm_accum : nullptr, st ? st->grad_count : nullptr, st ? st->grad3d_accum : nullptr);
-  }
-  dev_free(c, vsum);
+  cudaStream_t st = stream ? stream : c->stream;
+  KScope _ks(c, "K5_raster_chain", true, st);
+  // lanes per kernel: the widest power of two up to 4 that leaves at most ~10%
+  // of the (view, lane) slots idle (measured at cfg3, 75 views: 1 / 2 / 4 / 16
+  // lanes -> 0.42 / 0.35 / 0.34 / 0.45 ms; wider segments scatter the view
+  // records and statistics over more lines per load)
+  const int nv = std::max(0, v1 - v0);
+  int lanes = 4;
+  while (lanes > 1 && (long long)((nv + lanes - 1) / lanes) * lanes * 10 > 11LL * nv) lanes >>= 1;
+  static const int forced = [] {
+    const char* e = std::getenv("SCT_CHAIN_LANES");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) lanes = forced;
+  const int grid = grid_cap(c, s->m * lanes, 128);
+  const int32_t* off = per_item ? nullptr : s->d_offset;
+  if (s->det.parallel)
+    chain_launch<true>(lanes, grid, st, s->m, v0, v1, cl.pos, s->d_prep, s->d_views, s->det, s->rp, s->d_vis, off,
+                       pair_stats, vsum);
+  else
+    chain_launch<false>(lanes, grid, st, s->m, v0, v1, cl.pos, s->d_prep, s->d_views, s->det, s->rp, s->d_vis, off,
+                        pair_stats, vsum);
+}
+
+void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const double* vsum, int groups,
+                            sct_grads* g, sct_stats* st) {
+  if (s->m == 0) return;
+  KScope _ks(c, "K5_raster_finalize");
+  raster_finalize_kernel<<<grid_cap(c, s->m, 128), 128, 0, c->stream>>>(
+      s->m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, vsum, g->rho_raw, g->pos, g->scale_raw, g->rot,
+      st ? st->grad2d_norm_accum : nullptr, st ? st->grad_count : nullptr, st ? st->grad3d_accum : nullptr, groups);
 }
 
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,

@@ -69,13 +69,18 @@ __global__ void __launch_bounds__(256) tv3d_kernel(const float* __restrict__ vol
     for (int a = 0; a < 3; ++a) partials[3 * blockIdx.x + a] = red[a][0];
 }
 
+// fixed-order sum of the block partials: lane j sums partials j, j + 32, ... in
+// order, then a fixed xor tree (one warp)
 __global__ void tv3d_finish_kernel(const double* __restrict__ partials, int n_blocks, double inv_x, double inv_y,
                                    double inv_z, double* __restrict__ value) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int lane = threadIdx.x;
   double s[3] = {0, 0, 0};
-  for (int b = 0; b < n_blocks; ++b)
+  for (int b = lane; b < n_blocks; b += 32)
     for (int a = 0; a < 3; ++a) s[a] += partials[3 * b + a];
-  *value = s[0] * inv_x + s[1] * inv_y + s[2] * inv_z;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+    for (int a = 0; a < 3; ++a) s[a] += __shfl_xor_sync(0xffffffffu, s[a], off);
+  if (lane == 0) *value = s[0] * inv_x + s[1] * inv_y + s[2] * inv_z;
 }
 
 // ---------------------------------------------------------------- Adam

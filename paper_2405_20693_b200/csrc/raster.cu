@@ -1708,6 +1708,7 @@ __global__ void __launch_bounds__(256) tile_order_keys_kernel(const int2* __rest
 // workloads (n <= kSmallOrder)
 constexpr int kSmallOrderThreads = 512, kSmallOrderItems = 24;
 constexpr int kSmallOrder = kSmallOrderThreads * kSmallOrderItems;
+template <int kSmallOrderItems>
 __global__ void __launch_bounds__(kSmallOrderThreads) tile_order_small_kernel(const int2* __restrict__ ranges,
                                                                               long long base, int n,
                                                                               int32_t* __restrict__ order) {
@@ -1760,7 +1761,14 @@ static const int* tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
   int32_t* i1 = i0 + n;
   KScope _ks(c, "K2_tile_order");
   if (n <= kSmallOrder) {  // one CTA instead of the device-wide sort's launches (train step: 256 lists)
-    tile_order_small_kernel<<<1, kSmallOrderThreads, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
+    // items per thread sized to n (the 256-list train step sorts 512 keys, not 12288)
+    if (n <= kSmallOrderThreads)
+      tile_order_small_kernel<1><<<1, kSmallOrderThreads, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
+    else if (n <= 4 * kSmallOrderThreads)
+      tile_order_small_kernel<4><<<1, kSmallOrderThreads, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
+    else
+      tile_order_small_kernel<kSmallOrderItems>
+          <<<1, kSmallOrderThreads, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
     ++c->order_gen;
     return i0;
   }

@@ -309,11 +309,13 @@ void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t
                                  const int32_t* offset, const sct_cloud& cl, int64_t n_pairs, const float* dL,
                                  float4* pair_stats);
 // FP64 chain rules
-// per_item: pair_stats holds one pre-summed 8-float record per item (atomic mode)
-void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float4* pair_stats,
-                         float* item_grads, bool per_item = false, int64_t item0 = 0, int64_t item1 = -1,
-                         cudaStream_t stream = nullptr);
-void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float* item_grads,
+// per_item: pair_stats holds one pre-summed 8-float record per item (atomic mode).
+// The chain of views [v0, v1) writes one view-range partial (chain_sums_bytes(s, 1))
+// at vsum; finalize sums `groups` consecutive partials in order.
+int64_t chain_sums_bytes(const sct_fwd* s, int groups);
+void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const float4* pair_stats, double* vsum,
+                         bool per_item = false, int v0 = 0, int v1 = -1, cudaStream_t stream = nullptr);
+void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const double* vsum, int groups,
                             sct_grads* g, sct_stats* st);
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,
                         const float4* pair_stats, sct_grads* g);

@@ -29,6 +29,12 @@ for world in (1, 2, 4, 8):
         eng.render_backward(cloud, f, dL, grads)
         f.free()
 
+    eng.set_capacity(0, 0)
+    step()
+    f = eng.render(cloud, scanner, th, out=imgs)
+    n_pairs = f.work()[1]
+    f.free()
+    eng.set_capacity(int(n_pairs * 1.02) + 65536, 0)  # sync-free binning, as bench.py
     for _ in range(8):
         step()
     torch.cuda.synchronize()
