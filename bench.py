@@ -607,9 +607,40 @@ def run_e2e(args, eng, ca, scanner, thetas, up_host, n_total_views, world, dev):
     if world > 1:
         h2d += 11 * m * 4
         d2h += 11 * m * 4
-    return {"value": n_total_views * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "path": "C-ABI sct_render_fwd_host + sct_render_bwd_host (pinned host)",
-            "ms_per_step": 1000.0 * dt / args.steps}
+    res = {"value": n_total_views * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "path": "C-ABI sct_render_fwd_host + sct_render_bwd_host (pinned host)",
+           "ms_per_step": 1000.0 * dt / args.steps}
+    if world == 1:
+        # the reference trainer's granularity: one render + render_backward call per view
+        # (trainer.cpp:276-288), each call re-uploading the cloud (pageable-free: pinned)
+        def one_view(v):
+            C.memset(gbuf.data_ptr(), 0, gbuf_bytes)
+            st = C.c_void_p()
+            th1 = (C.c_double * 1)(thetas[v])
+            img1 = C.c_void_p(imgs.data_ptr() + v * imgs[0].numel() * 4)
+            rc = L.sct_render_fwd_host(eng._h, C.byref(cl), C.byref(sc), th1, 1, C.byref(op), img1, C.byref(st))
+            assert rc == 0, L.sct_last_error()
+            rc = L.sct_render_bwd_host(eng._h, st, C.byref(cl), C.c_void_p(dL.data_ptr() + v * dL[0].numel() * 4),
+                                       C.byref(g), None)
+            assert rc == 0, L.sct_last_error()
+            L.sct_fwd_free(st)
+            return float(gview[0])
+
+        for v in range(min(8, len(thetas))):
+            one_view(v)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for v in range(len(thetas)):
+            one_view(v)
+        torch.cuda.synchronize()
+        dtv = time.perf_counter() - t0
+        res["per_view_calls"] = {
+            "value": len(thetas) / dtv, "unit": UNIT, "ms_per_view": 1000.0 * dtv / len(thetas),
+            "h2d_bytes_per_view": int(2 * cloud_b + up_host[0].nbytes + 11 * m * 4),
+            "d2h_bytes_per_view": int(up_host[0].nbytes + 11 * m * 4),
+            "path": "one sct_render_fwd_host + sct_render_bwd_host call per view (trainer.cpp:276-288 granularity; "
+                    "the C++ drop-in include/splatct_b200.hpp render/render_backward make exactly these calls)"}
+    return res
 
 
 def run_train(args, eng, dev):

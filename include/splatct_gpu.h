@@ -230,6 +230,33 @@ int sct_adam_step(sct_ctx* ctx, sct_cloud* params, sct_adam_state* state, const 
                   const double lr[4], double beta1, double beta2, double eps);
 double sct_lr_at(double lr_init, double final_ratio, int32_t t, int32_t iters);
 
+/* ---- one training iteration in native code (trainer.cpp:268-319) ---------- */
+/* Render theta_rad, L1 + lambda_ssim D-SSIM against `measured` (device [H][W],
+ * normalised by the dataset maximum; render_scale / grad_scale as
+ * sct_photometric_loss), zero `grads` and accumulate render_backward (with the
+ * adaptive statistics when stats != NULL), the TV term on tv_grid when
+ * lambda_tv > 0 (voxelize / tv3d / voxelize_backward sharing one binning), then
+ * Adam step t with lr = {pos, rho, scale, rot} and the quaternion
+ * renormalisation. values_dev (device double [4]) receives l1, dssim, tv and
+ * total = l1 + lambda_ssim dssim + lambda_tv tv. Reads nothing back: with
+ * capacity-mode binning (sct_ctx_set_capacity) the call is sync-free. Replaces
+ * the body of the reference's train() loop, trainer.cpp:268-319; the caller
+ * draws the view and the sub-grid origin (sct_rng_*) and runs adaptive control. */
+typedef struct {
+  double theta_rad;
+  const float* measured;
+  float render_scale, grad_scale;
+  double lambda_ssim, lambda_tv;
+  sct_grid tv_grid;
+  double cull_mahalanobis; /* voxelizer cull (voxelizer.hpp: sqrt(chi2 99% dof 3)) */
+  int32_t t;
+  double lr[4];
+  double beta1, beta2, eps;
+  double* values_dev;
+} sct_train_args;
+int sct_train_step(sct_ctx* ctx, sct_cloud* cloud, sct_adam_state* adam, sct_stats* stats, sct_grads* grads,
+                   const sct_scanner* scanner, const sct_raster_opts* opts, const sct_train_args* args);
+
 /* ---- adaptive density control (trainer.cpp:167-230) ---------------------- */
 /* Two phases so the caller can size the new cloud: sct_adaptive_plan classifies
  * every kernel (prune rho < prune_density_threshold; clone or split kernels whose

@@ -54,6 +54,13 @@ class sct_adam_state(C.Structure):
                 ("m_rot", VP), ("v_rot", VP)]
 
 
+class sct_train_args(C.Structure):
+    _fields_ = [("theta_rad", C.c_double), ("measured", VP), ("render_scale", C.c_float), ("grad_scale", C.c_float),
+                ("lambda_ssim", C.c_double), ("lambda_tv", C.c_double), ("tv_grid", sct_grid),
+                ("cull_mahalanobis", C.c_double), ("t", C.c_int32), ("lr", C.c_double * 4), ("beta1", C.c_double),
+                ("beta2", C.c_double), ("eps", C.c_double), ("values_dev", VP)]
+
+
 P = C.POINTER
 
 SIGNATURES = {
@@ -96,6 +103,8 @@ SIGNATURES = {
     "sct_adam_step": (C.c_int, [VP, P(sct_cloud), P(sct_adam_state), P(sct_grads), C.c_int32, D, C.c_double,
                                 C.c_double, C.c_double]),
     "sct_lr_at": (C.c_double, [C.c_double, C.c_double, C.c_int32, C.c_int32]),
+    "sct_train_step": (C.c_int, [VP, P(sct_cloud), P(sct_adam_state), P(sct_stats), P(sct_grads), P(sct_scanner),
+                                 P(sct_raster_opts), P(sct_train_args)]),
     "sct_adaptive_plan": (C.c_int, [VP, P(sct_cloud), P(sct_stats), C.c_double, C.c_double, C.c_double, C.c_double,
                                     D, P(VP), I64, I64, I32]),
     "sct_adaptive_apply": (C.c_int, [VP, VP, P(sct_cloud), P(sct_adam_state), VP, VP, P(sct_cloud),

@@ -1622,7 +1622,11 @@ int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tile
   }();
   const int64_t tables = scatter_tables(tiles_x, tiles_y, tiles_z);
   const int64_t max_chunk = ((kScatterSmem - tables) / (2 * (int64_t)sizeof(short4))) / 256 * 256;
-  int64_t chunk = std::max<int64_t>(min_chunk, (m * n_views * T + target - 1) / target);
+  const int64_t need = (m * n_views * T + target - 1) / target;  // H within its budget
+  int64_t chunk = std::max<int64_t>(min_chunk, need);
+  // small workloads (the train step's single view): at least two blocks per SM
+  const int64_t par = (m * n_views + 2 * c->sm_count - 1) / (2 * c->sm_count);
+  chunk = std::max<int64_t>(need, std::min<int64_t>(chunk, std::max<int64_t>(256, par)));
   chunk = std::min<int64_t>(((chunk + 255) / 256) * 256, max_chunk);
   const int64_t n_chunks = (m + chunk - 1) / chunk;
   const int64_t rows = n_views * n_chunks;

@@ -115,8 +115,9 @@ struct Ctx {
   // context serialises its calls, so a slot is free again at the next call)
   // slots: 0-13 host-path staging, 14/15 backward statistics, 16/17 NCCL
   // scratch, 18/19 fixtures, 20 K3 work counter, 22 tile order, 23 photometric
-  // partials, 24 K3 partial tiles, 25 K7 partials, 27 K3 work items
-  static constexpr int kStageSlots = 28;
+  // partials, 24 K3 partial tiles, 25 K7 partials, 27 K3 work items, 28-31 the
+  // native train step's image / dL / volume / TV gradient
+  static constexpr int kStageSlots = 32;
   void* stage[kStageSlots] = {};
   size_t stage_bytes[kStageSlots] = {};
   // longest-first (view, tile) order of the last forward state / view range

@@ -474,6 +474,39 @@ class Engine:
         lrs = (C.c_double * 4)(*[float(x) for x in lr])
         _check(self.lib.sct_adam_step(self._h, C.byref(cl), C.byref(st), C.byref(g), int(t), lrs, beta1, beta2, eps))
 
+    def train_step(self, cloud: GaussianCloud, grads: CloudGrads, config: ScannerConfig, theta_rad: float,
+                   measured: torch.Tensor, t: int, lr: Sequence[float], values: torch.Tensor,
+                   opts: Optional[RasterOptions] = None, render_scale: float = 1.0, grad_scale: float = 1.0,
+                   lambda_ssim: float = 0.25, lambda_tv: float = 0.0, tv_grid: Optional[GridSpec] = None,
+                   accumulate_stats: bool = True, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-15,
+                   vox_opts: Optional[VoxelizeOptions] = None, _structs=None):
+        """One native training iteration (sct_train_step, trainer.cpp:268-319): render, L1 + D-SSIM,
+        zero grads + render_backward (+ adaptive stats), TV on tv_grid when lambda_tv > 0, Adam step t.
+        values (device float64 [4]) receives l1, dssim, tv, total. No host synchronisation in
+        capacity mode. _structs: cached (scanner, opts, cloud, adam, stats, grads) ctypes structs."""
+        if measured.shape != (config.height, config.width) or measured.dtype != torch.float32:
+            raise DimMismatch("train_step: measured must be float32 [H][W]")
+        if values.numel() < 4 or values.dtype != torch.float64:
+            raise DimMismatch("train_step: values must be float64 [4]")
+        if _structs is None:
+            _structs = ((config._c(), (opts or RasterOptions())._c()) +
+                        (cloud._c(), cloud._adam_c(), cloud._stats_c(), grads._c()))
+        sc, op, cl, ad, st, g = _structs
+        a = _capi.sct_train_args()
+        a.theta_rad = float(theta_rad)
+        a.measured = measured.data_ptr()
+        a.render_scale, a.grad_scale = float(render_scale), float(grad_scale)
+        a.lambda_ssim, a.lambda_tv = float(lambda_ssim), float(lambda_tv)
+        if lambda_tv > 0.0:
+            a.tv_grid = tv_grid._c()
+        a.cull_mahalanobis = float((vox_opts or VoxelizeOptions()).cull_mahalanobis)
+        a.t = int(t)
+        a.lr[:] = [float(x) for x in lr]
+        a.beta1, a.beta2, a.eps = float(beta1), float(beta2), float(eps)
+        a.values_dev = values.data_ptr()
+        _check(self.lib.sct_train_step(self._h, C.byref(cl), C.byref(ad), C.byref(st) if accumulate_stats else None,
+                                       C.byref(g), C.byref(sc), C.byref(op), C.byref(a)))
+
     # ------------------------------------------------------------- multi-GPU exchange (comm.cu)
     def comm_init(self, rank: int, world: int, unique_id: Optional[bytes] = None):
         """Context-owned NCCL communicator over `world` ranks. Without ``unique_id`` the id is

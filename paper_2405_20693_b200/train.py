@@ -59,6 +59,10 @@ class TrainConfig:  # trainer.hpp:13-44 (the fields the iteration uses)
     # non-finite check (every check_every iterations) and raises DataError.
     sync_free: bool = False
     capacity_margin: float = 3.0
+    # One native call per iteration (Engine.train_step -> sct_train_step, the same
+    # launches in the same order) instead of the call-by-call Python sequence below;
+    # calibration iterations of sync-free mode take the Python path (they read counts).
+    native: bool = True
 
 
 def random_subvolume_origin(lo, hi, spacing, d, u):
@@ -107,6 +111,8 @@ class Trainer:
         if view is None:
             view = self.next_view()
         calibrate = self._calibrate
+        if cfg.native and not calibrate:
+            return self._step_native(view, sub_origin)
         if calibrate:
             eng.set_capacity(0, 0)
         fwd = eng.render(cloud, self.scanner, self.angles[view], self.opts)
@@ -156,6 +162,43 @@ class Trainer:
                 and (t - cfg.adaptive_start) % cfg.densify_interval == 0):  # trainer.cpp:321-323
             adapted = self.adaptive_control()
         return {"iter": t, "view": view, "l1": vals[0, 0], "dssim": vals[0, 1], "tv": tv, "total": total,
+                "kernels": self.cloud.size(), "adaptive": adapted}
+
+    def _step_native(self, view: int, sub_origin: Optional[tuple]) -> dict:
+        """The iteration of step() as one sct_train_step call (same random draws, same order)."""
+        cfg, eng, t = self.cfg, self.eng, self.t
+        tv_grid = None
+        if cfg.lambda_tv > 0.0:
+            if sub_origin is None:
+                sub_origin = self.rng.subvolume_origin(self.scanner.extent_min_mm, self.scanner.extent_max_mm,
+                                                       self.output_spacing, cfg.tv_grid_dim)
+            d = cfg.tv_grid_dim
+            tv_grid = GridSpec((d, d, d), sub_origin, self.output_spacing)
+        key = (id(self.cloud), id(self.grads.buffer))
+        if getattr(self, "_structs_key", None) != key:  # rebuilt after adaptive control / resize
+            self._structs = ((self.scanner._c(), self.opts._c()) +
+                             (self.cloud._c(), self.cloud._adam_c(), self.cloud._stats_c(), self.grads._c()))
+            self._structs_key = key
+        vals = torch.empty(4, dtype=torch.float64, device=eng.device)
+        lrs = [lr_at(cfg.lr_position, cfg.lr_final_ratio, t, cfg.iters),
+               lr_at(cfg.lr_density, cfg.lr_final_ratio, t, cfg.iters),
+               lr_at(cfg.lr_scale, cfg.lr_final_ratio, t, cfg.iters),
+               lr_at(cfg.lr_rotation, cfg.lr_final_ratio, t, cfg.iters)]
+        eng.train_step(self.cloud, self.grads, self.scanner, self.angles[view], self.measured_norm[view], t, lrs,
+                       vals, render_scale=self.inv_norm, grad_scale=self.inv_norm, lambda_ssim=cfg.lambda_ssim,
+                       lambda_tv=cfg.lambda_tv, tv_grid=tv_grid, _structs=self._structs)
+        total = vals[3]
+        if cfg.check_every and t % cfg.check_every == 0:
+            if not math.isfinite(float(total.item())):
+                raise DivergenceDetected(f"non-finite loss at iteration {t}")
+            if cfg.sync_free and eng.take_overflow():
+                raise DataError(f"sync-free binning exceeded its pair capacity by iteration {t}; "
+                                "raise TrainConfig.capacity_margin")
+        adapted = None
+        if (cfg.adaptive_start <= t <= cfg.adaptive_end and t > cfg.adaptive_start
+                and (t - cfg.adaptive_start) % cfg.densify_interval == 0):  # trainer.cpp:321-323
+            adapted = self.adaptive_control()
+        return {"iter": t, "view": view, "l1": vals[0], "dssim": vals[1], "tv": vals[2], "total": total,
                 "kernels": self.cloud.size(), "adaptive": adapted}
 
     def adaptive_control(self, gauss: Optional[torch.Tensor] = None):

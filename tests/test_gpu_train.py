@@ -116,3 +116,41 @@ def test_train_with_adaptive_control():
         sizes.append(out["kernels"])
     assert tr.grads.flat().numel() == 11 * tr.cloud.size()
     assert len(set(sizes)) > 1, sizes
+
+
+@pytest.mark.parametrize("sync_free", [False, True])
+def test_native_step_equals_python_step(sync_free):
+    """sct_train_step (TrainConfig.native, one C-ABI call per iteration) issues the
+    same launches in the same order as the call-by-call Python iteration: with the
+    same seed, views, sub-grids and adaptive control, every loss value and every
+    parameter / Adam moment / statistic is bitwise equal (deterministic reduction)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_2405_20693_b200 as P
+    from paper_2405_20693_b200.train import TrainConfig, Trainer
+
+    res, n_views = 64, 6
+    scanner_o = O.test_scanner(res)
+    angles = O.full_circle_angles(n_views)
+    target = O.random_cloud(O.Rng(5), 80, 0.6, 0.05, 0.15)
+    meas = torch.from_numpy(np.stack([O.render(target, scanner_o, th).image for th in angles]).astype(np.float32))
+    oc = O.random_cloud(O.Rng(7), 300, 0.6, 0.01, 0.12)
+    f32 = [np.asarray(a, dtype=np.float32) for a in (oc.rho_raw, oc.pos, oc.scale_raw, oc.rot)]
+    runs = []
+    for native in (False, True):
+        cfg = TrainConfig(iters=40, output_dims=(32, 32, 32), tv_grid_dim=8, adaptive_start=3, densify_interval=4,
+                          densify_grad_threshold=1e-6, prune_density_threshold=0.05, seed=11, native=native,
+                          sync_free=sync_free, check_every=5)
+        eng = P.Engine(0)
+        tr = Trainer(eng, P.GaussianCloud(oc.s_min, *f32), P.ScannerConfig(detector_res_px=(res, res)), angles,
+                     meas, cfg)
+        losses = [float(tr.step()["total"]) for _ in range(12)]
+        c = tr.cloud
+        state = [c.rho_raw, c.pos, c.scale_raw, c.rot, c.grad2d_norm_accum, c.grad_count, c.grad3d_accum,
+                 *c.adam.values()]
+        runs.append((losses, [x.detach().cpu().clone() for x in state]))
+    (l0, s0), (l1, s1) = runs
+    assert l0 == l1
+    assert len(s0) == len(s1)
+    for a, b in zip(s0, s1):
+        assert torch.equal(a, b)
