@@ -127,6 +127,13 @@ __global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, con
 //                tile column / row give the exact stable rank;
 //   bin_ranges:  (view, tile) ranges straight from S.
 constexpr int kBinWarps = 4;
+// SCT_SCATTER_SBOX=1: the scatter keeps its chunk's boxes in shared memory
+// between the count and the write phase; 0: it re-reads them (L2) and needs
+// only the tables, so more blocks fit per SM (default: cfg3 0.355 -> 0.297 ms,
+// occupancy limited by registers instead of shared memory)
+#ifndef SCT_SCATTER_SBOX
+#define SCT_SCATTER_SBOX 0
+#endif
 // shared memory of the scatter: 4 warps x (tile counters + column and row
 // masks) words + a chunk of rectangles (>= 256)
 constexpr int64_t kScatterSmem = 225 * 1024;
@@ -309,8 +316,10 @@ __global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (i + 32 * k >= w1) continue;
-      sbox[2 * (i + 32 * k - i0)] = make_short4(r[k].x0, r[k].x1, r[k].y0, r[k].y1);
-      sbox[2 * (i + 32 * k - i0) + 1] = make_short4(r[k].z0, r[k].z1, 0, 0);
+      if (SCT_SCATTER_SBOX) {
+        sbox[2 * (i + 32 * k - i0)] = make_short4(r[k].x0, r[k].x1, r[k].y0, r[k].y1);
+        sbox[2 * (i + 32 * k - i0) + 1] = make_short4(r[k].z0, r[k].z1, 0, 0);
+      }
       if (box_empty(r[k])) continue;
       for (int tz = r[k].z0; tz <= r[k].z1; ++tz)
         for (int ty = r[k].y0; ty <= r[k].y1; ++ty)
@@ -338,9 +347,13 @@ __global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short
   for (long long base = w0; base < w1; base += 32) {
     const long long i = base + lane;
     Box r{0, -1, 0, -1, 0, -1};
-    if (i < w1) {
-      const short4 p = sbox[2 * (i - i0)], q = sbox[2 * (i - i0) + 1];
-      r = Box{p.x, p.y, p.z, p.w, q.x, q.y};
+    if (SCT_SCATTER_SBOX) {
+      if (i < w1) {
+        const short4 p = sbox[2 * (i - i0)], q = sbox[2 * (i - i0) + 1];
+        r = Box{p.x, p.y, p.z, p.w, q.x, q.y};
+      }
+    } else {
+      r = load_box(rect, hi, i, i < w1);
     }
     for (int k = lane; k < tiles_x; k += 32) mycol[k] = 0;
     for (int k = lane; k < tiles_y; k += 32) myrow[k] = 0;
@@ -717,6 +730,46 @@ __global__ void __launch_bounds__(256) k3_parts_kernel(const int2* __restrict__ 
     const int2 r = ranges[order[i]];
     count[i] = max(1, (r.y - r.x + part_len - 1) / part_len);
   }
+}
+
+// k3_parts + scan + k3_items + the tile counter reset in one CTA, for small
+// list counts (n <= kSmallWork; the train step and 8-rank shards): thread t
+// takes the lists [t * per, (t + 1) * per) of the order.
+constexpr int kSmallWorkThreads = 1024, kSmallWork = 16 * kSmallWorkThreads;
+__global__ void __launch_bounds__(kSmallWorkThreads) k3_work_small_kernel(
+    const int2* __restrict__ ranges, const int* __restrict__ order, int n, int part_len, int* __restrict__ first,
+    int4* __restrict__ items, int* __restrict__ n_items, int* __restrict__ tile_cnt, long long max_items) {
+  using Scan = cub::BlockScan<int, kSmallWorkThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int per = (n + kSmallWorkThreads - 1) / kSmallWorkThreads;
+  const int i0 = min(n, (int)threadIdx.x * per), i1 = min(n, i0 + per);
+  int cnt[16], w[16];
+  int mine = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int i = i0 + k;
+    cnt[k] = 0;
+    w[k] = 0;
+    if (i < i1) {
+      w[k] = order[i];
+      const int2 r = ranges[w[k]];
+      cnt[k] = max(1, (r.y - r.x + part_len - 1) / part_len);
+      mine += cnt[k];
+    }
+  }
+  int f = 0, total = 0;
+  Scan(tmp).ExclusiveSum(mine, f, total);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int i = i0 + k;
+    if (i < i1) {
+      first[i] = f;
+      for (int p = 0; p < cnt[k]; ++p) items[f + p] = make_int4(w[k], p, cnt[k], f);
+      f += cnt[k];
+    }
+  }
+  if (threadIdx.x == 0) *n_items = total;
+  for (long long j = threadIdx.x; j < max_items; j += kSmallWorkThreads) tile_cnt[j] = 0;
 }
 
 __global__ void __launch_bounds__(256) k3_items_kernel(const int* __restrict__ order, const int* __restrict__ count,
@@ -1652,7 +1705,7 @@ int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tile
   }
   {
     KScope _ks(c, "K2_bin_scatter");
-    const size_t smem = tables + chunk * 2 * sizeof(short4);
+    const size_t smem = tables + (SCT_SCATTER_SBOX ? chunk * 2 * sizeof(short4) : 0);
     static bool attr = false;
     if (!attr) {
       SCT_CUDA_TRY(cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1692,6 +1745,12 @@ void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16
         n_pairs, static_cast<const uint32_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
 }
 
+// list order key: the length octave, descending, clamped to 4 bits (lists of
+// >= 2^14 kernels share the first bucket)
+__device__ __forceinline__ uint32_t order_key4(int len) {
+  return 15u - (uint32_t)min(15, 32 - __clz(max(len, 0)));
+}
+
 // Longest-processing-time order of the (view, tile) lists of views
 // [v0, v0 + nv): local indices sorted by descending list length, so that K3's
 // persistent warps and K4's blocks start the long lists first and the kernels'
@@ -1703,38 +1762,39 @@ __global__ void __launch_bounds__(256) tile_order_keys_kernel(const int2* __rest
     const int2 r = ranges[base + w];
     // descending octave of the list length; the stable sort keeps the natural
     // (view-major, spatially coherent) order inside an octave for L2 locality
-    keys[w] = 31u - (uint32_t)(32 - __clz(max(r.y - r.x, 0)));
+    keys[w] = order_key4(r.y - r.x);
     idx[w] = w;
   }
 }
 
-// tile_order_keys_kernel + the stable 5-bit sort in one CTA, for small
-// workloads (n <= kSmallOrder)
-constexpr int kSmallOrderThreads = 512, kSmallOrderItems = 24;
+// tile_order_keys_kernel + the stable sort in one CTA, for small workloads
+// (n <= kSmallOrder). The key is the length octave clamped to 4 bits (lists of
+// >= 2^14 kernels share the first bucket), so the block sort is one radix pass.
+constexpr int kSmallOrderThreads = 1024, kSmallOrderItems = 8;
 constexpr int kSmallOrder = kSmallOrderThreads * kSmallOrderItems;
-template <int kSmallOrderItems>
+template <int kItems>
 __global__ void __launch_bounds__(kSmallOrderThreads) tile_order_small_kernel(const int2* __restrict__ ranges,
                                                                               long long base, int n,
                                                                               int32_t* __restrict__ order) {
-  using Sort = cub::BlockRadixSort<uint32_t, kSmallOrderThreads, kSmallOrderItems, int32_t>;
+  using Sort = cub::BlockRadixSort<uint32_t, kSmallOrderThreads, kItems, int32_t>;
   __shared__ typename Sort::TempStorage tmp;
-  uint32_t key[kSmallOrderItems];
-  int32_t idx[kSmallOrderItems];
+  uint32_t key[kItems];
+  int32_t idx[kItems];
 #pragma unroll
-  for (int i = 0; i < kSmallOrderItems; ++i) {
-    const int w = threadIdx.x * kSmallOrderItems + i;  // blocked arrangement: input order = w
+  for (int i = 0; i < kItems; ++i) {
+    const int w = threadIdx.x * kItems + i;  // blocked arrangement: input order = w
     if (w < n) {
       const int2 r = ranges[base + w];
-      key[i] = 31u - (uint32_t)(32 - __clz(max(r.y - r.x, 0)));
+      key[i] = order_key4(r.y - r.x);
     } else {
-      key[i] = 31u;  // padding sorts after every real list (stable, larger index)
+      key[i] = 15u;  // padding sorts after every real list (stable, larger index)
     }
     idx[i] = w;
   }
-  Sort(tmp).Sort(key, idx, 0, 5);
+  Sort(tmp).Sort(key, idx, 0, 4);
 #pragma unroll
-  for (int i = 0; i < kSmallOrderItems; ++i) {
-    const int w = threadIdx.x * kSmallOrderItems + i;
+  for (int i = 0; i < kItems; ++i) {
+    const int w = threadIdx.x * kItems + i;
     if (w < n) order[w] = idx[i];
   }
 }
@@ -1765,7 +1825,7 @@ static const int* tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
   int32_t* i1 = i0 + n;
   KScope _ks(c, "K2_tile_order");
   if (n <= kSmallOrder) {  // one CTA instead of the device-wide sort's launches (train step: 256 lists)
-    // items per thread sized to n (the 256-list train step sorts 512 keys, not 12288)
+    // items per thread sized to n (the 256-list train step sorts 1024 keys)
     if (n <= kSmallOrderThreads)
       tile_order_small_kernel<1><<<1, kSmallOrderThreads, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
     else if (n <= 4 * kSmallOrderThreads)
@@ -1780,10 +1840,10 @@ static const int* tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
   cub::DoubleBuffer<uint32_t> keys(k0, k1);
   cub::DoubleBuffer<int32_t> vals(i0, i1);
   size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, n, 0, 5, c->stream);
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, n, 0, 4, c->stream);
   if (ensure_cub_tmp(c, tmp) != SCT_OK) return nullptr;
   tmp = c->cub_tmp_bytes;
-  cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, vals, n, 0, 5, c->stream);
+  cub::DeviceRadixSort::SortPairs(c->cub_tmp, tmp, keys, vals, n, 0, 4, c->stream);
   ++c->order_gen;
   return vals.Current();
 }
@@ -1921,6 +1981,14 @@ static int list_work(Ctx* c, const sct_fwd* s, const int* order, const int2* ran
   key.gen = 0;
   {
     KScope _ks(c, "K2_k3_items");
+    if (n <= kSmallWork) {
+      k3_work_small_kernel<<<1, kSmallWorkThreads, 0, c->stream>>>(ranges, order, n, kw.part_len, first, items,
+                                                                  n_items, tile_cnt, max_items);
+      key.gen = c->order_gen;
+      key.part = kw.part_len;
+      key.n = n;
+      return SCT_OK;
+    }
     k3_parts_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(ranges, order, n, kw.part_len, count);
     size_t tmp = 0;
     SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, first, n, c->stream));
