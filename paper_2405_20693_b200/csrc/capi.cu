@@ -136,7 +136,18 @@ static int bits_for(uint64_t n) {  // smallest b with 2^b >= n (n >= 1)
 static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t* total, int64_t cap = 0,
                        short4* box_a = nullptr, short4* box_b = nullptr) {
   SCT_CUDA_TRY(cudaMemsetAsync(count + n, 0, sizeof(int32_t), c->stream));
-  {
+  if (n + 1 <= kCountScanSmall) {  // one CTA: scan, int64 total and capacity guard
+    {
+      KScope _ks(c, "K2_scan(cub)", false);
+      launch_count_scan_small(c, count, offset, n, cap, box_a, box_b);
+    }
+    if (cap > 0) {
+      *total = cap;
+      return SCT_OK;
+    }
+    SCT_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(c->pinned_count) + 64, c->sum64, sizeof(long long),
+                                 cudaMemcpyDeviceToHost, c->stream));
+  } else {
     long long* d_sum = c->sum64;
     size_t tmp = 0;
     SCT_CUDA_TRY(cub::DeviceReduce::Sum(nullptr, tmp, count, d_sum, n + 1, c->stream));
@@ -145,19 +156,19 @@ static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64
     SCT_CUDA_TRY(cub::DeviceReduce::Sum(c->cub_tmp, tmp, count, d_sum, n + 1, c->stream));
     SCT_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(c->pinned_count) + 64, d_sum, sizeof(long long),
                                  cudaMemcpyDeviceToHost, c->stream));
-  }
-  size_t tmp = 0;
-  SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, offset, n + 1, c->stream));
-  SCT_TRY(ensure_cub_tmp(c, tmp));
-  tmp = c->cub_tmp_bytes;
-  {
-    KScope _ks(c, "K2_scan(cub)", false);
-    SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, offset, n + 1, c->stream));
-  }
-  if (cap > 0) {
-    launch_capacity_guard(c, count, offset, n, box_a, box_b, cap);
-    *total = cap;
-    return SCT_OK;
+    tmp = 0;
+    SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, offset, n + 1, c->stream));
+    SCT_TRY(ensure_cub_tmp(c, tmp));
+    tmp = c->cub_tmp_bytes;
+    {
+      KScope _ks(c, "K2_scan(cub)", false);
+      SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, offset, n + 1, c->stream));
+    }
+    if (cap > 0) {
+      launch_capacity_guard(c, count, offset, n, box_a, box_b, cap);
+      *total = cap;
+      return SCT_OK;
+    }
   }
   int32_t t = 0;
   long long t64 = 0;

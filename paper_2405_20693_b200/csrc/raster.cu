@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "sct_internal.cuh"
 #include "tcgen05.cuh"
@@ -238,6 +239,62 @@ __global__ void __launch_bounds__(1024) bin_tilebase_kernel(const int32_t* __res
     tile_base[T] = part[threadIdx.x];
     if (total) *total = part[threadIdx.x];
     if ((long long)part[threadIdx.x] > cap) atomicOr(overflow, 1);
+  }
+}
+
+// The three scan passes + tile bases in one CTA for small tables (the train
+// step's single view, small TV grids): T <= 1024 columns, kSmallScanThreads / T
+// threads per column, each owning a contiguous row segment; segment sums ->
+// column totals -> exclusive scan of the totals -> in-place exclusive prefix.
+constexpr int kSmallScanThreads = 1024;
+constexpr long long kSmallScanEntries = 1ll << 18;
+__global__ void __launch_bounds__(kSmallScanThreads) bin_scan_small_kernel(int32_t* __restrict__ H, int n_rows,
+                                                                           int T, int32_t* __restrict__ tile_base,
+                                                                           long long cap, int* __restrict__ overflow,
+                                                                           int32_t* __restrict__ total) {
+  using Scan = cub::BlockScan<int32_t, kSmallScanThreads>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int32_t seg_sum[kSmallScanThreads];
+  __shared__ int32_t col[kSmallScanThreads + 1];
+  const int S = kSmallScanThreads / T;  // threads (segments) per column
+  const int tid = threadIdx.x;
+  const int t = tid % T, j = tid / T;
+  const bool active = j < S;
+  const int per = (n_rows + S - 1) / S;
+  const int r0 = min(n_rows, j * per), r1 = min(n_rows, r0 + per);
+  int32_t mine = 0;
+  if (active) {
+#pragma unroll 8
+    for (int r = r0; r < r1; ++r) mine += H[(long long)r * T + t];
+  }
+  seg_sum[tid] = mine;
+  __syncthreads();
+  int32_t c = 0;  // column total = its segments in order
+  if (tid < T)
+    for (int k = 0; k < S; ++k) c += seg_sum[k * T + tid];
+  int32_t base = 0, run_total = 0;
+  Scan(scan_tmp).ExclusiveSum(c, base, run_total);  // exclusive scan of the (<= 1024) column totals
+  if (tid < T) col[tid] = base;
+  if (tid == 0) {
+    col[T] = run_total;
+    if (total) *total = run_total;
+    if ((long long)run_total > cap) atomicOr(overflow, 1);
+  }
+  __syncthreads();
+  for (int k = tid; k <= T; k += kSmallScanThreads) tile_base[k] = col[k];
+  if (active) {
+    int32_t run = col[t];
+    for (int k = 0; k < j; ++k) run += seg_sum[k * T + t];
+    for (int rb = r0; rb < r1; rb += 8) {  // 8 loads in flight before the in-place stores
+      int32_t x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = rb + k < r1 ? H[(long long)(rb + k) * T + t] : 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (rb + k < r1) H[(long long)(rb + k) * T + t] = run;
+        run += x[k];
+      }
+    }
   }
 }
 
@@ -1177,41 +1234,42 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
 #else
       float (&acc2)[4] = acc;
 #endif
+      // the +15 exponent offset, or -1e30 for a slot past the list (E = 0)
+      const float2 off = make_float2(ok[0] ? 15.f : -1e30f, ok[1] ? 15.f : -1e30f);
+      // the 8 row pairs, the run mode chosen once per chunk (warp-uniform)
+      auto rows = [&](auto mode) {
+        constexpr int kMode = decltype(mode)::value;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float py = py_base + 2.f * q;
-        const float2 dy = __ffma2_rn(make_float2(-1.f, -1.f), cy, make_float2(py, py));
-        const float2 bdy = __fmul2_rn(B, dy);
-        const float2 apb = __fadd2_rn(A, bdy);
-        float2 cdy2o = __ffma2_rn(__fmul2_rn(Cc, dy), dy, make_float2(15.f, 15.f));
-        if (!ok[0]) cdy2o.x = -1e30f;
-        if (!ok[1]) cdy2o.y = -1e30f;
-        float2 e[8];
-        if (r8) {
-          run8x2(e, dx, A, A2, bdy, apb, cdy2o, K);
-        } else if (!direct) {
-          run4x2(e, dx, A, A2, bdy, apb, cdy2o, K);
-          run4x2(e + 4, dx4, A, A2, bdy, apb, cdy2o, K);
-        } else {
-          direct8x2(e, dx, A, bdy, cdy2o);
-        }
-        float E[2][8];
+        for (int q = 0; q < 8; ++q) {
+          const float py = py_base + 2.f * q;
+          const float2 dy = __ffma2_rn(make_float2(-1.f, -1.f), cy, make_float2(py, py));
+          const float2 bdy = __fmul2_rn(B, dy);
+          const float2 apb = __fadd2_rn(A, bdy);
+          const float2 cdy2o = __ffma2_rn(__fmul2_rn(Cc, dy), dy, off);
+          float2 e[8];
+          if (kMode == 0) {
+            run8x2(e, dx, A, A2, bdy, apb, cdy2o, K);
+          } else if (kMode == 1) {
+            run4x2(e, dx, A, A2, bdy, apb, cdy2o, K);
+            run4x2(e + 4, dx4, A, A2, bdy, apb, cdy2o, K);
+          } else {
+            direct8x2(e, dx, A, bdy, cdy2o);
+          }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          E[0][i] = e[i].x;
-          E[1][i] = e[i].y;
+          for (int h = 0; h < 2; ++h) {  // two m16n8k16 slices per row pair, four pixels each
+            const uint4 gb = s_g[2 * q + h][lane];
+            const __half2 a0 = __floats2half2_rn(e[4 * h].x, e[4 * h + 1].x);
+            const __half2 a1 = __floats2half2_rn(e[4 * h].y, e[4 * h + 1].y);
+            const __half2 a2 = __floats2half2_rn(e[4 * h + 2].x, e[4 * h + 3].x);
+            const __half2 a3 = __floats2half2_rn(e[4 * h + 2].y, e[4 * h + 3].y);
+            mma_f16(acc, a0, a1, a2, a3, gb.x, gb.y);
+            mma_f16(acc2, a0, a1, a2, a3, gb.z, gb.w);
+          }
         }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {  // two m16n8k16 slices per row pair, four pixels each
-          const uint4 gb = s_g[2 * q + h][lane];
-          const __half2 a0 = __floats2half2_rn(E[0][4 * h], E[0][4 * h + 1]);
-          const __half2 a1 = __floats2half2_rn(E[1][4 * h], E[1][4 * h + 1]);
-          const __half2 a2 = __floats2half2_rn(E[0][4 * h + 2], E[0][4 * h + 3]);
-          const __half2 a3 = __floats2half2_rn(E[1][4 * h + 2], E[1][4 * h + 3]);
-          mma_f16(acc, a0, a1, a2, a3, gb.x, gb.y);
-          mma_f16(acc2, a0, a1, a2, a3, gb.z, gb.w);
-        }
-      }
+      };
+      if (r8) rows(std::integral_constant<int, 0>{});
+      else if (!direct) rows(std::integral_constant<int, 1>{});
+      else rows(std::integral_constant<int, 2>{});
 #if SCT_K4_ACC2
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc[k] += acc2[k];
@@ -1651,6 +1709,57 @@ bool bin_scatter_fits(int tiles_x, int tiles_y, int tiles_z) {
 }
 bool raster_bin_scatter_fits(int tiles_x, int tiles_y) { return bin_scatter_fits(tiles_x, tiles_y, 1); }
 
+// exclusive scan of count[0..n] into offset[0..n] (count[n] == 0) with the int64
+// total into *sum64, in one CTA (small item counts: the train step's one view),
+// and — capacity mode (cap > 0) — the capacity guard of capacity_guard_kernel
+constexpr int kCountScanThreads = 1024;
+__global__ void __launch_bounds__(kCountScanThreads) count_scan_small_kernel(int32_t* __restrict__ count,
+                                                                             int32_t* __restrict__ offset, long long n,
+                                                                             long long* __restrict__ sum64,
+                                                                             long long cap, short4* __restrict__ box_a,
+                                                                             short4* __restrict__ box_b,
+                                                                             int* __restrict__ overflow) {
+  using Scan = cub::BlockScan<long long, kCountScanThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ long long s_total;
+  const long long per = (n + 1 + kCountScanThreads - 1) / kCountScanThreads;
+  const long long i0 = min(n + 1, (long long)threadIdx.x * per), i1 = min(n + 1, i0 + per);
+  long long mine = 0;
+  for (long long i = i0; i < i1; ++i) mine += count[i];
+  long long base = 0, total = 0;
+  Scan(tmp).ExclusiveSum(mine, base, total);
+  for (long long i = i0; i < i1; ++i) {
+    const int32_t x = count[i];
+    offset[i] = (int32_t)base;
+    base += x;
+  }
+  if (threadIdx.x == 0) {
+    *sum64 = total;
+    s_total = total;
+  }
+  __syncthreads();
+  if (cap > 0 && s_total > cap) {  // as capacity_guard_kernel: empty every item
+    if (threadIdx.x == 0) atomicOr(overflow, 1);
+    for (long long i = threadIdx.x; i <= n; i += kCountScanThreads) {
+      offset[i] = 0;
+      if (i == n) continue;
+      count[i] = 0;
+      if (box_b) {
+        const short4 a = box_a[i];
+        box_b[i] = make_short4((short)(a.x - 1), (short)(a.y - 1), (short)(a.z - 1), 0);
+      } else {
+        box_a[i] = make_short4(1, 0, 1, 0);
+      }
+    }
+  }
+}
+
+void launch_count_scan_small(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t cap, short4* box_a,
+                             short4* box_b) {
+  count_scan_small_kernel<<<1, kCountScanThreads, 0, c->stream>>>(count, offset, (long long)n, c->sum64,
+                                                                  (long long)cap, box_a, box_b, c->overflow);
+}
+
 void launch_capacity_guard(Ctx* c, int32_t* count, int32_t* offset, int64_t n, short4* box_a, short4* box_b,
                            int64_t cap) {
   capacity_guard_kernel<<<grid_cap(c, n + 1, 256), 256, 0, c->stream>>>(count, offset, n, box_a, box_b, c->sum64,
@@ -1695,7 +1804,11 @@ int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tile
     bin_count_kernel<<<grid, 256, T * sizeof(uint32_t), c->stream>>>(lo, hi, m, (int)chunk, (int)T, tiles_x, tiles_y,
                                                                      H);
   }
-  {
+  if (T <= kSmallScanThreads && rows * T <= kSmallScanEntries) {
+    KScope _ks(c, "K2_bin_scan");
+    bin_scan_small_kernel<<<1, kSmallScanThreads, 0, c->stream>>>(H, (int)rows, (int)T, tb2, (long long)cap,
+                                                                  c->overflow, total);
+  } else {
     KScope _ks(c, "K2_bin_scan");
     const dim3 g2((unsigned)((T + 255) / 256), (unsigned)n_seg);
     bin_colsum_kernel<<<g2, 256, 0, c->stream>>>(H, (int)rows, (int)T, seg);

@@ -279,6 +279,11 @@ void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32
 bool raster_bin_scatter_fits(int tiles_x, int tiles_y);
 int launch_raster_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, const short4* rect,
                               int32_t* vals, int2* ranges, int64_t n_pairs, int64_t cap, int32_t* total);
+// one-CTA count scan for n + 1 <= kCountScanSmall: offsets, int64 total into
+// c->sum64, and the capacity guard when cap > 0
+constexpr int64_t kCountScanSmall = 1 << 16;
+void launch_count_scan_small(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t cap, short4* box_a,
+                             short4* box_b);
 void launch_capacity_guard(Ctx* c, int32_t* count, int32_t* offset, int64_t n, short4* box_a, short4* box_b,
                            int64_t cap);
 bool bin_scatter_fits(int tiles_x, int tiles_y, int tiles_z);

@@ -10,7 +10,7 @@
 #   4. --set full of the two hottest raster kernels (K3, K4) -> ncu_summary
 TAG=${1:-r02}
 O=gpurun_out
-B="python bench.py --no-cpu --no-e2e --steps 2 --warmup 3"
+B="python bench.py --no-cpu --no-e2e --no-simt-arm --steps 2 --warmup 3"
 $B > $O/plain_$TAG.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$TAG.csv $B > $O/ncu_launch_$TAG.log 2>&1
 python tools/launch_shares.py $O/launches_$TAG.csv > $O/launch_shares_$TAG.txt
