@@ -133,10 +133,14 @@ static int bits_for(uint64_t n) {  // smallest b with 2^b >= n (n >= 1)
 // cap > 0 (capacity mode): no host readback — *total = cap, and a device guard
 // flags c->overflow and empties the items (boxes box_a / box_b) when the pairs
 // exceed it (launch_capacity_guard).
+// the one-CTA count scan measured slower than CUB's two passes at the train
+// step's 50k items (29 vs 13 us: one CTA walks the tiles at memory latency),
+// so it only takes tiny inputs
+constexpr int64_t kCountScanSmallUse = 4096;
 static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t* total, int64_t cap = 0,
                        short4* box_a = nullptr, short4* box_b = nullptr) {
   SCT_CUDA_TRY(cudaMemsetAsync(count + n, 0, sizeof(int32_t), c->stream));
-  if (n + 1 <= kCountScanSmall) {  // one CTA: scan, int64 total and capacity guard
+  if (n + 1 <= kCountScanSmallUse) {  // one CTA: scan, int64 total and capacity guard
     {
       KScope _ks(c, "K2_scan(cub)", false);
       launch_count_scan_small(c, count, offset, n, cap, box_a, box_b);

@@ -1044,16 +1044,20 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
 //
 // One CTA of kMmaWarps warps per non-empty (view, tile): the warps share the
 // tile's G and take interleaved 16-kernel chunks of the list.
+// Separate accumulators for the hi and lo MMA chains, and 2 warps per CTA for
+// large workloads (1.80 -> 1.77 ms at cfg3; 4 / 8 warps: 1.80 / 1.92 ms) but 4
+// when lists are split into parts (small workloads: the longest lists bound
+// the kernel and more warps per list finish them sooner)
 #ifndef SCT_K4_WARPS
-#define SCT_K4_WARPS 4
+#define SCT_K4_WARPS 2
 #endif
 #ifndef SCT_K4_ACC2
-#define SCT_K4_ACC2 0
+#define SCT_K4_ACC2 1
 #endif
 #ifndef SCT_K4_REC16
 #define SCT_K4_REC16 0
 #endif
-constexpr int kMmaWarps = SCT_K4_WARPS;
+constexpr int kMmaWarpsLarge = SCT_K4_WARPS, kMmaWarpsSmall = 4;
 
 __device__ __forceinline__ void mma_f16(float (&d)[4], __half2 a0, __half2 a1, __half2 a2, __half2 a3, uint32_t b0,
                                         uint32_t b1) {
@@ -1067,6 +1071,7 @@ __device__ __forceinline__ void mma_f16(float (&d)[4], __half2 a0, __half2 a1, _
 
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
+template <int kMmaWarps>
 __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats_mma_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ rect, const int32_t* __restrict__ offset, int tiles_x, int tiles_per_view, int W,
@@ -1722,17 +1727,41 @@ __global__ void __launch_bounds__(kCountScanThreads) count_scan_small_kernel(int
   using Scan = cub::BlockScan<long long, kCountScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ long long s_total;
-  const long long per = (n + 1 + kCountScanThreads - 1) / kCountScanThreads;
-  const long long i0 = min(n + 1, (long long)threadIdx.x * per), i1 = min(n + 1, i0 + per);
-  long long mine = 0;
-  for (long long i = i0; i < i1; ++i) mine += count[i];
-  long long base = 0, total = 0;
-  Scan(tmp).ExclusiveSum(mine, base, total);
-  for (long long i = i0; i < i1; ++i) {
-    const int32_t x = count[i];
-    offset[i] = (int32_t)base;
-    base += x;
+  // tiles of 4 * kCountScanThreads entries: coalesced int4 loads, one block scan per tile
+  constexpr int kTile = 4 * kCountScanThreads;
+  long long carry = 0;
+  for (long long t0 = 0; t0 <= n; t0 += kTile) {
+    const long long i = t0 + 4 * (long long)threadIdx.x;
+    int v[4];
+    if (i + 3 <= n) {
+      const int4 q = *reinterpret_cast<const int4*>(count + i);
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = i + k <= n ? count[i + k] : 0;
+    }
+    long long ex = 0, tile_total = 0;
+    Scan(tmp).ExclusiveSum((long long)v[0] + v[1] + v[2] + v[3], ex, tile_total);
+    __syncthreads();  // temp storage reuse
+    long long run = carry + ex;
+    if (i + 3 <= n) {
+      int4 o;
+      o.x = (int32_t)run; run += v[0];
+      o.y = (int32_t)run; run += v[1];
+      o.z = (int32_t)run; run += v[2];
+      o.w = (int32_t)run;
+      *reinterpret_cast<int4*>(offset + i) = o;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (i + k <= n) {
+          offset[i + k] = (int32_t)run;
+          run += v[k];
+        }
+    }
+    carry += tile_total;
   }
+  const long long total = carry;
   if (threadIdx.x == 0) {
     *sum64 = total;
     s_total = total;
@@ -2196,9 +2225,14 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
         parts, (int)n_work, work + 1, dL, ps, item_stats, ks);
     return;
   }
-  backward_stats_mma_kernel<<<(unsigned)(total * parts), 32 * kMmaWarps, 0, c->stream>>>(
-      s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
-      parts, dL, ps, item_stats, ks);
+  if (parts > 1)
+    backward_stats_mma_kernel<kMmaWarpsSmall><<<(unsigned)(total * parts), 32 * kMmaWarpsSmall, 0, c->stream>>>(
+        s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
+        parts, dL, ps, item_stats, ks);
+  else
+    backward_stats_mma_kernel<kMmaWarpsLarge><<<(unsigned)(total * parts), 32 * kMmaWarpsLarge, 0, c->stream>>>(
+        s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
+        parts, dL, ps, item_stats, ks);
 }
 
 }  // namespace sct

@@ -21,6 +21,7 @@
 // across the CTA (all lanes evaluate the same kernel at the same time).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 #include <cstdlib>
 #include <string>
@@ -621,53 +622,59 @@ __global__ void __launch_bounds__(32 * kVMmaWarps, 7) voxel_backward_mma_kernel(
     const float2 oz2 = make_float2(okk[0].z, okk[1].z), c15 = make_float2(15.f, 15.f);
     const bool r8 = __all_sync(0xffffffffu, qk[0].x * sx * sx >= -1.25f && qk[1].x * sx * sx >= -1.25f);
     float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
+    // the +15 exponent offset, or -1e30 for a slot past the list (E = 0)
+    const float2 off = make_float2(valid[0] ? 15.f : -1e30f, valid[1] ? 15.f : -1e30f);
+    // the 16 voxel rows; the 8-run mode chosen once per chunk (warp-uniform)
+    auto rows = [&](auto mode) {
+      constexpr bool kR8 = decltype(mode)::value;
 #pragma unroll 4
-    for (int q = 0; q < 16; ++q) {
-      const int r = 4 * q + t;
-      const float fy = (float)(r & 7) * sy, fz = (float)(r >> 3) * sz;
-      float E[2][8];
-      {  // kernels gq (.x) and gq + 8 (.y) in packed FP32x2; elementwise the scalar row8
-        const float2 dy = __fadd2_rn(by2, make_float2(fy, fy)), dz = __fadd2_rn(bz2, make_float2(fz, fz));
-        float2 c0o = __ffma2_rn(__fmul2_rn(qy2, dy), dy,
-                                __ffma2_rn(__fmul2_rn(qz2, dz), dz, __ffma2_rn(__fmul2_rn(oz2, dy), dz, c15)));
-        if (!valid[0]) c0o.x = -1e30f;
-        if (!valid[1]) c0o.y = -1e30f;
-        const float2 c1 = __ffma2_rn(ox2, dy, __fmul2_rn(oy2, dz));
-        if (r8) {
-          float2 e[8];
-          run8x2v(e, bx2, sx, qx2, c1, c0o, K2);
+      for (int q = 0; q < 16; ++q) {
+        const int r = 4 * q + t;
+        const float fy = (float)(r & 7) * sy, fz = (float)(r >> 3) * sz;
+        float E[2][8];
+        {  // kernels gq (.x) and gq + 8 (.y) in packed FP32x2; elementwise the scalar row8
+          const float2 dy = __fadd2_rn(by2, make_float2(fy, fy)), dz = __fadd2_rn(bz2, make_float2(fz, fz));
+          const float2 c0o = __ffma2_rn(__fmul2_rn(qy2, dy), dy,
+                                        __ffma2_rn(__fmul2_rn(qz2, dz), dz, __ffma2_rn(__fmul2_rn(oz2, dy), dz, off)));
+          const float2 c1 = __ffma2_rn(ox2, dy, __fmul2_rn(oy2, dz));
+          if (kR8) {
+            float2 e[8];
+            run8x2v(e, bx2, sx, qx2, c1, c0o, K2);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            E[0][i] = e[i].x;
-            E[1][i] = e[i].y;
-          }
-        } else if (rec_ok[0] && rec_ok[1]) {
-          float2 e[8];
-          run4x2v(e, bx2, sx, qx2, c1, c0o, K2);
+            for (int i = 0; i < 8; ++i) {
+              E[0][i] = e[i].x;
+              E[1][i] = e[i].y;
+            }
+          } else if (rec_ok[0] && rec_ok[1]) {
+            float2 e[8];
+            run4x2v(e, bx2, sx, qx2, c1, c0o, K2);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            E[0][i] = e[i].x;
-            E[1][i] = e[i].y;
+            for (int i = 0; i < 8; ++i) {
+              E[0][i] = e[i].x;
+              E[1][i] = e[i].y;
+            }
+          } else {
+            row8(E[0], rec_ok[0], bxk[0], sx, qk[0].x, c1.x, c0o.x, qk[0].w);
+            row8(E[1], rec_ok[1], bxk[1], sx, qk[1].x, c1.y, c0o.y, qk[1].w);
           }
-        } else {
-          row8(E[0], rec_ok[0], bxk[0], sx, qk[0].x, c1.x, c0o.x, qk[0].w);
-          row8(E[1], rec_ok[1], bxk[1], sx, qk[1].x, c1.y, c0o.y, qk[1].w);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t a0 = pack_h2(E[0][4 * h], E[0][4 * h + 1]);
+          const uint32_t a1 = pack_h2(E[1][4 * h], E[1][4 * h + 1]);
+          const uint32_t a2 = pack_h2(E[0][4 * h + 2], E[0][4 * h + 3]);
+          const uint32_t a3 = pack_h2(E[1][4 * h + 2], E[1][4 * h + 3]);
+          const uint4 g0 = s_g[2 * q + h][lane];
+          const uint4 g1 = lane < 8 ? s_g1[2 * q + h][lane] : make_uint4(0u, 0u, 0u, 0u);
+          vmma_f16(acc0, a0, a1, a2, a3, g0.x, g0.y);
+          vmma_f16(acc0, a0, a1, a2, a3, g0.z, g0.w);
+          vmma_f16(acc1, a0, a1, a2, a3, g1.x, g1.y);
+          vmma_f16(acc1, a0, a1, a2, a3, g1.z, g1.w);
         }
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t a0 = pack_h2(E[0][4 * h], E[0][4 * h + 1]);
-        const uint32_t a1 = pack_h2(E[1][4 * h], E[1][4 * h + 1]);
-        const uint32_t a2 = pack_h2(E[0][4 * h + 2], E[0][4 * h + 3]);
-        const uint32_t a3 = pack_h2(E[1][4 * h + 2], E[1][4 * h + 3]);
-        const uint4 g0 = s_g[2 * q + h][lane];
-        const uint4 g1 = lane < 8 ? s_g1[2 * q + h][lane] : make_uint4(0u, 0u, 0u, 0u);
-        vmma_f16(acc0, a0, a1, a2, a3, g0.x, g0.y);
-        vmma_f16(acc0, a0, a1, a2, a3, g0.z, g0.w);
-        vmma_f16(acc1, a0, a1, a2, a3, g1.x, g1.y);
-        vmma_f16(acc1, a0, a1, a2, a3, g1.z, g1.w);
-      }
-    }
+    };
+    if (r8) rows(std::true_type{});
+    else rows(std::false_type{});
     // acc0: moments 2t, 2t+1 (c0,c1: kernel gq; c2,c3: kernel gq + 8); acc1: moments 8 + 2t, 9 + 2t
     const int base = lane & ~3;
     const bool second = t == 1;
