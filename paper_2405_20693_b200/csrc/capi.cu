@@ -348,6 +348,13 @@ using namespace sct;
 
 static void free_state_buffers(sct_fwd* s) {
   Ctx* c = s->ctx;
+  if (s->defer) {  // a split scatter never completed (error path)
+    dev_free(c, s->defer->H);
+    dev_free(c, s->defer->seg);
+    dev_free(c, s->defer->tb);
+    delete s->defer;
+    s->defer = nullptr;
+  }
   dev_free(c, s->d_views);
   dev_free(c, s->d_rec);
   dev_free(c, s->d_rect);
@@ -632,8 +639,9 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   }();
   if ((!force_sort || cap > 0) && scatter) {
     if ((rc = dev_alloc(c, (void**)&s->d_vals, std::max<int64_t>(s->n_pairs, 1) * sizeof(int32_t)))) return fail(rc);
+    const int64_t split = images ? -1 : c->fwd_split_views;  // host path: the rest after the first composite
     if ((rc = launch_raster_bin_scatter(c, n_views, s->m, s->det.tiles_x, s->det.tiles_y, s->d_rect, s->d_vals,
-                                        s->d_ranges, s->n_pairs, s->n_pairs, s->d_total)))
+                                        s->d_ranges, s->n_pairs, s->n_pairs, s->d_total, split, &s->defer)))
       return fail(rc);
     if (images) launch_raster_composite(c, s, images);
     if (cudaGetLastError() != cudaSuccess) {
@@ -783,6 +791,15 @@ static int stream_write_flag(cudaStream_t st, uint32_t* flag, uint32_t epoch) {
 }
 
 // view units of a host transfer of `bytes` over n_views views: ~4 MB each
+// SCT_HOST_SPLIT=0 keeps the forward host path's binning in one piece
+static bool host_split_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SCT_HOST_SPLIT");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 static int host_units(int n_views, size_t bytes) {
   if (const char* e = std::getenv("SCT_UNIT_KB")) {
     const size_t per = (size_t)std::max(1, atoi(e)) << 10;
@@ -835,12 +852,12 @@ static int check_unit_err(Ctx* c) {
   return SCT_OK;
 }
 
-// chain groups of the units backward (measured at cfg3: 4 groups 3.13 ms,
-// 8 groups 3.19 ms, 2 groups 3.18 ms; a high-priority chain stream starts the
-// groups earlier but slows K4 by as much)
+// chain groups of the units backward (measured at cfg3 with the fused view-sum
+// chain, e2e per step: 1 / 2 / 4 groups 5.56 / 5.37 / 5.48 ms; a high-priority
+// chain stream starts the groups earlier but slows K4 by as much)
 static const int kChainGroups = [] {
   const char* e = std::getenv("SCT_CHAIN_GROUPS");
-  return e ? std::max(1, atoi(e)) : 4;
+  return e ? std::max(1, atoi(e)) : 2;
 }();
 
 // Backward with the upstream gradient landing in view units (unit_flags[1][u]
@@ -1068,14 +1085,25 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
   SCT_TRY(stage_buf(c, 4, n_views * px * sizeof(float), (void**)&dimg));
   SCT_TRY(stage_publish(c, c->copy_stream));
   // binning for all views, then one composite whose view units are copied
-  // to the host (copy stream) as they complete
+  // to the host (copy stream) as they complete. With stream memory operations
+  // the binning's last pass (the counting scatter) is split at a unit
+  // boundary near the middle: the composite of the first views starts — and
+  // their copies with it — while the scatter of the remaining views runs
+  // after it (sct_render_fwd leaves that half pending in the state).
+  const bool units_ok = memops().wait && images_host != nullptr;
+  const int units = host_units(n_views, n_views * px * sizeof(float));
+  const int u_split = units / 2;
+  const int v_split = (int)((int64_t)n_views * u_split / units);
+  c->fwd_split_views = (units_ok && host_split_enabled() && u_split > 0 && v_split > 0 && v_split < n_views)
+                           ? v_split
+                           : -1;
   int rc = sct_render_fwd(c, &d, scanner, thetas, n_views, opts, nullptr, state);
+  c->fwd_split_views = -1;
   if (rc != SCT_OK) return rc;
-  if (memops().wait && images_host && (*state)->n_pairs > 0 && raster_units_supported(c, *state)) {
+  if (units_ok && (*state)->n_pairs > 0 && raster_units_supported(c, *state)) {
     // one composite over all views; unit u's D2H copy starts when the
     // composite publishes unit_flags[0][u] (and at the latest after the
     // kernel, which re-publishes every unit)
-    const int units = host_units(n_views, n_views * px * sizeof(float));
     const uint32_t epoch = ++c->epoch;
     SCT_CUDA_TRY(cudaMemsetAsync(c->unit_done, 0, sizeof(int) * units, c->stream));
     UnitSync us;
@@ -1096,7 +1124,16 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
       for (int u = 0; u < units; ++u) cudaEventCreate(&ec[u]);
       cudaEventRecord(e0, c->stream);
     }
-    SCT_TRY(launch_raster_composite_units(c, *state, dimg, us));
+    if ((*state)->defer) {  // views [0, v_split): composite; then the rest of the scatter and its composite
+      const int T = (*state)->det.tiles_x * (*state)->det.tiles_y;
+      SCT_TRY(launch_raster_composite_units(c, *state, dimg, us, 0, T * v_split));
+      sct::BinDeferred* rest = (*state)->defer;
+      (*state)->defer = nullptr;
+      SCT_TRY(launch_bin_scatter_rest(c, rest));
+      SCT_TRY(launch_raster_composite_units(c, *state, dimg, us, T * v_split, -1));
+    } else {
+      SCT_TRY(launch_raster_composite_units(c, *state, dimg, us));
+    }
     if (dbg) cudaEventRecord(e1, c->stream);
     for (int u = 0; u < units; ++u) SCT_TRY(stream_write_flag(c->stream, c->unit_flags + u, epoch));
     for (int u = 0; u < units; ++u) {
@@ -1132,6 +1169,11 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
     return SCT_OK;
   }
   // without stream memory operations: one composite, then one copy
+  if ((*state)->defer) {
+    sct::BinDeferred* rest = (*state)->defer;
+    (*state)->defer = nullptr;
+    SCT_TRY(launch_bin_scatter_rest(c, rest));
+  }
   if ((*state)->n_pairs > 0)
     launch_raster_composite(c, *state, dimg);
   else

@@ -345,14 +345,15 @@ __global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short
                                                                      const short4* __restrict__ hi, long long m,
                                                                      int chunk, int T, int tiles_x, int tiles_y,
                                                                      int tiles_z, const int32_t* __restrict__ S,
-                                                                     int32_t* __restrict__ vals, uint32_t cap) {
+                                                                     int32_t* __restrict__ vals, uint32_t cap,
+                                                                     int v_off) {
   extern __shared__ uint32_t sm[];
   uint32_t* cnt = sm;                              // [kBinWarps][T]
   uint32_t* colm = sm + kBinWarps * T;             // [kBinWarps][tiles_x]
   uint32_t* rowm = colm + kBinWarps * tiles_x;     // [kBinWarps][tiles_y]
   uint32_t* laym = rowm + kBinWarps * tiles_y;     // [kBinWarps][tiles_z]
   short4* sbox = reinterpret_cast<short4*>(laym + kBinWarps * tiles_z);  // [chunk][2] the block's boxes
-  const int c = blockIdx.x, v = blockIdx.y;
+  const int c = blockIdx.x, v = blockIdx.y + v_off;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long i0 = (long long)v * m + (long long)c * chunk;
   const long long i1 = (long long)v * m + min((long long)(c + 1) * chunk, m);
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short
   }
   __syncthreads();
   // phase B: per tile, the block's global start plus the earlier warps' counts
-  const int32_t* sb = S + ((long long)v * gridDim.x + c) * T;
+  const int32_t* sb = S + ((long long)v * gridDim.x + c) * T;  // gridDim.x = chunks
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     uint32_t run = (uint32_t)sb[t];
 #pragma unroll
@@ -647,17 +648,19 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     int tiles_x, int tiles_per_view, int W, int H, const int4* __restrict__ items, const int* __restrict__ n_items,
     int part_len, int* __restrict__ work, int* __restrict__ tile_cnt, float* __restrict__ partial,
-    float* __restrict__ images, UnitSync us) {
+    float* __restrict__ images, UnitSync us, const int* __restrict__ item_lo, const int* __restrict__ item_hi) {
   // a chunk's 32 records as 16 kernel pairs, fields interleaved so that one
   // LDS.128 yields two float2 operands: [pair][0] = (cx0, cx1, cy0, cy1),
   // [1] = (amp0, amp1, K0, K1), [2] = (A0, A1, B0, B1), [3] = (C0, C1, 2A0, 2A1)
   __shared__ float4 sp[kCompWarps][16][4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = lane >> 1;
-  const int total = *n_items;
+  // the items [lo, hi): all of them, or one view part of the host path
+  const int lo = item_lo ? *item_lo : 0;
+  const int total = item_hi ? *item_hi : *n_items;
   for (;;) {
     int c = 0;
-    if (lane == 0) c = atomicAdd(work, 1);
+    if (lane == 0) c = atomicAdd(work, 1) + lo;
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= total) break;
     const int4 it = items[c];  // (view * T + tile, part, parts, first item of the list)
@@ -1801,7 +1804,8 @@ void launch_capacity_guard(Ctx* c, int32_t* count, int32_t* offset, int64_t n, s
 // c->overflow); total (nullable): device word receiving the pair count;
 // ranges [n_views][T] (nullable when only the totals are needed).
 int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, int tiles_z, const short4* lo,
-                       const short4* hi, int32_t* vals, int2* ranges, int64_t cap, int32_t* total) {
+                       const short4* hi, int32_t* vals, int2* ranges, int64_t cap, int32_t* total,
+                       int64_t scatter_views, BinDeferred** defer) {
   const int64_t T = (int64_t)tiles_x * tiles_y * tiles_z;
   if (m == 0 || n_views == 0) return SCT_OK;
   // chunk size: the count table H holds (V * chunks) x T entries (<= ~64M), and
@@ -1845,23 +1849,45 @@ int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tile
     bin_tilebase_kernel<<<1, 1024, 0, c->stream>>>(tb, (int)T, tb2, (long long)cap, c->overflow, total);
     bin_apply_kernel<<<g2, 256, 0, c->stream>>>(H, seg, tb2, (int)rows, (int)T);
   }
-  {
-    KScope _ks(c, "K2_bin_scatter");
-    const size_t smem = tables + (SCT_SCATTER_SBOX ? chunk * 2 * sizeof(short4) : 0);
-    static bool attr = false;
-    if (!attr) {
-      SCT_CUDA_TRY(cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)kScatterSmem));
-      attr = true;
-    }
-    bin_scatter_kernel<<<grid, 32 * kBinWarps, smem, c->stream>>>(
-        lo, hi, m, (int)chunk, (int)T, tiles_x, tiles_y, tiles_z, H, vals,
-        (uint32_t)std::min<int64_t>(cap, UINT32_MAX));
-  }
-  if (ranges) {
+  if (ranges) {  // from the scan alone: final before any pair is written
     KScope _ks(c, "K2_bin_ranges");
     bin_ranges_kernel<<<grid_cap(c, n_views * T, 256), 256, 0, c->stream>>>(H, tb2, (int)n_chunks, (int)n_views,
                                                                             (int)T, ranges);
+  }
+  static bool attr = false;
+  if (!attr) {
+    SCT_CUDA_TRY(cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kScatterSmem));
+    attr = true;
+  }
+  const size_t smem = tables + (SCT_SCATTER_SBOX ? chunk * 2 * sizeof(short4) : 0);
+  const int64_t v_now = (scatter_views > 0 && scatter_views < n_views && defer) ? scatter_views : n_views;
+  {
+    KScope _ks(c, "K2_bin_scatter");
+    bin_scatter_kernel<<<dim3((unsigned)n_chunks, (unsigned)v_now), 32 * kBinWarps, smem, c->stream>>>(
+        lo, hi, m, (int)chunk, (int)T, tiles_x, tiles_y, tiles_z, H, vals,
+        (uint32_t)std::min<int64_t>(cap, UINT32_MAX), 0);
+  }
+  if (v_now < n_views) {  // the rest later (launch_bin_scatter_rest)
+    auto* d = new BinDeferred();
+    d->H = H;
+    d->seg = seg;
+    d->tb = tb;
+    d->lo = lo;
+    d->hi = hi;
+    d->vals = vals;
+    d->m = m;
+    d->n_views = n_views;
+    d->v0 = v_now;
+    d->chunk = chunk;
+    d->n_chunks = n_chunks;
+    d->cap = cap;
+    d->tiles_x = tiles_x;
+    d->tiles_y = tiles_y;
+    d->tiles_z = tiles_z;
+    d->smem = smem;
+    *defer = d;
+    return SCT_OK;
   }
   dev_free(c, H);
   dev_free(c, seg);
@@ -1869,10 +1895,29 @@ int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tile
   return SCT_OK;
 }
 
+int launch_bin_scatter_rest(Ctx* c, BinDeferred* d) {
+  if (!d) return SCT_OK;
+  const int64_t T = (int64_t)d->tiles_x * d->tiles_y * d->tiles_z;
+  {
+    KScope _ks(c, "K2_bin_scatter");
+    bin_scatter_kernel<<<dim3((unsigned)d->n_chunks, (unsigned)(d->n_views - d->v0)), 32 * kBinWarps, d->smem,
+                         c->stream>>>(d->lo, d->hi, d->m, (int)d->chunk, (int)T, d->tiles_x, d->tiles_y, d->tiles_z,
+                                      d->H, d->vals, (uint32_t)std::min<int64_t>(d->cap, UINT32_MAX), (int)d->v0);
+  }
+  dev_free(c, d->H);
+  dev_free(c, d->seg);
+  dev_free(c, d->tb);
+  delete d;
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
+
 int launch_raster_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, const short4* rect,
-                              int32_t* vals, int2* ranges, int64_t n_pairs, int64_t cap, int32_t* total) {
+                              int32_t* vals, int2* ranges, int64_t n_pairs, int64_t cap, int32_t* total,
+                              int64_t scatter_views, BinDeferred** defer) {
   if (n_pairs == 0) return SCT_OK;
-  return launch_bin_scatter(c, n_views, m, tiles_x, tiles_y, 1, rect, nullptr, vals, ranges, cap, total);
+  return launch_bin_scatter(c, n_views, m, tiles_x, tiles_y, 1, rect, nullptr, vals, ranges, cap, total,
+                            scatter_views, defer);
 }
 
 void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,
@@ -2146,7 +2191,8 @@ static int list_work(Ctx* c, const sct_fwd* s, const int* order, const int2* ran
   return SCT_OK;
 }
 
-static int composite_launch(Ctx* c, const sct_fwd* s, const int* order, float* images, const UnitSync& us) {
+static int composite_launch(Ctx* c, const sct_fwd* s, const int* order, float* images, const UnitSync& us,
+                            int pos0 = 0, int pos1 = -1) {
   const int T = s->det.tiles_x * s->det.tiles_y;
   const int n = T * s->n_views;
   if (!order) {
@@ -2163,7 +2209,9 @@ static int composite_launch(Ctx* c, const sct_fwd* s, const int* order, float* i
   KScope _ks(c, "K3_composite");
   composite_kernel<<<blocks, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
                                                               s->det.w, s->det.h, kw.items, kw.n_items, kw.part_len,
-                                                              work, kw.tile_cnt, kw.partial, images, us);
+                                                              work, kw.tile_cnt, kw.partial, images, us,
+                                                              pos0 > 0 ? kw.first + pos0 : nullptr,
+                                                              pos1 >= 0 && pos1 < n ? kw.first + pos1 : nullptr);
   SCT_CUDA_TRY(cudaGetLastError());
   return SCT_OK;
 }
@@ -2179,9 +2227,9 @@ bool raster_units_supported(Ctx* c, const sct_fwd* s) { return !k4_simt(); }
 // Host-buffer forward: one composite over all views in unit order; the last
 // finished tile of unit u publishes unit_flags[u] (the copy stream waits on
 // it), so the D2H copies overlap the composite.
-int launch_raster_composite_units(Ctx* c, const sct_fwd* s, float* images, UnitSync us) {
+int launch_raster_composite_units(Ctx* c, const sct_fwd* s, float* images, UnitSync us, int pos0, int pos1) {
   us.per_view = s->det.tiles_x * s->det.tiles_y;
-  return composite_launch(c, s, unit_tile_order(c, s, us.units), images, us);
+  return composite_launch(c, s, unit_tile_order(c, s, us.units), images, us, pos0, pos1);
 }
 
 void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, float4* pair_stats, int v0, int nv,

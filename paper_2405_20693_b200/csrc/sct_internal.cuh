@@ -89,6 +89,9 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   bool deterministic = true;
   int64_t launches = 0;
+  // sct_render_fwd_host: scatter only views [0, fwd_split_views) inside
+  // sct_render_fwd and leave the rest pending in the state (-1: no split)
+  int64_t fwd_split_views = -1;
   // grow-only scratch reused across calls
   void* cub_tmp = nullptr;
   size_t cub_tmp_bytes = 0;
@@ -227,6 +230,22 @@ void dev_free(Ctx* c, void* p);
 }  // namespace sct
 
 // Forward state (opaque to callers).
+namespace sct {
+// a counting scatter split at a view (raster.cu): the count table and tile
+// bases stay alive until the remaining views are scattered
+struct BinDeferred {
+  int32_t* H = nullptr;
+  int32_t* seg = nullptr;
+  int32_t* tb = nullptr;
+  const short4* lo = nullptr;
+  const short4* hi = nullptr;
+  int32_t* vals = nullptr;
+  int64_t m = 0, n_views = 0, v0 = 0, chunk = 0, n_chunks = 0, cap = 0;
+  int tiles_x = 0, tiles_y = 0, tiles_z = 0;
+  size_t smem = 0;
+};
+}  // namespace sct
+
 struct sct_fwd {
   sct::Ctx* ctx = nullptr;
   uint64_t id = 0;  // unique per context (tile-order cache key)
@@ -254,6 +273,9 @@ struct sct_fwd {
   int32_t* d_total = nullptr;          // [1] pair count on the device (capacity mode)
   int2* d_ranges = nullptr;            // [V*T] [start,end) into sorted pairs
   double* d_prep = nullptr;            // [kPrepStride][m] (SoA) Sigma (9), rho, Sigma^-1 (6), det, FP64
+  // host path: the counting scatter of views [defer.v0, V) still pending
+  // (sct_render_fwd_host composites the first views while it runs)
+  sct::BinDeferred* defer = nullptr;
 };
 
 struct sct_ctx : public sct::Ctx {};
@@ -277,8 +299,14 @@ void launch_voxel_preprocess(Ctx* c, const sct_cloud& cl, const sct_grid& g, dou
 void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32_t* offset, int tiles_x,
                         void* keys, bool keys16, int32_t* vals);
 bool raster_bin_scatter_fits(int tiles_x, int tiles_y);
+// the second half of a split counting scatter: views [v0, n_views) of a binning
+// whose count / scan / ranges are done (launch_bin_scatter with scatter_views)
+int launch_bin_scatter_rest(Ctx* c, BinDeferred* d);
+// scatter_views in (0, n_views): scatter only views [0, scatter_views) now and
+// leave the rest in *defer (ranges of all views are final either way)
 int launch_raster_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, const short4* rect,
-                              int32_t* vals, int2* ranges, int64_t n_pairs, int64_t cap, int32_t* total);
+                              int32_t* vals, int2* ranges, int64_t n_pairs, int64_t cap, int32_t* total,
+                              int64_t scatter_views = -1, BinDeferred** defer = nullptr);
 // one-CTA count scan for n + 1 <= kCountScanSmall: offsets, int64 total into
 // c->sum64, and the capacity guard when cap > 0
 constexpr int64_t kCountScanSmall = 1 << 16;
@@ -288,13 +316,16 @@ void launch_capacity_guard(Ctx* c, int32_t* count, int32_t* offset, int64_t n, s
                            int64_t cap);
 bool bin_scatter_fits(int tiles_x, int tiles_y, int tiles_z);
 int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, int tiles_z, const short4* lo,
-                       const short4* hi, int32_t* vals, int2* ranges, int64_t cap, int32_t* total);
+                       const short4* hi, int32_t* vals, int2* ranges, int64_t cap, int32_t* total,
+                       int64_t scatter_views = -1, BinDeferred** defer = nullptr);
 void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, const int32_t* vals, int64_t m,
                           int64_t tiles_per_view, int2* ranges);
 void launch_raster_composite(Ctx* c, const sct_fwd* s, float* images);
 // unit-signalled host path (UnitSync): one composite / one K4 over all views
 bool raster_units_supported(Ctx* c, const sct_fwd* s);
-int launch_raster_composite_units(Ctx* c, const sct_fwd* s, float* images, UnitSync us);
+// items of the order positions [pos0, pos1) only (pos1 < 0: to the end)
+int launch_raster_composite_units(Ctx* c, const sct_fwd* s, float* images, UnitSync us, int pos0 = 0,
+                                  int pos1 = -1);
 // item_stats != nullptr: parallel-atomic mode, 8 floats per item accumulated
 // with atomics instead of per-pair slots; us != nullptr: all views, waiting
 // for and publishing view units
