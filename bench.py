@@ -36,7 +36,7 @@ UNIT = "projections/s"
 # Hardware-unit evidence per kernel (ncu, tools/profile_round2.sh -> tools/hw_units.py):
 # the busiest unit (issue slots, FP32/FP64/XU/tensor pipes, L1 wavefronts, L2, DRAM)
 # and its fraction of peak. Static: read from the committed profile, not measured here.
-HW_PROFILE = "profiles/r02d_hw_units.json"
+HW_PROFILE = "profiles/r02e_hw_units.json"
 NCU_NAMES = {
     "K0_gauss_prep": ["gauss_prep_kernel"], "K1_raster_preprocess": ["raster_preprocess_kernel"],
     "K2_bin_count": ["bin_count_kernel"],
@@ -44,7 +44,8 @@ NCU_NAMES = {
     "K2_bin_scatter": ["bin_scatter_kernel"], "K2_bin_ranges": ["bin_ranges_kernel"],
     "K2_tile_order": ["tile_order_keys_kernel", "tile_order_small_kernel<1>"],
     "K2_k3_items": ["k3_parts_kernel", "k3_items_kernel", "k3_work_small_kernel"],
-    "K3_composite": ["composite_kernel"], "K4_backward_stats": ["backward_stats_mma_kernel"],
+    "K3_composite": ["composite_kernel"],
+    "K4_backward_stats": ["backward_stats_mma_kernel<2>", "backward_stats_mma_kernel<4>", "backward_stats_mma_kernel"],
     "K5_raster_chain": ["raster_chain_kernel<0>"], "K5_view_sum": ["view_sum_kernel"],
     "K5_raster_finalize": ["raster_finalize_kernel"],
     "K6_voxel_preprocess": ["voxel_preprocess_kernel"], "K6_voxel_emit": ["voxel_emit_kernel<unsigned short>"],

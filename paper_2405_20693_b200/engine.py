@@ -484,8 +484,9 @@ class Engine:
         zero grads + render_backward (+ adaptive stats), TV on tv_grid when lambda_tv > 0, Adam step t.
         values (device float64 [4]) receives l1, dssim, tv, total. No host synchronisation in
         capacity mode. _structs: cached (scanner, opts, cloud, adam, stats, grads) ctypes structs."""
-        if measured.shape != (config.height, config.width) or measured.dtype != torch.float32:
-            raise DimMismatch("train_step: measured must be float32 [H][W]")
+        if (measured.shape != (config.height, config.width) or measured.dtype != torch.float32
+                or not measured.is_contiguous() or measured.device != self.device):
+            raise DimMismatch("train_step: measured must be a contiguous float32 [H][W] tensor on the engine's device")
         if values.numel() < 4 or values.dtype != torch.float64:
             raise DimMismatch("train_step: values must be float64 [4]")
         if _structs is None:

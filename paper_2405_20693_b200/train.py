@@ -174,7 +174,9 @@ class Trainer:
                                                        self.output_spacing, cfg.tv_grid_dim)
             d = cfg.tv_grid_dim
             tv_grid = GridSpec((d, d, d), sub_origin, self.output_spacing)
-        key = (id(self.cloud), id(self.grads.buffer))
+        cl = self.cloud
+        key = (cl.size(), cl.rho_raw.data_ptr(), cl.pos.data_ptr(), cl.scale_raw.data_ptr(), cl.rot.data_ptr(),
+               cl.grad2d_norm_accum.data_ptr(), cl.adam["m_rho"].data_ptr(), self.grads.buffer.data_ptr())
         if getattr(self, "_structs_key", None) != key:  # rebuilt after adaptive control / resize
             self._structs = ((self.scanner._c(), self.opts._c()) +
                              (self.cloud._c(), self.cloud._adam_c(), self.cloud._stats_c(), self.grads._c()))
