@@ -2252,7 +2252,14 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
     v0 = 0;
     nv = s->n_views;
   }
-  const int* order = us ? unit_tile_order(c, s, us->units) : cached_tile_order(c, s, v0, nv);
+  // SCT_K4_UNIT_ORDER=N (diagnostic): the device path in the host path's N-unit order
+  static const int dbg_units = [] {
+    const char* e = std::getenv("SCT_K4_UNIT_ORDER");
+    return e ? atoi(e) : 0;
+  }();
+  const int* order = us ? unit_tile_order(c, s, us->units)
+                        : (dbg_units > 0 && v0 == 0 && nv == s->n_views ? unit_tile_order(c, s, dbg_units)
+                                                                        : cached_tile_order(c, s, v0, nv));
   if (!order) return;
   // small workloads: several CTAs per list (>= 64 kernels each) until the
   // grid fills the CTA slots (8 per SM)

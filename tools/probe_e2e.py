@@ -12,7 +12,7 @@ import paper_2405_20693_b200 as P  # noqa: E402
 from paper_2405_20693_b200 import _capi, scenes  # noqa: E402
 
 ca = scenes.make_cloud(3)
-eng = P.Engine(0)
+eng = P.Engine(0, deterministic=os.environ.get("PROBE_DETERMINISTIC") == "1")  # bench.py: atomic
 L = _capi.load()
 thetas = [2 * np.pi * i / 75 for i in range(75)]
 pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
