@@ -2261,12 +2261,20 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
                         : (dbg_units > 0 && v0 == 0 && nv == s->n_views ? unit_tile_order(c, s, dbg_units)
                                                                         : cached_tile_order(c, s, v0, nv));
   if (!order) return;
-  // small workloads: several CTAs per list (>= 64 kernels each) until the
-  // grid fills the CTA slots (8 per SM)
+  // small workloads: several CTAs per list (>= 16 kernels each on average,
+  // up to 16 parts) while the grid stays within ~8 waves of 4-warp CTAs: the
+  // longest lists bound the kernel (cfg2 train step, one view of 256 tiles:
+  // 1 / 2 / 4 / 8 / 16 parts -> 188 / 56 / 37 / 30 / 28 us); large workloads
+  // (cfg3 and its 8-rank shards) keep one CTA per list
   const long long total = (long long)T * nv;
   const double avg_len = total > 0 ? (double)s->n_pairs / (double)total : 0.0;
   int parts = 1;
-  while (parts < 16 && total * parts * 2 <= (long long)c->sm_count * 8 && avg_len / (2 * parts) >= 64.0) parts *= 2;
+  while (parts < 16 && total * parts * 2 <= (long long)c->sm_count * 64 && avg_len / (2 * parts) >= 16.0) parts *= 2;
+  static const int forced_parts = [] {  // SCT_K4_PARTS (diagnostic): force the parts per list
+    const char* e = std::getenv("SCT_K4_PARTS");
+    return e ? std::max(1, std::min(64, atoi(e))) : 0;
+  }();
+  if (forced_parts && !us) parts = forced_parts;
   UnitSync ks = us ? *us : UnitSync{};
   ks.per_view = T * parts;
   if (k4_impl() == K4Impl::kTc && !ks.ready && !ks.done) {

@@ -824,7 +824,9 @@ void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t
   // fills the CTA slots (7 per SM)
   const double avg_len = (double)n_pairs / (double)nb;
   int parts = 1;
-  while (parts < 32 && nb * parts * 2 <= (long long)c->sm_count * 7 && avg_len / (2 * parts) >= 64.0) parts *= 2;
+  // small grids (the train step's TV sub-grid): up to 32 parts of >= 16 kernels
+  // on average while the grid stays within ~8 waves; large grids keep one CTA per brick
+  while (parts < 32 && nb * parts * 2 <= (long long)c->sm_count * 56 && avg_len / (2 * parts) >= 16.0) parts *= 2;
   // SCT_K8=simt selects the FP32 SIMT statistics kernel; default: tensor-core moments
   static const bool simt = [] {
     const char* e = std::getenv("SCT_K8");
