@@ -427,7 +427,7 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
   // each, measured 50x slower for K4)
   char* u = nullptr;
   const size_t words = (6 * Ctx::kMaxUnits * sizeof(uint32_t) + 15) & ~size_t(15);
-  if (cudaMalloc((void**)&u, words + 16) != cudaSuccess || cudaMemset(u, 0, words + 16) != cudaSuccess) {
+  if (cudaMalloc((void**)&u, words + 32) != cudaSuccess || cudaMemset(u, 0, words + 32) != cudaSuccess) {
     sct_ctx_destroy(c);
     set_error("CUDA error: context signal allocation failed");
     return SCT_ERR_CUDA;
@@ -437,6 +437,7 @@ int sct_ctx_create(int device, void* stream, sct_ctx** out) {
   c->unit_err = c->unit_done + 2 * Ctx::kMaxUnits;
   c->sum64 = reinterpret_cast<long long*>(u + words);
   c->overflow = reinterpret_cast<int*>(u + words + 8);
+  c->fin_counter = reinterpret_cast<int*>(u + words + 16);
   *out = c;
   return SCT_OK;
 }

@@ -21,9 +21,14 @@ namespace {
 // ---------------------------------------------------------------- TV
 __device__ __forceinline__ float sgnf(float d) { return d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f); }
 
+__device__ void tv3d_finish_warp(const double* partials, int n_blocks, double inv_x, double inv_y, double inv_z,
+                                 double* value);
+__device__ __forceinline__ bool last_block(int* counter, int n_blocks);
 __global__ void __launch_bounds__(256) tv3d_kernel(const float* __restrict__ vol, int nx, int ny, int nz,
                                                    float inv_x, float inv_y, float inv_z, float lambda,
-                                                   float* __restrict__ grad, double* __restrict__ partials) {
+                                                   float* __restrict__ grad, double* __restrict__ partials,
+                                                   double dinv_x, double dinv_y, double dinv_z,
+                                                   double* __restrict__ value, int* __restrict__ counter) {
   const long long n = (long long)nx * ny * nz;
   double sx = 0.0, sy = 0.0, sz = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -67,16 +72,19 @@ __global__ void __launch_bounds__(256) tv3d_kernel(const float* __restrict__ vol
   }
   if (threadIdx.x == 0)
     for (int a = 0; a < 3; ++a) partials[3 * blockIdx.x + a] = red[a][0];
+  // the last block sums the partials (the former tv3d_finish_kernel)
+  if (last_block(counter, (int)gridDim.x) && threadIdx.x < 32)
+    tv3d_finish_warp(partials, gridDim.x, dinv_x, dinv_y, dinv_z, value);
 }
 
 // fixed-order sum of the block partials: lane j sums partials j, j + 32, ... in
 // order, then a fixed xor tree (one warp)
-__global__ void tv3d_finish_kernel(const double* __restrict__ partials, int n_blocks, double inv_x, double inv_y,
-                                   double inv_z, double* __restrict__ value) {
-  const int lane = threadIdx.x;
+__device__ void tv3d_finish_warp(const double* partials, int n_blocks, double inv_x, double inv_y, double inv_z,
+                                 double* value) {
+  const int lane = threadIdx.x & 31;
   double s[3] = {0, 0, 0};
   for (int b = lane; b < n_blocks; b += 32)
-    for (int a = 0; a < 3; ++a) s[a] += partials[3 * b + a];
+    for (int a = 0; a < 3; ++a) s[a] += __ldcg(partials + 3 * b + a);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1)
     for (int a = 0; a < 3; ++a) s[a] += __shfl_xor_sync(0xffffffffu, s[a], off);
@@ -186,6 +194,41 @@ __device__ __forceinline__ void block_sum_to(double v, double* __restrict__ dst)
   }
 }
 
+// After every block has written its partial(s): true in exactly one block, the
+// last to arrive (which then finishes the reduction; counter self-resets).
+__device__ __forceinline__ bool last_block(int* counter, int n_blocks) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_last = atomicAdd(counter, 1) == n_blocks - 1;
+    if (s_last) *counter = 0;
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
+// values[i] = {L1 mean, D-SSIM}: the per-block partials added in block order
+// (one warp per image: lane-strided partial sums, then a fixed shuffle tree)
+__device__ __forceinline__ void photometric_finish_warp(const double* l1_part, int nb_l1, const double* ssim_part,
+                                                        int nb_ssim, double* values, int i, int W, int H) {
+  const int Wv = W - kWin + 1, Hv = H - kWin + 1;
+  const int lane = threadIdx.x & 31;
+  double a = 0.0, b = 0.0;
+  for (int k = lane; k < nb_l1; k += 32) a += __ldcg(l1_part + (long long)i * nb_l1 + k);
+  for (int k = lane; k < nb_ssim; k += 32) b += __ldcg(ssim_part + (long long)i * nb_ssim + k);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) {
+    values[2 * i] = a / ((double)W * H);
+    values[2 * i + 1] = 0.5 * (1.0 - b / ((double)Wv * Hv));
+  }
+}
+
 // vertical valid pass + per-window SSIM partials (objectives.cpp:93-149):
 // fields[img][5][Hv][Wv] = g1, g2, g2*mu1, g3, g3*mu2; SSIM-map sum per image
 // as per-block partials (grid: blocks per image x images).
@@ -253,7 +296,9 @@ __global__ void ssim_adj_v_kernel(const float* __restrict__ fields, int n, int W
 __global__ void __launch_bounds__(256) ssim_adj_h_kernel(const float* __restrict__ atmp, const float* __restrict__ r,
                                                          const float* __restrict__ mm, int n, int W, int H,
                                                          float rscale, Taps taps, float lambda_ssim, float grad_scale,
-                                                         float* __restrict__ dL, double* __restrict__ partial) {
+                                                         float* __restrict__ dL, double* __restrict__ partial,
+                                                         const double* __restrict__ ssim_part, int nb_ssim,
+                                                         double* __restrict__ values, int* __restrict__ counter) {
   const int Wv = W - kWin + 1, Hv = H - kWin + 1;
   const float inv_p = 1.f / ((float)Wv * (float)Hv);
   const float inv_n = 1.f / ((float)W * (float)H);
@@ -284,29 +329,10 @@ __global__ void __launch_bounds__(256) ssim_adj_h_kernel(const float* __restrict
     acc += (double)fabsf(d);
   }
   block_sum_to(acc, partial + img * gridDim.x + blockIdx.x);
-}
-
-// values[i] = {L1 mean, D-SSIM}: the per-block partials added in block order
-__global__ void photometric_finish_kernel(const double* __restrict__ l1_part, int nb_l1,
-                                          const double* __restrict__ ssim_part, int nb_ssim, double* values, int n,
-                                          int W, int H) {
-  // one warp per image: lane-strided partial sums, then a fixed shuffle tree
-  const int Wv = W - kWin + 1, Hv = H - kWin + 1;
-  const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x >> 5; i < n; i += blockDim.x >> 5) {
-    double a = 0.0, b = 0.0;
-    for (int k = lane; k < nb_l1; k += 32) a += l1_part[(long long)i * nb_l1 + k];
-    for (int k = lane; k < nb_ssim; k += 32) b += ssim_part[(long long)i * nb_ssim + k];
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b += __shfl_xor_sync(0xffffffffu, b, o);
-    }
-    if (lane == 0) {
-      values[2 * i] = a / ((double)W * H);
-      values[2 * i + 1] = 0.5 * (1.0 - b / ((double)Wv * Hv));
-    }
-  }
+  // the last block finishes both losses (the former photometric_finish_kernel)
+  if (last_block(counter, (int)(gridDim.x * gridDim.y)))
+    for (int i = threadIdx.x >> 5; i < n; i += blockDim.x >> 5)
+      photometric_finish_warp(partial, gridDim.x, ssim_part, nb_ssim, values, i, W, H);
 }
 
 int grid_cap(Ctx* c, long long n, int block) {
@@ -327,11 +353,7 @@ void launch_tv3d(Ctx* c, const float* vol, const int32_t dims[3], float lambda, 
   {
     KScope _ks(c, "K9_tv3d");
     tv3d_kernel<<<n_partials, 256, 0, c->stream>>>(vol, nx, ny, nz, (float)ix, (float)iy, (float)iz, lambda, grad,
-                                                   partials);
-  }
-  {
-    KScope _ks(c, "K9_tv3d_finish");
-    tv3d_finish_kernel<<<1, 32, 0, c->stream>>>(partials, n_partials, ix, iy, iz, value);
+                                                   partials, ix, iy, iz, value, c->fin_counter + 1);
   }
 }
 
@@ -396,11 +418,8 @@ int photometric_loss(Ctx* c, const float* rendered, const float* measured, int n
   {
     KScope _ks(c, "K11_ssim_adj_h");
     ssim_adj_h_kernel<<<dim3(nb_l1, n), 256, 0, c->stream>>>(tmp, rendered, measured, n, w, h, render_scale, taps,
-                                                             lambda_ssim, grad_scale, dL, l1_part);
-  }
-  {
-    KScope _ks(c, "K11_finish");
-    photometric_finish_kernel<<<1, 128, 0, c->stream>>>(l1_part, nb_l1, ssim_part, nb_ssim, values, n, w, h);
+                                                             lambda_ssim, grad_scale, dL, l1_part, ssim_part, nb_ssim,
+                                                             values, c->fin_counter);
   }
   dev_free(c, tmp);
   dev_free(c, fields);

@@ -102,6 +102,7 @@ struct Ctx {
   // set when a call's pairs exceed it (sct_ctx_take_overflow)
   int64_t cap_raster = 0, cap_voxel = 0;
   int* overflow = nullptr;
+  int* fin_counter = nullptr;  // [2] self-resetting last-block counters (photometric loss, TV)
   int sm_count = 148;
   // copy stream + events for the host-buffer entry points (H2D/D2H of view
   // chunks overlap the compute of neighbouring chunks)
