@@ -108,7 +108,13 @@ __global__ void __launch_bounds__(256) adam_kernel(long long m, float* __restric
                                                    const float* __restrict__ g_pos, const float* __restrict__ g_sc,
                                                    const float* __restrict__ g_rot, float lr_pos, float lr_rho,
                                                    float lr_sc, float lr_rot, float bc1, float bc2, float b1,
-                                                   float b2, float eps) {
+                                                   float b2, float eps, double* __restrict__ total,
+                                                   double lambda_ssim, double lambda_tv) {
+  // native train step: total = (l1 + lambda_ssim dssim) + lambda_tv tv from the
+  // loss values of this iteration (separately rounded products, as the host-side
+  // composition; trainer.cpp:302-303)
+  if (total && blockIdx.x == 0 && threadIdx.x == 0)
+    total[3] = __dadd_rn(__dadd_rn(total[0], __dmul_rn(lambda_ssim, total[1])), __dmul_rn(lambda_tv, total[2]));
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
 #pragma unroll
@@ -358,13 +364,15 @@ void launch_tv3d(Ctx* c, const float* vol, const int32_t dims[3], float lambda, 
 }
 
 void launch_adam(Ctx* c, sct_cloud* p, sct_adam_state* st, const sct_grads* g, const float lr[4], float bc1,
-                 float bc2, float beta1, float beta2, float eps) {
+                 float bc2, float beta1, float beta2, float eps, double* total, double lambda_ssim,
+                 double lambda_tv) {
   if (p->m == 0) return;
   {
     KScope _ks(c, "K10_adam");
     adam_kernel<<<grid_cap(c, p->m, 256), 256, 0, c->stream>>>(p->m, p->rho_raw, p->pos, p->scale_raw, p->rot, *st,
                                                                g->rho_raw, g->pos, g->scale_raw, g->rot, lr[0], lr[1],
-                                                               lr[2], lr[3], bc1, bc2, beta1, beta2, eps);
+                                                               lr[2], lr[3], bc1, bc2, beta1, beta2, eps, total,
+                                                               lambda_ssim, lambda_tv);
   }
 }
 

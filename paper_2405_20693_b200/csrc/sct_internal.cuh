@@ -364,7 +364,8 @@ void launch_project_export(Ctx* c, const sct_cloud& cl, const ViewParams* d_view
 void launch_tv3d(Ctx* c, const float* vol, const int32_t dims[3], float lambda, double* value, float* grad,
                  double* partials, int n_partials);
 void launch_adam(Ctx* c, sct_cloud* p, sct_adam_state* st, const sct_grads* g, const float lr[4], float bc1,
-                 float bc2, float beta1, float beta2, float eps);
+                 float bc2, float beta1, float beta2, float eps, double* total = nullptr,
+                 double lambda_ssim = 0.0, double lambda_tv = 0.0);
 int photometric_loss(Ctx* c, const float* rendered, const float* measured, int n, int w, int h,
                      float render_scale, float lambda_ssim, float grad_scale, double* values, float* dL);
 }  // namespace sct

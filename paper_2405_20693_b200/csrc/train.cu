@@ -15,6 +15,8 @@
 // of the GPU. Scratch images and volumes are grow-only context buffers.
 #include <cuda_runtime.h>
 
+#include <cmath>
+
 #include "sct_internal.cuh"
 
 namespace sct {
@@ -82,7 +84,18 @@ extern "C" int sct_train_step(sct_ctx* c, sct_cloud* cloud, sct_adam_state* adam
   } else {
     SCT_CUDA_TRY(cudaMemsetAsync(a->values_dev + 2, 0, sizeof(double), c->stream));
   }
-  train_total_kernel<<<1, 1, 0, c->stream>>>(a->values_dev, a->lambda_ssim, a->lambda_tv);
-  ++c->launches;
-  return sct_adam_step(c, cloud, adam, grads, a->t, a->lr, a->beta1, a->beta2, a->eps);
+  if (cloud->m == 0) {
+    train_total_kernel<<<1, 1, 0, c->stream>>>(a->values_dev, a->lambda_ssim, a->lambda_tv);
+    ++c->launches;
+    SCT_CUDA_TRY(cudaGetLastError());
+    return SCT_OK;
+  }
+  // Adam as sct_adam_step (trainer.cpp:152-153 bias corrections); its kernel
+  // also forms the total loss from values_dev (one launch fewer)
+  const double bc1 = 1.0 - std::pow(a->beta1, a->t), bc2 = 1.0 - std::pow(a->beta2, a->t);
+  const float lrf[4] = {(float)a->lr[0], (float)a->lr[1], (float)a->lr[2], (float)a->lr[3]};
+  launch_adam(c, cloud, adam, grads, lrf, (float)bc1, (float)bc2, (float)a->beta1, (float)a->beta2, (float)a->eps,
+              a->values_dev, a->lambda_ssim, a->lambda_tv);
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
 }
