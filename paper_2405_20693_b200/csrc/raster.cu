@@ -1061,6 +1061,10 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
 #define SCT_K4_REC16 0
 #endif
 constexpr int kMmaWarpsLarge = SCT_K4_WARPS, kMmaWarpsSmall = 4;
+#ifndef SCT_K4_LARGE_LISTS
+#define SCT_K4_LARGE_LISTS 32768
+#endif
+constexpr long long kK4LargeLists = SCT_K4_LARGE_LISTS;  // (view, tile) lists from which 2-warp CTAs pay
 
 __device__ __forceinline__ void mma_f16(float (&d)[4], __half2 a0, __half2 a1, __half2 a2, __half2 a3, uint32_t b0,
                                         uint32_t b1) {
@@ -2288,7 +2292,15 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
         parts, (int)n_work, work + 1, dL, ps, item_stats, ks);
     return;
   }
-  if (parts > 1)
+  // 2-warp CTAs only for large workloads: with fewer lists the longest list,
+  // worked by one CTA, becomes the kernel's tail (8-rank cfg3 shard, 10 views:
+  // 344 us with 2 warps vs 272 with 4; all 75 views: 1.77 vs 1.80 ms)
+  static const int forced_w = [] {  // SCT_K4_W=2|4 (diagnostic)
+    const char* e = std::getenv("SCT_K4_W");
+    return e ? atoi(e) : 0;
+  }();
+  const bool wide = forced_w ? forced_w == 4 : (parts > 1 || total < kK4LargeLists);
+  if (wide)
     backward_stats_mma_kernel<kMmaWarpsSmall><<<(unsigned)(total * parts), 32 * kMmaWarpsSmall, 0, c->stream>>>(
         s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
         parts, dL, ps, item_stats, ks);
