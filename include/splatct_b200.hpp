@@ -239,6 +239,23 @@ struct GradsF32 {
   }
 };
 
+// ProjectedGaussian2D (rasterizer.hpp:24-32), row-major 2x2 matrices.
+struct ProjectedGaussian2D {
+  double center_px[2] = {0.0, 0.0};
+  double cov_px[2][2] = {{1.0, 0.0}, {0.0, 1.0}};    // low-pass dilated
+  double conic_px[2][2] = {{1.0, 0.0}, {0.0, 1.0}};  // cov_px inverse
+  double amplitude = 0.0;
+  double mu = 0.0;
+  double depth_mm = 0.0;
+  int kernel_index = -1;
+};
+
+// project_kernel (rasterizer.hpp:36-38, rasterizer.cpp:103-110) for every kernel
+// of the cloud in one device call (FP64): the visible kernels in index order —
+// exactly RenderedProjection::visible of the reference's render()
+inline std::vector<ProjectedGaussian2D> project_kernels(const GaussianCloud& cloud, const ScannerConfig& config,
+                                                        double theta_rad, const RasterOptions& opts = {});
+
 // RenderedProjection (rasterizer.hpp:41-51): image + the device forward state.
 struct RenderedProjection {
   Image image;
@@ -259,7 +276,57 @@ struct RenderedProjection {
     for (int t = 0; t < T; ++t) out[t].assign(idx.begin() + off[t], idx.begin() + off[t + 1]);
     return out;
   }
+  int tile_of_pixel(int u, int v) const { return (v / 16) * tiles_x + (u / 16); }
+  // the reference's `visible` and `tile_visible` (indices into visible), built on
+  // request: the engine keeps its projection on the device, and an export costs
+  // an FP64 re-projection of every kernel (project_kernels) plus the tile lists
+  std::vector<ProjectedGaussian2D> visible(const GaussianCloud& cloud, const ScannerConfig& config) const {
+    return project_kernels(cloud, config, theta_rad, opts);
+  }
+  std::vector<std::vector<int>> tile_visible(const std::vector<ProjectedGaussian2D>& vis) const {
+    std::vector<int> pos_of;  // kernel index -> position in vis
+    for (size_t i = 0; i < vis.size(); ++i) {
+      const int k = vis[i].kernel_index;
+      if (k >= static_cast<int>(pos_of.size())) pos_of.resize(k + 1, -1);
+      pos_of[k] = static_cast<int>(i);
+    }
+    std::vector<std::vector<int>> out = tile_kernels();
+    for (auto& list : out)
+      for (int& k : list) k = pos_of[k];
+    return out;
+  }
 };
+
+inline std::vector<ProjectedGaussian2D> project_kernels(const GaussianCloud& cloud, const ScannerConfig& config,
+                                                        double theta_rad, const RasterOptions& opts) {
+  CloudF32 cf(cloud);
+  const sct_scanner sc = config.c();
+  const sct_raster_opts op = opts.c();
+  const int64_t m = cloud.size();
+  std::vector<int32_t> vis(m > 0 ? m : 1);
+  std::vector<double> rec(11 * (m > 0 ? m : 1));
+  check(sct_project_kernels(Context::get().handle(), &cf.c, &sc, theta_rad, &op, vis.data(), rec.data()));
+  std::vector<ProjectedGaussian2D> out;
+  for (int64_t i = 0; i < m; ++i) {
+    if (!vis[i]) continue;
+    const double* r = &rec[11 * i];  // cx cy cov00 cov01 cov11 conic00 conic01 conic11 amplitude mu depth
+    ProjectedGaussian2D g;
+    g.center_px[0] = r[0];
+    g.center_px[1] = r[1];
+    g.cov_px[0][0] = r[2];
+    g.cov_px[0][1] = g.cov_px[1][0] = r[3];
+    g.cov_px[1][1] = r[4];
+    g.conic_px[0][0] = r[5];
+    g.conic_px[0][1] = g.conic_px[1][0] = r[6];
+    g.conic_px[1][1] = r[7];
+    g.amplitude = r[8];
+    g.mu = r[9];
+    g.depth_mm = r[10];
+    g.kernel_index = static_cast<int>(i);
+    out.push_back(g);
+  }
+  return out;
+}
 
 // ---- the hot path --------------------------------------------------------------
 inline RenderedProjection render(const GaussianCloud& cloud, const ScannerConfig& config, double theta_rad,

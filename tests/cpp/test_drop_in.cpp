@@ -18,6 +18,9 @@ void* orc_render(int, double, const double*, const double*, const double*, const
                  const int*, double, const double*);
 void orc_render_free(void*);
 void orc_render_image(void*, double*);
+int orc_render_n_visible(void*);
+void orc_render_visible(void*, int32_t*, double*);
+void orc_render_tile_lists(void*, int64_t*, int32_t*);
 int orc_render_backward(void*, int, double, const double*, const double*, const double*, const double*,
                         const double*, const int*, double, const double*, const double*, double*, double*, double*,
                         double*, double*, int32_t*, double*);
@@ -74,6 +77,39 @@ int main() {
   std::vector<double> ref_img(129 * 129);
   orc_render_image(ref, ref_img.data());
   fails += report("render image", rel_l2(fwd.image.data, ref_img), 1e-4);
+  // RenderedProjection::visible / tile_visible (rasterizer.hpp:41-51) on request
+  {
+    const std::vector<S::ProjectedGaussian2D> vis = fwd.visible(cloud, cfg);
+    const int nv = orc_render_n_visible(ref);
+    std::vector<int32_t> rk(nv > 0 ? nv : 1);
+    std::vector<double> rr(11 * (nv > 0 ? nv : 1));
+    orc_render_visible(ref, rk.data(), rr.data());
+    int idx_bad = static_cast<int>(vis.size()) != nv;
+    std::vector<double> mine, theirs;
+    for (int i = 0; !idx_bad && i < nv; ++i) {
+      idx_bad += vis[i].kernel_index != rk[i];
+      const S::ProjectedGaussian2D& g = vis[i];
+      const double v[11] = {g.center_px[0], g.center_px[1], g.cov_px[0][0], g.cov_px[0][1], g.cov_px[1][1],
+                            g.conic_px[0][0], g.conic_px[0][1], g.conic_px[1][1], g.amplitude, g.mu, g.depth_mm};
+      for (int k = 0; k < 11; ++k) {
+        mine.push_back(v[k]);
+        theirs.push_back(rr[11 * i + k]);
+      }
+    }
+    fails += report("visible kernel indices (exact)", idx_bad, 0);
+    fails += report("visible records (FP64)", idx_bad ? 1.0 : rel_l2(mine, theirs), 1e-10);
+    const std::vector<std::vector<int>> tv = fwd.tile_visible(vis);
+    const int T = fwd.tiles_x * fwd.tiles_y;
+    std::vector<int64_t> off(T + 1);
+    std::vector<int32_t> tk(static_cast<size_t>(nv > 0 ? nv : 1) * T);  // bound: every visible kernel on every tile
+    orc_render_tile_lists(ref, off.data(), tk.data());
+    int tv_bad = static_cast<int>(tv.size()) != T;
+    for (int t = 0; !tv_bad && t < T; ++t) {
+      tv_bad += static_cast<int64_t>(tv[t].size()) != off[t + 1] - off[t];
+      for (size_t j = 0; !tv_bad && j < tv[t].size(); ++j) tv_bad += vis[tv[t][j]].kernel_index != tk[off[t] + j];
+    }
+    fails += report("tile_visible (exact)", tv_bad, 0);
+  }
 
   // render_backward (accumulate into zeroed grads, with adaptive stats)
   S::Image up(129, 129);
