@@ -305,7 +305,7 @@ inline std::vector<ProjectedGaussian2D> project_kernels(const GaussianCloud& clo
   const int64_t m = cloud.size();
   std::vector<int32_t> vis(m > 0 ? m : 1);
   std::vector<double> rec(11 * (m > 0 ? m : 1));
-  check(sct_project_kernels(Context::get().handle(), &cf.c, &sc, theta_rad, &op, vis.data(), rec.data()));
+  check(sct_project_kernels_host(Context::get().handle(), &cf.c, &sc, theta_rad, &op, vis.data(), rec.data()));
   std::vector<ProjectedGaussian2D> out;
   for (int64_t i = 0; i < m; ++i) {
     if (!vis[i]) continue;

@@ -171,6 +171,9 @@ int sct_fwd_tile_lists(sct_fwd* state, int32_t view, int64_t* offsets, int32_t* 
  * conic11 amplitude mu depth, computed in FP64. */
 int sct_project_kernels(sct_ctx* ctx, const sct_cloud* cloud, const sct_scanner* scanner, double theta,
                         const sct_raster_opts* opts, int32_t* visible, double* rec);
+/* the same with the cloud arrays in host memory */
+int sct_project_kernels_host(sct_ctx* ctx, const sct_cloud* cloud_host, const sct_scanner* scanner, double theta,
+                             const sct_raster_opts* opts, int32_t* visible, double* rec);
 
 /* Host-buffer entry points (reference-facing: host arrays in, host arrays out;
  * the H2D/D2H copies run on the context stream). cloud arrays are host fp32.

@@ -84,6 +84,8 @@ SIGNATURES = {
     "sct_fwd_info": (C.c_int, [VP, I64, I32, I32, I64]),
     "sct_fwd_tile_lists": (C.c_int, [VP, C.c_int32, I64, I32]),
     "sct_project_kernels": (C.c_int, [VP, P(sct_cloud), P(sct_scanner), C.c_double, P(sct_raster_opts), I32, D]),
+    "sct_project_kernels_host": (C.c_int, [VP, P(sct_cloud), P(sct_scanner), C.c_double, P(sct_raster_opts), I32,
+                                           D]),
     "sct_render_fwd_host": (C.c_int, [VP, P(sct_cloud), P(sct_scanner), D, C.c_int32, P(sct_raster_opts), VP,
                                       P(VP)]),
     "sct_render_bwd_host": (C.c_int, [VP, VP, P(sct_cloud), VP, P(sct_grads), P(sct_stats)]),

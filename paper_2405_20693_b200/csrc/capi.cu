@@ -1187,6 +1187,17 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
   return rc;
 }
 
+// sct_project_kernels with the cloud in host memory (the C++ drop-in's
+// RenderedProjection::visible / project_kernels)
+int sct_project_kernels_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scanner* scanner, double theta,
+                             const sct_raster_opts* opts, int32_t* visible, double* rec) {
+  SCT_TRY(check_cloud(cloud_host));
+  if (cloud_host->m == 0) return SCT_OK;
+  sct_cloud d;
+  SCT_TRY(upload_cloud(c, cloud_host, &d));
+  return sct_project_kernels(c, &d, scanner, theta, opts, visible, rec);
+}
+
 int sct_render_bwd_host(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud_host, const float* dL_host,
                         sct_grads* grads_host, sct_stats* stats_host) {
   if (!s || !grads_host || !dL_host) {
