@@ -13,6 +13,8 @@
 #pragma once
 
 #include <array>
+#include <chrono>
+#include <functional>
 #include <cmath>
 #include <cstdint>
 #include <memory>
@@ -416,6 +418,148 @@ inline void voxelize_backward(const GaussianCloud& cloud, const GridSpec& grid, 
   std::vector<float> dl(dL_dV.data.begin(), dL_dV.data.end());
   check(sct_voxelize_bwd_host(Context::get().handle(), &cf.c, &g, opts.cull_mahalanobis, dl.data(), &gf.c));
   gf.store(grads);
+}
+
+// ---- training (trainer.hpp / trainer.cpp:232-345) ------------------------------
+struct ProjectionSet {  // simulator.hpp:57-66 (the fields train() reads)
+  std::vector<Image> images;
+  std::vector<double> angles_rad;
+  ScannerConfig scanner;
+  int n_views() const { return static_cast<int>(images.size()); }
+};
+
+struct TrainConfig {  // trainer.hpp:13-44 (the fields the loop uses)
+  int iters = 30000;
+  double lr_position = 0.0002, lr_density = 0.01, lr_scale = 0.005, lr_rotation = 0.001;
+  double lr_final_ratio = 0.1;
+  double lambda_ssim = 0.25, lambda_tv = 0.05;
+  int tv_grid_dim = 32;
+  int adaptive_start = 500, adaptive_end = 15000, densify_interval = 100;
+  double densify_grad_threshold = 0.00005, prune_density_threshold = 0.005;
+  double split_scale_threshold_frac = 0.01, split_factor = 1.6;
+  uint64_t seed = 0;
+  RenderMode mode = RenderMode::kRectified;
+  std::array<int, 3> output_dims{64, 64, 64};
+  int history_interval = 10;
+  bool deterministic = false;  // zeroes wall-clock fields in history records
+  // engine extensions: sync-free binning after a calibration iteration (capacity
+  // = margin x measured pairs), and the non-finite check interval (1 = the reference)
+  bool sync_free = true;
+  double capacity_margin = 3.0;
+  int check_every = 1;
+};
+
+struct HistoryRecord {  // trainer.hpp:51-59
+  int iter = 0;
+  double l1 = 0.0, dssim = 0.0, tv = 0.0, total = 0.0;
+  int kernels = 0;
+  double wall_ms = 0.0;
+};
+
+struct TrainResult {  // trainer.hpp:80-84
+  GaussianCloud cloud;
+  std::vector<HistoryRecord> history;
+  double projection_norm = 1.0;
+};
+
+using TrainCallback = std::function<void(const HistoryRecord&)>;
+
+// train() (trainer.hpp:88-89): the whole loop on the device (sct_trainer_*), the
+// same random stream, adaptive control and history as the reference's.
+inline TrainResult train(GaussianCloud cloud, const ProjectionSet& projections, const TrainConfig& cfg,
+                         TrainCallback callback = nullptr) {
+  if (projections.n_views() < 1) throw DataError("InsufficientViews: train: need >= 1 projection");
+  if (cloud.size() < 1) throw ConfigError("train: empty initial cloud");
+  const ScannerConfig& config = projections.scanner;
+  const int w = config.detector_res_px[0], h = config.detector_res_px[1];
+  const size_t px = static_cast<size_t>(w) * h;
+  std::vector<float> proj(px * projections.n_views());
+  double norm = 0.0;
+  for (int v = 0; v < projections.n_views(); ++v) {
+    const Image& im = projections.images[v];
+    if (im.width != w || im.height != h) throw DimMismatch("train: projection dims differ from the detector");
+    for (size_t i = 0; i < px; ++i) {
+      proj[v * px + i] = static_cast<float>(im.data[i]);
+      norm = std::max(norm, static_cast<double>(proj[v * px + i]));
+    }
+  }
+  sct_train_cfg c{};
+  c.iters = cfg.iters;
+  c.lr_position = cfg.lr_position;
+  c.lr_density = cfg.lr_density;
+  c.lr_scale = cfg.lr_scale;
+  c.lr_rotation = cfg.lr_rotation;
+  c.lr_final_ratio = cfg.lr_final_ratio;
+  c.lambda_ssim = cfg.lambda_ssim;
+  c.lambda_tv = cfg.lambda_tv;
+  c.tv_grid_dim = cfg.tv_grid_dim;
+  c.adaptive_start = cfg.adaptive_start;
+  c.adaptive_end = cfg.adaptive_end;
+  c.densify_interval = cfg.densify_interval;
+  c.densify_grad_threshold = cfg.densify_grad_threshold;
+  c.prune_density_threshold = cfg.prune_density_threshold;
+  c.split_scale_threshold_frac = cfg.split_scale_threshold_frac;
+  c.split_factor = cfg.split_factor;
+  c.seed = cfg.seed;
+  c.mode = cfg.mode == RenderMode::kRectified ? SCT_MODE_RECTIFIED : SCT_MODE_BIASED;
+  for (int k = 0; k < 3; ++k) c.output_dims[k] = cfg.output_dims[k];
+  c.check_every = cfg.check_every;
+  c.sync_free = cfg.sync_free ? 1 : 0;
+  c.capacity_margin = cfg.capacity_margin;
+  CloudF32 cf(cloud);
+  const sct_scanner sc = config.c();
+  sct_trainer* tr = nullptr;
+  check(sct_trainer_create(Context::get().handle(), &cf.c, proj.data(), projections.angles_rad.data(),
+                           projections.n_views(), &sc, &c, &tr));
+  std::unique_ptr<sct_trainer, int (*)(sct_trainer*)> guard(tr, sct_trainer_destroy);
+  TrainResult result;
+  result.projection_norm = norm > 0.0 ? norm : 1.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  sct_train_record rec{};
+  for (int t = 1; t <= cfg.iters; ++t) {
+    check(sct_trainer_step(tr, nullptr));
+    if (t % cfg.history_interval == 0 || t == cfg.iters) {
+      check(sct_trainer_record(tr, &rec));
+      HistoryRecord hr;
+      hr.iter = t;
+      hr.l1 = rec.l1;
+      hr.dssim = rec.dssim;
+      hr.tv = rec.tv;
+      hr.total = rec.total;
+      hr.kernels = static_cast<int>(rec.kernels);
+      hr.wall_ms = cfg.deterministic ? 0.0
+                                     : std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                                           .count();
+      result.history.push_back(hr);
+      if (callback) callback(hr);
+    }
+  }
+  check(sct_trainer_record(tr, &rec));
+  const int64_t m = rec.kernels;
+  std::vector<float> p[4] = {std::vector<float>(m), std::vector<float>(3 * m), std::vector<float>(3 * m),
+                             std::vector<float>(4 * m)};
+  sct_cloud out{};
+  out.m = m;
+  out.rho_raw = p[0].data();
+  out.pos = p[1].data();
+  out.scale_raw = p[2].data();
+  out.rot = p[3].data();
+  std::vector<float> s_norm(m), s_3d(3 * m);
+  std::vector<int32_t> s_cnt(m);
+  sct_stats st{};
+  st.grad2d_norm_accum = s_norm.data();
+  st.grad_count = s_cnt.data();
+  st.grad3d_accum = s_3d.data();
+  check(sct_trainer_download(tr, &out, nullptr, &st));
+  result.cloud.s_min_mm = out.s_min_mm;
+  result.cloud.rho_raw.assign(p[0].begin(), p[0].end());
+  result.cloud.pos.assign(p[1].begin(), p[1].end());
+  result.cloud.scale_raw.assign(p[2].begin(), p[2].end());
+  result.cloud.rot.assign(p[3].begin(), p[3].end());
+  result.cloud.grad2d_norm_accum.assign(s_norm.begin(), s_norm.end());
+  result.cloud.grad_count.assign(s_cnt.begin(), s_cnt.end());
+  result.cloud.grad3d_accum.assign(s_3d.begin(), s_3d.end());
+  return result;
 }
 
 }  // namespace splatct_b200

@@ -260,6 +260,48 @@ typedef struct {
 int sct_train_step(sct_ctx* ctx, sct_cloud* cloud, sct_adam_state* adam, sct_stats* stats, sct_grads* grads,
                    const sct_scanner* scanner, const sct_raster_opts* opts, const sct_train_args* args);
 
+/* ---- the reference's train() loop as a native object (trainer.cpp:232-345) --- */
+/* The whole run on the device: sct_trainer_create uploads the cloud and the
+ * projections (normalised by their maximum, trainer.cpp:243-252); each
+ * sct_trainer_step draws the view (std::shuffle epochs) and the TV sub-grid
+ * origin from std::mt19937_64(seed), runs sct_train_step, the non-finite check
+ * every check_every iterations (the reference: 1) and adaptive control at the
+ * reference's iterations (split draws from the same stream). sync_free: binning
+ * in capacity mode (capacity_margin x the pairs measured on a calibration step,
+ * the first and after each adaptive control). sct_trainer_record syncs and
+ * returns the last iteration's losses (the reference's HistoryRecord without
+ * wall time); sct_trainer_download copies the cloud (and, when non-NULL, the
+ * Adam moments and statistics) into host arrays of the trainer's current size. */
+typedef struct {
+  int32_t iters;
+  double lr_position, lr_density, lr_scale, lr_rotation, lr_final_ratio;
+  double lambda_ssim, lambda_tv;
+  int32_t tv_grid_dim;
+  int32_t adaptive_start, adaptive_end, densify_interval;
+  double densify_grad_threshold, prune_density_threshold, split_scale_threshold_frac, split_factor;
+  uint64_t seed;
+  int32_t mode; /* SCT_MODE_RECTIFIED | SCT_MODE_BIASED */
+  int32_t output_dims[3];
+  int32_t check_every;
+  int32_t sync_free;
+  double capacity_margin;
+} sct_train_cfg;
+typedef struct {
+  int32_t iter, view;
+  double l1, dssim, tv, total;
+  int64_t kernels;
+  int32_t counts[3]; /* the last adaptive control's pruned, cloned, split */
+} sct_train_record;
+typedef struct sct_trainer sct_trainer;
+int sct_trainer_create(sct_ctx* ctx, const sct_cloud* cloud_host, const float* projections_host,
+                       const double* angles_rad, int32_t n_views, const sct_scanner* scanner,
+                       const sct_train_cfg* cfg, sct_trainer** out);
+int sct_trainer_step(sct_trainer* trainer, int32_t* adapted);
+int sct_trainer_record(sct_trainer* trainer, sct_train_record* rec);
+int sct_trainer_download(sct_trainer* trainer, sct_cloud* cloud_host, sct_adam_state* adam_host,
+                         sct_stats* stats_host);
+int sct_trainer_destroy(sct_trainer* trainer);
+
 /* ---- adaptive density control (trainer.cpp:167-230) ---------------------- */
 /* Two phases so the caller can size the new cloud: sct_adaptive_plan classifies
  * every kernel (prune rho < prune_density_threshold; clone or split kernels whose

@@ -61,6 +61,22 @@ class sct_train_args(C.Structure):
                 ("beta2", C.c_double), ("eps", C.c_double), ("values_dev", VP)]
 
 
+class sct_train_cfg(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("lr_position", C.c_double), ("lr_density", C.c_double),
+                ("lr_scale", C.c_double), ("lr_rotation", C.c_double), ("lr_final_ratio", C.c_double),
+                ("lambda_ssim", C.c_double), ("lambda_tv", C.c_double), ("tv_grid_dim", C.c_int32),
+                ("adaptive_start", C.c_int32), ("adaptive_end", C.c_int32), ("densify_interval", C.c_int32),
+                ("densify_grad_threshold", C.c_double), ("prune_density_threshold", C.c_double),
+                ("split_scale_threshold_frac", C.c_double), ("split_factor", C.c_double), ("seed", C.c_uint64),
+                ("mode", C.c_int32), ("output_dims", C.c_int32 * 3), ("check_every", C.c_int32),
+                ("sync_free", C.c_int32), ("capacity_margin", C.c_double)]
+
+
+class sct_train_record(C.Structure):
+    _fields_ = [("iter", C.c_int32), ("view", C.c_int32), ("l1", C.c_double), ("dssim", C.c_double),
+                ("tv", C.c_double), ("total", C.c_double), ("kernels", C.c_int64), ("counts", C.c_int32 * 3)]
+
+
 P = C.POINTER
 
 SIGNATURES = {
@@ -105,6 +121,11 @@ SIGNATURES = {
     "sct_adam_step": (C.c_int, [VP, P(sct_cloud), P(sct_adam_state), P(sct_grads), C.c_int32, D, C.c_double,
                                 C.c_double, C.c_double]),
     "sct_lr_at": (C.c_double, [C.c_double, C.c_double, C.c_int32, C.c_int32]),
+    "sct_trainer_create": (C.c_int, [VP, P(sct_cloud), VP, D, C.c_int32, P(sct_scanner), P(sct_train_cfg), P(VP)]),
+    "sct_trainer_step": (C.c_int, [VP, I32]),
+    "sct_trainer_record": (C.c_int, [VP, P(sct_train_record)]),
+    "sct_trainer_download": (C.c_int, [VP, P(sct_cloud), P(sct_adam_state), P(sct_stats)]),
+    "sct_trainer_destroy": (C.c_int, [VP]),
     "sct_train_step": (C.c_int, [VP, P(sct_cloud), P(sct_adam_state), P(sct_stats), P(sct_grads), P(sct_scanner),
                                  P(sct_raster_opts), P(sct_train_args)]),
     "sct_adaptive_plan": (C.c_int, [VP, P(sct_cloud), P(sct_stats), C.c_double, C.c_double, C.c_double, C.c_double,

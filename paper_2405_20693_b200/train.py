@@ -216,3 +216,98 @@ class Trainer:
         self.grads.resize(self.cloud.size(), device=self.eng.device)
         self._calibrate = cfg.sync_free  # new kernel count: re-measure the pair counts
         return counts
+
+
+class NativeTrainer:
+    """The reference's train() loop (trainer.cpp:232-345) run entirely in the engine
+    library (csrc/trainer.cu, sct_trainer_*): views, TV sub-grid origins and split draws
+    from the same std::mt19937_64(cfg.seed) stream as Trainer, adaptive control at the
+    same iterations, losses read back only by record(). Equal to Trainer bitwise."""
+
+    def __init__(self, engine: Engine, cloud, scanner: ScannerConfig, angles: Sequence[float],
+                 projections, cfg: TrainConfig):
+        import ctypes as C
+        from . import _capi
+        self.eng, self.cfg, self.lib = engine, cfg, _capi.load()
+        host = cloud.host_arrays() if isinstance(cloud, GaussianCloud) else cloud
+        self._host = {k: np.ascontiguousarray(host[k], dtype=np.float32) for k in ("rho_raw", "pos", "scale_raw",
+                                                                                    "rot")}
+        s_min = cloud.s_min if isinstance(cloud, GaussianCloud) else float(host["s_min"])
+        self.s_min = s_min
+        cl = _capi.sct_cloud()
+        cl.m, cl.s_min_mm = int(self._host["rho_raw"].size), s_min
+        for k, a in self._host.items():
+            setattr(cl, k, a.ctypes.data)
+        proj = projections.detach().cpu().numpy() if isinstance(projections, torch.Tensor) else projections
+        self._proj = np.ascontiguousarray(proj, dtype=np.float32)
+        self._angles = (C.c_double * len(angles))(*[float(a) for a in angles])
+        c = _capi.sct_train_cfg()
+        for k in ("iters", "tv_grid_dim", "adaptive_start", "adaptive_end", "densify_interval", "mode",
+                  "check_every"):
+            setattr(c, k, int(getattr(cfg, k)))
+        for k in ("lr_position", "lr_density", "lr_scale", "lr_rotation", "lr_final_ratio", "lambda_ssim",
+                  "lambda_tv", "densify_grad_threshold", "prune_density_threshold", "split_scale_threshold_frac",
+                  "split_factor", "capacity_margin"):
+            setattr(c, k, float(getattr(cfg, k)))
+        c.seed = int(cfg.seed) & ((1 << 64) - 1)
+        c.output_dims[:] = [int(x) for x in cfg.output_dims]
+        c.sync_free = int(bool(cfg.sync_free))
+        h = C.c_void_p()
+        sc = scanner._c()
+        rc = self.lib.sct_trainer_create(engine._h, C.byref(cl), self._proj.ctypes.data, self._angles, len(angles),
+                                         C.byref(sc), C.byref(c), C.byref(h))
+        from .engine import _check
+        _check(rc)
+        self._h = h
+
+    def step(self) -> bool:
+        """One iteration; True when adaptive control ran after it."""
+        import ctypes as C
+        from .engine import _check
+        ad = C.c_int32(0)
+        _check(self.lib.sct_trainer_step(self._h, C.byref(ad)))
+        return bool(ad.value)
+
+    def record(self) -> dict:
+        """The last iteration's losses (synchronises), as the reference's HistoryRecord."""
+        from . import _capi
+        from .engine import _check
+        import ctypes as C
+        r = _capi.sct_train_record()
+        _check(self.lib.sct_trainer_record(self._h, C.byref(r)))
+        return {"iter": r.iter, "view": r.view, "l1": r.l1, "dssim": r.dssim, "tv": r.tv, "total": r.total,
+                "kernels": int(r.kernels), "adaptive": tuple(r.counts)}
+
+    def state(self) -> dict:
+        """Host copies of the cloud, Adam moments and adaptive statistics."""
+        import ctypes as C
+        from . import _capi
+        from .engine import _check
+        m = self.record()["kernels"]
+        out = {k: np.zeros(n * m, dtype=np.float32) for k, n in (("rho_raw", 1), ("pos", 3), ("scale_raw", 3),
+                                                                  ("rot", 4))}
+        cl = _capi.sct_cloud()
+        cl.m = m
+        for k, a in out.items():
+            setattr(cl, k, a.ctypes.data)
+        adam = {f"{a}_{k}": np.zeros(n * m, dtype=np.float32) for a in ("m", "v")
+                for k, n in (("rho", 1), ("pos", 3), ("scale", 3), ("rot", 4))}
+        ad = _capi.sct_adam_state()
+        for k, a in adam.items():
+            setattr(ad, k, a.ctypes.data)
+        stats = {"grad2d_norm_accum": np.zeros(m, dtype=np.float32), "grad_count": np.zeros(m, dtype=np.int32),
+                 "grad3d_accum": np.zeros(3 * m, dtype=np.float32)}
+        st = _capi.sct_stats()
+        for k, a in stats.items():
+            setattr(st, k, a.ctypes.data)
+        _check(self.lib.sct_trainer_download(self._h, C.byref(cl), C.byref(ad), C.byref(st)))
+        return {**out, "adam": adam, **stats}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                self.lib.sct_trainer_destroy(h)
+            except Exception:  # noqa: BLE001 (interpreter shutdown)
+                pass
+            self._h = None

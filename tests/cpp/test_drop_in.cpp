@@ -183,6 +183,40 @@ int main() {
   } catch (const S::ConfigError&) {
     fails += report("ConfigError on opts mismatch", 0, 0);
   }
+  // train() (trainer.hpp:88-89) on the device: a short seeded run with TV and
+  // adaptive control; history bookkeeping and bit-reproducibility (test_trainer.cpp:87-105)
+  {
+    S::ProjectionSet ps;
+    ps.scanner = cfg;
+    for (int v = 0; v < 4; ++v) {
+      ps.angles_rad.push_back(2.0 * M_PI * v / 4);
+      ps.images.push_back(S::render(cloud, cfg, ps.angles_rad.back()).image);
+    }
+    S::GaussianCloud init = cloud;
+    for (double& x : init.rho_raw) x -= 0.3;  // start away from the target
+    S::TrainConfig tc;
+    tc.iters = 9;
+    tc.output_dims = {32, 32, 32};
+    tc.tv_grid_dim = 8;
+    tc.adaptive_start = 3;
+    tc.densify_interval = 3;
+    tc.densify_grad_threshold = 1e-7;
+    tc.history_interval = 1;
+    tc.deterministic = true;
+    tc.seed = 5;
+    int calls = 0;
+    const S::TrainResult r1 = S::train(init, ps, tc, [&](const S::HistoryRecord&) { ++calls; });
+    const S::TrainResult r2 = S::train(init, ps, tc);
+    int bad = static_cast<int>(r1.history.size()) != 9 || calls != 9;
+    for (size_t i = 0; !bad && i < r1.history.size(); ++i) {
+      const S::HistoryRecord &a = r1.history[i], &b = r2.history[i];
+      bad += a.iter != static_cast<int>(i) + 1 || !std::isfinite(a.total) || a.total != b.total || a.l1 != b.l1 ||
+             a.kernels != b.kernels || a.wall_ms != 0.0;
+    }
+    bad += r1.cloud.size() != r1.history.back().kernels || r1.cloud.pos != r2.cloud.pos ||
+           r1.cloud.rho_raw != r2.cloud.rho_raw;
+    fails += report("train(): history, determinism (exact)", bad, 0);
+  }
   orc_rng_free(rng);
   std::printf("%s (%d failures)\n", fails ? "FAIL" : "ALL PASS", fails);
   return fails;

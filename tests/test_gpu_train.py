@@ -154,3 +154,45 @@ def test_native_step_equals_python_step(sync_free):
     assert len(s0) == len(s1)
     for a, b in zip(s0, s1):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("sync_free", [False, True])
+def test_native_trainer_equals_trainer(sync_free):
+    """The engine-side train() loop (sct_trainer_*, csrc/trainer.cu) against the Python
+    Trainer on the same seed: the same views, losses, adaptive-control counts and final
+    cloud / Adam moments / statistics, bitwise (every draw from one std::mt19937_64)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_2405_20693_b200 as P
+    from paper_2405_20693_b200.train import NativeTrainer, TrainConfig, Trainer
+
+    res, n_views = 64, 6
+    scanner_o = O.test_scanner(res)
+    angles = O.full_circle_angles(n_views)
+    target = O.random_cloud(O.Rng(5), 80, 0.6, 0.05, 0.15)
+    meas = torch.from_numpy(np.stack([O.render(target, scanner_o, th).image for th in angles]).astype(np.float32))
+    oc = O.random_cloud(O.Rng(7), 300, 0.6, 0.01, 0.12)
+    f32 = [np.asarray(a, dtype=np.float32) for a in (oc.rho_raw, oc.pos, oc.scale_raw, oc.rot)]
+    cfg = TrainConfig(iters=40, output_dims=(32, 32, 32), tv_grid_dim=8, adaptive_start=3, densify_interval=4,
+                      densify_grad_threshold=1e-6, prune_density_threshold=0.05, seed=13, sync_free=sync_free,
+                      check_every=1)
+    sc = P.ScannerConfig(detector_res_px=(res, res))
+    tr = Trainer(P.Engine(0), P.GaussianCloud(oc.s_min, *f32), sc, angles, meas, cfg)
+    py = []
+    for _ in range(12):
+        out = tr.step()
+        py.append((out["view"], float(out["l1"]), float(out["dssim"]), float(out["tv"]), float(out["total"]),
+                   out["kernels"]))
+    nt = NativeTrainer(P.Engine(0), P.GaussianCloud(oc.s_min, *f32), sc, angles, meas, cfg)
+    nat = []
+    for _ in range(12):
+        nt.step()
+        r = nt.record()
+        nat.append((r["view"], r["l1"], r["dssim"], r["tv"], r["total"], r["kernels"]))
+    assert py == nat
+    st = nt.state()
+    c = tr.cloud
+    for k in ("rho_raw", "pos", "scale_raw", "rot", "grad2d_norm_accum", "grad_count", "grad3d_accum"):
+        np.testing.assert_array_equal(st[k], getattr(c, k).cpu().numpy(), err_msg=k)
+    for k, v in c.adam.items():
+        np.testing.assert_array_equal(st["adam"][k], v.cpu().numpy(), err_msg=k)
