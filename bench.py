@@ -655,7 +655,7 @@ def run_train(args, eng, dev):
 
     import paper_2405_20693_b200 as P
     from paper_2405_20693_b200 import scenes
-    from paper_2405_20693_b200.train import TrainConfig, Trainer
+    from paper_2405_20693_b200.train import NativeTrainer, TrainConfig
     w = scenes.CONFIGS[2]
     ca = scenes.make_cloud(2)
     angles = P.full_circle_angles(w.n_views)
@@ -668,7 +668,9 @@ def run_train(args, eng, dev):
     f.free()
     cloud = P.GaussianCloud(ca.s_min, ca.rho_raw, ca.pos, ca.scale_raw, ca.rot, device=dev)
     cfg = TrainConfig(iters=1000, output_dims=(w.n_vox,) * 3, tv_grid_dim=32, check_every=0, sync_free=True)
-    tr = Trainer(eng, cloud, sc, angles, meas, cfg)
+    # the reference's train() loop entirely in the engine library (sct_trainer_*):
+    # equal to train.py's Trainer bitwise (tests/test_gpu_train.py)
+    tr = NativeTrainer(eng, cloud, sc, angles, meas, cfg)
     warm_up(tr.step, max(3, args.warmup))
     n = max(10, args.steps)
     torch.cuda.synchronize()
@@ -676,16 +678,18 @@ def run_train(args, eng, dev):
     launches0 = eng.kernel_launches()
     a.record(eng.stream)
     for _ in range(n):
-        out = tr.step()
+        tr.step()
     b.record(eng.stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / n
+    out = tr.record()
     if eng.take_overflow():
         raise RuntimeError("train step: sync-free binning overflowed its capacity")
     eng.set_capacity(0, 0)
     return {"metric": "train iterations/sec", "value": 1000.0 / ms, "unit": "iters/s", "ms_per_iter": ms,
             "workload": "cfg2 (BASELINE configs[1]): " + w.description, "iters": n,
             "last_total_loss": float(out["total"]), "engine_launches_per_iter": (eng.kernel_launches() - launches0) / n,
+            "loop": "native (sct_trainer_step: view shuffle, sub-grid draw, sct_train_step, adaptive control)",
             "binning": "sync-free (TrainConfig.sync_free: capacity from a calibration iteration, overflow "
                        "checked after the timed region)",
             "note": "1 view per iteration as trainer.cpp:268-276; context: the paper's RTX 3090 CUDA code "
