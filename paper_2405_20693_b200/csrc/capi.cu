@@ -686,7 +686,8 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
 // chunks > 0: the upstream gradient arrives in `chunks` view chunks, chunk k
 // signalled by ctx->ev_copy[k]; K4 for chunk k waits only for its own copy.
 int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL, sct_grads* grads,
-                         sct_stats* stats, int chunks) {
+                         sct_stats* stats, int chunks, double** defer_vsum, int* defer_groups) {
+  if (defer_vsum) *defer_vsum = nullptr;
   if (!c || !s || !grads || !dL) {
     set_error("ConfigError: null argument");
     return SCT_ERR_CONFIG;
@@ -739,6 +740,12 @@ int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
   if (nch > 1) {
     SCT_CUDA_TRY(cudaEventRecord(c->ev_join, c->aux_stream));
     SCT_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  }
+  if (defer_vsum) {
+    *defer_vsum = vsum;
+    if (defer_groups) *defer_groups = nch;
+    SCT_CUDA_TRY(cudaGetLastError());
+    return SCT_OK;
   }
   launch_raster_finalize(c, s, *cloud, vsum, nch, grads, stats);
   SCT_CUDA_TRY(cudaGetLastError());

@@ -20,6 +20,7 @@
 
 #include <cstdlib>
 
+#include "adam.cuh"
 #include "fp64_math.cuh"
 #include "project.cuh"
 #include "sct_internal.cuh"
@@ -350,6 +351,70 @@ __global__ void __launch_bounds__(128) raster_finalize_kernel(
   }
 }
 
+// The native train step's tail (sct_train_step): raster_finalize_kernel's
+// per-kernel chain added to gradients that already hold the TV contribution
+// (the same two float additions as finalize-then-voxelize_backward: a + b ==
+// b + a), the adaptive statistics, and Adam — one pass over the kernels instead
+// of two, and the gradients never written back.
+__global__ void __launch_bounds__(128) raster_finalize_adam_kernel(
+    long long m, double s_min, float* __restrict__ rho_raw, float* __restrict__ pos, float* __restrict__ scale_raw,
+    float* __restrict__ rot, const double* __restrict__ vsum, int groups, const float* __restrict__ g_rho,
+    const float* __restrict__ g_pos, const float* __restrict__ g_scale, const float* __restrict__ g_rotp,
+    float* __restrict__ st_norm, int32_t* __restrict__ st_count, float* __restrict__ st_3d, sct_adam_state adam,
+    AdamParams ap, double* __restrict__ total, double lambda_ssim, double lambda_tv) {
+  if (total && blockIdx.x == 0 && threadIdx.x == 0) train_total(total, lambda_ssim, lambda_tv);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    float g[11];
+    g[0] = g_rho[i];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g[1 + k] = g_pos[3 * i + k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g[4 + k] = g_scale[3 * i + k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) g[7 + k] = g_rotp[4 * i + k];
+    if (vsum) {
+      double acc[kItemOut];
+#pragma unroll
+      for (int a = 0; a < kItemOut; ++a) acc[a] = vsum[a * m + i];
+      double nv = vsum[kItemOut * m + i];
+      for (int gi = 1; gi < groups; ++gi) {
+        const double* p = vsum + (long long)gi * (kItemOut + 1) * m;
+#pragma unroll
+        for (int a = 0; a < kItemOut; ++a) acc[a] += p[a * m + i];
+        nv += p[kItemOut * m + i];
+      }
+      const int nvis = (int)nv;
+      if (nvis > 0) {  // as raster_finalize_kernel
+        const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
+        g[0] += (float)(acc[0] * d_act_density_grad(k.rho_raw));
+#pragma unroll
+        for (int a = 0; a < 3; ++a) g[1 + a] += (float)acc[1 + a];
+        dM3 Gs;
+        Gs.m[0][0] = acc[4];
+        Gs.m[1][1] = acc[5];
+        Gs.m[2][2] = acc[6];
+        Gs.m[0][1] = Gs.m[1][0] = acc[7];
+        Gs.m[0][2] = Gs.m[2][0] = acc[8];
+        Gs.m[1][2] = Gs.m[2][1] = acc[9];
+        double gs[3], gr[4];
+        d_cov_param_grads(k, Gs, gs, gr);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) g[4 + a] += (float)gs[a];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) g[7 + a] += (float)gr[a];
+        if (st_norm) {
+          st_norm[i] += (float)acc[10];
+          st_count[i] += nvis;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) st_3d[3 * i + a] += (float)acc[1 + a];
+        }
+      }
+    }
+    adam_kernel_update(i, rho_raw, pos, scale_raw, rot, adam, g, ap);
+  }
+}
+
 // The 10 pair-statistic sums of every kernel (FP64): eight lanes per kernel,
 // lane j summing pairs j, j + 8, ... in order, then a fixed xor-shuffle tree
 // — deterministic, and eight times the threads of the one-thread-per-kernel
@@ -513,6 +578,20 @@ void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const
   raster_finalize_kernel<<<grid_cap(c, s->m, 128), 128, 0, c->stream>>>(
       s->m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, vsum, g->rho_raw, g->pos, g->scale_raw, g->rot,
       st ? st->grad2d_norm_accum : nullptr, st ? st->grad_count : nullptr, st ? st->grad3d_accum : nullptr, groups);
+}
+
+void launch_raster_finalize_adam(Ctx* c, int64_t m, const sct_fwd* s, sct_cloud* cl, const double* vsum, int groups,
+                                 const sct_grads* g, sct_stats* st, sct_adam_state* adam, const float lr[4],
+                                 float bc1, float bc2, float b1, float b2, float eps, double* total,
+                                 double lambda_ssim, double lambda_tv) {
+  if (m == 0) return;
+  (void)s;
+  KScope _ks(c, "K10_finalize_adam");
+  const AdamParams ap{lr[0], lr[1], lr[2], lr[3], bc1, bc2, b1, b2, eps};
+  raster_finalize_adam_kernel<<<grid_cap(c, m, 128), 128, 0, c->stream>>>(
+      m, cl->s_min_mm, cl->rho_raw, cl->pos, cl->scale_raw, cl->rot, vsum, groups, g->rho_raw, g->pos, g->scale_raw,
+      g->rot, st ? st->grad2d_norm_accum : nullptr, st ? st->grad_count : nullptr, st ? st->grad3d_accum : nullptr,
+      *adam, ap, total, lambda_ssim, lambda_tv);
 }
 
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "adam.cuh"
 #include "sct_internal.cuh"
 
 namespace sct {
@@ -92,61 +93,26 @@ __device__ void tv3d_finish_warp(const double* partials, int n_blocks, double in
 }
 
 // ---------------------------------------------------------------- Adam
-__device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, float lr, float bc1, float bc2,
-                                      float b1, float b2, float eps) {
-  m = b1 * m + (1.f - b1) * g;
-  v = b2 * v + (1.f - b2) * g * g;
-  const float mhat = m / bc1;
-  const float vhat = v / bc2;
-  p -= lr * mhat / (sqrtf(vhat) + eps);
-}
-
-// One thread per kernel: rho (1), pos (3), scale (3), rot (4) + renormalisation.
+// One thread per kernel: rho (1), pos (3), scale (3), rot (4) + renormalisation (adam.cuh).
 __global__ void __launch_bounds__(256) adam_kernel(long long m, float* __restrict__ rho, float* __restrict__ pos,
                                                    float* __restrict__ sc, float* __restrict__ rot,
                                                    sct_adam_state st, const float* __restrict__ g_rho,
                                                    const float* __restrict__ g_pos, const float* __restrict__ g_sc,
-                                                   const float* __restrict__ g_rot, float lr_pos, float lr_rho,
-                                                   float lr_sc, float lr_rot, float bc1, float bc2, float b1,
-                                                   float b2, float eps, double* __restrict__ total,
-                                                   double lambda_ssim, double lambda_tv) {
-  // native train step: total = (l1 + lambda_ssim dssim) + lambda_tv tv from the
-  // loss values of this iteration (separately rounded products, as the host-side
-  // composition; trainer.cpp:302-303)
-  if (total && blockIdx.x == 0 && threadIdx.x == 0)
-    total[3] = __dadd_rn(__dadd_rn(total[0], __dmul_rn(lambda_ssim, total[1])), __dmul_rn(lambda_tv, total[2]));
+                                                   const float* __restrict__ g_rot, AdamParams ap,
+                                                   double* __restrict__ total, double lambda_ssim, double lambda_tv) {
+  // native train step: the total loss of this iteration
+  if (total && blockIdx.x == 0 && threadIdx.x == 0) train_total(total, lambda_ssim, lambda_tv);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
+    float g[11];
+    g[0] = g_rho[i];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const long long j = 3 * i + a;
-      float p = pos[j], mm = st.m_pos[j], vv = st.v_pos[j];
-      adam1(p, mm, vv, g_pos[j], lr_pos, bc1, bc2, b1, b2, eps);
-      pos[j] = p; st.m_pos[j] = mm; st.v_pos[j] = vv;
-    }
-    {
-      float p = rho[i], mm = st.m_rho[i], vv = st.v_rho[i];
-      adam1(p, mm, vv, g_rho[i], lr_rho, bc1, bc2, b1, b2, eps);
-      rho[i] = p; st.m_rho[i] = mm; st.v_rho[i] = vv;
-    }
+    for (int k = 0; k < 3; ++k) g[1 + k] = g_pos[3 * i + k];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const long long j = 3 * i + a;
-      float p = sc[j], mm = st.m_scale[j], vv = st.v_scale[j];
-      adam1(p, mm, vv, g_sc[j], lr_sc, bc1, bc2, b1, b2, eps);
-      sc[j] = p; st.m_scale[j] = mm; st.v_scale[j] = vv;
-    }
-    float q[4];
+    for (int k = 0; k < 3; ++k) g[4 + k] = g_sc[3 * i + k];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const long long j = 4 * i + a;
-      float p = rot[j], mm = st.m_rot[j], vv = st.v_rot[j];
-      adam1(p, mm, vv, g_rot[j], lr_rot, bc1, bc2, b1, b2, eps);
-      q[a] = p; st.m_rot[j] = mm; st.v_rot[j] = vv;
-    }
-    const float n = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-#pragma unroll
-    for (int a = 0; a < 4; ++a) rot[4 * i + a] = q[a] / n;
+    for (int k = 0; k < 4; ++k) g[7 + k] = g_rot[4 * i + k];
+    adam_kernel_update(i, rho, pos, sc, rot, st, g, ap);
   }
 }
 
@@ -369,9 +335,9 @@ void launch_adam(Ctx* c, sct_cloud* p, sct_adam_state* st, const sct_grads* g, c
   if (p->m == 0) return;
   {
     KScope _ks(c, "K10_adam");
+    const AdamParams ap{lr[0], lr[1], lr[2], lr[3], bc1, bc2, beta1, beta2, eps};
     adam_kernel<<<grid_cap(c, p->m, 256), 256, 0, c->stream>>>(p->m, p->rho_raw, p->pos, p->scale_raw, p->rot, *st,
-                                                               g->rho_raw, g->pos, g->scale_raw, g->rot, lr[0], lr[1],
-                                                               lr[2], lr[3], bc1, bc2, beta1, beta2, eps, total,
+                                                               g->rho_raw, g->pos, g->scale_raw, g->rot, ap, total,
                                                                lambda_ssim, lambda_tv);
   }
 }

@@ -283,8 +283,12 @@ struct sct_ctx : public sct::Ctx {};
 
 // render backward with optional view-chunk pipelining (capi.cu; chunks = 0:
 // the device-resident path); shared by the plain and the NCCL entry points
+// defer_vsum != nullptr: stop before the finalize and hand back the chain's
+// view-range partials (staging slot 15) and their count (the native train step
+// finalizes them inside its Adam kernel); *defer_vsum = nullptr: no visible item
 extern "C" int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const float* dL,
-                                      sct_grads* grads, sct_stats* stats, int chunks);
+                                      sct_grads* grads, sct_stats* stats, int chunks,
+                                      double** defer_vsum = nullptr, int* defer_groups = nullptr);
 
 // ------------------------------------------------------------------ kernel entry points
 namespace sct {
@@ -355,6 +359,14 @@ void launch_raster_chain(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const fl
                          bool per_item = false, int v0 = 0, int v1 = -1, cudaStream_t stream = nullptr);
 void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const double* vsum, int groups,
                             sct_grads* g, sct_stats* st);
+// the finalize fused with Adam (native train step): grads already hold the TV
+// contribution; the raster part is added per kernel, the statistics updated, and
+// the Adam step (+ quaternion renormalisation, + the total loss) applied at once.
+// vsum == nullptr: no raster contribution this iteration
+void launch_raster_finalize_adam(Ctx* c, int64_t m, const sct_fwd* s, sct_cloud* cl, const double* vsum, int groups,
+                                 const sct_grads* g, sct_stats* st, sct_adam_state* adam, const float lr[4],
+                                 float bc1, float bc2, float b1, float b2, float eps, double* total,
+                                 double lambda_ssim, double lambda_tv);
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,
                         const float4* pair_stats, sct_grads* g);
 // project_kernel export (FP64)

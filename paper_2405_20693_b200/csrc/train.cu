@@ -66,7 +66,11 @@ extern "C" int sct_train_step(sct_ctx* c, sct_cloud* cloud, sct_adam_state* adam
   int rc = sct_photometric_loss(c, img, a->measured, 1, w, h, a->render_scale, (float)a->lambda_ssim,
                                 a->grad_scale, a->values_dev, dl);
   if (rc == SCT_OK) rc = zero_grads(c, grads, cloud->m);
-  if (rc == SCT_OK) rc = sct_render_bwd(c, fwd, cloud, dl, grads, stats);
+  // the backward up to the chain's view-range partials; their finalize runs
+  // inside the Adam kernel below, after the TV term added its gradients
+  double* vsum = nullptr;
+  int groups = 0;
+  if (rc == SCT_OK) rc = sct_render_bwd_chunked(c, fwd, cloud, dl, grads, stats, 0, &vsum, &groups);
   sct_fwd_free(fwd);
   SCT_TRY(rc);
   if (a->lambda_tv > 0.0) {
@@ -90,12 +94,13 @@ extern "C" int sct_train_step(sct_ctx* c, sct_cloud* cloud, sct_adam_state* adam
     SCT_CUDA_TRY(cudaGetLastError());
     return SCT_OK;
   }
-  // Adam as sct_adam_step (trainer.cpp:152-153 bias corrections); its kernel
-  // also forms the total loss from values_dev (one launch fewer)
+  // raster finalize + Adam (sct_adam_step's bias corrections, trainer.cpp:152-153)
+  // + the total loss, in one kernel
   const double bc1 = 1.0 - std::pow(a->beta1, a->t), bc2 = 1.0 - std::pow(a->beta2, a->t);
   const float lrf[4] = {(float)a->lr[0], (float)a->lr[1], (float)a->lr[2], (float)a->lr[3]};
-  launch_adam(c, cloud, adam, grads, lrf, (float)bc1, (float)bc2, (float)a->beta1, (float)a->beta2, (float)a->eps,
-              a->values_dev, a->lambda_ssim, a->lambda_tv);
+  launch_raster_finalize_adam(c, cloud->m, nullptr, cloud, vsum, groups, grads, stats, adam, lrf, (float)bc1,
+                              (float)bc2, (float)a->beta1, (float)a->beta2, (float)a->eps, a->values_dev,
+                              a->lambda_ssim, a->lambda_tv);
   SCT_CUDA_TRY(cudaGetLastError());
   return SCT_OK;
 }
