@@ -1339,7 +1339,7 @@ int sct_voxelize_bwd(sct_ctx* c, const sct_cloud* cloud, const sct_grid* grid, d
   if (rc == SCT_OK) {
     launch_voxel_backward_stats(c, *grid, b.zb0, b.zb1, b.bx, b.by, b.ranges, b.vals, b.rec, b.lo, b.hi, b.offset,
                                 *cloud, b.n_pairs, dL, ps);
-    launch_voxel_chain(c, *cloud, b.offset, b.count, ps, grads);
+    launch_voxel_chain(c, *cloud, b.offset, b.count, ps, grads, (int64_t)b.bx * b.by * (b.zb1 - b.zb0));
   }
   dev_free(c, ps);
   b.release(c);
@@ -1406,7 +1406,8 @@ int sct_voxelize_bwd_state(sct_ctx* c, sct_vox_state* s, const sct_cloud* cloud,
   SCT_TRY(dev_alloc(c, (void**)&ps, 3 * s->b.n_pairs * sizeof(float4)));
   launch_voxel_backward_stats(c, s->grid, s->b.zb0, s->b.zb1, s->b.bx, s->b.by, s->b.ranges, s->b.vals, s->b.rec,
                               s->b.lo, s->b.hi, s->b.offset, *cloud, s->b.n_pairs, dL, ps);
-  launch_voxel_chain(c, *cloud, s->b.offset, s->b.count, ps, grads);
+  launch_voxel_chain(c, *cloud, s->b.offset, s->b.count, ps, grads,
+                     (int64_t)s->b.bx * s->b.by * (s->b.zb1 - s->b.zb0));
   dev_free(c, ps);
   if (cudaGetLastError() != cudaSuccess) {
     set_error("CUDA error: kernel launch in sct_voxelize_bwd_state");

@@ -595,9 +595,16 @@ void launch_raster_finalize_adam(Ctx* c, int64_t m, const sct_fwd* s, sct_cloud*
 }
 
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,
-                        const float4* pair_stats, sct_grads* g) {
+                        const float4* pair_stats, sct_grads* g, int64_t n_bricks) {
   if (cl.m == 0) return;
   double* sums = nullptr;
+  if (n_bricks >= 0 && n_bricks <= 512) {  // few pairs per kernel: summed in the chain thread, one launch
+    KScope _ks(c, "K8_voxel_chain");
+    voxel_chain_kernel<<<grid_cap(c, cl.m, 128), 128, 0, c->stream>>>(cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
+                                                                     cl.scale_raw, cl.rot, offset, count, pair_stats,
+                                                                     nullptr, g->rho_raw, g->pos, g->scale_raw, g->rot);
+    return;
+  }
   if (dev_alloc(c, (void**)&sums, 10 * cl.m * sizeof(double)) != SCT_OK) return;
   {
     KScope _ks(c, "K8_voxel_pair_sum");

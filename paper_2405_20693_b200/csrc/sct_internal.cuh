@@ -367,8 +367,11 @@ void launch_raster_finalize_adam(Ctx* c, int64_t m, const sct_fwd* s, sct_cloud*
                                  const sct_grads* g, sct_stats* st, sct_adam_state* adam, const float lr[4],
                                  float bc1, float bc2, float b1, float b2, float eps, double* total,
                                  double lambda_ssim, double lambda_tv);
+// n_bricks: bricks of the binned grid; small grids (the train step's TV
+// sub-grid) sum each kernel's few pairs inside the chain instead of a separate
+// 8-lanes-per-kernel pass
 void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, const int32_t* count,
-                        const float4* pair_stats, sct_grads* g);
+                        const float4* pair_stats, sct_grads* g, int64_t n_bricks = -1);
 // project_kernel export (FP64)
 void launch_project_export(Ctx* c, const sct_cloud& cl, const ViewParams* d_view, const DetParams& det,
                            const RasterParams& rp, int32_t* vis, double* rec);
