@@ -137,8 +137,12 @@ static int bits_for(uint64_t n) {  // smallest b with 2^b >= n (n >= 1)
 // step's 50k items (29 vs 13 us: one CTA walks the tiles at memory latency),
 // so it only takes tiny inputs
 constexpr int64_t kCountScanSmallUse = 4096;
+// max_per_item > 0: no item counts more than that, so when (n + 1) * max_per_item
+// fits in int32 the int32 scan cannot wrap and the int64 reduction is skipped
+// (two launches fewer: the train step's single-view and TV binnings)
 static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t* total, int64_t cap = 0,
-                       short4* box_a = nullptr, short4* box_b = nullptr) {
+                       short4* box_a = nullptr, short4* box_b = nullptr, int64_t max_per_item = 0) {
+  const bool no_wrap = max_per_item > 0 && (n + 1) * max_per_item < (int64_t)INT32_MAX;
   SCT_CUDA_TRY(cudaMemsetAsync(count + n, 0, sizeof(int32_t), c->stream));
   if (n + 1 <= kCountScanSmallUse) {  // one CTA: scan, int64 total and capacity guard
     {
@@ -154,12 +158,14 @@ static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64
   } else {
     long long* d_sum = c->sum64;
     size_t tmp = 0;
-    SCT_CUDA_TRY(cub::DeviceReduce::Sum(nullptr, tmp, count, d_sum, n + 1, c->stream));
-    SCT_TRY(ensure_cub_tmp(c, tmp));
-    tmp = c->cub_tmp_bytes;
-    SCT_CUDA_TRY(cub::DeviceReduce::Sum(c->cub_tmp, tmp, count, d_sum, n + 1, c->stream));
-    SCT_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(c->pinned_count) + 64, d_sum, sizeof(long long),
-                                 cudaMemcpyDeviceToHost, c->stream));
+    if (!no_wrap) {
+      SCT_CUDA_TRY(cub::DeviceReduce::Sum(nullptr, tmp, count, d_sum, n + 1, c->stream));
+      SCT_TRY(ensure_cub_tmp(c, tmp));
+      tmp = c->cub_tmp_bytes;
+      SCT_CUDA_TRY(cub::DeviceReduce::Sum(c->cub_tmp, tmp, count, d_sum, n + 1, c->stream));
+      SCT_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(c->pinned_count) + 64, d_sum, sizeof(long long),
+                                   cudaMemcpyDeviceToHost, c->stream));
+    }
     tmp = 0;
     SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, offset, n + 1, c->stream));
     SCT_TRY(ensure_cub_tmp(c, tmp));
@@ -169,7 +175,7 @@ static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64
       SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, offset, n + 1, c->stream));
     }
     if (cap > 0) {
-      launch_capacity_guard(c, count, offset, n, box_a, box_b, cap);
+      launch_capacity_guard(c, count, offset, n, box_a, box_b, cap, no_wrap);
       *total = cap;
       return SCT_OK;
     }
@@ -179,7 +185,10 @@ static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64
   SCT_CUDA_TRY(cudaMemcpyAsync(c->pinned_count, offset + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
   std::memcpy(&t, c->pinned_count, sizeof(int32_t));
-  std::memcpy(&t64, reinterpret_cast<char*>(c->pinned_count) + 64, sizeof(long long));
+  if (no_wrap)
+    t64 = t;
+  else
+    std::memcpy(&t64, reinterpret_cast<char*>(c->pinned_count) + 64, sizeof(long long));
   if (t64 > INT32_MAX || t < 0) {
     set_error("DataError: more than 2^31-1 (tile, kernel) pairs in one call; split the views into batches");
     return SCT_ERR_DATA;
@@ -309,7 +318,7 @@ static int voxel_bin(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull
   // key beyond every brick id, so it sorts last and the range scan skips it).
   const bool scatter = bin_scatter_fits(b.bx, b.by, b.bz);
   const int64_t cap = c->cap_voxel;
-  SCT_TRY(scan_counts(c, b.count, b.offset, m, &b.n_pairs, cap, b.lo, b.hi));
+  SCT_TRY(scan_counts(c, b.count, b.offset, m, &b.n_pairs, cap, b.lo, b.hi, (int64_t)b.bx * b.by * b.bz));
   if (scatter) {
     SCT_TRY(dev_alloc(c, (void**)&b.vals, std::max<int64_t>(b.n_pairs, 1) * sizeof(int32_t)));
     SCT_TRY(launch_bin_scatter(c, 1, m, b.bx, b.by, b.bz, b.lo, b.hi, b.vals, b.ranges, b.n_pairs, nullptr));
@@ -622,7 +631,9 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   // sort needs the exact count on the host)
   const bool scatter = raster_bin_scatter_fits(s->det.tiles_x, s->det.tiles_y);
   const int64_t cap = (c->cap_raster > 0 && scatter) ? c->cap_raster : 0;
-  if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs, cap, s->d_rect, nullptr))) return fail(rc);
+  if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs, cap, s->d_rect, nullptr,
+                        (int64_t)s->det.tiles_x * s->det.tiles_y)))
+    return fail(rc);
   if (cap > 0) {
     s->exact = false;
     if ((rc = dev_alloc(c, (void**)&s->d_total, sizeof(int32_t)))) return fail(rc);

@@ -307,7 +307,8 @@ __global__ void __launch_bounds__(256) capacity_guard_kernel(int32_t* __restrict
                                                              short4* __restrict__ box_b,
                                                              const long long* __restrict__ sum64, long long cap,
                                                              int* __restrict__ overflow) {
-  const long long total = *sum64;
+  // sum64 == nullptr: the int32 scan cannot have wrapped, offset[n] is the total
+  const long long total = sum64 ? *sum64 : (long long)offset[n];
   if (total <= cap && offset[n] >= 0) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(overflow, 1);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x) {
@@ -1797,9 +1798,9 @@ void launch_count_scan_small(Ctx* c, int32_t* count, int32_t* offset, int64_t n,
 }
 
 void launch_capacity_guard(Ctx* c, int32_t* count, int32_t* offset, int64_t n, short4* box_a, short4* box_b,
-                           int64_t cap) {
-  capacity_guard_kernel<<<grid_cap(c, n + 1, 256), 256, 0, c->stream>>>(count, offset, n, box_a, box_b, c->sum64,
-                                                                        (long long)cap, c->overflow);
+                           int64_t cap, bool no_wrap) {
+  capacity_guard_kernel<<<grid_cap(c, n + 1, 256), 256, 0, c->stream>>>(
+      count, offset, n, box_a, box_b, no_wrap ? nullptr : c->sum64, (long long)cap, c->overflow);
 }
 
 // Stable counting-scatter binning of n_views x m items with boxes (lo, hi)

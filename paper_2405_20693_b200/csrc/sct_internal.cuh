@@ -318,7 +318,8 @@ constexpr int64_t kCountScanSmall = 1 << 16;
 void launch_count_scan_small(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t cap, short4* box_a,
                              short4* box_b);
 void launch_capacity_guard(Ctx* c, int32_t* count, int32_t* offset, int64_t n, short4* box_a, short4* box_b,
-                           int64_t cap);
+                           int64_t cap,
+                           bool no_wrap = false);
 bool bin_scatter_fits(int tiles_x, int tiles_y, int tiles_z);
 int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tiles_y, int tiles_z, const short4* lo,
                        const short4* hi, int32_t* vals, int2* ranges, int64_t cap, int32_t* total,
