@@ -309,14 +309,15 @@ static int voxel_bin(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull
   SCT_TRY(dev_alloc(c, (void**)&b.count, (m + 1) * sizeof(int32_t)));
   SCT_TRY(dev_alloc(c, (void**)&b.offset, (m + 1) * sizeof(int32_t)));
   SCT_TRY(dev_alloc(c, (void**)&b.ranges, nbr * sizeof(int2)));
-  SCT_CUDA_TRY(cudaMemsetAsync(b.ranges, 0, nbr * sizeof(int2), c->stream));
+  // the counting scatter writes every brick range from its scan (m > 0)
+  const bool scatter = bin_scatter_fits(b.bx, b.by, b.bz);
+  if (!scatter || m == 0) SCT_CUDA_TRY(cudaMemsetAsync(b.ranges, 0, nbr * sizeof(int2), c->stream));
   launch_voxel_preprocess(c, cl, g, cull, b.zb0, b.zb1, b.bx, b.by, b.rec, b.lo, b.hi, b.count);
   // Brick lists: the stable counting scatter (raster.cu launch_bin_scatter)
   // when the brick table fits in shared memory, else emit + radix sort.
   // Capacity mode (sct_ctx_set_capacity): no host readback of the pair count;
   // the buffers hold cap pairs (sort path: the unused tail carries a padding
   // key beyond every brick id, so it sorts last and the range scan skips it).
-  const bool scatter = bin_scatter_fits(b.bx, b.by, b.bz);
   const int64_t cap = c->cap_voxel;
   SCT_TRY(scan_counts(c, b.count, b.offset, m, &b.n_pairs, cap, b.lo, b.hi, (int64_t)b.bx * b.by * b.bz));
   if (scatter) {
@@ -351,6 +352,42 @@ static int voxel_bin(Ctx* c, const sct_cloud& cl, const sct_grid& g, double cull
   return SCT_OK;
 }
 
+}  // namespace sct
+
+namespace sct {
+namespace {
+// Forward-state initialisation in one launch: the view matrices arrive as a
+// kernel parameter (no pageable host->device copy, whose copy-engine round trip
+// costs more than a launch), the tile ranges are zeroed and the capacity-mode
+// pair total reset.
+constexpr int kViewPack = 16;
+struct ViewPack {
+  ViewParams v[kViewPack];
+};
+__global__ void fwd_init_kernel(ViewPack p, int nv, ViewParams* dst, int2* ranges, int64_t n_ranges, int32_t* total) {
+  if (blockIdx.x == 0 && threadIdx.x < nv) dst[threadIdx.x] = p.v[threadIdx.x];
+  if (total && blockIdx.x == 0 && threadIdx.x == 0) *total = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_ranges; i += (int64_t)gridDim.x * blockDim.x)
+    ranges[i] = make_int2(0, 0);
+}
+
+int fwd_init(Ctx* c, const std::vector<ViewParams>& hv, ViewParams* d_views, int2* ranges, int64_t n_ranges,
+             int32_t* total) {
+  for (size_t v0 = 0; v0 < hv.size() || v0 == 0; v0 += kViewPack) {
+    ViewPack p;
+    const int nv = (int)std::min<size_t>(kViewPack, hv.size() - v0);
+    for (int k = 0; k < nv; ++k) p.v[k] = hv[v0 + k];
+    const bool first = v0 == 0;
+    const int grid = first ? (int)std::max<int64_t>(1, std::min<int64_t>((n_ranges + 255) / 256, 4 * c->sm_count)) : 1;
+    fwd_init_kernel<<<grid, 256, 0, c->stream>>>(p, nv, d_views + v0, ranges, first ? n_ranges : 0,
+                                                 first ? total : nullptr);
+    ++c->launches;
+    if (hv.empty()) break;
+  }
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
+}  // namespace
 }  // namespace sct
 
 using namespace sct;
@@ -607,11 +644,6 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   std::vector<ViewParams> hv(n_views);
   for (int v = 0; v < n_views; ++v) hv[v] = make_view(*scanner, thetas[v]);
   if ((rc = dev_alloc(c, (void**)&s->d_views, n_views * sizeof(ViewParams)))) return fail(rc);
-  if (cudaMemcpyAsync(s->d_views, hv.data(), n_views * sizeof(ViewParams), cudaMemcpyHostToDevice, c->stream) !=
-      cudaSuccess) {
-    set_error("CUDA error: view upload");
-    return fail(SCT_ERR_CUDA);
-  }
   const int64_t ni = s->n_items;
   if ((rc = dev_alloc(c, (void**)&s->d_rec, 2 * ni * sizeof(float4)))) return fail(rc);
   if ((rc = dev_alloc(c, (void**)&s->d_rect, ni * sizeof(short4)))) return fail(rc);
@@ -619,29 +651,20 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   if ((rc = dev_alloc(c, (void**)&s->d_offset, (ni + 1) * sizeof(int32_t)))) return fail(rc);
   if ((rc = dev_alloc(c, (void**)&s->d_vis, ni + 1))) return fail(rc);
   if ((rc = dev_alloc(c, (void**)&s->d_ranges, n_views * T * sizeof(int2)))) return fail(rc);
-  if (cudaMemsetAsync(s->d_ranges, 0, n_views * T * sizeof(int2), c->stream) != cudaSuccess) {
-    set_error("CUDA error: memset");
-    return fail(SCT_ERR_CUDA);
-  }
-  if ((rc = dev_alloc(c, (void**)&s->d_prep, kPrepStride * s->m * sizeof(double)))) return fail(rc);
-  launch_gauss_prep(c, *cloud, s->d_prep);
-  launch_raster_preprocess(c, *cloud, s->d_prep, s->d_views, n_views, s->det, s->rp, s->d_rec, s->d_rect,
-                           s->d_count, s->d_vis);
   // capacity mode: sync-free when the counting scatter applies (the radix
   // sort needs the exact count on the host)
   const bool scatter = raster_bin_scatter_fits(s->det.tiles_x, s->det.tiles_y);
   const int64_t cap = (c->cap_raster > 0 && scatter) ? c->cap_raster : 0;
+  if (cap > 0 && (rc = dev_alloc(c, (void**)&s->d_total, sizeof(int32_t)))) return fail(rc);
+  if ((rc = fwd_init(c, hv, s->d_views, s->d_ranges, n_views * T, s->d_total))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&s->d_prep, kPrepStride * s->m * sizeof(double)))) return fail(rc);
+  launch_gauss_prep(c, *cloud, s->d_prep);
+  launch_raster_preprocess(c, *cloud, s->d_prep, s->d_views, n_views, s->det, s->rp, s->d_rec, s->d_rect,
+                           s->d_count, s->d_vis);
   if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs, cap, s->d_rect, nullptr,
                         (int64_t)s->det.tiles_x * s->det.tiles_y)))
     return fail(rc);
-  if (cap > 0) {
-    s->exact = false;
-    if ((rc = dev_alloc(c, (void**)&s->d_total, sizeof(int32_t)))) return fail(rc);
-    if (cudaMemsetAsync(s->d_total, 0, sizeof(int32_t), c->stream) != cudaSuccess) {
-      set_error("CUDA error: memset");
-      return fail(SCT_ERR_CUDA);
-    }
-  }
+  if (cap > 0) s->exact = false;
   // Binning: one stable counting scatter straight into (tile, view, kernel)
   // order when the tile table fits in shared memory (raster.cu bin_*), else
   // emit + radix sort. SCT_BIN=sort forces the latter.
