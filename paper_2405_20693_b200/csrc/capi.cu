@@ -1121,6 +1121,7 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
     return SCT_ERR_CONFIG;
   }
   sct_cloud d;
+  g_dbg.mark(c->stream, "start");
   SCT_TRY(upload_cloud(c, cloud_host, &d));
   const size_t px = (size_t)scanner->det_res_px[0] * scanner->det_res_px[1];
   float* dimg = nullptr;
@@ -1142,6 +1143,7 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
   int rc = sct_render_fwd(c, &d, scanner, thetas, n_views, opts, nullptr, state);
   c->fwd_split_views = -1;
   if (rc != SCT_OK) return rc;
+  g_dbg.mark(c->stream, "binned");
   if (units_ok && (*state)->n_pairs > 0 && raster_units_supported(c, *state)) {
     // one composite over all views; unit u's D2H copy starts when the
     // composite publishes unit_flags[0][u] (and at the latest after the
@@ -1169,10 +1171,13 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
     if ((*state)->defer) {  // views [0, v_split): composite; then the rest of the scatter and its composite
       const int T = (*state)->det.tiles_x * (*state)->det.tiles_y;
       SCT_TRY(launch_raster_composite_units(c, *state, dimg, us, 0, T * v_split));
+      g_dbg.mark(c->stream, "comp1");
       sct::BinDeferred* rest = (*state)->defer;
       (*state)->defer = nullptr;
       SCT_TRY(launch_bin_scatter_rest(c, rest));
+      g_dbg.mark(c->stream, "scatter2");
       SCT_TRY(launch_raster_composite_units(c, *state, dimg, us, T * v_split, -1));
+      g_dbg.mark(c->stream, "comp2");
     } else {
       SCT_TRY(launch_raster_composite_units(c, *state, dimg, us));
     }
@@ -1184,6 +1189,7 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
       SCT_CUDA_TRY(cudaMemcpyAsync(images_host + v0 * px, dimg + v0 * px, (v1 - v0) * px * sizeof(float),
                                    cudaMemcpyDeviceToHost, c->copy_stream));
       if (dbg) cudaEventRecord(ec[u], c->copy_stream);
+      if (u == 0 || u == units / 2 || u == units - 1) g_dbg.mark(c->copy_stream, "d2h" + std::to_string(u));
     }
     SCT_CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
     SCT_CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1208,6 +1214,7 @@ int sct_render_fwd_host(sct_ctx* c, const sct_cloud* cloud_host, const sct_scann
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
     }
+    g_dbg.report("fwd_host");
     return SCT_OK;
   }
   // without stream memory operations: one composite, then one copy

@@ -63,6 +63,12 @@ t0 = time.perf_counter()
 x.copy_(dL.view(-1), non_blocking=True)
 torch.cuda.synchronize()
 print(f"torch H2D 78.6MB {1e3*(time.perf_counter()-t0):.2f} ms")
+for _ in range(2):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    imgs.view(-1).copy_(x, non_blocking=True)
+    torch.cuda.synchronize()
+    print(f"torch D2H 78.6MB {1e3*(time.perf_counter()-t0):.2f} ms")
 
 # long loops: per-step wall times of the host path and the device path
 import subprocess
