@@ -204,12 +204,19 @@ __global__ void __launch_bounds__(256) bin_segscan_kernel(int32_t* __restrict__ 
                                                           int32_t* __restrict__ coltot) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
+  // 16 loads in flight before the in-place stores (a load after a store to
+  // the same array is not hoisted: one L2 round trip per segment otherwise,
+  // 34 us at cfg3's 115 segments)
   int32_t run = 0;
-#pragma unroll 8
-  for (int g = 0; g < n_seg; ++g) {
-    const int32_t x = seg[(long long)g * T + t];
-    seg[(long long)g * T + t] = run;
-    run += x;
+  for (int g0 = 0; g0 < n_seg; g0 += 16) {
+    int32_t x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = g0 + k < n_seg ? seg[(long long)(g0 + k) * T + t] : 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (g0 + k < n_seg) seg[(long long)(g0 + k) * T + t] = run;
+      run += x[k];
+    }
   }
   coltot[t] = run;
 }
@@ -793,54 +800,52 @@ __global__ void __launch_bounds__(256) k3_parts_kernel(const int2* __restrict__ 
   }
 }
 
-// k3_parts + scan + k3_items + the tile counter reset in one CTA, for small
-// list counts (n <= kSmallWork; the train step and 8-rank shards): thread t
-// takes the lists [t * per, (t + 1) * per) of the order.
+// k3_parts + the scan in one CTA, for small list counts (n <= kSmallWork; the
+// train step and 8-rank shards): thread t takes the lists [t * per, (t + 1) *
+// per) of the order in two passes (part counts, then after the block scan the
+// first item of each list). The items themselves are written by the
+// multi-CTA k3_items_kernel: from one SM the scattered 16-byte item stores
+// were the bottleneck (34 us for the 10-view shard's 26k items).
 constexpr int kSmallWorkThreads = 1024, kSmallWork = 16 * kSmallWorkThreads;
-__global__ void __launch_bounds__(kSmallWorkThreads) k3_work_small_kernel(
-    const int2* __restrict__ ranges, const int* __restrict__ order, int n, int part_len, int* __restrict__ first,
-    int4* __restrict__ items, int* __restrict__ n_items, int* __restrict__ tile_cnt, long long max_items) {
+__global__ void __launch_bounds__(kSmallWorkThreads) k3_first_small_kernel(const int2* __restrict__ ranges,
+                                                                           const int* __restrict__ order, int n,
+                                                                           int part_len, int* __restrict__ count,
+                                                                           int* __restrict__ first) {
   using Scan = cub::BlockScan<int, kSmallWorkThreads>;
   __shared__ typename Scan::TempStorage tmp;
   const int per = (n + kSmallWorkThreads - 1) / kSmallWorkThreads;
   const int i0 = min(n, (int)threadIdx.x * per), i1 = min(n, i0 + per);
-  int cnt[16], w[16];
+  auto parts_of = [&](int w) {
+    const int2 r = ranges[w];
+    return max(1, (r.y - r.x + part_len - 1) / part_len);
+  };
   int mine = 0;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int i = i0 + k;
-    cnt[k] = 0;
-    w[k] = 0;
-    if (i < i1) {
-      w[k] = order[i];
-      const int2 r = ranges[w[k]];
-      cnt[k] = max(1, (r.y - r.x + part_len - 1) / part_len);
-      mine += cnt[k];
-    }
+#pragma unroll 4
+  for (int i = i0; i < i1; ++i) {
+    const int k = parts_of(order[i]);
+    count[i] = k;
+    mine += k;
   }
-  int f = 0, total = 0;
-  Scan(tmp).ExclusiveSum(mine, f, total);
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int i = i0 + k;
-    if (i < i1) {
-      first[i] = f;
-      for (int p = 0; p < cnt[k]; ++p) items[f + p] = make_int4(w[k], p, cnt[k], f);
-      f += cnt[k];
-    }
+  int f = 0;
+  Scan(tmp).ExclusiveSum(mine, f);
+  for (int i = i0; i < i1; ++i) {
+    first[i] = f;
+    f += count[i];
   }
-  if (threadIdx.x == 0) *n_items = total;
-  for (long long j = threadIdx.x; j < max_items; j += kSmallWorkThreads) tile_cnt[j] = 0;
 }
 
+// the items of every list, and the reset of K3's per-item tile counters
 __global__ void __launch_bounds__(256) k3_items_kernel(const int* __restrict__ order, const int* __restrict__ count,
                                                        const int* __restrict__ first, int n,
-                                                       int4* __restrict__ items, int* __restrict__ n_items) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+                                                       int4* __restrict__ items, int* __restrict__ n_items,
+                                                       int* __restrict__ tile_cnt, long long max_items) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int)stride) {
     const int k = count[i], f = first[i], w = order[i];
     for (int p = 0; p < k; ++p) items[f + p] = make_int4(w, p, k, f);
     if (i == n - 1) *n_items = f + k;
   }
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < max_items; j += stride) tile_cnt[j] = 0;
 }
 
 // K4: Gaussian-major backward statistics. One 256-thread CTA per non-empty
@@ -1991,6 +1996,47 @@ __global__ void __launch_bounds__(kSmallOrderThreads) tile_order_small_kernel(co
   }
 }
 
+// The same stable 16-bucket order by a one-CTA counting sort, for list counts
+// beyond the block radix sort's register tile (kSmallOrder < n <= kMidOrder:
+// 8-rank cfg3 shards, 10 views = 10 240 lists; the device-wide sort took four
+// launches, 28 us). Thread t owns lists [t * per, (t + 1) * per); the counts
+// cnt[bucket][thread] are exclusive-scanned in (bucket, thread) order, which is
+// exactly the stable output position of each thread's first list per bucket.
+constexpr int kMidOrderThreads = 1024, kMidOrderPer = 64;
+constexpr int kMidOrder = kMidOrderThreads * kMidOrderPer;
+__global__ void __launch_bounds__(kMidOrderThreads) tile_order_mid_kernel(const int2* __restrict__ ranges,
+                                                                          long long base, int n,
+                                                                          int32_t* __restrict__ order) {
+  using Scan = cub::BlockScan<int32_t, kMidOrderThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  extern __shared__ int32_t cnt[];  // [16][kMidOrderThreads]
+  const int tid = threadIdx.x;
+  const int per = (n + kMidOrderThreads - 1) / kMidOrderThreads;
+  const int w0 = min(n, tid * per), w1 = min(n, w0 + per);
+#pragma unroll
+  for (int b = 0; b < 16; ++b) cnt[b * kMidOrderThreads + tid] = 0;
+#pragma unroll 4
+  for (int w = w0; w < w1; ++w) {
+    const int2 r = ranges[base + w];
+    ++cnt[order_key4(r.y - r.x) * kMidOrderThreads + tid];  // own column: no atomics
+  }
+  __syncthreads();
+  // exclusive scan of the 16 * 1024 counts in (bucket, thread) order: thread j
+  // scans entries [16 j, 16 j + 16)
+  int32_t v[16], x[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = cnt[16 * tid + k];
+  Scan(tmp).ExclusiveSum(v, x);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 16; ++k) cnt[16 * tid + k] = x[k];
+  __syncthreads();
+  for (int w = w0; w < w1; ++w) {
+    const int2 r = ranges[base + w];
+    order[cnt[order_key4(r.y - r.x) * kMidOrderThreads + tid]++] = w;
+  }
+}
+
 // keys for the chunked order: (chunk of the view, descending length octave)
 __global__ void __launch_bounds__(256) tile_order_chunk_keys_kernel(const int2* __restrict__ ranges, int n,
                                                                     int tiles_per_view, int n_views, int chunks,
@@ -2025,6 +2071,22 @@ static const int* tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
     else
       tile_order_small_kernel<kSmallOrderItems>
           <<<1, kSmallOrderThreads, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
+    ++c->order_gen;
+    return i0;
+  }
+  static const bool mid_ok = [] {  // SCT_ORDER_MID=0 (diagnostic): the device-wide sort instead
+    const char* e = std::getenv("SCT_ORDER_MID");
+    return !(e && atoi(e) == 0);
+  }();
+  if (mid_ok && n <= kMidOrder) {
+    static bool attr = false;
+    const int smem = 16 * kMidOrderThreads * (int)sizeof(int32_t);
+    if (!attr) {
+      if (cudaFuncSetAttribute(tile_order_mid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return nullptr;
+      attr = true;
+    }
+    tile_order_mid_kernel<<<1, kMidOrderThreads, smem, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
     ++c->order_gen;
     return i0;
   }
@@ -2173,22 +2235,24 @@ static int list_work(Ctx* c, const sct_fwd* s, const int* order, const int2* ran
   key.gen = 0;
   {
     KScope _ks(c, "K2_k3_items");
-    if (n <= kSmallWork) {
-      k3_work_small_kernel<<<1, kSmallWorkThreads, 0, c->stream>>>(ranges, order, n, kw.part_len, first, items,
-                                                                  n_items, tile_cnt, max_items);
-      key.gen = c->order_gen;
-      key.part = kw.part_len;
-      key.n = n;
-      return SCT_OK;
+    // the one-CTA scan up to 4096 lists (train step: 256); beyond, the
+    // multi-CTA parts + CUB scan (10-view shard, 10 240 lists: 19 vs 24 us)
+    static const int small_max = [] {  // SCT_K3_SMALL (diagnostic): the one-CTA scan's list-count limit
+      const char* e = std::getenv("SCT_K3_SMALL");
+      return e ? std::min(kSmallWork, atoi(e)) : 4096;
+    }();
+    if (n <= small_max) {
+      k3_first_small_kernel<<<1, kSmallWorkThreads, 0, c->stream>>>(ranges, order, n, kw.part_len, count, first);
+    } else {
+      k3_parts_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(ranges, order, n, kw.part_len, count);
+      size_t tmp = 0;
+      SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, first, n, c->stream));
+      SCT_TRY(ensure_cub_tmp(c, tmp));
+      tmp = c->cub_tmp_bytes;
+      SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, first, n, c->stream));
     }
-    k3_parts_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(ranges, order, n, kw.part_len, count);
-    size_t tmp = 0;
-    SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, first, n, c->stream));
-    SCT_TRY(ensure_cub_tmp(c, tmp));
-    tmp = c->cub_tmp_bytes;
-    SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, first, n, c->stream));
-    k3_items_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(order, count, first, n, items, n_items);
-    SCT_CUDA_TRY(cudaMemsetAsync(tile_cnt, 0, sizeof(int) * max_items, c->stream));
+    k3_items_kernel<<<grid_cap(c, std::max<long long>(n, max_items / 4), 256), 256, 0, c->stream>>>(
+        order, count, first, n, items, n_items, tile_cnt, max_items);
   }
   key.gen = c->order_gen;
   key.part = kw.part_len;
