@@ -515,3 +515,43 @@ print(json.dumps(out))
         assert p.returncode == 0, p.stderr[-2000:]
         res[mode] = json.loads(p.stdout.strip().splitlines()[-1])
     assert res["scatter"] == res["sort"]
+
+
+def test_list_schedules_agree():
+    """K3/K4 process the (view, tile) lists in a longest-first order built by
+    one of three sorts by list count (one-CTA block radix sort, one-CTA
+    counting sort for mid sizes — the 8-rank shards —, device-wide radix sort)
+    and cut into K3 work items by a one-CTA or a multi-CTA scan. The schedule
+    must not change a bit of the images or the (deterministic-mode) gradients:
+    40 views at 256^2 = 10 240 lists, run with each path forced."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, hashlib, numpy as np, torch
+sys.path.insert(0, ".")
+import paper_2405_20693_b200 as P
+from oracle import oracle as O
+oc = O.random_cloud(O.Rng(11), 2000, 0.8, 0.005, 0.12)
+f32 = [np.asarray(a, dtype=np.float32) for a in (oc.rho_raw, oc.pos, oc.scale_raw, oc.rot)]
+cloud = P.GaussianCloud(oc.s_min, *f32)
+eng = P.Engine(0)
+th = [2 * np.pi * i / 40 for i in range(40)]
+fwd = eng.render(cloud, P.ScannerConfig(detector_res_px=(256, 256)), th)
+g = torch.Generator().manual_seed(4)
+up = (torch.rand(40, 256, 256, generator=g) - 0.5).cuda()
+gr = P.CloudGrads(cloud.size())
+eng.render_backward(cloud, fwd, up, gr)
+h = hashlib.sha256(fwd.images.cpu().numpy().tobytes() + gr.flat().cpu().numpy().tobytes()).hexdigest()
+print(h, float(fwd.images.abs().sum()))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for name, env in (("mid", {}), ("device_sort", {"SCT_ORDER_MID": "0"}),
+                      ("one_cta_items", {"SCT_K3_SMALL": "16384"})):
+        p = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env), capture_output=True,
+                           text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[name] = p.stdout.strip().splitlines()[-1].split()
+    assert float(out["mid"][1]) > 0
+    assert out["mid"][0] == out["device_sort"][0] == out["one_cta_items"][0], out
