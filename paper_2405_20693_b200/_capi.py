@@ -11,8 +11,10 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # SCT_LIB_VARIANT selects an alternative in-tree build for A/B measurements
-# (tools/variants.sh); the default is the product library.
-LIB_PATH = os.path.join(_HERE, os.environ.get("SCT_LIB_VARIANT", "libsplatct_b200.so"))
+# (tools/variants.sh); SCT_CHECKED=1 the checked build (device invariant
+# checks, `make checked`); the default is the product library.
+LIB_PATH = os.path.join(_HERE, os.environ.get(
+    "SCT_LIB_VARIANT", "libsplatct_b200_checked.so" if os.environ.get("SCT_CHECKED") == "1" else "libsplatct_b200.so"))
 
 F = C.POINTER(C.c_float)
 D = C.POINTER(C.c_double)

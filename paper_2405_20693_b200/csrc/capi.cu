@@ -678,6 +678,13 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
     if ((rc = launch_raster_bin_scatter(c, n_views, s->m, s->det.tiles_x, s->det.tiles_y, s->d_rect, s->d_vals,
                                         s->d_ranges, s->n_pairs, s->n_pairs, s->d_total, split, &s->defer)))
       return fail(rc);
+#if SCT_CHECKED
+    if (std::getenv("SCT_DCHECK_SELFTEST")) {  // checked build only: an invalid list range K3 must reject
+      static const int2 bad = make_int2(1, 0);
+      cudaMemcpyAsync(s->d_ranges, &bad, sizeof(int2), cudaMemcpyHostToDevice, c->stream);
+      cudaStreamSynchronize(c->stream);
+    }
+#endif
     if (images) launch_raster_composite(c, s, images);
     if (cudaGetLastError() != cudaSuccess) {
       set_error("CUDA error: kernel launch in sct_render_fwd");

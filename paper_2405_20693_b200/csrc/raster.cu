@@ -465,6 +465,7 @@ __global__ void __launch_bounds__(256) bin_ranges_kernel(const int32_t* __restri
     const int v = (int)(k / T), t = (int)(k % T);
     const int32_t a = S[(long long)v * n_chunks * T + t];
     const int32_t b = v + 1 < n_views ? S[(long long)(v + 1) * n_chunks * T + t] : tile_base[t + 1];
+    SCT_DCHECK(0 <= a && a <= b && b <= tile_base[T]);
     ranges[k] = make_int2(a, b);
   }
 }
@@ -672,6 +673,7 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= total) break;
     const int4 it = items[c];  // (view * T + tile, part, parts, first item of the list)
+    SCT_DCHECK(c >= 0 && it.x >= 0 && it.y >= 0 && it.y < it.z && it.w >= 0 && it.w <= c);
     if (us.stamp && lane == 0) atomicMin(us.stamp + Ctx::kMaxUnits, (unsigned long long)global_ns());
     const int w = it.x, part = it.y, parts = it.z;
     const int view = w / tiles_per_view;
@@ -682,8 +684,10 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     const float py = (float)v + 0.5f;
     const float px0 = (float)u0 + 0.5f;
     int2 rg = ranges[w];
+    SCT_DCHECK(0 <= rg.x && rg.x <= rg.y);
     rg.x += part * part_len;
     rg.y = min(rg.y, rg.x + part_len);
+    SCT_DCHECK(rg.x <= rg.y);
     // even and odd kernels of the list accumulate in the two halves of acc2
     float2 acc2[8];
 #pragma unroll
@@ -691,6 +695,7 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na;  // past the list: amplitude 0
     if (rg.x + lane < rg.y) {
       const long long item = vals[rg.x + lane];
+      SCT_DCHECK(item >= 0);
       na = __ldg(rec + 2 * item);
       nb = __ldg(rec + 2 * item + 1);
     }
@@ -750,7 +755,9 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
       __syncwarp();
       int done = 0;
       if (lane == 0) {
-        done = atomicAdd(tile_cnt + it.w, 1) == parts - 1;
+        const int old = atomicAdd(tile_cnt + it.w, 1);
+        SCT_DCHECK(old < parts);  // each part of the list counts once; the last one resets
+        done = old == parts - 1;
         if (done) tile_cnt[it.w] = 0;  // ready for the next launch
       }
       done = __shfl_sync(0xffffffffu, done, 0);
@@ -1121,6 +1128,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
       rg.x = s0 + (int)((long long)len * part / parts);
       rg.y = s0 + (int)((long long)len * (part + 1) / parts);
     }
+    SCT_DCHECK(0 <= rg.x && rg.x <= rg.y);
     if (rg.y <= rg.x) {
       if (threadIdx.x == 0) unit_signal(us, unit);
       return;
@@ -1182,7 +1190,11 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
     // (two-deep pipeline); lane quads then read their pair gq
     constexpr int kStride = 16 * kMmaWarps;
     const int ck = lane >> 1, ch = lane & 1;
-    auto load_idx = [&](int cb) { return cb + ck < n_list ? vals[rg.x + cb + ck] : -1; };
+    auto load_idx = [&](int cb) {
+      const int v = cb + ck < n_list ? vals[rg.x + cb + ck] : -1;
+      SCT_DCHECK(cb + ck >= n_list || v >= 0);
+      return v;
+    };
     auto issue = [&](int buf, int it) {
 #if SCT_K4_REC16
       // plain layout [kernel][2] float4: one 16-byte cp.async per lane

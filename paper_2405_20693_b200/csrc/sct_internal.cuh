@@ -9,6 +9,31 @@
 
 #include "splatct_gpu.h"
 
+// Checked build (make checked -> libsplatct_b200_checked.so, loaded with
+// SCT_CHECKED=1): device-side invariant checks on the cross-CTA protocols and
+// every gathered index — list ranges, pair and item indices, the K3 last-part
+// and view-unit counters, the work counter. A failed check prints its
+// condition and traps (the launch fails, the process sees a CUDA error). It
+// stands in for compute-sanitizer, which this GPU pool does not run.
+#ifndef SCT_CHECKED
+#define SCT_CHECKED 0
+#endif
+#if SCT_CHECKED
+#include <cstdio>
+#define SCT_DCHECK(cond)                                                                \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("SCT_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                        \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define SCT_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace sct {
 
 constexpr int kTilePx = 16;   // common.hpp:24 kImageTilePx
@@ -204,7 +229,10 @@ __device__ __forceinline__ void unit_signal(const UnitSync& us, int u) {
   if (!us.done) return;
   const int v0 = (int)((long long)us.n_views * u / us.units);
   const int v1 = (int)((long long)us.n_views * (u + 1) / us.units);
-  if (atomicAdd(us.done + u, 1) == us.per_view * (v1 - v0) - 1) {
+  SCT_DCHECK(u >= 0 && u < us.units);
+  const int old = atomicAdd(us.done + u, 1);
+  SCT_DCHECK(old < us.per_view * (v1 - v0));  // every list of the unit signals exactly once
+  if (old == us.per_view * (v1 - v0) - 1) {
     __threadfence_system();
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(us.done_flag + u), "r"(us.epoch) : "memory");
     if (us.stamp) us.stamp[u] = global_ns();

@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(32 * kEvalWarps) voxel_eval_kernel(BrickGeo G,
   brick_of(G, b, tx, ty, tz);
   const int brick = (tz * G.by + ty) * G.bx + tx;
   int2 rg = ranges[brick];
+  SCT_DCHECK(0 <= rg.x && rg.x <= rg.y);
   if (splits > 1) {  // small grids: several warps per brick list, summed by voxel_reduce
     const int len = rg.y - rg.x, s0 = rg.x;
     rg.x = s0 + (int)((long long)len * part / splits);
@@ -318,6 +319,7 @@ __global__ void __launch_bounds__(32 * kEvalWarps) voxel_eval_kernel(BrickGeo G,
   float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na, nc = na;
   auto fetch = [&](int p) {
     const long long i = vals[p];
+    SCT_DCHECK(i >= 0);
     const float4 a = __ldg(rec + 3 * i);
     na = make_float4((float)(c0x - (double)a.x), (float)(c0y - (double)a.y), (float)(c0z - (double)a.z),
                      a.w * 0x1p-64f);
@@ -528,6 +530,7 @@ __global__ void __launch_bounds__(32 * kVMmaWarps, 7) voxel_backward_mma_kernel(
   brick_of(G, blockIdx.x / parts, tx, ty, tz);
   const int brick = (tz * G.by + ty) * G.bx + tx;
   int2 rg = ranges[brick];
+  SCT_DCHECK(0 <= rg.x && rg.x <= rg.y);
   if (parts > 1) {  // part of the list (small grids)
     const int len = rg.y - rg.x, s0 = rg.x, part = blockIdx.x % parts;
     rg.x = s0 + (int)((long long)len * part / parts);
