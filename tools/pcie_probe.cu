@@ -2,7 +2,8 @@
 // stack (75 x 512^2 fp32) as one copy and as 19 unit copies, against SM-driven
 // transfers (a grid-stride float4 kernel storing to / loading from mapped
 // pinned host memory) at several grid sizes.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/pcie_probe tools/pcie_probe.cu
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/pcie_probe tools/pcie_probe.cu -lcuda
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -49,6 +50,27 @@ int main() {
     for (int u = 0; u < 19; ++u) {
       const size_t o = bytes * u / 19, e = bytes * (u + 1) / 19;
       cudaMemcpyAsync((char*)d + o, (char*)h + o, e - o, cudaMemcpyHostToDevice, st);
+    }
+  });
+  // unit copies each followed by a stream write-value flag (the host path's publication)
+  uint32_t* flags = nullptr;
+  cudaMalloc(&flags, 64 * sizeof(uint32_t));
+  uint32_t ep = 0;
+  time("CE H2D 19 copies + write flags", [&] {
+    ++ep;
+    for (int u = 0; u < 19; ++u) {
+      const size_t o = bytes * u / 19, e = bytes * (u + 1) / 19;
+      cudaMemcpyAsync((char*)d + o, (char*)h + o, e - o, cudaMemcpyHostToDevice, st);
+      cuStreamWriteValue32((CUstream)st, (CUdeviceptr)(flags + u), ep, 0);
+    }
+  });
+  time("CE D2H 19 copies after wait flags", [&] {
+    ++ep;
+    for (int u = 0; u < 19; ++u) cuStreamWriteValue32((CUstream)st, (CUdeviceptr)(flags + u), ep, 0);
+    for (int u = 0; u < 19; ++u) {
+      const size_t o = bytes * u / 19, e = bytes * (u + 1) / 19;
+      cuStreamWaitValue32((CUstream)st, (CUdeviceptr)(flags + u), ep, CU_STREAM_WAIT_VALUE_GEQ);
+      cudaMemcpyAsync((char*)h + o, (char*)d + o, e - o, cudaMemcpyDeviceToHost, st);
     }
   });
   const long long n4 = bytes / 16;
