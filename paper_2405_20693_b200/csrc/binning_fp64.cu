@@ -52,6 +52,99 @@ __global__ void __launch_bounds__(256) gauss_prep_kernel(long long m, double s_m
 // kernel index exactly like the reference's serial push_back, rasterizer.cpp:124-133).
 // (3 CTAs per SM: 80 registers with a small spill beat 95 registers at two
 // CTAs — FP64 latency-bound; 0.293 -> 0.285 ms at cfg3)
+// K1's projection of one (view, kernel) item. The binning quantities — the
+// near-plane test, the centre, the low-pass-dilated 2D covariance and the cull
+// — follow d_project (project.cuh) operation for operation: only rows 0-1 of
+// A = J W and the top-left 2x2 block of A Sigma A^T reach them, so the tile
+// lists stay bit-identical to the oracle's. The record-only quantities (mu,
+// amplitude, conic) use det(A Sigma A^T) = det(J)^2 det(Sigma) (det W = 1;
+// det J = fx fy n / z^3 for the cone beam, fx fy for the parallel beam) instead
+// of the full 3x3 product and its determinant, and the Newton reciprocals /
+// roots of fp64_math.cuh: they feed only the FP32 records of K3/K4.
+struct BinProj {
+  dProj g;  // cx, cy, cov (the tile range's inputs)
+  double q00, q01, q11, amp;
+};
+__device__ __forceinline__ bool d_project_bin(const double p[3], const dM3& sigma, double rho, double det_sigma,
+                                              const ViewParams& v, const DetParams& det, const RasterParams& rp,
+                                              BinProj& o) {
+  double ps[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    ps[i] = v.rot[3 * i + 0] * p[0] + v.rot[3 * i + 1] * p[1] + v.rot[3 * i + 2] * p[2];
+    ps[i] = ps[i] + v.t[i];
+  }
+  const bool par = det.parallel != 0;
+  if (!par && ps[2] < det.near_clip) return false;
+  const double x = ps[0], y = ps[1], z = ps[2];
+  double jac[2][3];
+  if (par) {
+    jac[0][0] = det.fx;
+    jac[0][1] = 0.0;
+    jac[0][2] = 0.0;
+    jac[1][0] = 0.0;
+    jac[1][1] = det.fy;
+    jac[1][2] = 0.0;
+  } else {
+    jac[0][0] = det.fx / z;
+    jac[0][1] = 0.0;
+    jac[0][2] = -det.fx * x / (z * z);
+    jac[1][0] = 0.0;
+    jac[1][1] = det.fy / z;
+    jac[1][2] = -det.fy * y / (z * z);
+  }
+  // rows 0-1 of d_mul(jac, W), d_mul(a, sigma) and d_mul_bt(., a)
+  double a[2][3], X[2][3], sr[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      a[i][j] = jac[i][0] * v.rot[j] + jac[i][1] * v.rot[3 + j] + jac[i][2] * v.rot[6 + j];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      X[i][j] = a[i][0] * sigma.m[0][j] + a[i][1] * sigma.m[1][j] + a[i][2] * sigma.m[2][j];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) sr[i][j] = X[i][0] * a[j][0] + X[i][1] * a[j][1] + X[i][2] * a[j][2];
+  const double d2r = sr[0][0] * sr[1][1] - sr[1][0] * sr[0][1];
+  dM2& s2 = o.g.cov;
+  s2.m[0][0] = sr[0][0] + rp.eps2;
+  s2.m[0][1] = sr[0][1];
+  s2.m[1][0] = sr[1][0];
+  s2.m[1][1] = sr[1][1] + rp.eps2;
+  const double cx = par ? det.fx * x + det.cx : det.fx * x / z + det.cx;
+  const double cy = par ? det.fy * y + det.cy : det.fy * y / z + det.cy;
+  const double rx = rp.cull * sqrt(s2.m[0][0]);
+  const double ry = rp.cull * sqrt(s2.m[1][1]);
+  if (cx + rx < 0.0 || cx - rx > (double)det.w || cy + ry < 0.0 || cy - ry > (double)det.h) return false;
+  o.g.cx = cx;
+  o.g.cy = cy;
+  // record-only part
+  double det_j = det.fx * det.fy;
+  if (!par) {
+    const double n2 = fma(x, x, fma(y, y, z * z));
+    const double iz = d_fast_rcp(z);
+    det_j = det_j * (n2 * d_fast_rsqrt(n2)) * (iz * iz * iz);
+  }
+  const double d3 = det_j * det_j * det_sigma;
+  const double mu = d_fast_sqrt(2.0 * kPi * d3 * d_fast_rcp(d2r));
+  double amp = (rp.mode == SCT_MODE_RECTIFIED) ? mu * rho : rho;
+  const double inv = d_fast_rcp(s2.m[0][0] * s2.m[1][1] - s2.m[1][0] * s2.m[0][1]);
+  if (rp.dilation_compensation) amp *= d_fast_sqrt(d2r * inv);
+  o.q00 = s2.m[1][1] * inv;
+  o.q01 = -s2.m[0][1] * inv;
+  o.q11 = s2.m[0][0] * inv;
+  o.amp = amp;
+  return true;
+}
+
+#ifndef SCT_K1_FAST
+#define SCT_K1_FAST 1
+#endif
+
 __global__ void __launch_bounds__(256, 3) raster_preprocess_kernel(
     long long m, long long n_items, const float* __restrict__ pos, const double* __restrict__ prep,
     const ViewParams* __restrict__ views, DetParams det, RasterParams rp, float4* __restrict__ rec,
@@ -67,8 +160,15 @@ __global__ void __launch_bounds__(256, 3) raster_preprocess_kernel(
 #pragma unroll
     for (int a = 0; a < 9; ++a) sigma.m[a / 3][a % 3] = pr(a);
     const ViewParams view = views[v];
+#if SCT_K1_FAST
+    BinProj bp;
+    const bool ok = d_project_bin(p, sigma, pr(9), pr(16), view, det, rp, bp);
+    const dProj& g = bp.g;
+#else
     dProj g;
-    if (!d_project(p, sigma, pr(9), view, det, rp, g)) {
+    const bool ok = d_project(p, sigma, pr(9), view, det, rp, g);
+#endif
+    if (!ok) {
       count[item] = 0;
       vis[item] = 0;
       rect[item] = make_short4(1, 0, 1, 0);
@@ -85,10 +185,16 @@ __global__ void __launch_bounds__(256, 3) raster_preprocess_kernel(
     // evaluate it as 2^(L + 64) along 4-pixel runs with the ratio recurrence
     // E(dx+1) = E(dx) * 2^(2A dx + A + B dy), ratio(dx+1) = ratio(dx) * 2^(2A);
     // the record carries amp * 2^-64 and K = 2^(2A) for that.
+#if SCT_K1_FAST
+    const double A = kA * bp.q00;
+    rec[2 * item + 0] = make_float4((float)g.cx, (float)g.cy, (float)(bp.amp * 0x1p-64), exp2f((float)(2.0 * A)));
+    rec[2 * item + 1] = make_float4((float)A, (float)(2.0 * kA * bp.q01), (float)(kA * bp.q11), (float)(2.0 * A));
+#else
     const double A = kA * g.conic.m[0][0];
     rec[2 * item + 0] = make_float4((float)g.cx, (float)g.cy, (float)(g.amp * 0x1p-64), (float)exp2(2.0 * A));
     rec[2 * item + 1] = make_float4((float)A, (float)(2.0 * kA * g.conic.m[0][1]), (float)(kA * g.conic.m[1][1]),
                                     (float)(2.0 * A));
+#endif
   }
 }
 

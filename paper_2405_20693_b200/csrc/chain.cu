@@ -31,52 +31,6 @@ namespace {
 
 constexpr int kItemOut = 11;  // g_rho, g_pos[3], g_sigma (xx yy zz xy xz yz), ndc_norm
 
-// FP64 reciprocal and square roots for the item chain: the MUFU seed
-// (rcp / rsqrt .approx.ftz.f64, ~2^-22 relative) and two Newton steps
-// (quadratic: < 2^-52, within an ulp or two of the correctly rounded result).
-// The IEEE-rounded division and square root are subroutine calls of ~30
-// instructions each with a slow path; the chain evaluates eight of them per
-// (view, kernel) item. The chain feeds no binning decision, and its outputs
-// stay far inside the 1e-3 gradient bar. SCT_CHAIN_FASTDIV=0 restores them.
-#ifndef SCT_CHAIN_FASTDIV
-#define SCT_CHAIN_FASTDIV 1
-#endif
-__device__ __forceinline__ double chain_rcp(double x) {
-#if SCT_CHAIN_FASTDIV
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-#else
-  return 1.0 / x;
-#endif
-}
-// 1 / sqrt(x) for x > 0
-__device__ __forceinline__ double chain_rsqrt(double x) {
-#if SCT_CHAIN_FASTDIV
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  return y * fma(-hx * y, y, 1.5);
-#else
-  return 1.0 / sqrt(x);
-#endif
-}
-// sqrt(x) for x >= 0 (0 -> 0)
-__device__ __forceinline__ double chain_sqrt(double x) {
-#if SCT_CHAIN_FASTDIV
-  if (!(x > 0.0)) return x == 0.0 ? 0.0 : sqrt(x);
-  const double y = chain_rsqrt(x);
-  const double r = x * y;
-  return fma(fma(-r, r, x), 0.5 * y, r);  // one Newton correction of the root
-#else
-  return sqrt(x);
-#endif
-}
-
 // Symmetric 3x3 as (xx, xy, xz, yy, yz, zz).
 struct Sym3 {
   double xx, xy, xz, yy, yz, zz;
@@ -122,9 +76,9 @@ __device__ __forceinline__ void item_chain(long long m, long long v, long long i
     const double x = fma(W[0], px, fma(W[1], py, W[2] * pz)) + V.t[0];
     const double y = fma(W[3], px, fma(W[4], py, W[5] * pz)) + V.t[1];
     const double z = fma(W[6], px, fma(W[7], py, W[8] * pz)) + V.t[2];
-    const double iz = chain_rcp(z);
+    const double iz = d_fast_rcp(z);
     const double n2 = fma(x, x, fma(y, y, z * z));
-    const double in = chain_rsqrt(n2);
+    const double in = d_fast_rsqrt(n2);
     // J (geometry.cpp:111-123): rows (a 0 b), (0 c d), (e f g)
     // parallel beam: J = diag(fx, fy, 1), constant
     constexpr bool par = kParallel;
@@ -157,12 +111,12 @@ __device__ __forceinline__ void item_chain(long long m, long long v, long long i
     const double C20 = -jb * jc, C21 = -ja * jd, C22 = ja * jc;
     const double detJ = fma(ja, C00, jb * C02);
     const double d3 = detJ * detJ * detS;
-    const double id2r = chain_rcp(d2r);
-    const double mu = chain_sqrt(2.0 * kPi * d3 * id2r);
+    const double id2r = d_fast_rcp(d2r);
+    const double mu = d_fast_sqrt(2.0 * kPi * d3 * id2r);
     const double amp_pre = (rp.mode == SCT_MODE_RECTIFIED) ? mu * rho : rho;
     const double s00 = Rxx + rp.eps2, s11 = Ryy + rp.eps2, s01 = Rxy;
-    const double id2 = chain_rcp(fma(s00, s11, -s01 * s01));
-    const double comp = rp.dilation_compensation ? chain_sqrt(d2r * id2) : 1.0;
+    const double id2 = d_fast_rcp(fma(s00, s11, -s01 * s01));
+    const double comp = rp.dilation_compensation ? d_fast_sqrt(d2r * id2) : 1.0;
     const double amp = amp_pre * comp;
     const double q00 = s11 * id2, q01 = -s01 * id2, q11 = s00 * id2;  // conic
     // rasterizer.cpp:277-281
@@ -227,7 +181,7 @@ __device__ __forceinline__ void item_chain(long long m, long long v, long long i
         X[r][1] = fma(Vr[r][0], Sg.xy, fma(Vr[r][1], Sg.yy, Vr[r][2] * Sg.yz));
         X[r][2] = fma(Vr[r][0], Sg.xz, fma(Vr[r][1], Sg.yz, Vr[r][2] * Sg.zz));
       }
-      const double k2 = 2.0 * hm * chain_rcp(detJ);
+      const double k2 = 2.0 * hm * d_fast_rcp(detJ);
       double gJ[3][3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -266,7 +220,7 @@ __device__ __forceinline__ void item_chain(long long m, long long v, long long i
     out[7] = gS.xy;
     out[8] = gS.xz;
     out[9] = gS.yz;
-    out[10] = chain_sqrt(fma(nx, nx, ny * ny));
+    out[10] = d_fast_sqrt(fma(nx, nx, ny * ny));
   }
 }
 

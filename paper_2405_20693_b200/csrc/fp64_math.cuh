@@ -23,6 +23,52 @@ struct dV3 {
   double v[3];
 };
 
+// FP64 reciprocal and square roots for values that feed no binning decision
+// (the K5 item chain, K1's record fields): the MUFU seed (rcp / rsqrt
+// .approx.ftz.f64, ~2^-22 relative) and two Newton steps (quadratic: < 2^-52,
+// within an ulp or two of the correctly rounded result). The IEEE-rounded
+// division and square root are subroutine calls of ~30 instructions each with
+// a slow path. Explicit fma() calls, so -fmad=false translation units keep
+// them. SCT_FASTDIV=0 restores the IEEE operations.
+#ifndef SCT_FASTDIV
+#define SCT_FASTDIV 1
+#endif
+__device__ __forceinline__ double d_fast_rcp(double x) {
+#if SCT_FASTDIV
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+// 1 / sqrt(x) for x > 0
+__device__ __forceinline__ double d_fast_rsqrt(double x) {
+#if SCT_FASTDIV
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+#else
+  return 1.0 / sqrt(x);
+#endif
+}
+// sqrt(x) for x >= 0 (0 -> 0; negative or NaN -> NaN as sqrt)
+__device__ __forceinline__ double d_fast_sqrt(double x) {
+#if SCT_FASTDIV
+  if (!(x > 0.0)) return x == 0.0 ? 0.0 : sqrt(x);
+  const double y = d_fast_rsqrt(x);
+  const double r = x * y;
+  return fma(fma(-r, r, x), 0.5 * y, r);  // one Newton correction of the root
+#else
+  return sqrt(x);
+#endif
+}
+
 __device__ __forceinline__ dM3 d_zero3() {
   dM3 r;
 #pragma unroll
