@@ -429,9 +429,12 @@ __global__ void __launch_bounds__(256) voxel_pair_sum_kernel(long long m, const 
     const bool live = g < m;
     const int32_t n = live ? count[g] : 0;
     const long long p0 = live ? offset[g] : 0;
-    double s[10];
+    // FP32 lane sums and tree (the per-pair float -> double conversions and
+    // FP64 shuffles bound the kernel on the XU pipe: 0.117 ms at cfg4); the
+    // kernel's total is widened once. Same fixed order, so still deterministic.
+    float s[10];
 #pragma unroll
-    for (int a = 0; a < 10; ++a) s[a] = 0.0;
+    for (int a = 0; a < 10; ++a) s[a] = 0.f;
     for (int q = j; q < n; q += 8) {
       const float4 a = __ldg(ps + 3 * (p0 + q)), b = __ldg(ps + 3 * (p0 + q) + 1), c = __ldg(ps + 3 * (p0 + q) + 2);
       s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
@@ -445,7 +448,7 @@ __global__ void __launch_bounds__(256) voxel_pair_sum_kernel(long long m, const 
     if (live) {  // lane j writes sums j and j + 8 (all lanes hold all ten)
 #pragma unroll
       for (int a = 0; a < 10; ++a)
-        if ((a & 7) == j) sums[a * m + g] = s[a];
+        if ((a & 7) == j) sums[a * m + g] = (double)s[a];
     }
   }
 }
