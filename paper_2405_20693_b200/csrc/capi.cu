@@ -392,6 +392,17 @@ int fwd_init(Ctx* c, const std::vector<ViewParams>& hv, ViewParams* d_views, int
 
 using namespace sct;
 
+// the per-item offsets of a state binned without them (atomic-mode forward)
+// when a deterministic backward needs its slots
+static int ensure_item_offsets(Ctx* c, sct_fwd* s) {
+  if (s->offsets_ready) return SCT_OK;
+  int64_t total = 0;
+  SCT_TRY(scan_counts(c, s->d_count, s->d_offset, s->n_items, &total, s->n_pairs, s->d_rect, nullptr,
+                      (int64_t)s->det.tiles_x * s->det.tiles_y));
+  s->offsets_ready = true;
+  return SCT_OK;
+}
+
 static void free_state_buffers(sct_fwd* s) {
   Ctx* c = s->ctx;
   if (s->defer) {  // a split scatter never completed (error path)
@@ -661,10 +672,6 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
   launch_gauss_prep(c, *cloud, s->d_prep);
   launch_raster_preprocess(c, *cloud, s->d_prep, s->d_views, n_views, s->det, s->rp, s->d_rec, s->d_rect,
                            s->d_count, s->d_vis);
-  if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs, cap, s->d_rect, nullptr,
-                        (int64_t)s->det.tiles_x * s->det.tiles_y)))
-    return fail(rc);
-  if (cap > 0) s->exact = false;
   // Binning: one stable counting scatter straight into (tile, view, kernel)
   // order when the tile table fits in shared memory (raster.cu bin_*), else
   // emit + radix sort. SCT_BIN=sort forces the latter.
@@ -672,6 +679,20 @@ int sct_render_fwd(sct_ctx* c, const sct_cloud* cloud, const sct_scanner* scanne
     const char* e = std::getenv("SCT_BIN");
     return e && std::string(e) == "sort";
   }();
+  // The per-item pair offsets (scan of the counts) serve the deterministic
+  // backward's slots, the emit + sort path and the exact host-side count. A
+  // sync-free scatter binning in the parallel-atomic mode needs none of them:
+  // the column scan yields the total and flags an overflow, and the ranges
+  // come out empty then (bin_ranges_kernel), so the scan is deferred to a
+  // deterministic backward of this state, if one ever runs.
+  if (cap > 0 && scatter && !force_sort && !c->deterministic) {
+    s->n_pairs = cap;
+    s->offsets_ready = false;
+  } else if ((rc = scan_counts(c, s->d_count, s->d_offset, ni, &s->n_pairs, cap, s->d_rect, nullptr,
+                               (int64_t)s->det.tiles_x * s->det.tiles_y))) {
+    return fail(rc);
+  }
+  if (cap > 0) s->exact = false;
   if ((!force_sort || cap > 0) && scatter) {
     if ((rc = dev_alloc(c, (void**)&s->d_vals, std::max<int64_t>(s->n_pairs, 1) * sizeof(int32_t)))) return fail(rc);
     const int64_t split = images ? -1 : c->fwd_split_views;  // host path: the rest after the first composite
@@ -746,6 +767,7 @@ int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
   // SPEC.md:224-226 accumulates straight into 8-float per-item records.
   // (grow-only context buffers: slot 14 statistics, slot 15 item outputs)
   const bool atomic = !c->deterministic;
+  if (!atomic) SCT_TRY(ensure_item_offsets(c, s));
   float* item_stats = nullptr;
   if (atomic) {
     SCT_TRY(stage_buf(c, 14, 8 * s->n_items * sizeof(float), (void**)&item_stats));
@@ -923,6 +945,7 @@ static int render_bwd_units(Ctx* c, sct_fwd* s, const sct_cloud* cloud, const fl
   }
   if (s->n_items == 0) return SCT_OK;
   const bool atomic = !c->deterministic;
+  if (!atomic) SCT_TRY(ensure_item_offsets(c, s));
   float4* pair_stats = nullptr;
   float* item_stats = nullptr;
   double* vsum = nullptr;

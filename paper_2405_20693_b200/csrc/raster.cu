@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(1024) bin_tilebase_kernel(const int32_t* __res
   }
   if (threadIdx.x == blockDim.x - 1) {
     tile_base[T] = part[threadIdx.x];
-    if (total) *total = part[threadIdx.x];
+    if (total) *total = (long long)part[threadIdx.x] > cap ? 0 : part[threadIdx.x];  // overflow: emptied
     if ((long long)part[threadIdx.x] > cap) atomicOr(overflow, 1);
   }
 }
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kSmallScanThreads) bin_scan_small_kernel(int32
   if (tid < T) col[tid] = base;
   if (tid == 0) {
     col[T] = run_total;
-    if (total) *total = run_total;
+    if (total) *total = (long long)run_total > cap ? 0 : run_total;  // overflow: emptied
     if ((long long)run_total > cap) atomicOr(overflow, 1);
   }
   __syncthreads();
@@ -459,14 +459,18 @@ __global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short
 // base (tile_base[t + 1]).
 __global__ void __launch_bounds__(256) bin_ranges_kernel(const int32_t* __restrict__ S,
                                                          const int32_t* __restrict__ tile_base, int n_chunks,
-                                                         int n_views, int T, int2* __restrict__ ranges) {
+                                                         int n_views, int T, int2* __restrict__ ranges,
+                                                         long long cap) {
   const long long n = (long long)n_views * T;
+  // capacity overflow (flagged by the column scan): empty lists, so nothing
+  // downstream reads past the cap-sized pair buffer
+  const bool over = (long long)tile_base[T] > cap;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
     const int v = (int)(k / T), t = (int)(k % T);
     const int32_t a = S[(long long)v * n_chunks * T + t];
     const int32_t b = v + 1 < n_views ? S[(long long)(v + 1) * n_chunks * T + t] : tile_base[t + 1];
-    SCT_DCHECK(0 <= a && a <= b && b <= tile_base[T]);
-    ranges[k] = make_int2(a, b);
+    SCT_DCHECK(over || (0 <= a && a <= b && b <= tile_base[T]));
+    ranges[k] = over ? make_int2(0, 0) : make_int2(a, b);
   }
 }
 
@@ -1874,7 +1878,7 @@ int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tile
   if (ranges) {  // from the scan alone: final before any pair is written
     KScope _ks(c, "K2_bin_ranges");
     bin_ranges_kernel<<<grid_cap(c, n_views * T, 256), 256, 0, c->stream>>>(H, tb2, (int)n_chunks, (int)n_views,
-                                                                            (int)T, ranges);
+                                                                            (int)T, ranges, (long long)cap);
   }
   static bool attr = false;
   if (!attr) {

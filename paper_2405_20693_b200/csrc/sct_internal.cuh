@@ -299,6 +299,7 @@ struct sct_fwd {
   void* d_keys = nullptr;              // [pairs] sorted tile keys (uint16 if tile_bits <= 16, else uint32)
   int32_t* d_vals = nullptr;           // [pairs] sorted item index
   bool exact = true;                   // n_pairs is the pair count (else the capacity; count in d_total)
+  bool offsets_ready = true;           // d_offset holds the per-item pair offsets (ensure_item_offsets)
   int32_t* d_total = nullptr;          // [1] pair count on the device (capacity mode)
   int2* d_ranges = nullptr;            // [V*T] [start,end) into sorted pairs
   double* d_prep = nullptr;            // [kPrepStride][m] (SoA) Sigma (9), rho, Sigma^-1 (6), det, FP64

@@ -285,6 +285,11 @@ class Engine:
                 pass
             self._h = None
 
+    def set_deterministic(self, deterministic: bool = True):
+        """Backward reduction: fixed-order per-(tile, kernel) slots (default) or the
+        parallel-atomic per-item accumulation (sct_ctx_set_deterministic)."""
+        _check(self.lib.sct_ctx_set_deterministic(self._h, int(deterministic)))
+
     def set_stream(self, stream: torch.cuda.Stream):
         self.stream = stream
         _check(self.lib.sct_ctx_set_stream(self._h, C.c_void_p(stream.cuda_stream)))

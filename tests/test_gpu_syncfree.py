@@ -30,7 +30,10 @@ def _cloud(P, seed=4, m=3000):
                                                                             oc.rot)])
 
 
-def test_capacity_mode_matches_exact_mode():
+@pytest.mark.parametrize("deterministic", [True, False])
+def test_capacity_mode_matches_exact_mode(deterministic):
+    """(atomic mode: the sync-free raster binning skips the per-item offset
+    scan, which a later deterministic backward of the same state runs)"""
     _need_cuda()
     import paper_2405_20693_b200 as P
     c = _cloud(P)
@@ -41,7 +44,7 @@ def test_capacity_mode_matches_exact_mode():
     vup = torch.rand(grid.shape_zyx, device="cuda") - 0.5
     out = {}
     for mode in ("exact", "capacity"):
-        eng = P.Engine(0, deterministic=True)
+        eng = P.Engine(0, deterministic=deterministic)
         if mode == "capacity":
             eng.set_capacity(400000, 400000)
         f = eng.render(c, sc, th)
@@ -64,11 +67,12 @@ def test_capacity_mode_matches_exact_mode():
     assert a[5] == b[5] and not b[6]
 
 
-def test_capacity_overflow_is_flagged():
+@pytest.mark.parametrize("deterministic", [True, False])
+def test_capacity_overflow_is_flagged(deterministic):
     _need_cuda()
     import paper_2405_20693_b200 as P
     c = _cloud(P)
-    eng = P.Engine(0)
+    eng = P.Engine(0, deterministic=deterministic)
     eng.set_capacity(1000, 1000)
     f = eng.render(c, P.ScannerConfig(detector_res_px=(128, 128)), [0.3])
     # an overflowing call is emptied (no pair is written beyond the buffers) and flagged
@@ -105,3 +109,28 @@ def test_sync_free_training_matches_exact_training():
     for k in ("rho_raw", "pos", "scale_raw", "rot"):
         x, y = getattr(runs[False][1], k).double(), getattr(runs[True][1], k).double()
         assert float(torch.linalg.norm(x - y) / torch.linalg.norm(x)) < 1e-4, k
+
+
+def test_atomic_forward_then_deterministic_backward():
+    """A state binned in the atomic mode without per-item offsets gets them
+    when the context switches to the deterministic backward."""
+    _need_cuda()
+    import paper_2405_20693_b200 as P
+    c = _cloud(P)
+    sc = P.ScannerConfig(detector_res_px=(160, 120))
+    th = [0.5, 2.5]
+    up = torch.rand((2, 120, 160), device="cuda") - 0.5
+    ref = P.Engine(0, deterministic=True)
+    ref.set_capacity(400000, 400000)
+    f0 = ref.render(c, sc, th)
+    g0 = P.CloudGrads(c.size())
+    ref.render_backward(c, f0, up, g0)
+    eng = P.Engine(0, deterministic=False)
+    eng.set_capacity(400000, 400000)
+    f = eng.render(c, sc, th)
+    eng.set_deterministic(True)
+    g = P.CloudGrads(c.size())
+    eng.render_backward(c, f, up, g)
+    torch.cuda.synchronize()
+    assert torch.equal(g.flat(), g0.flat())  # same slots, same fixed-order sums
+    assert not eng.take_overflow()
