@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(256) gauss_prep_kernel(long long m, double s_m
                                                          const float* __restrict__ pos,
                                                          const float* __restrict__ scale_raw,
                                                          const float* __restrict__ rot, double* __restrict__ prep) {
+  pdl_prologue();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(256, 3) raster_preprocess_kernel(
     long long m, long long n_items, const float* __restrict__ pos, const double* __restrict__ prep,
     const ViewParams* __restrict__ views, DetParams det, RasterParams rp, float4* __restrict__ rec,
     short4* __restrict__ rect, int32_t* __restrict__ count, uint8_t* __restrict__ vis) {
+  pdl_prologue();
   const double kA = -0.5 * kLog2e;
   for (long long item = blockIdx.x * (long long)blockDim.x + threadIdx.x; item < n_items;
        item += (long long)gridDim.x * blockDim.x) {
@@ -206,6 +208,7 @@ __global__ void __launch_bounds__(256) voxel_preprocess_kernel(
     const float* __restrict__ scale_raw, const float* __restrict__ rot, int3 dims, double3 origin,
     double3 spacing, double cull, int32_t zb0, int32_t zb1, float4* __restrict__ rec,
     short4* __restrict__ lo_out, short4* __restrict__ hi_out, int32_t* __restrict__ count) {
+  pdl_prologue();
   const double kA = -0.5 * kLog2e;
   const int dimv[3] = {dims.x, dims.y, dims.z};
   const double org[3] = {origin.x, origin.y, origin.z};
@@ -257,6 +260,7 @@ __global__ void project_export_kernel(long long m, double s_min, const float* __
                                       const float* __restrict__ rot, const ViewParams* __restrict__ view,
                                       DetParams det, RasterParams rp, int32_t* __restrict__ vis,
                                       double* __restrict__ out) {
+  pdl_prologue();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     const dKernel k = d_load_kernel(pos, scale_raw, rot, rho_raw, i, s_min);
@@ -295,7 +299,7 @@ int grid_for(Ctx* c, long long n, int block) {
 void launch_gauss_prep(Ctx* c, const sct_cloud& cl, double* prep) {
   if (cl.m == 0) return;
   KScope _ks(c, "K0_gauss_prep");
-  gauss_prep_kernel<<<grid_for(c, cl.m, 256), 256, 0, c->stream>>>(cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
+  pdl_launch(gauss_prep_kernel, dim3(grid_for(c, cl.m, 256)), dim3(256), 0, c->stream, cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
                                                                    cl.scale_raw, cl.rot, prep);
 }
 
@@ -305,7 +309,7 @@ void launch_raster_preprocess(Ctx* c, const sct_cloud& cl, const double* prep, c
   const long long n_items = (long long)cl.m * n_views;
   if (n_items == 0) return;
   KScope _ks(c, "K1_raster_preprocess");
-  raster_preprocess_kernel<<<grid_for(c, n_items, 256), 256, 0, c->stream>>>(cl.m, n_items, cl.pos, prep, d_views,
+  pdl_launch(raster_preprocess_kernel, dim3(grid_for(c, n_items, 256)), dim3(256), 0, c->stream, cl.m, n_items, cl.pos, prep, d_views,
                                                                              det, rp, rec, rect, count, vis);
 }
 
@@ -315,8 +319,7 @@ void launch_voxel_preprocess(Ctx* c, const sct_cloud& cl, const sct_grid& g, dou
   if (cl.m == 0) return;
   {
     KScope _ks(c, "K6_voxel_preprocess");
-    voxel_preprocess_kernel<<<grid_for(c, cl.m, 256), 256, 0, c->stream>>>(
-        cl.m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, make_int3(g.dims[0], g.dims[1], g.dims[2]),
+    pdl_launch(voxel_preprocess_kernel, dim3(grid_for(c, cl.m, 256)), dim3(256), 0, c->stream, cl.m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, make_int3(g.dims[0], g.dims[1], g.dims[2]),
         make_double3(g.origin_mm[0], g.origin_mm[1], g.origin_mm[2]),
         make_double3(g.spacing_mm[0], g.spacing_mm[1], g.spacing_mm[2]), cull, zb0, zb1, rec, rect_lo, rect_hi,
         count);
@@ -328,8 +331,7 @@ void launch_project_export(Ctx* c, const sct_cloud& cl, const ViewParams* d_view
   if (cl.m == 0) return;
   {
     KScope _ks(c, "project_export");
-    project_export_kernel<<<grid_for(c, cl.m, 128), 128, 0, c->stream>>>(
-        cl.m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, d_view, det, rp, vis, rec);
+    pdl_launch(project_export_kernel, dim3(grid_for(c, cl.m, 128)), dim3(128), 0, c->stream, cl.m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, d_view, det, rp, vis, rec);
   }
 }
 

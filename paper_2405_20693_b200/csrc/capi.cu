@@ -20,6 +20,14 @@
 namespace sct {
 
 static thread_local std::string g_last_error;
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SCT_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
 void set_error(const std::string& msg) { g_last_error = msg; }
 
 DetParams make_det(const sct_scanner& s) {  // geometry.cpp:88-98
@@ -365,6 +373,7 @@ struct ViewPack {
   ViewParams v[kViewPack];
 };
 __global__ void fwd_init_kernel(ViewPack p, int nv, ViewParams* dst, int2* ranges, int64_t n_ranges, int32_t* total) {
+  pdl_prologue();
   if (blockIdx.x == 0 && threadIdx.x < nv) dst[threadIdx.x] = p.v[threadIdx.x];
   if (total && blockIdx.x == 0 && threadIdx.x == 0) *total = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_ranges; i += (int64_t)gridDim.x * blockDim.x)
@@ -379,7 +388,7 @@ int fwd_init(Ctx* c, const std::vector<ViewParams>& hv, ViewParams* d_views, int
     for (int k = 0; k < nv; ++k) p.v[k] = hv[v0 + k];
     const bool first = v0 == 0;
     const int grid = first ? (int)std::max<int64_t>(1, std::min<int64_t>((n_ranges + 255) / 256, 4 * c->sm_count)) : 1;
-    fwd_init_kernel<<<grid, 256, 0, c->stream>>>(p, nv, d_views + v0, ranges, first ? n_ranges : 0,
+    pdl_launch(fwd_init_kernel, dim3(grid), dim3(256), 0, c->stream, p, nv, d_views + v0, ranges, first ? n_ranges : 0,
                                                  first ? total : nullptr);
     ++c->launches;
     if (hv.empty()) break;

@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(128, SCT_CHAIN_MINB) raster_chain_kernel(
     long long m, int v0, int v1, const float* __restrict__ pos, const double* __restrict__ prep,
     const ViewParams* __restrict__ views, DetParams det, RasterParams rp, const uint8_t* __restrict__ vis,
     const int32_t* __restrict__ offset, const float4* __restrict__ pair_stats, double* __restrict__ vsum) {
+  pdl_prologue();
   // lane-private running sums in shared memory ([a][thread], FP64): keeps the
   // chain's register budget at 128 without spills
   __shared__ double s_acc[kItemOut + 1][128];
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(128) raster_finalize_kernel(
     float* __restrict__ g_rho, float* __restrict__ g_pos,
     float* __restrict__ g_scale, float* __restrict__ g_rotp, float* __restrict__ st_norm,
     int32_t* __restrict__ st_count, float* __restrict__ st_3d, int groups) {
+  pdl_prologue();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     // view-range partials from raster_chain_kernel: [groups][kItemOut + 1][m], summed in range order
@@ -362,6 +364,7 @@ __global__ void __launch_bounds__(128) raster_finalize_adam_kernel(
     const float* __restrict__ g_pos, const float* __restrict__ g_scale, const float* __restrict__ g_rotp,
     float* __restrict__ st_norm, int32_t* __restrict__ st_count, float* __restrict__ st_3d, sct_adam_state adam,
     AdamParams ap, double* __restrict__ total, double lambda_ssim, double lambda_tv) {
+  pdl_prologue();
   if (total && blockIdx.x == 0 && threadIdx.x == 0) train_total(total, lambda_ssim, lambda_tv);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
@@ -423,6 +426,7 @@ __global__ void __launch_bounds__(256) voxel_pair_sum_kernel(long long m, const 
                                                              const int32_t* __restrict__ count,
                                                              const float4* __restrict__ ps,
                                                              double* __restrict__ sums) {
+  pdl_prologue();
   const int j = threadIdx.x & 7;
   for (long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3; g < ((m + 3) & ~3LL);
        g += ((long long)gridDim.x * blockDim.x) >> 3) {  // all lanes of a warp iterate together
@@ -460,6 +464,7 @@ __global__ void __launch_bounds__(128) voxel_chain_kernel(
     const int32_t* __restrict__ count, const float4* __restrict__ ps, const double* __restrict__ sums,
     float* __restrict__ g_rho, float* __restrict__ g_pos, float* __restrict__ g_scale,
     float* __restrict__ g_rotp) {
+  pdl_prologue();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     const int32_t n = count[i];
@@ -533,7 +538,7 @@ static void chain_launch(int lanes, int grid, cudaStream_t st, long long m, int 
                          const uint8_t* vis, const int32_t* offset, const float4* ps, double* vsum) {
 #define SCT_CHAIN_L(L) \
   case L:              \
-    raster_chain_kernel<P, L><<<grid, 128, 0, st>>>(m, v0, v1, pos, prep, views, det, rp, vis, offset, ps, vsum); \
+    pdl_launch(raster_chain_kernel<P, L>, dim3(grid), dim3(128), 0, st, m, v0, v1, pos, prep, views, det, rp, vis, offset, ps, vsum); \
     break;
   switch (lanes) {
     SCT_CHAIN_L(1)
@@ -578,8 +583,7 @@ void launch_raster_finalize(Ctx* c, const sct_fwd* s, const sct_cloud& cl, const
                             sct_grads* g, sct_stats* st) {
   if (s->m == 0) return;
   KScope _ks(c, "K5_raster_finalize");
-  raster_finalize_kernel<<<grid_cap(c, s->m, 128), 128, 0, c->stream>>>(
-      s->m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, vsum, g->rho_raw, g->pos, g->scale_raw, g->rot,
+  pdl_launch(raster_finalize_kernel, dim3(grid_cap(c, s->m, 128)), dim3(128), 0, c->stream, s->m, cl.s_min_mm, cl.rho_raw, cl.pos, cl.scale_raw, cl.rot, vsum, g->rho_raw, g->pos, g->scale_raw, g->rot,
       st ? st->grad2d_norm_accum : nullptr, st ? st->grad_count : nullptr, st ? st->grad3d_accum : nullptr, groups);
 }
 
@@ -591,8 +595,7 @@ void launch_raster_finalize_adam(Ctx* c, int64_t m, const sct_fwd* s, sct_cloud*
   (void)s;
   KScope _ks(c, "K10_finalize_adam");
   const AdamParams ap{lr[0], lr[1], lr[2], lr[3], bc1, bc2, b1, b2, eps};
-  raster_finalize_adam_kernel<<<grid_cap(c, m, 128), 128, 0, c->stream>>>(
-      m, cl->s_min_mm, cl->rho_raw, cl->pos, cl->scale_raw, cl->rot, vsum, groups, g->rho_raw, g->pos, g->scale_raw,
+  pdl_launch(raster_finalize_adam_kernel, dim3(grid_cap(c, m, 128)), dim3(128), 0, c->stream, m, cl->s_min_mm, cl->rho_raw, cl->pos, cl->scale_raw, cl->rot, vsum, groups, g->rho_raw, g->pos, g->scale_raw,
       g->rot, st ? st->grad2d_norm_accum : nullptr, st ? st->grad_count : nullptr, st ? st->grad3d_accum : nullptr,
       *adam, ap, total, lambda_ssim, lambda_tv);
 }
@@ -603,7 +606,7 @@ void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, cons
   double* sums = nullptr;
   if (n_bricks >= 0 && n_bricks <= 512) {  // few pairs per kernel: summed in the chain thread, one launch
     KScope _ks(c, "K8_voxel_chain");
-    voxel_chain_kernel<<<grid_cap(c, cl.m, 128), 128, 0, c->stream>>>(cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
+    pdl_launch(voxel_chain_kernel, dim3(grid_cap(c, cl.m, 128)), dim3(128), 0, c->stream, cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
                                                                      cl.scale_raw, cl.rot, offset, count, pair_stats,
                                                                      nullptr, g->rho_raw, g->pos, g->scale_raw, g->rot);
     return;
@@ -611,12 +614,12 @@ void launch_voxel_chain(Ctx* c, const sct_cloud& cl, const int32_t* offset, cons
   if (dev_alloc(c, (void**)&sums, 10 * cl.m * sizeof(double)) != SCT_OK) return;
   {
     KScope _ks(c, "K8_voxel_pair_sum");
-    voxel_pair_sum_kernel<<<grid_cap(c, 8 * cl.m, 256), 256, 0, c->stream>>>(cl.m, offset, count, pair_stats,
+    pdl_launch(voxel_pair_sum_kernel, dim3(grid_cap(c, 8 * cl.m, 256)), dim3(256), 0, c->stream, cl.m, offset, count, pair_stats,
                                                                               sums);
   }
   {
     KScope _ks(c, "K8_voxel_chain");
-    voxel_chain_kernel<<<grid_cap(c, cl.m, 128), 128, 0, c->stream>>>(cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
+    pdl_launch(voxel_chain_kernel, dim3(grid_cap(c, cl.m, 128)), dim3(128), 0, c->stream, cl.m, cl.s_min_mm, cl.rho_raw, cl.pos,
                                                                      cl.scale_raw, cl.rot, offset, count, pair_stats,
                                                                      sums, g->rho_raw, g->pos, g->scale_raw, g->rot);
   }

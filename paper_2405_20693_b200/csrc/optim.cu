@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(256) tv3d_kernel(const float* __restrict__ vol
                                                    float* __restrict__ grad, double* __restrict__ partials,
                                                    double dinv_x, double dinv_y, double dinv_z,
                                                    double* __restrict__ value, int* __restrict__ counter) {
+  pdl_prologue();
   const long long n = (long long)nx * ny * nz;
   double sx = 0.0, sy = 0.0, sz = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(256) adam_kernel(long long m, float* __restric
                                                    const float* __restrict__ g_pos, const float* __restrict__ g_sc,
                                                    const float* __restrict__ g_rot, AdamParams ap,
                                                    double* __restrict__ total, double lambda_ssim, double lambda_tv) {
+  pdl_prologue();
   // native train step: the total loss of this iteration
   if (total && blockIdx.x == 0 && threadIdx.x == 0) train_total(total, lambda_ssim, lambda_tv);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
@@ -125,6 +127,7 @@ struct Taps {
 // horizontal valid pass of the five SSIM moments: tmp[img][5][H][Wv]
 __global__ void ssim_h_kernel(const float* __restrict__ r, const float* __restrict__ mm, int n, int W, int H,
                               float rscale, Taps taps, float* __restrict__ tmp) {
+  pdl_prologue();
   const int Wv = W - kWin + 1;
   const long long total = (long long)n * H * Wv;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -206,6 +209,7 @@ __device__ __forceinline__ void photometric_finish_warp(const double* l1_part, i
 // as per-block partials (grid: blocks per image x images).
 __global__ void __launch_bounds__(256) ssim_v_kernel(const float* __restrict__ tmp, int n, int W, int H, Taps taps,
                                                      float* __restrict__ fields, double* __restrict__ partial) {
+  pdl_prologue();
   const float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
   const int Wv = W - kWin + 1, Hv = H - kWin + 1;
   const long long img = blockIdx.y;
@@ -241,6 +245,7 @@ __global__ void __launch_bounds__(256) ssim_v_kernel(const float* __restrict__ t
 // adjoint vertical pass: atmp[img][5][H][Wv]
 __global__ void ssim_adj_v_kernel(const float* __restrict__ fields, int n, int W, int H, Taps taps,
                                   float* __restrict__ atmp) {
+  pdl_prologue();
   const int Wv = W - kWin + 1, Hv = H - kWin + 1;
   const long long total = (long long)n * H * Wv;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -271,6 +276,7 @@ __global__ void __launch_bounds__(256) ssim_adj_h_kernel(const float* __restrict
                                                          float* __restrict__ dL, double* __restrict__ partial,
                                                          const double* __restrict__ ssim_part, int nb_ssim,
                                                          double* __restrict__ values, int* __restrict__ counter) {
+  pdl_prologue();
   const int Wv = W - kWin + 1, Hv = H - kWin + 1;
   const float inv_p = 1.f / ((float)Wv * (float)Hv);
   const float inv_n = 1.f / ((float)W * (float)H);
@@ -324,7 +330,7 @@ void launch_tv3d(Ctx* c, const float* vol, const int32_t dims[3], float lambda, 
   const double ix = cx > 0 ? 1.0 / cx : 0.0, iy = cy > 0 ? 1.0 / cy : 0.0, iz = cz > 0 ? 1.0 / cz : 0.0;
   {
     KScope _ks(c, "K9_tv3d");
-    tv3d_kernel<<<n_partials, 256, 0, c->stream>>>(vol, nx, ny, nz, (float)ix, (float)iy, (float)iz, lambda, grad,
+    pdl_launch(tv3d_kernel, dim3(n_partials), dim3(256), 0, c->stream, vol, nx, ny, nz, (float)ix, (float)iy, (float)iz, lambda, grad,
                                                    partials, ix, iy, iz, value, c->fin_counter + 1);
   }
 }
@@ -336,7 +342,7 @@ void launch_adam(Ctx* c, sct_cloud* p, sct_adam_state* st, const sct_grads* g, c
   {
     KScope _ks(c, "K10_adam");
     const AdamParams ap{lr[0], lr[1], lr[2], lr[3], bc1, bc2, beta1, beta2, eps};
-    adam_kernel<<<grid_cap(c, p->m, 256), 256, 0, c->stream>>>(p->m, p->rho_raw, p->pos, p->scale_raw, p->rot, *st,
+    pdl_launch(adam_kernel, dim3(grid_cap(c, p->m, 256)), dim3(256), 0, c->stream, p->m, p->rho_raw, p->pos, p->scale_raw, p->rot, *st,
                                                                g->rho_raw, g->pos, g->scale_raw, g->rot, ap, total,
                                                                lambda_ssim, lambda_tv);
   }
@@ -378,20 +384,20 @@ int photometric_loss(Ctx* c, const float* rendered, const float* measured, int n
   double* l1_part = part + (size_t)n * nb_ssim;
   {
     KScope _ks(c, "K11_ssim_h");
-    ssim_h_kernel<<<grid_cap(c, (long long)n * h * Wv, 256), 256, 0, c->stream>>>(rendered, measured, n, w, h,
+    pdl_launch(ssim_h_kernel, dim3(grid_cap(c, (long long)n * h * Wv, 256)), dim3(256), 0, c->stream, rendered, measured, n, w, h,
                                                                                    render_scale, taps, tmp);
   }
   {
     KScope _ks(c, "K11_ssim_v");
-    ssim_v_kernel<<<dim3(nb_ssim, n), 256, 0, c->stream>>>(tmp, n, w, h, taps, fields, ssim_part);
+    pdl_launch(ssim_v_kernel, dim3(dim3(nb_ssim, n)), dim3(256), 0, c->stream, tmp, n, w, h, taps, fields, ssim_part);
   }
   {
     KScope _ks(c, "K11_ssim_adj_v");
-    ssim_adj_v_kernel<<<grid_cap(c, (long long)n * h * Wv, 256), 256, 0, c->stream>>>(fields, n, w, h, taps, tmp);
+    pdl_launch(ssim_adj_v_kernel, dim3(grid_cap(c, (long long)n * h * Wv, 256)), dim3(256), 0, c->stream, fields, n, w, h, taps, tmp);
   }
   {
     KScope _ks(c, "K11_ssim_adj_h");
-    ssim_adj_h_kernel<<<dim3(nb_l1, n), 256, 0, c->stream>>>(tmp, rendered, measured, n, w, h, render_scale, taps,
+    pdl_launch(ssim_adj_h_kernel, dim3(dim3(nb_l1, n)), dim3(256), 0, c->stream, tmp, rendered, measured, n, w, h, render_scale, taps,
                                                              lambda_ssim, grad_scale, dL, l1_part, ssim_part, nb_ssim,
                                                              values, c->fin_counter);
   }

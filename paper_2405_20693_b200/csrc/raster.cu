@@ -61,6 +61,7 @@ template <typename KeyT>
 __global__ void __launch_bounds__(256) raster_emit_kernel(long long n_items, const short4* __restrict__ rect,
                                                           const int32_t* __restrict__ offset, int tiles_x,
                                                           KeyT* __restrict__ keys, int32_t* __restrict__ vals) {
+  pdl_prologue();
   // Warp-cooperative: a warp owns 32 consecutive items, whose pairs occupy one
   // contiguous output range (exclusive-scan order); lanes stride over that
   // range so the key/value stores are coalesced. Each output slot finds its
@@ -159,6 +160,7 @@ __device__ __forceinline__ bool box_empty(const Box& r) { return r.x1 < r.x0 || 
 __global__ void __launch_bounds__(256) bin_count_kernel(const short4* __restrict__ rect, const short4* __restrict__ hi,
                                                         long long m, int chunk, int T, int tiles_x, int tiles_y,
                                                         int32_t* __restrict__ H) {
+  pdl_prologue();
   extern __shared__ uint32_t hist[];
   const int c = blockIdx.x, v = blockIdx.y;
   for (int t = threadIdx.x; t < T; t += blockDim.x) hist[t] = 0;
@@ -192,6 +194,7 @@ __global__ void __launch_bounds__(256) bin_count_kernel(const short4* __restrict
 constexpr int kSegRows = 64;
 __global__ void __launch_bounds__(256) bin_colsum_kernel(const int32_t* __restrict__ H, int n_rows, int T,
                                                          int32_t* __restrict__ seg) {
+  pdl_prologue();
   const int t = blockIdx.x * blockDim.x + threadIdx.x, g = blockIdx.y;
   if (t >= T) return;
   const int r0 = g * kSegRows, r1 = min(n_rows, r0 + kSegRows);
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(256) bin_colsum_kernel(const int32_t* __restri
 }
 __global__ void __launch_bounds__(256) bin_segscan_kernel(int32_t* __restrict__ seg, int n_seg, int T,
                                                           int32_t* __restrict__ coltot) {
+  pdl_prologue();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   // 16 loads in flight before the in-place stores (a load after a store to
@@ -224,6 +228,7 @@ __global__ void __launch_bounds__(256) bin_segscan_kernel(int32_t* __restrict__ 
 __global__ void __launch_bounds__(1024) bin_tilebase_kernel(const int32_t* __restrict__ coltot, int T,
                                                             int32_t* __restrict__ tile_base, long long cap,
                                                             int* __restrict__ overflow, int32_t* __restrict__ total) {
+  pdl_prologue();
   __shared__ int32_t part[1024];
   const int per = (T + blockDim.x - 1) / blockDim.x;
   const int t0 = min(T, (int)threadIdx.x * per), t1 = min(T, t0 + per);
@@ -259,6 +264,7 @@ __global__ void __launch_bounds__(kSmallScanThreads) bin_scan_small_kernel(int32
                                                                            int T, int32_t* __restrict__ tile_base,
                                                                            long long cap, int* __restrict__ overflow,
                                                                            int32_t* __restrict__ total) {
+  pdl_prologue();
   using Scan = cub::BlockScan<int32_t, kSmallScanThreads>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ int32_t seg_sum[kSmallScanThreads];
@@ -314,6 +320,7 @@ __global__ void __launch_bounds__(256) capacity_guard_kernel(int32_t* __restrict
                                                              short4* __restrict__ box_b,
                                                              const long long* __restrict__ sum64, long long cap,
                                                              int* __restrict__ overflow) {
+  pdl_prologue();
   // sum64 == nullptr: the int32 scan cannot have wrapped, offset[n] is the total
   const long long total = sum64 ? *sum64 : (long long)offset[n];
   if (total <= cap && offset[n] >= 0) return;
@@ -332,6 +339,7 @@ __global__ void __launch_bounds__(256) capacity_guard_kernel(int32_t* __restrict
 }
 __global__ void __launch_bounds__(256) bin_apply_kernel(int32_t* __restrict__ H, const int32_t* __restrict__ seg,
                                                         const int32_t* __restrict__ tile_base, int n_rows, int T) {
+  pdl_prologue();
   const int t = blockIdx.x * blockDim.x + threadIdx.x, g = blockIdx.y;
   if (t >= T) return;
   const int r0 = g * kSegRows, r1 = min(n_rows, r0 + kSegRows);
@@ -355,6 +363,7 @@ __global__ void __launch_bounds__(32 * kBinWarps) bin_scatter_kernel(const short
                                                                      int tiles_z, const int32_t* __restrict__ S,
                                                                      int32_t* __restrict__ vals, uint32_t cap,
                                                                      int v_off) {
+  pdl_prologue();
   extern __shared__ uint32_t sm[];
   uint32_t* cnt = sm;                              // [kBinWarps][T]
   uint32_t* colm = sm + kBinWarps * T;             // [kBinWarps][tiles_x]
@@ -461,6 +470,7 @@ __global__ void __launch_bounds__(256) bin_ranges_kernel(const int32_t* __restri
                                                          const int32_t* __restrict__ tile_base, int n_chunks,
                                                          int n_views, int T, int2* __restrict__ ranges,
                                                          long long cap) {
+  pdl_prologue();
   const long long n = (long long)n_views * T;
   // capacity overflow (flagged by the column scan): empty lists, so nothing
   // downstream reads past the cap-sized pair buffer
@@ -492,6 +502,7 @@ template <typename KeyT>
 __global__ void __launch_bounds__(256) raster_ranges_kernel(long long n_pairs, const KeyT* __restrict__ keys,
                                                             const int32_t* __restrict__ vals, int m, float inv_m,
                                                             long long tiles_per_view, int2* __restrict__ ranges) {
+  pdl_prologue();
   const long long groups = (n_pairs + 7) / 8;
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < groups;
        g += (long long)gridDim.x * blockDim.x) {
@@ -662,6 +673,7 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
     int tiles_x, int tiles_per_view, int W, int H, const int4* __restrict__ items, const int* __restrict__ n_items,
     int part_len, int* __restrict__ work, int* __restrict__ tile_cnt, float* __restrict__ partial,
     float* __restrict__ images, UnitSync us, const int* __restrict__ item_lo, const int* __restrict__ item_hi) {
+  pdl_prologue();
   // a chunk's 32 records as 16 kernel pairs, fields interleaved so that one
   // LDS.128 yields two float2 operands: [pair][0] = (cx0, cx1, cy0, cy1),
   // [1] = (amp0, amp1, K0, K1), [2] = (A0, A1, B0, B1), [3] = (C0, C1, 2A0, 2A1)
@@ -805,6 +817,7 @@ __global__ void __launch_bounds__(32 * kCompWarps) composite_kernel(
 // max(1, ceil(n / part_len)) consecutive items (exclusive scan `first`).
 __global__ void __launch_bounds__(256) k3_parts_kernel(const int2* __restrict__ ranges, const int* __restrict__ order,
                                                        int n, int part_len, int* __restrict__ count) {
+  pdl_prologue();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int2 r = ranges[order[i]];
     count[i] = max(1, (r.y - r.x + part_len - 1) / part_len);
@@ -822,6 +835,7 @@ __global__ void __launch_bounds__(kSmallWorkThreads) k3_first_small_kernel(const
                                                                            const int* __restrict__ order, int n,
                                                                            int part_len, int* __restrict__ count,
                                                                            int* __restrict__ first) {
+  pdl_prologue();
   using Scan = cub::BlockScan<int, kSmallWorkThreads>;
   __shared__ typename Scan::TempStorage tmp;
   const int per = (n + kSmallWorkThreads - 1) / kSmallWorkThreads;
@@ -850,6 +864,7 @@ __global__ void __launch_bounds__(256) k3_items_kernel(const int* __restrict__ o
                                                        const int* __restrict__ first, int n,
                                                        int4* __restrict__ items, int* __restrict__ n_items,
                                                        int* __restrict__ tile_cnt, long long max_items) {
+  pdl_prologue();
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int)stride) {
     const int k = count[i], f = first[i], w = order[i];
@@ -875,6 +890,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) backward_stats_kernel(
     const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ rect, const int32_t* __restrict__ offset, int tiles_x, int tiles_per_view, int W,
     int H, int view0, const float* __restrict__ dL, float* __restrict__ pair_stats, float* __restrict__ item_stats) {
+  pdl_prologue();
   const int tile = blockIdx.x;
   const int view = view0 + blockIdx.y;
   const int2 rg = ranges[(long long)view * tiles_per_view + tile];
@@ -1102,6 +1118,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 32 / kMmaWarps) backward_stats
     int H, int view0, const int* __restrict__ order, int parts, const float* __restrict__ dL,
     float* __restrict__ pair_stats,
     float* __restrict__ item_stats, UnitSync us) {
+  pdl_prologue();
   __shared__ uint4 s_g[16][32];  // [slice][lane] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}
   __shared__ float s_gmax[kMmaWarps];
   // per-warp double buffer of the 16 records (and items) of a chunk, filled
@@ -1457,6 +1474,7 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtas) backward_stats_tc_kernel(
     const short4* __restrict__ rect, const int32_t* __restrict__ offset, int tiles_x, int tiles_per_view, int W,
     int H, int view0, const int* __restrict__ order, int parts, int n_work, int* __restrict__ work,
     const float* __restrict__ dL, float* __restrict__ pair_stats, float* __restrict__ item_stats, UnitSync us) {
+  pdl_prologue();
   __shared__ __align__(1024) unsigned char s_g[16 * 256 * 2];
   __shared__ __align__(8) uint64_t bar_afull[kTcABuf], bar_aempty[kTcABuf], bar_dfull[2], bar_dempty[2];
   __shared__ __align__(16) float4 s_rec[2][32 * kTcWarps][2];  // per-thread staging (own slots)
@@ -1723,11 +1741,9 @@ void launch_raster_emit(Ctx* c, int64_t n_items, const short4* rect, const int32
   if (n_items == 0) return;
   KScope _ks(c, "K2_raster_emit");
   if (keys16)
-    raster_emit_kernel<uint16_t><<<grid_cap(c, n_items, 256), 256, 0, c->stream>>>(
-        n_items, rect, offset, tiles_x, static_cast<uint16_t*>(keys), vals);
+    pdl_launch(raster_emit_kernel<uint16_t>, dim3(grid_cap(c, n_items, 256)), dim3(256), 0, c->stream, n_items, rect, offset, tiles_x, static_cast<uint16_t*>(keys), vals);
   else
-    raster_emit_kernel<uint32_t><<<grid_cap(c, n_items, 256), 256, 0, c->stream>>>(
-        n_items, rect, offset, tiles_x, static_cast<uint32_t*>(keys), vals);
+    pdl_launch(raster_emit_kernel<uint32_t>, dim3(grid_cap(c, n_items, 256)), dim3(256), 0, c->stream, n_items, rect, offset, tiles_x, static_cast<uint32_t*>(keys), vals);
 }
 
 // Counting-scatter binning (bin_* kernels above). Needs the per-warp tile
@@ -1753,6 +1769,7 @@ __global__ void __launch_bounds__(kCountScanThreads) count_scan_small_kernel(int
                                                                              long long cap, short4* __restrict__ box_a,
                                                                              short4* __restrict__ box_b,
                                                                              int* __restrict__ overflow) {
+  pdl_prologue();
   using Scan = cub::BlockScan<long long, kCountScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ long long s_total;
@@ -1814,14 +1831,13 @@ __global__ void __launch_bounds__(kCountScanThreads) count_scan_small_kernel(int
 
 void launch_count_scan_small(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t cap, short4* box_a,
                              short4* box_b) {
-  count_scan_small_kernel<<<1, kCountScanThreads, 0, c->stream>>>(count, offset, (long long)n, c->sum64,
+  pdl_launch(count_scan_small_kernel, dim3(1), dim3(kCountScanThreads), 0, c->stream, count, offset, (long long)n, c->sum64,
                                                                   (long long)cap, box_a, box_b, c->overflow);
 }
 
 void launch_capacity_guard(Ctx* c, int32_t* count, int32_t* offset, int64_t n, short4* box_a, short4* box_b,
                            int64_t cap, bool no_wrap) {
-  capacity_guard_kernel<<<grid_cap(c, n + 1, 256), 256, 0, c->stream>>>(
-      count, offset, n, box_a, box_b, no_wrap ? nullptr : c->sum64, (long long)cap, c->overflow);
+  pdl_launch(capacity_guard_kernel, dim3(grid_cap(c, n + 1, 256)), dim3(256), 0, c->stream, count, offset, n, box_a, box_b, no_wrap ? nullptr : c->sum64, (long long)cap, c->overflow);
 }
 
 // Stable counting-scatter binning of n_views x m items with boxes (lo, hi)
@@ -1860,24 +1876,24 @@ int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tile
   const dim3 grid((unsigned)n_chunks, (unsigned)n_views);
   {
     KScope _ks(c, "K2_bin_count");
-    bin_count_kernel<<<grid, 256, T * sizeof(uint32_t), c->stream>>>(lo, hi, m, (int)chunk, (int)T, tiles_x, tiles_y,
+    pdl_launch(bin_count_kernel, dim3(grid), dim3(256), T * sizeof(uint32_t), c->stream, lo, hi, m, (int)chunk, (int)T, tiles_x, tiles_y,
                                                                      H);
   }
   if (T <= kSmallScanThreads && rows * T <= kSmallScanEntries) {
     KScope _ks(c, "K2_bin_scan");
-    bin_scan_small_kernel<<<1, kSmallScanThreads, 0, c->stream>>>(H, (int)rows, (int)T, tb2, (long long)cap,
+    pdl_launch(bin_scan_small_kernel, dim3(1), dim3(kSmallScanThreads), 0, c->stream, H, (int)rows, (int)T, tb2, (long long)cap,
                                                                   c->overflow, total);
   } else {
     KScope _ks(c, "K2_bin_scan");
     const dim3 g2((unsigned)((T + 255) / 256), (unsigned)n_seg);
-    bin_colsum_kernel<<<g2, 256, 0, c->stream>>>(H, (int)rows, (int)T, seg);
-    bin_segscan_kernel<<<(unsigned)((T + 255) / 256), 256, 0, c->stream>>>(seg, (int)n_seg, (int)T, tb);
-    bin_tilebase_kernel<<<1, 1024, 0, c->stream>>>(tb, (int)T, tb2, (long long)cap, c->overflow, total);
-    bin_apply_kernel<<<g2, 256, 0, c->stream>>>(H, seg, tb2, (int)rows, (int)T);
+    pdl_launch(bin_colsum_kernel, dim3(g2), dim3(256), 0, c->stream, H, (int)rows, (int)T, seg);
+    pdl_launch(bin_segscan_kernel, dim3((unsigned)((T + 255) / 256)), dim3(256), 0, c->stream, seg, (int)n_seg, (int)T, tb);
+    pdl_launch(bin_tilebase_kernel, dim3(1), dim3(1024), 0, c->stream, tb, (int)T, tb2, (long long)cap, c->overflow, total);
+    pdl_launch(bin_apply_kernel, dim3(g2), dim3(256), 0, c->stream, H, seg, tb2, (int)rows, (int)T);
   }
   if (ranges) {  // from the scan alone: final before any pair is written
     KScope _ks(c, "K2_bin_ranges");
-    bin_ranges_kernel<<<grid_cap(c, n_views * T, 256), 256, 0, c->stream>>>(H, tb2, (int)n_chunks, (int)n_views,
+    pdl_launch(bin_ranges_kernel, dim3(grid_cap(c, n_views * T, 256)), dim3(256), 0, c->stream, H, tb2, (int)n_chunks, (int)n_views,
                                                                             (int)T, ranges, (long long)cap);
   }
   static bool attr = false;
@@ -1890,8 +1906,7 @@ int launch_bin_scatter(Ctx* c, int64_t n_views, int64_t m, int tiles_x, int tile
   const int64_t v_now = (scatter_views > 0 && scatter_views < n_views && defer) ? scatter_views : n_views;
   {
     KScope _ks(c, "K2_bin_scatter");
-    bin_scatter_kernel<<<dim3((unsigned)n_chunks, (unsigned)v_now), 32 * kBinWarps, smem, c->stream>>>(
-        lo, hi, m, (int)chunk, (int)T, tiles_x, tiles_y, tiles_z, H, vals,
+    pdl_launch(bin_scatter_kernel, dim3(dim3((unsigned)n_chunks, (unsigned)v_now)), dim3(32 * kBinWarps), smem, c->stream, lo, hi, m, (int)chunk, (int)T, tiles_x, tiles_y, tiles_z, H, vals,
         (uint32_t)std::min<int64_t>(cap, UINT32_MAX), 0);
   }
   if (v_now < n_views) {  // the rest later (launch_bin_scatter_rest)
@@ -1926,8 +1941,7 @@ int launch_bin_scatter_rest(Ctx* c, BinDeferred* d) {
   const int64_t T = (int64_t)d->tiles_x * d->tiles_y * d->tiles_z;
   {
     KScope _ks(c, "K2_bin_scatter");
-    bin_scatter_kernel<<<dim3((unsigned)d->n_chunks, (unsigned)(d->n_views - d->v0)), 32 * kBinWarps, d->smem,
-                         c->stream>>>(d->lo, d->hi, d->m, (int)d->chunk, (int)T, d->tiles_x, d->tiles_y, d->tiles_z,
+    pdl_launch(bin_scatter_kernel, dim3(dim3((unsigned)d->n_chunks, (unsigned)(d->n_views - d->v0))), dim3(32 * kBinWarps), d->smem, c->stream, d->lo, d->hi, d->m, (int)d->chunk, (int)T, d->tiles_x, d->tiles_y, d->tiles_z,
                                       d->H, d->vals, (uint32_t)std::min<int64_t>(d->cap, UINT32_MAX), (int)d->v0);
   }
   dev_free(c, d->H);
@@ -1951,11 +1965,9 @@ void launch_raster_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16
   if (n_pairs == 0) return;
   KScope _ks(c, "K2_ranges");
   if (keys16)
-    raster_ranges_kernel<uint16_t><<<grid_cap(c, (n_pairs + 7) / 8, 256), 256, 0, c->stream>>>(
-        n_pairs, static_cast<const uint16_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
+    pdl_launch(raster_ranges_kernel<uint16_t>, dim3(grid_cap(c, (n_pairs + 7) / 8, 256)), dim3(256), 0, c->stream, n_pairs, static_cast<const uint16_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
   else
-    raster_ranges_kernel<uint32_t><<<grid_cap(c, (n_pairs + 7) / 8, 256), 256, 0, c->stream>>>(
-        n_pairs, static_cast<const uint32_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
+    pdl_launch(raster_ranges_kernel<uint32_t>, dim3(grid_cap(c, (n_pairs + 7) / 8, 256)), dim3(256), 0, c->stream, n_pairs, static_cast<const uint32_t*>(keys), vals, (int)m, 1.f / (float)m, tiles_per_view, ranges);
 }
 
 // list order key: the length octave, descending, clamped to 4 bits (lists of
@@ -1971,6 +1983,7 @@ __device__ __forceinline__ uint32_t order_key4(int len) {
 __global__ void __launch_bounds__(256) tile_order_keys_kernel(const int2* __restrict__ ranges, long long base,
                                                               int n, uint32_t* __restrict__ keys,
                                                               int32_t* __restrict__ idx) {
+  pdl_prologue();
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
     const int2 r = ranges[base + w];
     // descending octave of the list length; the stable sort keeps the natural
@@ -1989,6 +2002,7 @@ template <int kItems>
 __global__ void __launch_bounds__(kSmallOrderThreads) tile_order_small_kernel(const int2* __restrict__ ranges,
                                                                               long long base, int n,
                                                                               int32_t* __restrict__ order) {
+  pdl_prologue();
   using Sort = cub::BlockRadixSort<uint32_t, kSmallOrderThreads, kItems, int32_t>;
   __shared__ typename Sort::TempStorage tmp;
   uint32_t key[kItems];
@@ -2023,6 +2037,7 @@ constexpr int kMidOrder = kMidOrderThreads * kMidOrderPer;
 __global__ void __launch_bounds__(kMidOrderThreads) tile_order_mid_kernel(const int2* __restrict__ ranges,
                                                                           long long base, int n,
                                                                           int32_t* __restrict__ order) {
+  pdl_prologue();
   using Scan = cub::BlockScan<int32_t, kMidOrderThreads>;
   __shared__ typename Scan::TempStorage tmp;
   extern __shared__ int32_t cnt[];  // [16][kMidOrderThreads]
@@ -2058,6 +2073,7 @@ __global__ void __launch_bounds__(256) tile_order_chunk_keys_kernel(const int2* 
                                                                     int tiles_per_view, int n_views, int chunks,
                                                                     uint32_t* __restrict__ keys,
                                                                     int32_t* __restrict__ idx) {
+  pdl_prologue();
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
     const int2 r = ranges[w];
     const int v = w / tiles_per_view;
@@ -2081,12 +2097,11 @@ static const int* tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
   if (n <= kSmallOrder) {  // one CTA instead of the device-wide sort's launches (train step: 256 lists)
     // items per thread sized to n (the 256-list train step sorts 1024 keys)
     if (n <= kSmallOrderThreads)
-      tile_order_small_kernel<1><<<1, kSmallOrderThreads, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
+      pdl_launch(tile_order_small_kernel<1>, dim3(1), dim3(kSmallOrderThreads), 0, c->stream, s->d_ranges, (long long)v0 * T, n, i0);
     else if (n <= 4 * kSmallOrderThreads)
-      tile_order_small_kernel<4><<<1, kSmallOrderThreads, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
+      pdl_launch(tile_order_small_kernel<4>, dim3(1), dim3(kSmallOrderThreads), 0, c->stream, s->d_ranges, (long long)v0 * T, n, i0);
     else
-      tile_order_small_kernel<kSmallOrderItems>
-          <<<1, kSmallOrderThreads, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
+      pdl_launch(tile_order_small_kernel<kSmallOrderItems>, dim3(1), dim3(kSmallOrderThreads), 0, c->stream, s->d_ranges, (long long)v0 * T, n, i0);
     ++c->order_gen;
     return i0;
   }
@@ -2102,11 +2117,11 @@ static const int* tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
         return nullptr;
       attr = true;
     }
-    tile_order_mid_kernel<<<1, kMidOrderThreads, smem, c->stream>>>(s->d_ranges, (long long)v0 * T, n, i0);
+    pdl_launch(tile_order_mid_kernel, dim3(1), dim3(kMidOrderThreads), smem, c->stream, s->d_ranges, (long long)v0 * T, n, i0);
     ++c->order_gen;
     return i0;
   }
-  tile_order_keys_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(s->d_ranges, (long long)v0 * T, n, k0, i0);
+  pdl_launch(tile_order_keys_kernel, dim3(grid_cap(c, n, 256)), dim3(256), 0, c->stream, s->d_ranges, (long long)v0 * T, n, k0, i0);
   cub::DoubleBuffer<uint32_t> keys(k0, k1);
   cub::DoubleBuffer<int32_t> vals(i0, i1);
   size_t tmp = 0;
@@ -2146,7 +2161,7 @@ static const int* unit_tile_order(Ctx* c, const sct_fwd* s, int units) {
   int32_t* i1 = i0 + n;
   {
     KScope _ks(c, "K2_tile_order");
-    tile_order_chunk_keys_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(s->d_ranges, n, T, V, units, k0, i0);
+    pdl_launch(tile_order_chunk_keys_kernel, dim3(grid_cap(c, n, 256)), dim3(256), 0, c->stream, s->d_ranges, n, T, V, units, k0, i0);
   }
   cub::DoubleBuffer<uint32_t> keys(k0, k1);
   cub::DoubleBuffer<int32_t> vals(i0, i1);
@@ -2258,17 +2273,16 @@ static int list_work(Ctx* c, const sct_fwd* s, const int* order, const int2* ran
       return e ? std::min(kSmallWork, atoi(e)) : 4096;
     }();
     if (n <= small_max) {
-      k3_first_small_kernel<<<1, kSmallWorkThreads, 0, c->stream>>>(ranges, order, n, kw.part_len, count, first);
+      pdl_launch(k3_first_small_kernel, dim3(1), dim3(kSmallWorkThreads), 0, c->stream, ranges, order, n, kw.part_len, count, first);
     } else {
-      k3_parts_kernel<<<grid_cap(c, n, 256), 256, 0, c->stream>>>(ranges, order, n, kw.part_len, count);
+      pdl_launch(k3_parts_kernel, dim3(grid_cap(c, n, 256)), dim3(256), 0, c->stream, ranges, order, n, kw.part_len, count);
       size_t tmp = 0;
       SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, first, n, c->stream));
       SCT_TRY(ensure_cub_tmp(c, tmp));
       tmp = c->cub_tmp_bytes;
       SCT_CUDA_TRY(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tmp, count, first, n, c->stream));
     }
-    k3_items_kernel<<<grid_cap(c, std::max<long long>(n, max_items / 4), 256), 256, 0, c->stream>>>(
-        order, count, first, n, items, n_items, tile_cnt, max_items);
+    pdl_launch(k3_items_kernel, dim3(grid_cap(c, std::max<long long>(n, max_items / 4), 256)), dim3(256), 0, c->stream, order, count, first, n, items, n_items, tile_cnt, max_items);
   }
   key.gen = c->order_gen;
   key.part = kw.part_len;
@@ -2292,7 +2306,7 @@ static int composite_launch(Ctx* c, const sct_fwd* s, const int* order, float* i
   const int blocks = (int)std::min<long long>((long long)c->sm_count * composite_per_sm(),
                                               (kw.max_items + kCompWarps - 1) / kCompWarps);
   KScope _ks(c, "K3_composite");
-  composite_kernel<<<blocks, 32 * kCompWarps, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
+  pdl_launch(composite_kernel, dim3(blocks), dim3(32 * kCompWarps), 0, c->stream, s->d_ranges, s->d_vals, s->d_rec, s->det.tiles_x, T,
                                                               s->det.w, s->det.h, kw.items, kw.n_items, kw.part_len,
                                                               work, kw.tile_cnt, kw.partial, images, us,
                                                               pos0 > 0 ? kw.first + pos0 : nullptr,
@@ -2328,7 +2342,7 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
   KScope _ks(c, "K4_backward_stats");
   float* ps = reinterpret_cast<float*>(pair_stats);
   if (simt) {
-    backward_stats_kernel<<<grid, kBwdThreads, 0, c->stream>>>(s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
+    pdl_launch(backward_stats_kernel, dim3(grid), dim3(kBwdThreads), 0, c->stream, s->d_ranges, s->d_vals, s->d_rec, s->d_rect,
                                                                s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h,
                                                                v0, dL, ps, item_stats);
     return;
@@ -2368,8 +2382,7 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
     cudaMemsetAsync(work + 1, 0, sizeof(int), c->stream);
     const long long n_work = total * parts;
     const int blocks = (int)std::max<long long>(1, std::min<long long>((long long)c->sm_count * kTcCtas, n_work));
-    backward_stats_tc_kernel<<<blocks, kTcThreads, 0, c->stream>>>(
-        s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
+    pdl_launch(backward_stats_tc_kernel, dim3(blocks), dim3(kTcThreads), 0, c->stream, s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
         parts, (int)n_work, work + 1, dL, ps, item_stats, ks);
     return;
   }
@@ -2382,12 +2395,10 @@ void launch_raster_backward_stats(Ctx* c, const sct_fwd* s, const float* dL, flo
   }();
   const bool wide = forced_w ? forced_w == 4 : (parts > 1 || total < kK4LargeLists);
   if (wide)
-    backward_stats_mma_kernel<kMmaWarpsSmall><<<(unsigned)(total * parts), 32 * kMmaWarpsSmall, 0, c->stream>>>(
-        s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
+    pdl_launch(backward_stats_mma_kernel<kMmaWarpsSmall>, dim3((unsigned)(total * parts)), dim3(32 * kMmaWarpsSmall), 0, c->stream, s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
         parts, dL, ps, item_stats, ks);
   else
-    backward_stats_mma_kernel<kMmaWarpsLarge><<<(unsigned)(total * parts), 32 * kMmaWarpsLarge, 0, c->stream>>>(
-        s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
+    pdl_launch(backward_stats_mma_kernel<kMmaWarpsLarge>, dim3((unsigned)(total * parts)), dim3(32 * kMmaWarpsLarge), 0, c->stream, s->d_ranges, s->d_vals, s->d_rec, s->d_rect, s->d_offset, s->det.tiles_x, T, s->det.w, s->det.h, v0, order,
         parts, dL, ps, item_stats, ks);
 }
 

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "splatct_gpu.h"
@@ -243,6 +244,38 @@ void comm_release(Ctx* c);
 int stage_buf(Ctx* c, int slot, size_t bytes, void** p);
 
 int ensure_cub_tmp(Ctx* c, size_t bytes);
+
+// Programmatic dependent launch (sm_90+): every engine kernel is launched with
+// programmatic stream serialisation (pdl_launch) and begins with
+// pdl_prologue(): it lets the next kernel of the stream be scheduled once all
+// of its own blocks are running, then waits until the previous kernel has
+// completed and its writes are visible. So a dependent kernel's launch and
+// block ramp overlap its predecessor's tail instead of following it — the
+// train step is a chain of ~30 small dependent kernels. (Both instructions
+// are no-ops for a kernel launched without the attribute; SCT_PDL=0 launches
+// without it.)
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#endif
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // RAII scope recording a start/stop event pair around one kernel launch when
 // timing is enabled; also counts the launch.

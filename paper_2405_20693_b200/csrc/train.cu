@@ -25,6 +25,7 @@ namespace {
 // (l1 + lambda_ssim dssim) + lambda_tv tv with separately rounded products, as the
 // host-side composition does (no FMA contraction)
 __global__ void train_total_kernel(double* v, double lambda_ssim, double lambda_tv) {
+  pdl_prologue();
   v[3] = __dadd_rn(__dadd_rn(v[0], __dmul_rn(lambda_ssim, v[1])), __dmul_rn(lambda_tv, v[2]));
 }
 
@@ -89,7 +90,7 @@ extern "C" int sct_train_step(sct_ctx* c, sct_cloud* cloud, sct_adam_state* adam
     SCT_CUDA_TRY(cudaMemsetAsync(a->values_dev + 2, 0, sizeof(double), c->stream));
   }
   if (cloud->m == 0) {
-    train_total_kernel<<<1, 1, 0, c->stream>>>(a->values_dev, a->lambda_ssim, a->lambda_tv);
+    pdl_launch(train_total_kernel, dim3(1), dim3(1), 0, c->stream, a->values_dev, a->lambda_ssim, a->lambda_tv);
     ++c->launches;
     SCT_CUDA_TRY(cudaGetLastError());
     return SCT_OK;

@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(256) voxel_emit_kernel(long long m, const shor
                                                          const int32_t* __restrict__ offset, int bx, int by,
                                                          KeyT* __restrict__ keys, int32_t* __restrict__ vals,
                                                          long long cap) {
+  pdl_prologue();
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long w0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < m;
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(256) voxel_emit_kernel(long long m, const shor
 template <typename KeyT>
 __global__ void __launch_bounds__(256) key_ranges_kernel(long long n_pairs, const KeyT* __restrict__ keys,
                                                          int2* __restrict__ ranges, long long n_keys) {
+  pdl_prologue();
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_pairs;
        p += (long long)gridDim.x * blockDim.x) {
     const KeyT k = keys[p];
@@ -287,6 +289,7 @@ __global__ void __launch_bounds__(32 * kEvalWarps) voxel_eval_kernel(BrickGeo G,
                                                                      const float4* __restrict__ rec, int splits,
                                                                      float* __restrict__ partial,
                                                                      float* __restrict__ vol) {
+  pdl_prologue();
   __shared__ float4 sA[kEvalWarps][32];  // base offset xyz, rho*2^-64
   __shared__ float4 sB[kEvalWarps][32];  // Qxx Qyy Qzz K
   __shared__ float4 sC[kEvalWarps][32];  // Qxy Qxz Qyz
@@ -390,6 +393,7 @@ __global__ void __launch_bounds__(kVBwdThreads, 3) voxel_backward_stats_kernel(
     BrickGeo G, const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ lo, const short4* __restrict__ hi, const int32_t* __restrict__ offset,
     const float* __restrict__ dL, float* __restrict__ pair_stats) {
+  pdl_prologue();
   int tx, ty, tz;
   brick_of(G, blockIdx.x, tx, ty, tz);
   const int brick = (tz * G.by + ty) * G.bx + tx;
@@ -521,6 +525,7 @@ __global__ void __launch_bounds__(32 * kVMmaWarps, 7) voxel_backward_mma_kernel(
     BrickGeo G, const int2* __restrict__ ranges, const int32_t* __restrict__ vals, const float4* __restrict__ rec,
     const short4* __restrict__ lo, const short4* __restrict__ hi, const int32_t* __restrict__ offset,
     const float* __restrict__ dL, float* __restrict__ pair_stats, int parts) {
+  pdl_prologue();
   // B fragments [slice][lane] = {hi k0-1, hi k8-9, lo k0-1, lo k8-9}: n tile 0
   // (moments 0-7) for all lanes; n tile 1 holds moments 8, 9 only (lanes 0-7)
   __shared__ uint4 s_g[32][32];
@@ -730,6 +735,7 @@ __global__ void __launch_bounds__(32 * kVMmaWarps, 7) voxel_backward_mma_kernel(
 // vol[i] = sum over parts (in part order) of the split evaluation's partials
 __global__ void __launch_bounds__(256) voxel_reduce_kernel(const float* __restrict__ partial, int splits,
                                                            long long stride, long long n, float* __restrict__ vol) {
+  pdl_prologue();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     float s = 0.f;
@@ -760,10 +766,10 @@ void launch_voxel_emit(Ctx* c, int64_t m, const short4* lo, const short4* hi, co
   if (b > (long long)c->sm_count * 16) b = (long long)c->sm_count * 16;
   KScope _ks(c, "K6_voxel_emit");
   if (keys16)
-    voxel_emit_kernel<uint16_t><<<(int)b, 256, 0, c->stream>>>(m, lo, hi, offset, bricks_x, bricks_y,
+    pdl_launch(voxel_emit_kernel<uint16_t>, dim3((int)b), dim3(256), 0, c->stream, m, lo, hi, offset, bricks_x, bricks_y,
                                                                static_cast<uint16_t*>(keys), vals, (long long)cap);
   else
-    voxel_emit_kernel<uint32_t><<<(int)b, 256, 0, c->stream>>>(m, lo, hi, offset, bricks_x, bricks_y,
+    pdl_launch(voxel_emit_kernel<uint32_t>, dim3((int)b), dim3(256), 0, c->stream, m, lo, hi, offset, bricks_x, bricks_y,
                                                                static_cast<uint32_t*>(keys), vals, (long long)cap);
 }
 
@@ -773,10 +779,10 @@ void launch_key_ranges(Ctx* c, int64_t n_pairs, const void* keys, bool keys16, i
   if (b > (long long)c->sm_count * 16) b = (long long)c->sm_count * 16;
   KScope _ks(c, "K2_ranges");
   if (keys16)
-    key_ranges_kernel<uint16_t><<<(int)b, 256, 0, c->stream>>>(n_pairs, static_cast<const uint16_t*>(keys), ranges,
+    pdl_launch(key_ranges_kernel<uint16_t>, dim3((int)b), dim3(256), 0, c->stream, n_pairs, static_cast<const uint16_t*>(keys), ranges,
                                                                 (long long)n_keys);
   else
-    key_ranges_kernel<uint32_t><<<(int)b, 256, 0, c->stream>>>(n_pairs, static_cast<const uint32_t*>(keys), ranges,
+    pdl_launch(key_ranges_kernel<uint32_t>, dim3((int)b), dim3(256), 0, c->stream, n_pairs, static_cast<const uint32_t*>(keys), ranges,
                                                                 (long long)n_keys);
 }
 
@@ -802,8 +808,7 @@ void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int3
   {
     KScope _ks(c, "K7_voxel_eval");
     const long long warps = nb * splits;
-    voxel_eval_kernel<<<(unsigned)((warps + kEvalWarps - 1) / kEvalWarps), 32 * kEvalWarps, 0, c->stream>>>(
-        make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, splits, partial, vol);
+    pdl_launch(voxel_eval_kernel, dim3((unsigned)((warps + kEvalWarps - 1) / kEvalWarps)), dim3(32 * kEvalWarps), 0, c->stream, make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, splits, partial, vol);
   }
   if (splits > 1) {
     KScope _ks(c, "K7_reduce");
@@ -811,8 +816,7 @@ void launch_voxel_eval(Ctx* c, const sct_grid& g, int32_t zb0, int32_t zb1, int3
     const long long plane = (long long)g.dims[0] * g.dims[1];
     const long long n = (z1 - z0) * plane;
     if (n > 0)
-      voxel_reduce_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, (long long)c->sm_count * 16), 256, 0,
-                            c->stream>>>(partial + z0 * plane, splits, nvox, n, vol + z0 * plane);
+      pdl_launch(voxel_reduce_kernel, dim3((unsigned)std::min<long long>((n + 255) / 256, (long long)c->sm_count * 16)), dim3(256), 0, c->stream, partial + z0 * plane, splits, nvox, n, vol + z0 * plane);
   }
 }
 
@@ -837,12 +841,10 @@ void launch_voxel_backward_stats(Ctx* c, const sct_grid& g, int32_t zb0, int32_t
   }();
   KScope _ks(c, "K8_voxel_backward_stats");
   if (simt)
-    voxel_backward_stats_kernel<<<(unsigned)nb, kVBwdThreads, 0, c->stream>>>(
-        make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL,
+    pdl_launch(voxel_backward_stats_kernel, dim3((unsigned)nb), dim3(kVBwdThreads), 0, c->stream, make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL,
         reinterpret_cast<float*>(pair_stats));
   else
-    voxel_backward_mma_kernel<<<(unsigned)(nb * parts), 32 * kVMmaWarps, 0, c->stream>>>(
-        make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL,
+    pdl_launch(voxel_backward_mma_kernel, dim3((unsigned)(nb * parts)), dim3(32 * kVMmaWarps), 0, c->stream, make_geo(g, zb0, zb1, bricks_x, bricks_y), ranges, vals, rec, lo, hi, offset, dL,
         reinterpret_cast<float*>(pair_stats), parts);
 }
 
