@@ -151,7 +151,7 @@ constexpr int64_t kCountScanSmallUse = 4096;
 static int scan_counts(Ctx* c, int32_t* count, int32_t* offset, int64_t n, int64_t* total, int64_t cap = 0,
                        short4* box_a = nullptr, short4* box_b = nullptr, int64_t max_per_item = 0) {
   const bool no_wrap = max_per_item > 0 && (n + 1) * max_per_item < (int64_t)INT32_MAX;
-  SCT_CUDA_TRY(cudaMemsetAsync(count + n, 0, sizeof(int32_t), c->stream));
+  SCT_TRY(launch_zero(c, count + n, sizeof(int32_t)));
   if (n + 1 <= kCountScanSmallUse) {  // one CTA: scan, int64 total and capacity guard
     {
       KScope _ks(c, "K2_scan(cub)", false);
@@ -380,6 +380,16 @@ __global__ void fwd_init_kernel(ViewPack p, int nv, ViewParams* dst, int2* range
     ranges[i] = make_int2(0, 0);
 }
 
+__global__ void __launch_bounds__(256) zero_kernel(uint32_t* __restrict__ p, long long n_words) {
+  pdl_prologue();
+  const long long n4 = (reinterpret_cast<uintptr_t>(p) & 15) == 0 ? n_words / 4 : 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  uint4* p4 = reinterpret_cast<uint4*>(p);
+  for (long long i = t; i < n4; i += stride) p4[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (long long i = 4 * n4 + t; i < n_words; i += stride) p[i] = 0u;
+}
+
 int fwd_init(Ctx* c, const std::vector<ViewParams>& hv, ViewParams* d_views, int2* ranges, int64_t n_ranges,
              int32_t* total) {
   for (size_t v0 = 0; v0 < hv.size() || v0 == 0; v0 += kViewPack) {
@@ -397,6 +407,16 @@ int fwd_init(Ctx* c, const std::vector<ViewParams>& hv, ViewParams* d_views, int
   return SCT_OK;
 }
 }  // namespace
+
+int launch_zero(Ctx* c, void* p, size_t bytes) {
+  const long long words = (long long)(bytes / 4);
+  if (words == 0) return SCT_OK;
+  const long long b = std::min<long long>((words / 4 + 255) / 256 + 1, (long long)c->sm_count * 8);
+  pdl_launch(zero_kernel, dim3((unsigned)b), dim3(256), 0, c->stream, static_cast<uint32_t*>(p), words);
+  ++c->launches;
+  SCT_CUDA_TRY(cudaGetLastError());
+  return SCT_OK;
+}
 }  // namespace sct
 
 using namespace sct;
@@ -780,7 +800,7 @@ int sct_render_bwd_chunked(sct_ctx* c, sct_fwd* s, const sct_cloud* cloud, const
   float* item_stats = nullptr;
   if (atomic) {
     SCT_TRY(stage_buf(c, 14, 8 * s->n_items * sizeof(float), (void**)&item_stats));
-    SCT_CUDA_TRY(cudaMemsetAsync(item_stats, 0, 8 * s->n_items * sizeof(float), c->stream));
+    SCT_TRY(launch_zero(c, item_stats, 8 * s->n_items * sizeof(float)));
   } else {
     SCT_TRY(stage_buf(c, 14, 2 * s->n_pairs * sizeof(float4), (void**)&pair_stats));
   }

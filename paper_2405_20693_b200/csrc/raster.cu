@@ -2302,7 +2302,7 @@ static int composite_launch(Ctx* c, const sct_fwd* s, const int* order, float* i
   SCT_TRY(list_work(c, s, order, s->d_ranges, n, composite_part_len(c, s), kw));
   int* work = nullptr;
   SCT_TRY(stage_buf(c, 20, sizeof(int) * 4, (void**)&work));
-  SCT_CUDA_TRY(cudaMemsetAsync(work, 0, sizeof(int), c->stream));
+  SCT_TRY(launch_zero(c, work, sizeof(int)));
   const int blocks = (int)std::min<long long>((long long)c->sm_count * composite_per_sm(),
                                               (kw.max_items + kCompWarps - 1) / kCompWarps);
   KScope _ks(c, "K3_composite");

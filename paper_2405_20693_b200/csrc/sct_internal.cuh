@@ -261,6 +261,9 @@ __device__ __forceinline__ void pdl_prologue() {
 }
 #endif
 bool pdl_enabled();
+// zero `bytes` (a multiple of 4) at p with a PDL-launched kernel instead of a
+// cudaMemsetAsync, which would break the dependent-launch chain
+int launch_zero(Ctx* c, void* p, size_t bytes);
 template <typename... KArgs, typename... Args>
 inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {

@@ -32,8 +32,7 @@ __global__ void train_total_kernel(double* v, double lambda_ssim, double lambda_
 int zero_grads(Ctx* c, const sct_grads* g, int64_t m) {
   const size_t f = sizeof(float);
   if (g->pos == g->rho_raw + m && g->scale_raw == g->pos + 3 * m && g->rot == g->scale_raw + 3 * m) {
-    SCT_CUDA_TRY(cudaMemsetAsync(g->rho_raw, 0, 11 * m * f, c->stream));  // one contiguous 11*M buffer
-    return SCT_OK;
+    return launch_zero(c, g->rho_raw, 11 * m * f);  // one contiguous 11*M buffer (PDL chain kept)
   }
   SCT_CUDA_TRY(cudaMemsetAsync(g->rho_raw, 0, m * f, c->stream));
   SCT_CUDA_TRY(cudaMemsetAsync(g->pos, 0, 3 * m * f, c->stream));
