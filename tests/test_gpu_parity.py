@@ -555,3 +555,46 @@ print(h, float(fwd.images.abs().sum()))
         out[name] = p.stdout.strip().splitlines()[-1].split()
     assert float(out["mid"][1]) > 0
     assert out["mid"][0] == out["device_sort"][0] == out["one_cta_items"][0], out
+
+
+def test_dependent_launch_changes_no_bit():
+    """Programmatic dependent launch (every engine kernel; SCT_PDL=0 disables
+    it) only overlaps a kernel's launch with its predecessor's tail: images,
+    deterministic gradients and a sync-free native train step are bitwise the
+    same with and without it."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, hashlib, numpy as np, torch
+sys.path.insert(0, ".")
+import paper_2405_20693_b200 as P
+from oracle import oracle as O
+oc = O.random_cloud(O.Rng(12), 3000, 0.8, 0.005, 0.12)
+f32 = [np.asarray(a, dtype=np.float32) for a in (oc.rho_raw, oc.pos, oc.scale_raw, oc.rot)]
+cloud = P.GaussianCloud(oc.s_min, *f32)
+eng = P.Engine(0)
+eng.set_capacity(2000000, 2000000)
+th = [2 * np.pi * i / 12 for i in range(12)]
+fwd = eng.render(cloud, P.ScannerConfig(detector_res_px=(192, 160)), th)
+g = torch.Generator().manual_seed(5)
+up = (torch.rand(12, 160, 192, generator=g) - 0.5).cuda()
+gr = P.CloudGrads(cloud.size())
+eng.render_backward(cloud, fwd, up, gr)
+grid = P.grid_for_extent((-1, -1, -1), (1, 1, 1), (40, 40, 40))
+vol = eng.voxelize(cloud, grid)
+vg = P.CloudGrads(cloud.size())
+eng.voxelize_backward(cloud, grid, (torch.rand(grid.shape_zyx, generator=g) - 0.5).cuda(), vg)
+torch.cuda.synchronize()
+assert not eng.take_overflow()
+blob = b"".join(t.cpu().numpy().tobytes() for t in (fwd.images, gr.flat(), vol, vg.flat()))
+print(hashlib.sha256(blob).hexdigest())
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for pdl in ("1", "0"):
+        p = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, SCT_PDL=pdl),
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[pdl] = p.stdout.strip().splitlines()[-1]
+    assert out["1"] == out["0"], out
