@@ -2026,46 +2026,74 @@ __global__ void __launch_bounds__(kSmallOrderThreads) tile_order_small_kernel(co
   }
 }
 
-// The same stable 16-bucket order by a one-CTA counting sort, for list counts
-// beyond the block radix sort's register tile (kSmallOrder < n <= kMidOrder:
-// 8-rank cfg3 shards, 10 views = 10 240 lists; the device-wide sort took four
-// launches, 28 us). Thread t owns lists [t * per, (t + 1) * per); the counts
-// cnt[bucket][thread] are exclusive-scanned in (bucket, thread) order, which is
-// exactly the stable output position of each thread's first list per bucket.
-constexpr int kMidOrderThreads = 1024, kMidOrderPer = 64;
-constexpr int kMidOrder = kMidOrderThreads * kMidOrderPer;
-__global__ void __launch_bounds__(kMidOrderThreads) tile_order_mid_kernel(const int2* __restrict__ ranges,
-                                                                          long long base, int n,
-                                                                          int32_t* __restrict__ order) {
+// The same stable 16-bucket order for larger list counts in two multi-CTA
+// passes (cfg3, 76 800 lists: 31 -> 11 us against the device-wide radix sort's
+// four launches; the 8-rank shard's 10 240: 28 -> 9 us, a one-CTA counting sort
+// took 16):
+// pass 1 counts each 1024-list block's buckets, pass 2 ranks every list — the
+// bucket start over all blocks, the earlier blocks' and earlier warps' counts
+// of its bucket, and its rank among the warp's lanes of the same bucket
+// (__match_any_sync) — and writes it to its stable position.
+constexpr int kOrderBlock = 1024;
+__global__ void __launch_bounds__(kOrderBlock) tile_order_hist_kernel(const int2* __restrict__ ranges, long long base,
+                                                                      int n, int32_t* __restrict__ hist) {
   pdl_prologue();
-  using Scan = cub::BlockScan<int32_t, kMidOrderThreads>;
-  __shared__ typename Scan::TempStorage tmp;
-  extern __shared__ int32_t cnt[];  // [16][kMidOrderThreads]
-  const int tid = threadIdx.x;
-  const int per = (n + kMidOrderThreads - 1) / kMidOrderThreads;
-  const int w0 = min(n, tid * per), w1 = min(n, w0 + per);
-#pragma unroll
-  for (int b = 0; b < 16; ++b) cnt[b * kMidOrderThreads + tid] = 0;
-#pragma unroll 4
-  for (int w = w0; w < w1; ++w) {
+  __shared__ int32_t h[16];
+  if (threadIdx.x < 16) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int w = blockIdx.x * kOrderBlock + threadIdx.x;
+  if (w < n) {
     const int2 r = ranges[base + w];
-    ++cnt[order_key4(r.y - r.x) * kMidOrderThreads + tid];  // own column: no atomics
+    atomicAdd(&h[order_key4(r.y - r.x)], 1);
   }
   __syncthreads();
-  // exclusive scan of the 16 * 1024 counts in (bucket, thread) order: thread j
-  // scans entries [16 j, 16 j + 16)
-  int32_t v[16], x[16];
+  if (threadIdx.x < 16) hist[blockIdx.x * 16 + threadIdx.x] = h[threadIdx.x];
+}
+__global__ void __launch_bounds__(kOrderBlock) tile_order_rank_kernel(const int2* __restrict__ ranges, long long base,
+                                                                      int n, const int32_t* __restrict__ hist,
+                                                                      int32_t* __restrict__ order) {
+  pdl_prologue();
+  __shared__ int32_t s_base[16];
+  __shared__ int32_t s_wc[kOrderBlock / 32][16];  // per-warp bucket counts, then their exclusive prefix
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w = blockIdx.x * kOrderBlock + threadIdx.x;
+  if (warp == 0) {  // bucket starts over all blocks + this bucket's count in earlier blocks
+    int tot = 0, before = 0;
+    if (lane < 16)
+      for (int b = 0; b < (int)gridDim.x; ++b) {
+        const int v = hist[b * 16 + lane];
+        tot += v;
+        if (b < (int)blockIdx.x) before += v;
+      }
+    int incl = tot;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) v[k] = cnt[16 * tid + k];
-  Scan(tmp).ExclusiveSum(v, x);
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < 16; ++k) cnt[16 * tid + k] = x[k];
-  __syncthreads();
-  for (int w = w0; w < w1; ++w) {
-    const int2 r = ranges[base + w];
-    order[cnt[order_key4(r.y - r.x) * kMidOrderThreads + tid]++] = w;
+    for (int d = 1; d < 16; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    if (lane < 16) s_base[lane] = incl - tot + before;
   }
+  for (int i = threadIdx.x; i < (kOrderBlock / 32) * 16; i += blockDim.x) (&s_wc[0][0])[i] = 0;
+  __syncthreads();
+  uint32_t key = 16;  // past the end: no bucket
+  if (w < n) {
+    const int2 r = ranges[base + w];
+    key = order_key4(r.y - r.x);
+  }
+  const uint32_t same = __match_any_sync(0xffffffffu, key);
+  const int rank = __popc(same & ((1u << lane) - 1u));
+  if (key < 16 && rank == 0) s_wc[warp][key] = __popc(same);
+  __syncthreads();
+  if (threadIdx.x < 16) {  // exclusive prefix over the warps, per bucket
+    int run = 0;
+    for (int k = 0; k < kOrderBlock / 32; ++k) {
+      const int v = s_wc[k][threadIdx.x];
+      s_wc[k][threadIdx.x] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  if (key < 16) order[s_base[key] + s_wc[warp][key] + rank] = w;
 }
 
 // keys for the chunked order: (chunk of the view, descending length octave)
@@ -2105,19 +2133,17 @@ static const int* tile_order(Ctx* c, const sct_fwd* s, int v0, int nv) {
     ++c->order_gen;
     return i0;
   }
-  static const bool mid_ok = [] {  // SCT_ORDER_MID=0 (diagnostic): the device-wide sort instead
+  static const bool mid_ok = [] {  // SCT_ORDER_MID=0 (diagnostic): the device-wide radix sort instead
     const char* e = std::getenv("SCT_ORDER_MID");
     return !(e && atoi(e) == 0);
   }();
-  if (mid_ok && n <= kMidOrder) {
-    static bool attr = false;
-    const int smem = 16 * kMidOrderThreads * (int)sizeof(int32_t);
-    if (!attr) {
-      if (cudaFuncSetAttribute(tile_order_mid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-        return nullptr;
-      attr = true;
-    }
-    pdl_launch(tile_order_mid_kernel, dim3(1), dim3(kMidOrderThreads), smem, c->stream, s->d_ranges, (long long)v0 * T, n, i0);
+  if (mid_ok) {  // two multi-CTA passes (SCT_ORDER_MID=0: the device-wide radix sort below)
+    const int nb = (n + kOrderBlock - 1) / kOrderBlock;
+    int32_t* hist = reinterpret_cast<int32_t*>(k1);  // nb * 16 <= n entries
+    pdl_launch(tile_order_hist_kernel, dim3(nb), dim3(kOrderBlock), 0, c->stream, s->d_ranges, (long long)v0 * T, n,
+               hist);
+    pdl_launch(tile_order_rank_kernel, dim3(nb), dim3(kOrderBlock), 0, c->stream, s->d_ranges, (long long)v0 * T, n,
+               (const int32_t*)hist, i0);
     ++c->order_gen;
     return i0;
   }

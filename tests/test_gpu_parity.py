@@ -519,11 +519,12 @@ print(json.dumps(out))
 
 def test_list_schedules_agree():
     """K3/K4 process the (view, tile) lists in a longest-first order built by
-    one of three sorts by list count (one-CTA block radix sort, one-CTA
-    counting sort for mid sizes — the 8-rank shards —, device-wide radix sort)
-    and cut into K3 work items by a one-CTA or a multi-CTA scan. The schedule
-    must not change a bit of the images or the (deterministic-mode) gradients:
-    40 views at 256^2 = 10 240 lists, run with each path forced."""
+    one of three sorts by list count (one-CTA block radix sort up to 8 192
+    lists, a two-pass multi-CTA counting sort beyond — the 8-rank shards and
+    cfg3 —, or the device-wide radix sort, SCT_ORDER_MID=0) and cut into K3 work
+    items by a one-CTA or a multi-CTA scan. The schedule must not change a bit
+    of the images or the (deterministic-mode) gradients: 40 views at 256^2 =
+    10 240 lists, run with each path forced."""
     import os
     import subprocess
     import sys
