@@ -36,7 +36,7 @@ UNIT = "projections/s"
 # Hardware-unit evidence per kernel (ncu, tools/profile_round2.sh -> tools/hw_units.py):
 # the busiest unit (issue slots, FP32/FP64/XU/tensor pipes, L1 wavefronts, L2, DRAM)
 # and its fraction of peak. Static: read from the committed profile, not measured here.
-HW_PROFILE = "profiles/r02i_hw_units.json"
+HW_PROFILE = "profiles/r02j_hw_units.json"
 NCU_NAMES = {
     "K0_gauss_prep": ["gauss_prep_kernel"], "K1_raster_preprocess": ["raster_preprocess_kernel"],
     "K2_bin_count": ["bin_count_kernel"],
