@@ -43,7 +43,7 @@ NCU_NAMES = {
     "K2_bin_scan": ["bin_colsum_kernel", "bin_segscan_kernel", "bin_tilebase_kernel", "bin_apply_kernel"],
     "K2_bin_scatter": ["bin_scatter_kernel"], "K2_bin_ranges": ["bin_ranges_kernel"],
     "K2_tile_order": ["tile_order_keys_kernel", "tile_order_small_kernel<1>", "tile_order_hist_kernel", "tile_order_rank_kernel"],
-    "K2_k3_items": ["k3_parts_kernel", "k3_items_kernel", "k3_first_small_kernel"],
+    "K2_k3_items": ["k3_parts_kernel", "k3_items_kernel", "k3_first_small_kernel", "k3_block_parts_kernel", "k3_block_items_kernel"],
     "K3_composite": ["composite_kernel"],
     "K4_backward_stats": ["backward_stats_mma_kernel<2>", "backward_stats_mma_kernel<4>", "backward_stats_mma_kernel"],
     "K5_raster_chain": ["raster_chain_kernel<0>"], "K5_view_sum": ["view_sum_kernel"],

@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -857,6 +859,60 @@ __global__ void __launch_bounds__(kSmallWorkThreads) k3_first_small_kernel(const
     first[i] = f;
     f += count[i];
   }
+}
+
+// K3 work items for larger list counts in two multi-CTA passes (replacing
+// k3_parts + CUB's two-kernel scan + k3_items): per 1024-list block the part
+// counts and their sum, then each block's base (the earlier blocks' sums), a
+// block scan, the lists' first items and the items themselves.
+constexpr int kK3Block = 1024;
+__global__ void __launch_bounds__(kK3Block) k3_block_parts_kernel(const int2* __restrict__ ranges,
+                                                                  const int* __restrict__ order, int n, int part_len,
+                                                                  int* __restrict__ count, int* __restrict__ bsum) {
+  pdl_prologue();
+  using Reduce = cub::BlockReduce<int, kK3Block>;
+  __shared__ typename Reduce::TempStorage tmp;
+  const int i = blockIdx.x * kK3Block + threadIdx.x;
+  int k = 0;
+  if (i < n) {
+    const int2 r = ranges[order[i]];
+    k = max(1, (r.y - r.x + part_len - 1) / part_len);
+    count[i] = k;
+  }
+  const int sum = Reduce(tmp).Sum(k);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = sum;
+}
+__global__ void __launch_bounds__(kK3Block) k3_block_items_kernel(const int* __restrict__ order,
+                                                                  const int* __restrict__ count, int n,
+                                                                  const int* __restrict__ bsum, int* __restrict__ first,
+                                                                  int4* __restrict__ items, int* __restrict__ n_items,
+                                                                  int* __restrict__ tile_cnt, long long max_items) {
+  pdl_prologue();
+  using Scan = cub::BlockScan<int, kK3Block>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_base;
+  if (threadIdx.x < 32) {  // sum of the earlier blocks (fixed order: lane-strided, then a shuffle tree)
+    int b = 0;
+    for (int j = threadIdx.x; j < (int)blockIdx.x; j += 32) b += bsum[j];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if (threadIdx.x == 0) s_base = b;
+  }
+  const int i = blockIdx.x * kK3Block + threadIdx.x;
+  const int k = i < n ? count[i] : 0;
+  int f = 0;
+  Scan(tmp).ExclusiveSum(k, f);
+  __syncthreads();
+  f += s_base;
+  if (i < n) {
+    const int w = order[i];
+    first[i] = f;
+    for (int p = 0; p < k; ++p) items[f + p] = make_int4(w, p, k, f);
+    if (i == n - 1) *n_items = f + k;
+  }
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < max_items;
+       j += (long long)gridDim.x * blockDim.x)
+    tile_cnt[j] = 0;
 }
 
 // the items of every list, and the reset of K3's per-item tile counters
@@ -2266,6 +2322,13 @@ struct K3Work {
 // ranges: the lists the order's indices refer to (s->d_ranges + T v0 for a
 // view-range order). Cached: rebuilt only when the order (generation), the
 // part length or the list count changed.
+static bool k3_two_pass() {  // SCT_K3_TWOPASS=0 (diagnostic): k3_parts + CUB scan + k3_items
+  static const bool on = [] {
+    const char* e = std::getenv("SCT_K3_TWOPASS");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
 static int list_work(Ctx* c, const sct_fwd* s, const int* order, const int2* ranges, int n, int part_len,
                      K3Work& kw) {
   kw.part_len = part_len;
@@ -2300,6 +2363,18 @@ static int list_work(Ctx* c, const sct_fwd* s, const int* order, const int2* ran
     }();
     if (n <= small_max) {
       pdl_launch(k3_first_small_kernel, dim3(1), dim3(kSmallWorkThreads), 0, c->stream, ranges, order, n, kw.part_len, count, first);
+    } else if (k3_two_pass()) {
+      const int nb = (n + kK3Block - 1) / kK3Block;
+      int* bsum = nullptr;
+      SCT_TRY(stage_buf(c, 26, sizeof(int) * (size_t)nb, (void**)&bsum));
+      pdl_launch(k3_block_parts_kernel, dim3(nb), dim3(kK3Block), 0, c->stream, ranges, order, n, kw.part_len, count,
+                 bsum);
+      pdl_launch(k3_block_items_kernel, dim3(nb), dim3(kK3Block), 0, c->stream, (const int*)order, (const int*)count,
+                 n, (const int*)bsum, first, items, n_items, tile_cnt, max_items);
+      key.gen = c->order_gen;
+      key.part = kw.part_len;
+      key.n = n;
+      return SCT_OK;
     } else {
       pdl_launch(k3_parts_kernel, dim3(grid_cap(c, n, 256)), dim3(256), 0, c->stream, ranges, order, n, kw.part_len, count);
       size_t tmp = 0;

@@ -549,13 +549,13 @@ print(h, float(fwd.images.abs().sum()))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
     for name, env in (("mid", {}), ("device_sort", {"SCT_ORDER_MID": "0"}),
-                      ("one_cta_items", {"SCT_K3_SMALL": "16384"})):
+                      ("one_cta_items", {"SCT_K3_SMALL": "16384"}), ("cub_items", {"SCT_K3_TWOPASS": "0"})):
         p = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env), capture_output=True,
                            text=True, timeout=300)
         assert p.returncode == 0, p.stderr[-2000:]
         out[name] = p.stdout.strip().splitlines()[-1].split()
     assert float(out["mid"][1]) > 0
-    assert out["mid"][0] == out["device_sort"][0] == out["one_cta_items"][0], out
+    assert out["mid"][0] == out["device_sort"][0] == out["one_cta_items"][0] == out["cub_items"][0], out
 
 
 def test_dependent_launch_changes_no_bit():
