@@ -285,10 +285,11 @@ __device__ __forceinline__ void d_cov_param_grads(const dKernel& k, const dM3& G
 #pragma unroll
   for (int a = 0; a < 3; ++a) g_scale[a] = g_d.m[a][a] * 2.0 * k.s[a] * exp(k.sraw[a]);
   // rotation_matrix_jacobian with the normalisation chain
-  const double nrm = sqrt(k.q[0] * k.q[0] + k.q[1] * k.q[1] + k.q[2] * k.q[2] + k.q[3] * k.q[3]);
+  // (the Newton reciprocal / root of fp64_math.cuh: gradients only)
+  const double inv_nrm = d_fast_rsqrt(k.q[0] * k.q[0] + k.q[1] * k.q[1] + k.q[2] * k.q[2] + k.q[3] * k.q[3]);
   double qn[4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a) qn[a] = k.q[a] / nrm;
+  for (int a = 0; a < 4; ++a) qn[a] = k.q[a] * inv_nrm;
   const double w = qn[0], x = qn[1], y = qn[2], z = qn[3];
   // dR/d(qn_l) contracted with g_r: c_l = 2 * sum(g_r .* dn_l)
   double c[4];
@@ -302,7 +303,7 @@ __device__ __forceinline__ void d_cov_param_grads(const dKernel& k, const dM3& G
                 g_r.m[1][1] * (-2 * z) + g_r.m[1][2] * y + g_r.m[2][0] * x + g_r.m[2][1] * y);
   const double qc = qn[0] * c[0] + qn[1] * c[1] + qn[2] * c[2] + qn[3] * c[3];
 #pragma unroll
-  for (int kk = 0; kk < 4; ++kk) g_rot[kk] = (c[kk] - qn[kk] * qc) / nrm;
+  for (int kk = 0; kk < 4; ++kk) g_rot[kk] = (c[kk] - qn[kk] * qc) * inv_nrm;
 }
 
 __global__ void __launch_bounds__(128) raster_finalize_kernel(
